@@ -1,0 +1,173 @@
+/* sconv_b200 — B200-native sparse-convolution engine (Minuet Map + GMaS), C ABI.
+ *
+ * Drop-in boundary for the reference's SC-layer API. The reference (arXiv 2401.06145
+ * artifact) is a header-only C++20 library in namespace `sconv`; its hot path exists as
+ * the types in proj/include/sconv/geometry.hpp plus the SPEC.md operation signatures.
+ * Each entry point below names the reference interface it replaces. No exceptions and
+ * no C++/torch types cross this boundary: plain pointers, sizes and status codes. The
+ * header-only C++ adapter include/sconv_b200.hpp rethrows the reference exception types.
+ *
+ * Status mapping (reference exception -> status):
+ *   std::invalid_argument -> SCONV_ERR_ARG    (geometry.hpp:90,134-136,162,186,189)
+ *   std::out_of_range     -> SCONV_ERR_RANGE  (geometry.hpp:53 "coordinate x out of range: v")
+ *   std::logic_error      -> SCONV_ERR_STATE  (SPEC.md:327 invariant violations)
+ * The message text (sconv_last_error) is identical to the reference's where one exists.
+ *
+ * Threading: one context per (host thread, device). Calls on a context are serialised
+ * on its CUDA stream. Results are deterministic and independent of grid sizes.
+ */
+#ifndef SCONV_B200_H_
+#define SCONV_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SCONV_OK = 0,
+  SCONV_ERR_ARG = 1,
+  SCONV_ERR_RANGE = 2,
+  SCONV_ERR_CUDA = 3,
+  SCONV_ERR_OOM = 4,
+  SCONV_ERR_STATE = 5
+} sconv_status;
+
+typedef enum { SCONV_MEM_HOST = 0, SCONV_MEM_DEVICE = 1 } sconv_mem;
+typedef enum { SCONV_F32 = 0, SCONV_F16 = 1, SCONV_BF16 = 2 } sconv_dtype;
+typedef enum { SCONV_GROUP_MAP_ORDER = 0, SCONV_GROUP_SORTED = 1 } sconv_group_policy;
+
+typedef struct sconv_ctx sconv_ctx;
+typedef struct sconv_map sconv_map;
+typedef struct sconv_weights sconv_weights;
+
+/* Layer geometry + Map hyperparameters.
+ * SPEC-literal sc_layer_forward(cloud, W, K, s, cfg) is
+ * {kernel_size=K, offset_scale=s, out_stride=s, transposed=0}. SURVEY §2.2 extensions:
+ * even K (t in [0,K-1]), tensor strides (offset_scale != out_stride) and transposed
+ * maps (queries = target coordinates, offsets negated). */
+typedef struct {
+  int kernel_size;  /* K */
+  int offset_scale; /* weight offsets = t * offset_scale */
+  int out_stride;   /* Eq. 1 stride for the output coordinates (ignored when transposed) */
+  int transposed;   /* 1: output coordinates = target, offsets negated */
+  int block_B;      /* source block size B (SPEC.md:247 default 256) */
+  int block_C;      /* balanced query-block cap C (default 512) */
+} sconv_map_cfg;
+
+/* GMaS configuration (SPEC.md:359 config{grouping policy, eps, max_batch, tiles}). */
+typedef struct {
+  int policy;         /* sconv_group_policy, default SORTED */
+  double epsilon;     /* padding threshold, default 0.25 */
+  int max_batch;      /* max GEMMs per group, default 16 */
+  int gather_tile;    /* T_g channels per work item; 0 = autotuned / heuristic */
+  int scatter_tile;   /* T_s; 0 = autotuned / heuristic */
+  int compute_dtype;  /* GEMM operand type: SCONV_F16 (default) or SCONV_BF16 */
+} sconv_exec_cfg;
+
+typedef struct {
+  int64_t num_inputs;      /* |P| */
+  int64_t num_outputs;     /* |Q| */
+  int32_t num_offsets;     /* K^3 (or K^3 for even K) */
+  int64_t total_matches;   /* |M| */
+  int64_t buffer_length;   /* R_pad of the last layer_forward on this map (0 before) */
+  int32_t groups;          /* GEMM groups of the last layer_forward */
+  double padding_overhead; /* x / y (Fig. 6) of the last layer_forward */
+  int32_t gather_tile, scatter_tile;
+} sconv_map_info;
+
+/* ---------------- context ---------------- */
+sconv_status sconv_ctx_create(int device, sconv_ctx** out);
+void sconv_ctx_destroy(sconv_ctx* ctx);
+const char* sconv_last_error(const sconv_ctx* ctx);
+/* Use an existing cudaStream_t (NULL = the context's own stream). */
+sconv_status sconv_ctx_set_stream(sconv_ctx* ctx, void* cuda_stream);
+void* sconv_ctx_stream(const sconv_ctx* ctx);
+sconv_status sconv_ctx_synchronize(sconv_ctx* ctx);
+/* Kernel launches issued by this context so far (gpu_launches accounting). */
+int64_t sconv_ctx_launch_count(const sconv_ctx* ctx);
+/* Per-kernel CUDA-event timing on the context stream (0 = off). */
+sconv_status sconv_ctx_set_profiling(sconv_ctx* ctx, int enabled);
+/* Accumulated profile: kernel i -> name, launches, total ms. Returns count. */
+int sconv_ctx_profile_count(const sconv_ctx* ctx);
+sconv_status sconv_ctx_profile_entry(sconv_ctx* ctx, int i, const char** name, int64_t* launches, double* total_ms);
+sconv_status sconv_ctx_profile_reset(sconv_ctx* ctx);
+/* Write `bytes` to a scratch buffer (L2 flush between timed iterations). */
+sconv_status sconv_ctx_flush_l2(sconv_ctx* ctx, size_t bytes);
+
+/* ---------------- device buffers (for callers without their own allocator) ------ */
+sconv_status sconv_device_alloc(sconv_ctx* ctx, size_t bytes, void** out);
+sconv_status sconv_device_free(sconv_ctx* ctx, void* ptr);
+sconv_status sconv_memcpy(sconv_ctx* ctx, void* dst, const void* src, size_t bytes, int kind /*cudaMemcpyKind*/);
+
+/* ---------------- Map step ----------------
+ * Replaces build_kernel_map_sorted(P, Q, offsets, B, C) together with
+ * generate_output_coords(P, s) (geometry.hpp:161-178) and weight_offsets(K, s)
+ * (geometry.hpp:133-148), as sc_layer_forward composes them.
+ * xyz: n x 3 int32 (x,y,z) rows of P in `mem`. in_sorted: P.sorted (SPEC.md:193 sort reuse).
+ * target_xyz/n_target: transposed layers only (sorted unique output coordinates).
+ * Output coordinates Q are sorted; for stride 1 with sorted P they alias P (geometry.hpp:163).
+ * Map indices: j = row of P as given, i = row of Q. */
+sconv_status sconv_map_build(sconv_ctx* ctx, const int32_t* xyz, int64_t n, int mem, int in_sorted,
+                             const sconv_map_cfg* cfg, const int32_t* target_xyz, int64_t n_target, int target_mem,
+                             sconv_map** out);
+/* Chain: P = the output coordinates of `prev` (device-resident, sorted; SPEC.md:528 reuse). */
+sconv_status sconv_map_build_chained(sconv_ctx* ctx, const sconv_map* prev, const sconv_map_cfg* cfg,
+                                     const sconv_map* target_of, sconv_map** out);
+sconv_status sconv_map_get_info(sconv_ctx* ctx, const sconv_map* map, sconv_map_info* info);
+/* KernelMap readback in canonical order (per offset k, sorted by output index i;
+ * SPEC.md:109). sizes: num_offsets; in_idx/out_idx: total_matches; out_xyz: num_outputs x 3.
+ * Any pointer may be NULL. Host memory. */
+sconv_status sconv_map_read(sconv_ctx* ctx, const sconv_map* map, int32_t* out_xyz, int64_t* sizes, int32_t* in_idx,
+                            int32_t* out_idx);
+/* Device views (valid until sconv_map_free): packed sorted output keys, canonical pairs. */
+sconv_status sconv_map_device_views(const sconv_map* map, const uint64_t** out_keys, const int32_t** in_idx,
+                                    const int32_t** out_idx);
+void sconv_map_free(sconv_ctx* ctx, sconv_map* map);
+
+/* ---------------- weights ----------------
+ * WeightSet: num_offsets matrices c_in x c_out, fp32 row-major [k][cin][cout].
+ * Stored on device in the GEMM operand type, K-major (transposed) for the tensor cores. */
+sconv_status sconv_weights_create(sconv_ctx* ctx, const float* w, int mem, int num_offsets, int c_in, int c_out,
+                                  int dtype, sconv_weights** out);
+void sconv_weights_free(sconv_ctx* ctx, sconv_weights* w);
+
+/* ---------------- GMaS step ----------------
+ * Replaces group_gemms + build_metadata_tables + gather + gemm_execute + scatter
+ * as composed by sc_layer_forward. f_in: num_inputs x c_in rows in
+ * P order (dtype f_in_dtype, memory f_in_mem). f_out: num_outputs x c_out in Q order. */
+sconv_status sconv_layer_forward(sconv_ctx* ctx, sconv_map* map, const sconv_weights* w, const void* f_in,
+                                 int f_in_dtype, int f_in_mem, const sconv_exec_cfg* cfg, void* f_out, int f_out_dtype,
+                                 int f_out_mem);
+
+/* Alg. 2: profile every divisor tile for gather and scatter on this
+ * map (1 warm-up + `rounds`, median of CUDA-event times), keep the argmin (smallest tile
+ * on ties) and remember it for layers with the same (c_in, c_out). latencies_ms (optional)
+ * receives [gather per candidate..., scatter per candidate...]. */
+sconv_status sconv_tune_layer(sconv_ctx* ctx, sconv_map* map, const sconv_weights* w, const void* f_in,
+                              int f_in_dtype, int rounds, int* gather_tile, int* scatter_tile,
+                              double* latencies_ms, int* n_latencies);
+
+/* One-shot SPEC-literal sc_layer_forward on host buffers:
+ * coords + fp32 features in, sorted output coords + fp32 features out. out_xyz must hold
+ * n rows (|Q| <= |P|), f_out n x c_out. */
+sconv_status sconv_sc_layer_forward(sconv_ctx* ctx, const int32_t* xyz, int64_t n, int in_sorted, const float* f_in,
+                                    int c_in, const float* w, int c_out, int K, int s, const sconv_exec_cfg* cfg,
+                                    int32_t* out_xyz, int64_t* n_out, float* f_out);
+
+/* ---------------- utilities (cli gen) ----------------
+ * N unique coordinates uniform in [0,E)^3 from Rng(stream_seed(seed,0)) (x,y,z order,
+ * duplicates rejected), then N x C features U[0,1) from the same stream. Host buffers. */
+sconv_status sconv_generate_synthetic(int64_t N, int64_t E, int64_t C, uint64_t seed, int32_t* xyz, float* feats);
+/* WeightSet from Rng(stream_seed(seed, stream)), U[-0.1, 0.1], order [k][cin][cout]. */
+sconv_status sconv_generate_weights(uint64_t seed, uint64_t stream, int num_offsets, int c_in, int c_out, float* w);
+/* Thread-independent last error (for failures before a context exists). */
+const char* sconv_global_last_error(void);
+const char* sconv_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SCONV_B200_H_ */

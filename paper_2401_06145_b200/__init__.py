@@ -1,0 +1,13 @@
+"""B200-native sparse-convolution engine (Minuet Map + GMaS) behind the reference SC-layer API.
+
+The compute path is libsconv_b200.so (hand-written sm_100a CUDA behind a C ABI,
+include/sconv_b200.h); this package is its Python binding. No CPU fallback exists.
+"""
+from .sconv import (  # noqa: F401
+    BF16, F16, F32, GROUP_MAP_ORDER, GROUP_SORTED, MEM_DEVICE, MEM_HOST, Context, CudaError, ExecCfg,
+    InvalidArgument, KernelMap, LogicError, MapCfg, OutOfRange, PointCloud, SconvError, Weights,
+    build_kernel_map_sorted, exec_cfg, generate_synthetic, generate_weights, layer_forward, layer_forward_device,
+    load, map_cfg, sc_layer_forward, tune_layer, weight_offsets,
+)
+
+__all__ = [n for n in dir() if not n.startswith("_")]

@@ -1,0 +1,491 @@
+// C ABI of libsconv_b200 (include/sconv_b200.h): exception-free boundary, context runtime,
+// tile autotuner (Alg. 2), synthetic-input generator (SPEC cli gen).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <unordered_set>
+#include <vector>
+
+#include "common.cuh"
+#include "ctx.hpp"
+#include "gmas.hpp"
+#include "map.hpp"
+
+namespace sconvb {
+
+cudaEvent_t Ctx::take_event() {
+  if (!event_pool.empty()) {
+    cudaEvent_t e = event_pool.back();
+    event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  SCONV_CUDA(cudaEventCreate(&e));
+  return e;
+}
+
+void Ctx::resolve_profile() {
+  if (pending.empty()) return;
+  SCONV_CUDA(cudaEventSynchronize(pending.back().b));
+  for (auto& p : pending) {
+    float ms = 0.f;
+    SCONV_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
+    auto it = profile.find(p.name);
+    if (it == profile.end()) {
+      profile_names.push_back(p.name);
+      it = profile.emplace(p.name, ProfileEntry{}).first;
+    }
+    it->second.launches += 1;
+    it->second.total_ms += ms;
+    last_records.emplace_back(p.name, ms);
+    event_pool.push_back(p.a);
+    event_pool.push_back(p.b);
+  }
+  pending.clear();
+}
+
+namespace {
+
+std::mutex g_err_mu;
+std::string g_err;
+
+template <class Fn>
+sconv_status guarded(sconv_ctx* ctx, Fn&& fn) {
+  try {
+    fn();
+    return SCONV_OK;
+  } catch (const Error& e) {
+    if (ctx) ctx->err = e.what();
+    std::lock_guard<std::mutex> l(g_err_mu);
+    g_err = e.what();
+    return e.status;
+  } catch (const std::bad_alloc&) {
+    if (ctx) ctx->err = "host allocation failed";
+    return SCONV_ERR_OOM;
+  } catch (const std::exception& e) {
+    if (ctx) ctx->err = e.what();
+    std::lock_guard<std::mutex> l(g_err_mu);
+    g_err = e.what();
+    return SCONV_ERR_STATE;
+  }
+}
+
+sconv_map_cfg default_map_cfg(int K, int s) {
+  sconv_map_cfg c;
+  c.kernel_size = K;
+  c.offset_scale = s;
+  c.out_stride = s;
+  c.transposed = 0;
+  c.block_B = 256;
+  c.block_C = 512;
+  return c;
+}
+
+sconv_exec_cfg normalize(const sconv_exec_cfg* cfg) {
+  sconv_exec_cfg c;
+  c.policy = SCONV_GROUP_SORTED;
+  c.epsilon = 0.25;
+  c.max_batch = 16;
+  c.gather_tile = 0;
+  c.scatter_tile = 0;
+  c.compute_dtype = SCONV_F16;
+  if (cfg) c = *cfg;
+  if (c.compute_dtype != SCONV_F16 && c.compute_dtype != SCONV_BF16) fail(SCONV_ERR_ARG, "compute dtype must be f16 or bf16");
+  return c;
+}
+
+sconv_map* wrap(std::unique_ptr<MapData> m) {
+  auto* out = new sconv_map;
+  static_cast<MapData&>(*out) = std::move(*m);
+  return out;
+}
+
+// SplitMix64 (reference prng.hpp:19-54), restated for the product's synthetic generator.
+struct SplitMix {
+  uint64_t s;
+  uint64_t next() {
+    s += 0x9E3779B97F4A7C15ull;
+    uint64_t z = s;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+  }
+  double unit() { return static_cast<double>(next() >> 11) * (1.0 / 9007199254740992.0); }
+  uint64_t below(uint64_t bound) {
+    const uint64_t limit = uint64_t{0} - ((uint64_t{0} - bound) % bound);
+    for (;;) {
+      const uint64_t r = next();
+      if (limit == 0 || r < limit) return r % bound;
+    }
+  }
+};
+uint64_t stream_seed(uint64_t seed, uint64_t idx) { return seed ^ ((idx + 1) * 0x9E3779B97F4A7C15ull); }
+
+double median(std::vector<double> v) {
+  std::sort(v.begin(), v.end());
+  const size_t n = v.size();
+  return n % 2 ? v[n / 2] : 0.5 * (v[n / 2 - 1] + v[n / 2]);
+}
+
+}  // namespace
+}  // namespace sconvb
+
+using namespace sconvb;
+
+extern "C" {
+
+const char* sconv_version(void) { return "sconv_b200 0.1 (sm_100a)"; }
+
+const char* sconv_global_last_error(void) {
+  std::lock_guard<std::mutex> l(g_err_mu);
+  static thread_local std::string copy;
+  copy = g_err;
+  return copy.c_str();
+}
+
+sconv_status sconv_ctx_create(int device, sconv_ctx** out) {
+  if (!out) return SCONV_ERR_ARG;
+  *out = nullptr;
+  auto* ctx = new sconv_ctx;
+  const sconv_status st = guarded(nullptr, [&] {
+    ctx->device = device;
+    SCONV_CUDA(cudaSetDevice(device));
+    SCONV_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device));
+    SCONV_CUDA(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
+    ctx->stream = ctx->own_stream;
+    cudaMemPool_t pool;
+    SCONV_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t threshold = UINT64_MAX;
+    SCONV_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
+    SCONV_CUDA(cudaMallocHost(reinterpret_cast<void**>(&ctx->pinned),
+                              Ctx::kPinFlagsBytes + Ctx::kPinReadbackBytes + Ctx::kPinPlanBytes));
+  });
+  if (st != SCONV_OK) {
+    delete ctx;
+    return st;
+  }
+  *out = ctx;
+  return SCONV_OK;
+}
+
+void sconv_ctx_destroy(sconv_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  {
+    // release buffers on the stream before it is destroyed
+    ctx->scratch_sort.release();
+    ctx->scratch_misc.release();
+    ctx->flush_buf.release();
+    ctx->gather_buf.release();
+    ctx->gemm_out.release();
+    ctx->plan_dev.release();
+  }
+  cudaStreamSynchronize(ctx->stream);
+  for (auto& p : ctx->pending) {
+    cudaEventDestroy(p.a);
+    cudaEventDestroy(p.b);
+  }
+  for (auto e : ctx->event_pool) cudaEventDestroy(e);
+  if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  delete ctx;
+}
+
+const char* sconv_last_error(const sconv_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+sconv_status sconv_ctx_set_stream(sconv_ctx* ctx, void* s) {
+  return guarded(ctx, [&] {
+    SCONV_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->stream = s ? static_cast<cudaStream_t>(s) : ctx->own_stream;
+  });
+}
+void* sconv_ctx_stream(const sconv_ctx* ctx) { return ctx->stream; }
+sconv_status sconv_ctx_synchronize(sconv_ctx* ctx) {
+  return guarded(ctx, [&] {
+    ctx->sync();
+    ctx->resolve_profile();
+  });
+}
+int64_t sconv_ctx_launch_count(const sconv_ctx* ctx) { return ctx->launches; }
+sconv_status sconv_ctx_set_profiling(sconv_ctx* ctx, int enabled) {
+  return guarded(ctx, [&] {
+    ctx->resolve_profile();
+    ctx->profiling = enabled != 0;
+  });
+}
+int sconv_ctx_profile_count(const sconv_ctx* ctx) { return static_cast<int>(ctx->profile_names.size()); }
+sconv_status sconv_ctx_profile_entry(sconv_ctx* ctx, int i, const char** name, int64_t* launches, double* total_ms) {
+  return guarded(ctx, [&] {
+    ctx->resolve_profile();
+    if (i < 0 || i >= static_cast<int>(ctx->profile_names.size())) fail(SCONV_ERR_ARG, "profile index out of range");
+    const auto& n = ctx->profile_names[i];
+    const auto& e = ctx->profile.at(n);
+    if (name) *name = n.c_str();
+    if (launches) *launches = e.launches;
+    if (total_ms) *total_ms = e.total_ms;
+  });
+}
+sconv_status sconv_ctx_profile_reset(sconv_ctx* ctx) {
+  return guarded(ctx, [&] {
+    ctx->resolve_profile();
+    ctx->profile.clear();
+    ctx->profile_names.clear();
+    ctx->last_records.clear();
+  });
+}
+sconv_status sconv_ctx_flush_l2(sconv_ctx* ctx, size_t bytes) {
+  return guarded(ctx, [&] {
+    ctx->flush_buf.reserve(bytes, ctx->stream);
+    SCONV_CUDA(cudaMemsetAsync(ctx->flush_buf.get(), ctx->launches & 0xFF, bytes, ctx->stream));
+  });
+}
+
+sconv_status sconv_device_alloc(sconv_ctx* ctx, size_t bytes, void** out) {
+  return guarded(ctx, [&] { SCONV_CUDA(cudaMalloc(out, std::max<size_t>(bytes, 1))); });
+}
+sconv_status sconv_device_free(sconv_ctx* ctx, void* ptr) {
+  return guarded(ctx, [&] {
+    SCONV_CUDA(cudaStreamSynchronize(ctx->stream));
+    SCONV_CUDA(cudaFree(ptr));
+  });
+}
+sconv_status sconv_memcpy(sconv_ctx* ctx, void* dst, const void* src, size_t bytes, int kind) {
+  return guarded(ctx, [&] {
+    SCONV_CUDA(cudaMemcpyAsync(dst, src, bytes, static_cast<cudaMemcpyKind>(kind), ctx->stream));
+    ctx->sync();
+  });
+}
+
+sconv_status sconv_map_build(sconv_ctx* ctx, const int32_t* xyz, int64_t n, int mem, int in_sorted,
+                             const sconv_map_cfg* cfg, const int32_t* target_xyz, int64_t n_target, int target_mem,
+                             sconv_map** out) {
+  return guarded(ctx, [&] {
+    if (!cfg || !out) fail(SCONV_ERR_ARG, "null argument");
+    if (n > 0 && !xyz) fail(SCONV_ERR_ARG, "null coordinates");
+    MapSource P;
+    P.xyz = xyz;
+    P.n = n;
+    P.mem = mem;
+    P.sorted = in_sorted != 0;
+    MapSource T;
+    T.xyz = target_xyz;
+    T.n = n_target;
+    T.mem = target_mem;
+    T.sorted = true;
+    *out = wrap(build_map(*ctx, P, *cfg, cfg->transposed ? &T : nullptr));
+  });
+}
+
+sconv_status sconv_map_build_chained(sconv_ctx* ctx, const sconv_map* prev, const sconv_map_cfg* cfg,
+                                     const sconv_map* target_of, sconv_map** out) {
+  return guarded(ctx, [&] {
+    if (!prev || !cfg || !out) fail(SCONV_ERR_ARG, "null argument");
+    MapSource P;
+    P.keys = prev->q_keys;
+    P.n = prev->n_out;
+    P.sorted = true;
+    MapSource T;
+    if (cfg->transposed) {
+      if (!target_of) fail(SCONV_ERR_ARG, "transposed layer needs target coordinates");
+      if (!target_of->src_identity) fail(SCONV_ERR_ARG, "target map input must be sorted");
+      T.keys = target_of->src_keys;
+      T.n = target_of->n_in;
+      T.sorted = true;
+    }
+    *out = wrap(build_map(*ctx, P, *cfg, cfg->transposed ? &T : nullptr));
+  });
+}
+
+sconv_status sconv_map_get_info(sconv_ctx* ctx, const sconv_map* m, sconv_map_info* info) {
+  return guarded(ctx, [&] {
+    if (!m || !info) fail(SCONV_ERR_ARG, "null argument");
+    info->num_inputs = m->n_in;
+    info->num_outputs = m->n_out;
+    info->num_offsets = m->K3;
+    info->total_matches = m->total;
+    info->buffer_length = m->buffer_length;
+    info->groups = m->groups;
+    info->padding_overhead = m->padding_overhead;
+    info->gather_tile = m->gather_tile;
+    info->scatter_tile = m->scatter_tile;
+  });
+}
+
+sconv_status sconv_map_read(sconv_ctx* ctx, const sconv_map* m, int32_t* out_xyz, int64_t* sizes, int32_t* in_idx,
+                            int32_t* out_idx) {
+  return guarded(ctx, [&] {
+    if (!m) fail(SCONV_ERR_ARG, "null map");
+    if (out_xyz && m->n_out > 0) {
+      std::vector<uint64_t> keys(m->n_out);
+      SCONV_CUDA(cudaMemcpyAsync(keys.data(), m->q_keys_ptr(), keys.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+      ctx->sync();
+      for (int64_t i = 0; i < m->n_out; ++i) unpack_key(keys[i], out_xyz[3 * i], out_xyz[3 * i + 1], out_xyz[3 * i + 2]);
+    }
+    if (sizes)
+      for (int k = 0; k < m->K3; ++k) sizes[k] = m->sizes[k];
+    if (in_idx && m->total > 0)
+      SCONV_CUDA(cudaMemcpyAsync(in_idx, m->pair_in.get(), m->total * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    if (out_idx && m->total > 0)
+      SCONV_CUDA(cudaMemcpyAsync(out_idx, m->pair_out.get(), m->total * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->sync();
+  });
+}
+
+sconv_status sconv_map_device_views(const sconv_map* m, const uint64_t** out_keys, const int32_t** in_idx,
+                                    const int32_t** out_idx) {
+  if (!m) return SCONV_ERR_ARG;
+  if (out_keys) *out_keys = m->q_keys_ptr();
+  if (in_idx) *in_idx = m->pair_in.get<int32_t>();
+  if (out_idx) *out_idx = m->pair_out.get<int32_t>();
+  return SCONV_OK;
+}
+
+void sconv_map_free(sconv_ctx* ctx, sconv_map* m) {
+  (void)ctx;
+  delete m;
+}
+
+sconv_status sconv_weights_create(sconv_ctx* ctx, const float* w, int mem, int num_offsets, int c_in, int c_out,
+                                  int dtype, sconv_weights** out) {
+  return guarded(ctx, [&] {
+    if (!w || !out) fail(SCONV_ERR_ARG, "null argument");
+    auto wd = create_weights(*ctx, w, mem, num_offsets, c_in, c_out, dtype);
+    auto* o = new sconv_weights;
+    static_cast<WeightData&>(*o) = std::move(*wd);
+    *out = o;
+  });
+}
+void sconv_weights_free(sconv_ctx* ctx, sconv_weights* w) {
+  (void)ctx;
+  delete w;
+}
+
+sconv_status sconv_layer_forward(sconv_ctx* ctx, sconv_map* map, const sconv_weights* w, const void* f_in,
+                                 int f_in_dtype, int f_in_mem, const sconv_exec_cfg* cfg, void* f_out, int f_out_dtype,
+                                 int f_out_mem) {
+  return guarded(ctx, [&] {
+    if (!map || !w) fail(SCONV_ERR_ARG, "null argument");
+    if ((map->n_in > 0 && !f_in) || (map->n_out > 0 && !f_out)) fail(SCONV_ERR_ARG, "null feature buffer");
+    const sconv_exec_cfg c = normalize(cfg);
+    layer_forward(*ctx, *map, *w, f_in, f_in_dtype, f_in_mem, c, f_out, f_out_dtype, f_out_mem);
+  });
+}
+
+sconv_status sconv_tune_layer(sconv_ctx* ctx, sconv_map* map, const sconv_weights* w, const void* f_in, int f_in_dtype,
+                              int rounds, int* gather_tile, int* scatter_tile, double* lat, int* n_lat) {
+  return guarded(ctx, [&] {
+    if (!map || !w || !f_in) fail(SCONV_ERR_ARG, "null argument");
+    if (rounds < 1) fail(SCONV_ERR_ARG, "rounds must be positive");
+    const bool was = ctx->profiling;
+    ctx->resolve_profile();
+    ctx->profiling = true;
+    DevBuf out;
+    out.alloc(static_cast<size_t>(std::max<int64_t>(1, map->n_out)) * w->c_out * 4, ctx->stream);
+    auto time_kernel = [&](const char* name, int tg, int ts) {
+      sconv_exec_cfg c = normalize(nullptr);
+      c.compute_dtype = w->dtype;
+      c.gather_tile = tg;
+      c.scatter_tile = ts;
+      std::vector<double> samples;
+      for (int r = 0; r <= rounds; ++r) {  // 1 warm-up + R measured
+        ctx->last_records.clear();
+        layer_forward(*ctx, *map, *w, f_in, f_in_dtype, SCONV_MEM_DEVICE, c, out.get(), SCONV_F32, SCONV_MEM_DEVICE);
+        ctx->resolve_profile();
+        double ms = 0;
+        for (auto& rec : ctx->last_records)
+          if (rec.first == name) ms += rec.second;
+        if (r > 0) samples.push_back(ms);
+      }
+      return median(samples);
+    };
+    std::vector<double> all;
+    auto pick = [&](const char* name, int channels, bool gather) {
+      int best = -1;
+      double best_ms = 0;
+      for (int t : candidate_tiles(channels)) {
+        const double ms = gather ? time_kernel(name, t, default_tile(w->c_out, false))
+                                 : time_kernel(name, default_tile(w->c_in, true), t);
+        all.push_back(ms);
+        if (best < 0 || ms < best_ms) {  // strict: smallest tile wins ties
+          best = t;
+          best_ms = ms;
+        }
+      }
+      return best;
+    };
+    const int tg = pick("k_gather", w->c_in, true);
+    const int ts = pick("k_scatter", w->c_out, false);
+    ctx->profiling = was;
+    ctx->tuned[{w->c_in, w->c_out, w->dtype}] = {tg, ts};
+    if (gather_tile) *gather_tile = tg;
+    if (scatter_tile) *scatter_tile = ts;
+    if (n_lat) {
+      if (lat)
+        for (size_t i = 0; i < all.size() && static_cast<int>(i) < *n_lat; ++i) lat[i] = all[i];
+      *n_lat = static_cast<int>(all.size());
+    }
+  });
+}
+
+sconv_status sconv_sc_layer_forward(sconv_ctx* ctx, const int32_t* xyz, int64_t n, int in_sorted, const float* f_in,
+                                    int c_in, const float* w, int c_out, int K, int s, const sconv_exec_cfg* cfg,
+                                    int32_t* out_xyz, int64_t* n_out, float* f_out) {
+  return guarded(ctx, [&] {
+    const sconv_exec_cfg c = normalize(cfg);
+    if (K < 1 || K % 2 == 0) fail(SCONV_ERR_ARG, "kernel size must be a positive odd integer");
+    if (s < 1) fail(SCONV_ERR_ARG, "stride must be positive");
+    const sconv_map_cfg mc = default_map_cfg(K, s);
+    MapSource P;
+    P.xyz = xyz;
+    P.n = n;
+    P.mem = SCONV_MEM_HOST;
+    P.sorted = in_sorted != 0;
+    auto m = build_map(*ctx, P, mc, nullptr);
+    auto wd = create_weights(*ctx, w, SCONV_MEM_HOST, m->K3, c_in, c_out, c.compute_dtype);
+    layer_forward(*ctx, *m, *wd, f_in, SCONV_F32, SCONV_MEM_HOST, c, f_out, SCONV_F32, SCONV_MEM_HOST);
+    *n_out = m->n_out;
+    if (out_xyz && m->n_out > 0) {
+      std::vector<uint64_t> keys(m->n_out);
+      SCONV_CUDA(cudaMemcpyAsync(keys.data(), m->q_keys_ptr(), keys.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+      ctx->sync();
+      for (int64_t i = 0; i < m->n_out; ++i) unpack_key(keys[i], out_xyz[3 * i], out_xyz[3 * i + 1], out_xyz[3 * i + 2]);
+    }
+  });
+}
+
+sconv_status sconv_generate_synthetic(int64_t N, int64_t E, int64_t C, uint64_t seed, int32_t* xyz, float* feats) {
+  return guarded(nullptr, [&] {
+    if (N < 0 || E < 1 || C < 0) fail(SCONV_ERR_ARG, "invalid synthetic cloud parameters");
+    if (static_cast<double>(N) > static_cast<double>(E) * E * E) fail(SCONV_ERR_ARG, "infeasible: N > E^3");
+    if (E - 1 > kCoordMax) fail(SCONV_ERR_RANGE, "extent out of coordinate range");
+    SplitMix r{stream_seed(seed, 0)};
+    std::unordered_set<uint64_t> seen;
+    seen.reserve(static_cast<size_t>(N) * 2);
+    int64_t got = 0;
+    while (got < N) {
+      const int32_t x = static_cast<int32_t>(r.below(static_cast<uint64_t>(E)));
+      const int32_t y = static_cast<int32_t>(r.below(static_cast<uint64_t>(E)));
+      const int32_t z = static_cast<int32_t>(r.below(static_cast<uint64_t>(E)));
+      if (!seen.insert(pack_key_unchecked(x, y, z)).second) continue;
+      xyz[3 * got] = x;
+      xyz[3 * got + 1] = y;
+      xyz[3 * got + 2] = z;
+      ++got;
+    }
+    for (int64_t i = 0; i < N * C; ++i) feats[i] = static_cast<float>(r.unit());
+  });
+}
+
+sconv_status sconv_generate_weights(uint64_t seed, uint64_t stream, int num_offsets, int c_in, int c_out, float* w) {
+  return guarded(nullptr, [&] {
+    SplitMix r{stream_seed(seed, stream)};
+    const int64_t n = int64_t{num_offsets} * c_in * c_out;
+    for (int64_t i = 0; i < n; ++i) w[i] = static_cast<float>(-0.1 + 0.2 * r.unit());
+  });
+}
+
+}  // extern "C"

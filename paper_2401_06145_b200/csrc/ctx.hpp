@@ -1,0 +1,153 @@
+// Host runtime: context, stream-ordered device memory, launch accounting, profiling.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <tuple>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../include/sconv_b200.h"
+
+namespace sconvb {
+
+// Internal error carrying a C-ABI status; converted at the boundary (capi.cu).
+struct Error : std::runtime_error {
+  sconv_status status;
+  Error(sconv_status s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+[[noreturn]] inline void fail(sconv_status s, const std::string& m) { throw Error(s, m); }
+inline void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    if (e == cudaErrorMemoryAllocation) fail(SCONV_ERR_OOM, std::string(what) + ": " + cudaGetErrorString(e));
+    fail(SCONV_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+#define SCONV_CUDA(expr) ::sconvb::cuda_check((expr), #expr)
+
+struct Ctx;
+
+// Stream-ordered device allocation (cudaMallocAsync on the context stream; the pool keeps
+// freed memory cached so steady-state layers do not hit the driver).
+class DevBuf {
+ public:
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept { *this = std::move(o); }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      ptr_ = o.ptr_;
+      bytes_ = o.bytes_;
+      stream_ = o.stream_;
+      o.ptr_ = nullptr;
+      o.bytes_ = 0;
+    }
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void alloc(size_t bytes, cudaStream_t s) {
+    release();
+    stream_ = s;
+    if (bytes == 0) return;
+    SCONV_CUDA(cudaMallocAsync(&ptr_, bytes, s));
+    bytes_ = bytes;
+  }
+  // grow-only reuse for scratch
+  void reserve(size_t bytes, cudaStream_t s) {
+    if (bytes <= bytes_ && s == stream_) return;
+    alloc(bytes, s);
+  }
+  void release() {
+    if (ptr_) cudaFreeAsync(ptr_, stream_);
+    ptr_ = nullptr;
+    bytes_ = 0;
+  }
+  template <class T = void>
+  T* get() const {
+    return static_cast<T*>(ptr_);
+  }
+  size_t bytes() const { return bytes_; }
+
+ private:
+  void* ptr_ = nullptr;
+  size_t bytes_ = 0;
+  cudaStream_t stream_ = nullptr;
+};
+
+struct ProfileEntry {
+  int64_t launches = 0;
+  double total_ms = 0.0;
+};
+
+struct TuneKey {
+  int c_in, c_out, dtype;
+  bool operator<(const TuneKey& o) const {
+    return std::tie(c_in, c_out, dtype) < std::tie(o.c_in, o.c_out, o.dtype);
+  }
+};
+
+struct Ctx {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  cudaStream_t own_stream = nullptr;
+  std::string err;
+  int64_t launches = 0;
+
+  // profiling (CUDA events around every launch on the context stream)
+  bool profiling = false;
+  struct Pending {
+    std::string name;
+    cudaEvent_t a, b;
+  };
+  std::vector<Pending> pending;
+  std::vector<cudaEvent_t> event_pool;
+  std::map<std::string, ProfileEntry> profile;
+  std::vector<std::string> profile_names;  // stable order for the C API
+  std::vector<std::pair<std::string, double>> last_records;  // individual launches since last clear
+
+  // scratch (grow-only, stream ordered)
+  DevBuf scratch_sort, scratch_misc, flush_buf;
+  DevBuf gather_buf, gemm_out, plan_dev;
+  // Pinned host staging, carved into fixed regions so an in-flight async copy from one
+  // region is never overwritten by another purpose. Every map build ends with a stream
+  // sync, so a region's next reuse always follows completion of its previous copy.
+  static constexpr size_t kPinFlagsBytes = 4096, kPinReadbackBytes = 16384, kPinPlanBytes = 1 << 20;
+  unsigned char* pinned = nullptr;
+  void* pin_flags() { return pinned; }
+  void* pin_readback() { return pinned + kPinFlagsBytes; }
+  void* pin_plan() { return pinned + kPinFlagsBytes + kPinReadbackBytes; }
+
+  std::map<TuneKey, std::pair<int, int>> tuned;  // (T_g, T_s)
+
+  cudaEvent_t take_event();
+  void resolve_profile();
+
+  template <class F>
+  void launch(const char* name, F&& f) {
+    cudaEvent_t a = nullptr, b = nullptr;
+    if (profiling) {
+      a = take_event();
+      b = take_event();
+      SCONV_CUDA(cudaEventRecord(a, stream));
+    }
+    f();
+    SCONV_CUDA(cudaGetLastError());
+    ++launches;
+    if (profiling) {
+      SCONV_CUDA(cudaEventRecord(b, stream));
+      pending.push_back({name, a, b});
+    }
+  }
+  void sync() { SCONV_CUDA(cudaStreamSynchronize(stream)); }
+};
+
+}  // namespace sconvb
+
+struct sconv_ctx : sconvb::Ctx {};

@@ -1,0 +1,464 @@
+// GMaS step on sm_100a (Minuet §5.2): padding-efficient grouping,
+// tiled gather, tcgen05 grouped GEMM, deterministic tiled scatter, Alg. 2 tile tuner.
+//
+//   group_gemms      host, 27-element plan ("<4% of layer time")
+//   k_gather<T>      one thread per (buffer slot, channel tile of T): reads the input row
+//                    index once per tile (IMT lookup), converts fp32/f16 -> operand type,
+//                    16-byte vector stores; padded rows written as zeros
+//   grouped GEMM     gemm_sm100.cu
+//   k_scatter<T>     one thread per (output row, tile): ascending-k fp32 reduction of the
+//                    row's slots (deterministic, tile invariant)
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+#include <vector>
+
+#include "common.cuh"
+#include "gemm_sm100.hpp"
+#include "gmas.hpp"
+#include "map.hpp"
+
+namespace sconvb {
+
+// ---------------------------------------------------------------- host plan
+GroupPlan group_gemms(const std::vector<int64_t>& sizes, int policy, double eps, int max_batch) {
+  if (eps < 0) fail(SCONV_ERR_ARG, "epsilon must be nonnegative");
+  if (max_batch < 1) fail(SCONV_ERR_ARG, "max_batch must be positive");
+  GroupPlan p;
+  std::vector<int> order(sizes.size());
+  std::iota(order.begin(), order.end(), 0);
+  if (policy == SCONV_GROUP_SORTED)
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return sizes[a] < sizes[b]; });
+  for (int k : order)
+    if (sizes[k] > 0) p.order.push_back(k);
+  int64_t gmax = 0, gsum = 0;
+  for (int pos = 0; pos < static_cast<int>(p.order.size()); ++pos) {
+    const int64_t n = sizes[p.order[pos]];
+    bool extend = false;
+    if (!p.groups.empty()) {
+      const int64_t card = p.groups.back().end - p.groups.back().begin;
+      const int64_t nmax = std::max(gmax, n), nsum = gsum + n;
+      extend = card < max_batch &&
+               static_cast<double>((card + 1) * nmax - nsum) / static_cast<double>(nsum) <= eps;
+    }
+    if (extend) {
+      p.groups.back().end = pos + 1;
+      gmax = std::max(gmax, n);
+      gsum += n;
+    } else {
+      p.groups.push_back({pos, pos + 1, 0});
+      gmax = n;
+      gsum = n;
+    }
+    p.groups.back().height = gmax;
+  }
+  p.buffer_offsets.assign(sizes.size(), -1);
+  int64_t base = 0;
+  for (const auto& g : p.groups) {
+    for (int q = g.begin; q < g.end; ++q) p.buffer_offsets[p.order[q]] = base + (q - g.begin) * g.height;
+    base += (g.end - g.begin) * g.height;
+  }
+  p.buffer_length = base;
+  for (int k : p.order) p.real_rows += sizes[k];
+  return p;
+}
+
+namespace {
+
+// ---------------------------------------------------------------- conversions
+template <class T>
+struct Cvt;
+template <>
+struct Cvt<__half> {
+  static __device__ __forceinline__ __half from(float v) { return __float2half_rn(v); }
+  static __device__ __forceinline__ float to(__half v) { return __half2float(v); }
+};
+template <>
+struct Cvt<__nv_bfloat16> {
+  static __device__ __forceinline__ __nv_bfloat16 from(float v) { return __float2bfloat16_rn(v); }
+  static __device__ __forceinline__ float to(__nv_bfloat16 v) { return __bfloat162float(v); }
+};
+template <>
+struct Cvt<float> {
+  static __device__ __forceinline__ float from(float v) { return v; }
+  static __device__ __forceinline__ float to(float v) { return v; }
+};
+
+// Member table entry in buffer order: {k, row0, n_k, height}.
+// k_gather: slot s -> member (binary search over row0 in shared memory) -> canonical
+// pair m = map_start[k] + r -> input row j = pair_in[m].
+template <int T, class TIn, class TOp>
+__global__ void __launch_bounds__(256) k_gather(const TIn* __restrict__ f_in, int c_in, const int4* __restrict__ members,
+                                                int num_members, const int32_t* __restrict__ map_start,
+                                                const int32_t* __restrict__ pair_in, int64_t rows, int k_pad,
+                                                TOp* __restrict__ buf) {
+  __shared__ int4 s_mem[kMaxOffsets];
+  for (int t = threadIdx.x; t < num_members; t += blockDim.x) s_mem[t] = members[t];
+  __syncthreads();
+  const int tiles = c_in / T;
+  const int64_t gid = blockIdx.x * int64_t{blockDim.x} + threadIdx.x;
+  if (gid >= rows * tiles) return;
+  const int64_t s = gid / tiles;
+  const int t = static_cast<int>(gid - s * tiles);
+  int lo = 0, hi = num_members - 1;  // last member with row0 <= s
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (s_mem[mid].y <= s)
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  const int4 mb = s_mem[lo];
+  const int64_t r = s - mb.y;
+  TOp* dst = buf + s * k_pad + t * T;
+  float v[T];
+  if (r < mb.z) {
+    const int32_t j = __ldg(pair_in + __ldg(map_start + mb.x) + r);
+    const TIn* src = f_in + static_cast<int64_t>(j) * c_in + t * T;
+    if constexpr (std::is_same<TIn, float>::value && T % 4 == 0) {
+#pragma unroll
+      for (int e = 0; e < T; e += 4) {
+        const float4 x = __ldg(reinterpret_cast<const float4*>(src + e));
+        v[e] = x.x;
+        v[e + 1] = x.y;
+        v[e + 2] = x.z;
+        v[e + 3] = x.w;
+      }
+    } else if constexpr (!std::is_same<TIn, float>::value && T % 8 == 0) {
+#pragma unroll
+      for (int e = 0; e < T; e += 8) {
+        const uint4 x = __ldg(reinterpret_cast<const uint4*>(src + e));
+        const TIn* h = reinterpret_cast<const TIn*>(&x);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[e + q] = Cvt<TIn>::to(h[q]);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < T; ++e) v[e] = Cvt<TIn>::to(src[e]);
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < T; ++e) v[e] = 0.f;  // padded rows stay exactly zero
+  }
+  if constexpr (T % 8 == 0) {
+#pragma unroll
+    for (int e = 0; e < T; e += 8) {
+      uint4 o;
+      TOp* h = reinterpret_cast<TOp*>(&o);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) h[q] = Cvt<TOp>::from(v[e + q]);
+      *reinterpret_cast<uint4*>(dst + e) = o;
+    }
+  } else if constexpr (T == 4) {
+    uint2 o;
+    TOp* h = reinterpret_cast<TOp*>(&o);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) h[q] = Cvt<TOp>::from(v[q]);
+    *reinterpret_cast<uint2*>(dst) = o;
+  } else {
+#pragma unroll
+    for (int e = 0; e < T; ++e) dst[e] = Cvt<TOp>::from(v[e]);
+  }
+}
+
+// out[i, tile] = sum_{k ascending} gemm_out[m(k,i) + delta[k], tile]  (fp32 accumulate)
+template <int T, class TOut>
+__global__ void __launch_bounds__(256) k_scatter(const float* __restrict__ gemm_out, int c_out,
+                                                 const int32_t* __restrict__ nbr_pos, int64_t n_out, int K3,
+                                                 const int32_t* __restrict__ delta, TOut* __restrict__ f_out) {
+  __shared__ int32_t s_delta[kMaxOffsets];
+  for (int t = threadIdx.x; t < K3; t += blockDim.x) s_delta[t] = delta[t];
+  __syncthreads();
+  const int tiles = c_out / T;
+  const int64_t gid = blockIdx.x * int64_t{blockDim.x} + threadIdx.x;
+  if (gid >= n_out * tiles) return;
+  const int64_t i = gid / tiles;
+  const int t = static_cast<int>(gid - i * tiles);
+  float acc[T];
+#pragma unroll
+  for (int e = 0; e < T; ++e) acc[e] = 0.f;
+  for (int k = 0; k < K3; ++k) {
+    const int32_t m = __ldg(nbr_pos + int64_t{k} * n_out + i);
+    if (m < 0) continue;
+    const float* src = gemm_out + static_cast<int64_t>(m + s_delta[k]) * c_out + t * T;
+    if constexpr (T % 4 == 0) {
+#pragma unroll
+      for (int e = 0; e < T; e += 4) {
+        const float4 x = __ldg(reinterpret_cast<const float4*>(src + e));
+        acc[e] += x.x;
+        acc[e + 1] += x.y;
+        acc[e + 2] += x.z;
+        acc[e + 3] += x.w;
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < T; ++e) acc[e] += __ldg(src + e);
+    }
+  }
+  TOut* dst = f_out + i * c_out + t * T;
+  if constexpr (std::is_same<TOut, float>::value && T % 4 == 0) {
+#pragma unroll
+    for (int e = 0; e < T; e += 4) *reinterpret_cast<float4*>(dst + e) = make_float4(acc[e], acc[e + 1], acc[e + 2], acc[e + 3]);
+  } else {
+#pragma unroll
+    for (int e = 0; e < T; ++e) dst[e] = Cvt<TOut>::from(acc[e]);
+  }
+}
+
+constexpr int kBlock = 256;
+inline unsigned blocks_for(int64_t n) { return static_cast<unsigned>(std::max<int64_t>(1, ceil_div<int64_t>(n, kBlock))); }
+
+template <class TIn, class TOp>
+void gather_dispatch(Ctx& ctx, int T, const void* f_in, int c_in, const int4* members, int nm, const int32_t* starts,
+                     const int32_t* pair_in, int64_t rows, int k_pad, void* buf) {
+  const int64_t work = rows * (c_in / T);
+  auto go = [&](auto kern) {
+    ctx.launch("k_gather", [&] {
+      kern<<<blocks_for(work), kBlock, 0, ctx.stream>>>(static_cast<const TIn*>(f_in), c_in, members, nm, starts,
+                                                        pair_in, rows, k_pad, static_cast<TOp*>(buf));
+    });
+  };
+  switch (T) {
+    case 1: go(k_gather<1, TIn, TOp>); break;
+    case 2: go(k_gather<2, TIn, TOp>); break;
+    case 3: go(k_gather<3, TIn, TOp>); break;
+    case 4: go(k_gather<4, TIn, TOp>); break;
+    case 6: go(k_gather<6, TIn, TOp>); break;
+    case 8: go(k_gather<8, TIn, TOp>); break;
+    case 12: go(k_gather<12, TIn, TOp>); break;
+    case 16: go(k_gather<16, TIn, TOp>); break;
+    case 24: go(k_gather<24, TIn, TOp>); break;
+    case 32: go(k_gather<32, TIn, TOp>); break;
+    case 48: go(k_gather<48, TIn, TOp>); break;
+    case 64: go(k_gather<64, TIn, TOp>); break;
+    default: fail(SCONV_ERR_ARG, "unsupported gather tile size " + std::to_string(T));
+  }
+}
+
+template <class TOut>
+void scatter_dispatch(Ctx& ctx, int T, const float* gemm_out, int c_out, const int32_t* nbr, int64_t n_out, int K3,
+                      const int32_t* delta, void* f_out) {
+  const int64_t work = n_out * (c_out / T);
+  auto go = [&](auto kern) {
+    ctx.launch("k_scatter", [&] {
+      kern<<<blocks_for(work), kBlock, 0, ctx.stream>>>(gemm_out, c_out, nbr, n_out, K3, delta,
+                                                        static_cast<TOut*>(f_out));
+    });
+  };
+  switch (T) {
+    case 1: go(k_scatter<1, TOut>); break;
+    case 2: go(k_scatter<2, TOut>); break;
+    case 3: go(k_scatter<3, TOut>); break;
+    case 4: go(k_scatter<4, TOut>); break;
+    case 6: go(k_scatter<6, TOut>); break;
+    case 8: go(k_scatter<8, TOut>); break;
+    case 12: go(k_scatter<12, TOut>); break;
+    case 16: go(k_scatter<16, TOut>); break;
+    case 24: go(k_scatter<24, TOut>); break;
+    case 32: go(k_scatter<32, TOut>); break;
+    case 48: go(k_scatter<48, TOut>); break;
+    case 64: go(k_scatter<64, TOut>); break;
+    default: fail(SCONV_ERR_ARG, "unsupported scatter tile size " + std::to_string(T));
+  }
+}
+
+size_t dtype_size(int d) { return d == SCONV_F32 ? 4 : 2; }
+
+}  // namespace
+
+std::vector<int> candidate_tiles(int channels) {
+  std::vector<int> d;
+  for (int t = 1; t <= channels; ++t)
+    if (channels % t == 0 && is_supported_tile(t)) d.push_back(t);
+  return d;
+}
+
+bool is_supported_tile(int t) {
+  switch (t) {
+    case 1: case 2: case 3: case 4: case 6: case 8: case 12: case 16: case 24: case 32: case 48: case 64:
+      return true;
+    default:
+      return false;
+  }
+}
+
+int default_tile(int channels, bool gather) {
+  // Heuristic before tuning: 16-byte operand stores for gather, float4 reads for scatter.
+  const int pref = gather ? 8 : 4;
+  for (int t = pref; t >= 1; --t)
+    if (channels % t == 0 && is_supported_tile(t)) return t;
+  return 1;
+}
+
+int padded_k(int c_in) { return (c_in + 15) / 16 * 16; }
+
+// ---------------------------------------------------------------- weights
+std::unique_ptr<WeightData> create_weights(Ctx& ctx, const float* w, int mem, int K3, int c_in, int c_out, int dtype) {
+  if (K3 < 1 || K3 > kMaxOffsets) fail(SCONV_ERR_ARG, "offset count out of supported range");
+  if (c_in < 1 || c_out < 1) fail(SCONV_ERR_ARG, "channel counts must be positive");
+  if (dtype != SCONV_F16 && dtype != SCONV_BF16) fail(SCONV_ERR_ARG, "weight dtype must be f16 or bf16");
+  auto wd = std::make_unique<WeightData>();
+  wd->K3 = K3;
+  wd->c_in = c_in;
+  wd->c_out = c_out;
+  wd->dtype = dtype;
+  wd->k_pad = padded_k(c_in);
+  wd->n_pad = (c_out + 15) / 16 * 16;
+  std::vector<float> host;
+  const float* src = w;
+  if (mem == SCONV_MEM_DEVICE) {
+    host.resize(static_cast<size_t>(K3) * c_in * c_out);
+    SCONV_CUDA(cudaMemcpy(host.data(), w, host.size() * sizeof(float), cudaMemcpyDeviceToHost));
+    src = host.data();
+  }
+  std::vector<uint16_t> t(static_cast<size_t>(K3) * wd->n_pad * wd->k_pad, 0);
+  for (int k = 0; k < K3; ++k)
+    for (int ci = 0; ci < c_in; ++ci)
+      for (int co = 0; co < c_out; ++co) {
+        const float v = src[(static_cast<size_t>(k) * c_in + ci) * c_out + co];
+        uint16_t bits;
+        if (dtype == SCONV_F16) {
+          const __half h = __float2half_rn(v);
+          std::memcpy(&bits, &h, 2);
+        } else {
+          const __nv_bfloat16 h = __float2bfloat16_rn(v);
+          std::memcpy(&bits, &h, 2);
+        }
+        t[(static_cast<size_t>(k) * wd->n_pad + co) * wd->k_pad + ci] = bits;  // W_k^T, K-major
+      }
+  wd->buf.alloc(t.size() * 2, ctx.stream);
+  SCONV_CUDA(cudaMemcpyAsync(wd->buf.get(), t.data(), t.size() * 2, cudaMemcpyHostToDevice, ctx.stream));
+  ctx.sync();
+  return wd;
+}
+
+// ---------------------------------------------------------------- layer forward
+void layer_forward(Ctx& ctx, MapData& m, const WeightData& w, const void* f_in, int f_in_dtype, int f_in_mem,
+                   const sconv_exec_cfg& cfg, void* f_out, int f_out_dtype, int f_out_mem) {
+  if (w.K3 != m.K3) fail(SCONV_ERR_ARG, "weight count does not match the kernel volume");
+  if (f_in_dtype != SCONV_F32 && f_in_dtype != SCONV_F16 && f_in_dtype != SCONV_BF16)
+    fail(SCONV_ERR_ARG, "unsupported input dtype");
+  if (f_out_dtype != SCONV_F32 && f_out_dtype != SCONV_F16 && f_out_dtype != SCONV_BF16)
+    fail(SCONV_ERR_ARG, "unsupported output dtype");
+  if (f_in_dtype != SCONV_F32 && f_in_dtype != w.dtype) fail(SCONV_ERR_ARG, "16-bit input must match the weight dtype");
+  const cudaStream_t st = ctx.stream;
+  const int c_in = w.c_in, c_out = w.c_out, K3 = m.K3;
+  int Tg = cfg.gather_tile, Ts = cfg.scatter_tile;
+  if (Tg <= 0 || Ts <= 0) {
+    const auto it = ctx.tuned.find({c_in, c_out, w.dtype});
+    if (Tg <= 0) Tg = it != ctx.tuned.end() ? it->second.first : default_tile(c_in, true);
+    if (Ts <= 0) Ts = it != ctx.tuned.end() ? it->second.second : default_tile(c_out, false);
+  }
+  if (c_in % Tg != 0 || c_out % Ts != 0) fail(SCONV_ERR_ARG, "tile size must divide the channel count");
+  if (!is_supported_tile(Tg) || !is_supported_tile(Ts)) fail(SCONV_ERR_ARG, "unsupported tile size");
+
+  const GroupPlan plan = group_gemms(m.sizes, cfg.policy, cfg.epsilon, cfg.max_batch);
+  m.buffer_length = plan.buffer_length;
+  m.groups = static_cast<int>(plan.groups.size());
+  m.padding_overhead = plan.real_rows > 0 ? static_cast<double>(plan.buffer_length - plan.real_rows) / plan.real_rows : 0.0;
+  m.gather_tile = Tg;
+  m.scatter_tile = Ts;
+  const int64_t R = plan.buffer_length;
+
+  // input features to device if needed
+  DevBuf fin_dev, fout_dev;
+  const void* fin = f_in;
+  if (f_in_mem == SCONV_MEM_HOST && m.n_in > 0) {
+    const size_t bytes = dtype_size(f_in_dtype) * m.n_in * c_in;
+    fin_dev.alloc(bytes, st);
+    SCONV_CUDA(cudaMemcpyAsync(fin_dev.get(), f_in, bytes, cudaMemcpyHostToDevice, st));
+    fin = fin_dev.get();
+  }
+  void* fout = f_out;
+  const size_t out_bytes = dtype_size(f_out_dtype) * m.n_out * c_out;
+  if (f_out_mem == SCONV_MEM_HOST && m.n_out > 0) {
+    fout_dev.alloc(out_bytes, st);
+    fout = fout_dev.get();
+  }
+  if (m.n_out > 0 && (R == 0 || m.n_in == 0)) {
+    SCONV_CUDA(cudaMemsetAsync(fout, 0, out_bytes, st));
+  } else if (m.n_out > 0) {
+    // ---- plan tables -> device (members, GEMM tiles, scatter deltas)
+    std::vector<int4> members;
+    for (const auto& g : plan.groups)
+      for (int q = g.begin; q < g.end; ++q) {
+        const int k = plan.order[q];
+        members.push_back(make_int4(k, static_cast<int>(plan.buffer_offsets[k]), static_cast<int>(m.sizes[k]),
+                                    static_cast<int>(g.height)));
+      }
+    const int block_n = std::min(w.n_pad, 256);
+    std::vector<int4> tiles;
+    for (const auto& mb : members)
+      for (int r0 = 0; r0 < mb.w; r0 += 128)
+        for (int n0 = 0; n0 < w.n_pad; n0 += block_n)
+          tiles.push_back(make_int4(mb.y + r0, std::min(128, mb.w - r0), mb.x, n0));
+    std::vector<int32_t> delta(K3, 0);
+    for (int k = 0; k < K3; ++k)
+      if (plan.buffer_offsets[k] >= 0) delta[k] = static_cast<int32_t>(plan.buffer_offsets[k] - m.starts[k]);
+    const size_t bytes_members = members.size() * sizeof(int4), bytes_tiles = tiles.size() * sizeof(int4),
+                 bytes_delta = delta.size() * sizeof(int32_t);
+    const size_t total = bytes_members + bytes_tiles + bytes_delta;
+    if (total > Ctx::kPinPlanBytes) fail(SCONV_ERR_ARG, "layer plan too large");
+    auto* pin = static_cast<unsigned char*>(ctx.pin_plan());
+    std::memcpy(pin, members.data(), bytes_members);
+    std::memcpy(pin + bytes_members, tiles.data(), bytes_tiles);
+    std::memcpy(pin + bytes_members + bytes_tiles, delta.data(), bytes_delta);
+    ctx.plan_dev.reserve(total, st);
+    SCONV_CUDA(cudaMemcpyAsync(ctx.plan_dev.get(), pin, total, cudaMemcpyHostToDevice, st));
+    const auto* d_members = reinterpret_cast<const int4*>(ctx.plan_dev.get<unsigned char>());
+    const auto* d_tiles = reinterpret_cast<const int4*>(ctx.plan_dev.get<unsigned char>() + bytes_members);
+    const auto* d_delta = reinterpret_cast<const int32_t*>(ctx.plan_dev.get<unsigned char>() + bytes_members + bytes_tiles);
+
+    // ---- gather
+    const int k_pad = w.k_pad;
+    ctx.gather_buf.reserve(static_cast<size_t>(R) * k_pad * 2, st);
+    if (k_pad != c_in) SCONV_CUDA(cudaMemsetAsync(ctx.gather_buf.get(), 0, static_cast<size_t>(R) * k_pad * 2, st));
+    const int nm = static_cast<int>(members.size());
+    const int32_t* starts = m.map_start.get<int32_t>();
+    const int32_t* pin_idx = m.pair_in.get<int32_t>();
+    if (w.dtype == SCONV_F16) {
+      if (f_in_dtype == SCONV_F32)
+        gather_dispatch<float, __half>(ctx, Tg, fin, c_in, d_members, nm, starts, pin_idx, R, k_pad, ctx.gather_buf.get());
+      else
+        gather_dispatch<__half, __half>(ctx, Tg, fin, c_in, d_members, nm, starts, pin_idx, R, k_pad, ctx.gather_buf.get());
+    } else {
+      if (f_in_dtype == SCONV_F32)
+        gather_dispatch<float, __nv_bfloat16>(ctx, Tg, fin, c_in, d_members, nm, starts, pin_idx, R, k_pad,
+                                              ctx.gather_buf.get());
+      else
+        gather_dispatch<__nv_bfloat16, __nv_bfloat16>(ctx, Tg, fin, c_in, d_members, nm, starts, pin_idx, R, k_pad,
+                                                      ctx.gather_buf.get());
+    }
+    // ---- grouped GEMM
+    ctx.gemm_out.reserve(static_cast<size_t>(R) * c_out * 4, st);
+    GemmArgs ga;
+    ga.a = ctx.gather_buf.get();
+    ga.b = w.buf.get();
+    ga.tiles = d_tiles;
+    ga.num_tiles = static_cast<int>(tiles.size());
+    ga.rows = R;
+    ga.k_pad = k_pad;
+    ga.num_kb = k_pad / gemm_chunk(k_pad);
+    ga.n_pad = w.n_pad;
+    ga.block_n = block_n;
+    ga.c_out = c_out;
+    ga.num_offsets = K3;
+    ga.dtype = w.dtype;
+    ga.out = ctx.gemm_out.get<float>();
+    launch_grouped_gemm(ctx, ga);
+    // ---- scatter
+    const int32_t* nbr = m.nbr_pos.get<int32_t>();
+    if (f_out_dtype == SCONV_F32)
+      scatter_dispatch<float>(ctx, Ts, ctx.gemm_out.get<float>(), c_out, nbr, m.n_out, K3, d_delta, fout);
+    else if (f_out_dtype == SCONV_F16)
+      scatter_dispatch<__half>(ctx, Ts, ctx.gemm_out.get<float>(), c_out, nbr, m.n_out, K3, d_delta, fout);
+    else
+      scatter_dispatch<__nv_bfloat16>(ctx, Ts, ctx.gemm_out.get<float>(), c_out, nbr, m.n_out, K3, d_delta, fout);
+  }
+  if (f_out_mem == SCONV_MEM_HOST && m.n_out > 0) {
+    SCONV_CUDA(cudaMemcpyAsync(f_out, fout, out_bytes, cudaMemcpyDeviceToHost, st));
+    ctx.sync();
+  }
+}
+
+}  // namespace sconvb

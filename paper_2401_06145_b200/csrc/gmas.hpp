@@ -1,0 +1,47 @@
+// GMaS host interfaces (gmas.cu).
+#pragma once
+
+#include <memory>
+#include <vector>
+
+#include "ctx.hpp"
+
+namespace sconvb {
+
+constexpr int kMaxOffsets = 512;  // K <= 8
+
+struct MapData;
+
+// GemmGroupPlan: order = chosen offset order without empty offsets.
+struct GroupPlan {
+  struct Group {
+    int begin, end;
+    int64_t height;
+  };
+  std::vector<int> order;
+  std::vector<Group> groups;
+  std::vector<int64_t> buffer_offsets;  // per offset, -1 if n_k = 0
+  int64_t buffer_length = 0;
+  int64_t real_rows = 0;
+};
+GroupPlan group_gemms(const std::vector<int64_t>& sizes, int policy, double eps, int max_batch);
+
+// WeightSet on device: [K3][n_pad][k_pad] (W_k transposed, K-major), f16/bf16.
+struct WeightData {
+  int K3 = 0, c_in = 0, c_out = 0, dtype = SCONV_F16;
+  int k_pad = 0, n_pad = 0;
+  DevBuf buf;
+};
+std::unique_ptr<WeightData> create_weights(Ctx& ctx, const float* w, int mem, int K3, int c_in, int c_out, int dtype);
+
+std::vector<int> candidate_tiles(int channels);  // supported divisors, ascending
+bool is_supported_tile(int t);
+int default_tile(int channels, bool gather);
+int padded_k(int c_in);
+
+void layer_forward(Ctx& ctx, MapData& m, const WeightData& w, const void* f_in, int f_in_dtype, int f_in_mem,
+                   const sconv_exec_cfg& cfg, void* f_out, int f_out_dtype, int f_out_mem);
+
+}  // namespace sconvb
+
+struct sconv_weights : sconvb::WeightData {};

@@ -1,0 +1,54 @@
+// Device-resident kernel map (the product's KernelMap).
+#pragma once
+
+#include <memory>
+#include <vector>
+
+#include "ctx.hpp"
+
+namespace sconvb {
+
+struct MapData {
+  int64_t n_in = 0, n_out = 0;
+  int K3 = 0;
+  sconv_map_cfg cfg{};
+  // sorted source (P) keys and original indices (null idx = identity, P was sorted)
+  std::shared_ptr<DevBuf> src_keys;
+  DevBuf src_idx;
+  bool src_identity = true;
+  // sorted output (Q) keys; aliases src_keys for stride 1 (geometry.hpp:163)
+  std::shared_ptr<DevBuf> q_keys;
+  DevBuf offsets;    // int3 x K3 (search offsets: negated when transposed)
+  DevBuf map_start;  // int32 x (K3 + 1): canonical list starts
+  DevBuf pair_in, pair_out;  // int32 x |M|, canonical order (k, then i)
+  DevBuf nbr_pos;            // int32 x K3 x n_out: canonical position m of (k, i) or -1
+  std::vector<int64_t> sizes;      // n_k (host)
+  std::vector<int32_t> starts;     // map_start (host copy)
+  int64_t total = 0;
+  // last GMaS stats
+  int64_t buffer_length = 0;
+  int groups = 0;
+  double padding_overhead = 0.0;
+  int gather_tile = 0, scatter_tile = 0;
+
+  const uint64_t* src_keys_ptr() const { return src_keys ? src_keys->get<uint64_t>() : nullptr; }
+  const uint64_t* q_keys_ptr() const { return q_keys ? q_keys->get<uint64_t>() : nullptr; }
+};
+
+// Build from coordinates (host or device) or from a sorted device key array.
+struct MapSource {
+  const int32_t* xyz = nullptr;  // n x 3
+  int mem = SCONV_MEM_HOST;
+  bool sorted = false;
+  std::shared_ptr<DevBuf> keys;  // alternative: sorted device keys (chained layers)
+  int64_t n = 0;
+};
+
+std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map_cfg& cfg, const MapSource* target);
+
+// Weight offsets (reference weight_offsets + SURVEY §2.2 even-K extension), lexicographic.
+std::vector<int3> weight_offsets_ext(int K, int scale);
+
+}  // namespace sconvb
+
+struct sconv_map : sconvb::MapData {};

@@ -1,0 +1,20 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA B200 (runs through libsconv_b200.so)")
+
+
+@pytest.fixture(scope="session")
+def ctx():
+    import paper_2401_06145_b200 as sc
+    c = sc.Context(0)
+    yield c
+    c.close()

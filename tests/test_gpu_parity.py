@@ -1,0 +1,203 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the CPU oracle.
+
+Kernel maps and output coordinates must be bit-exact in canonical order (per offset k,
+sorted by output index i). Features: (a) bit-level agreement with the oracle run on the
+SAME 16-bit-rounded operands (only fp32 accumulation order may differ: tolerance 2e-6 of
+the layer's max |output|), and (b) the north_star tolerance against the plain fp32
+oracle: max |g - r| / max|r| <= 1e-2 and mean|g - r| / mean|r| <= 1e-3 (fp16 operands).
+"""
+import numpy as np
+import pytest
+
+import paper_2401_06145_b200 as sc
+from oracle_lib import load_oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def oracle():
+    return load_oracle()
+
+
+def random_cloud(rng, n, extent, origin=0):
+    n = min(n, extent ** 3)
+    flat = rng.choice(extent ** 3, size=n, replace=False)
+    xyz = np.stack(np.unravel_index(flat, (extent,) * 3), 1).astype(np.int32) + origin
+    return xyz
+
+
+def sort_rows(xyz):
+    return xyz[np.lexsort((xyz[:, 2], xyz[:, 1], xyz[:, 0]))]
+
+
+def assert_map_equal(gpu, ora):
+    gq, gs, gj, gi = gpu
+    oq, osz, oj, oi, _ = ora
+    np.testing.assert_array_equal(gq, oq)
+    np.testing.assert_array_equal(gs, osz)
+    np.testing.assert_array_equal(gj, oj)
+    np.testing.assert_array_equal(gi, oi)
+
+
+@pytest.mark.parametrize("K,s,n,extent,presorted,B,Cq", [
+    (3, 1, 20000, 40, False, 256, 512),   # dense submanifold
+    (3, 1, 20000, 400, False, 256, 512),  # C1-like sparse
+    (3, 1, 5000, 30, True, 256, 512),     # sorted input: no sort
+    (5, 1, 3000, 20, False, 64, 100),
+    (1, 1, 1000, 30, False, 256, 512),
+    (3, 2, 20000, 50, False, 256, 512),   # strided (SPEC-literal offsets s*t)
+    (5, 2, 4000, 25, True, 32, 40),
+    (3, 1, 7, 5, False, 256, 512),
+    (3, 1, 30000, 60, False, 17, 33),     # odd B/C exercise balancing + tails
+])
+def test_map_parity(ctx, oracle, K, s, n, extent, presorted, B, Cq):
+    rng = np.random.default_rng(K * 1000 + s * 100 + n)
+    xyz = random_cloud(rng, n, extent, origin=-extent // 3)
+    if presorted:
+        xyz = sort_rows(xyz)
+    m = sc.KernelMap.build(ctx, xyz, presorted, K, s, s, B=B, Cq=Cq)
+    gpu = m.read()
+    m.free()
+    ora = oracle.layer_map(xyz, presorted, K, s, s, backend=0, B=B, Cq=Cq)
+    assert_map_equal(gpu, ora)
+
+
+def test_map_range_edges(ctx, oracle):
+    """Clouds touching COORD_MIN / COORD_MAX (the SPEC sentinel edge case)."""
+    rng = np.random.default_rng(5)
+    lo = random_cloud(rng, 300, 6, origin=-(2 ** 20 - 1))
+    hi = random_cloud(rng, 300, 6, origin=2 ** 20 - 6)
+    xyz = np.concatenate([lo, hi])
+    m = sc.KernelMap.build(ctx, xyz, False, 5, 1, 1, B=16, Cq=32)
+    gpu = m.read()
+    ora = oracle.layer_map(xyz, False, 5, 1, 1, backend=2)
+    assert_map_equal(gpu, ora)
+
+
+def test_map_even_kernel_and_transposed(ctx, oracle):
+    rng = np.random.default_rng(11)
+    fine = sort_rows(random_cloud(rng, 6000, 32))
+    down = sc.KernelMap.build(ctx, fine, True, 2, 1, 2)
+    gd = down.read()
+    od = oracle.layer_map(fine, True, 2, 1, 2)
+    assert_map_equal(gd, od)
+    assert gd[1].sum() == len(fine)  # every fine voxel lands in exactly one coarse cell
+    coarse = gd[0]
+    up = sc.KernelMap.build(ctx, coarse, True, 2, 1, 1, transposed=True, target=fine)
+    gu = up.read()
+    ou = oracle.layer_map(coarse, True, 2, 1, 1, transposed=True, target=fine)
+    assert_map_equal(gu, ou)
+    # chained builds reuse device keys (no host round trip)
+    up2 = sc.KernelMap.chained(ctx, down, 2, 1, 1, transposed=True, target_of=down)
+    assert_map_equal(up2.read(), ou)
+
+
+def test_map_empty_and_single(ctx, oracle):
+    m = sc.KernelMap.build(ctx, np.zeros((0, 3), np.int32), False, 3, 1, 1)
+    q, sizes, j, i = m.read()
+    assert len(q) == 0 and sizes.sum() == 0
+    one = np.array([[0, 0, 0]], np.int32)
+    q, sizes, j, i = sc.KernelMap.build(ctx, one, False, 3, 1, 1).read()
+    assert sizes.sum() == 1 and sizes[13] == 1
+
+
+def test_map_errors(ctx):
+    bad = np.array([[0, 0, 0], [2 ** 20, 0, 0]], np.int32)
+    with pytest.raises(sc.OutOfRange, match=r"^coordinate x out of range: 1048576$"):
+        sc.KernelMap.build(ctx, bad, False, 3, 1, 1)
+    bad = np.array([[0, 0, 0], [1, -(2 ** 20), 3]], np.int32)
+    with pytest.raises(sc.OutOfRange, match=r"^coordinate y out of range: -1048576$"):
+        sc.KernelMap.build(ctx, bad, False, 3, 1, 1)
+    with pytest.raises(sc.InvalidArgument):
+        sc.KernelMap.build(ctx, np.array([[1, 0, 0], [0, 0, 0]], np.int32), True, 3, 1, 1)  # flagged sorted, is not
+
+
+def rel_errors(g, r):
+    d = np.abs(g.astype(np.float64) - r.astype(np.float64))
+    scale = np.abs(r).max()
+    return d.max() / scale, d.mean() / np.abs(r).mean()
+
+
+def f16(a):
+    return a.astype(np.float16).astype(np.float32)
+
+
+@pytest.mark.parametrize("K,s,n,extent,cin,cout", [
+    (3, 1, 20000, 40, 32, 32),
+    (3, 1, 20000, 400, 32, 32),
+    (3, 2, 8000, 30, 16, 64),
+    (5, 1, 3000, 20, 64, 32),
+    (3, 1, 4000, 25, 4, 16),     # K-padding (C_in < 16)
+    (3, 1, 4000, 25, 96, 128),
+    (3, 1, 3000, 25, 128, 256),
+    (1, 1, 1000, 20, 32, 48),
+])
+def test_layer_parity(ctx, oracle, K, s, n, extent, cin, cout):
+    rng = np.random.default_rng(n + cin)
+    xyz = random_cloud(rng, n, extent)
+    F = rng.random((len(xyz), cin), dtype=np.float32)
+    W = ((rng.random((K ** 3, cin, cout)) * 0.2 - 0.1)).astype(np.float32)
+    out = sc.sc_layer_forward(ctx, sc.PointCloud(xyz, F, False), W, K, s)
+    oq, of, st = oracle.layer_forward(xyz, False, f16(F), f16(W), K, s, s)
+    np.testing.assert_array_equal(out.coords, oq)
+    mx, _ = rel_errors(out.features, of)
+    assert mx <= 2e-6, f"same-operand parity {mx}"
+    _, of32, _ = oracle.layer_forward(xyz, False, F, W, K, s, s)
+    mx, mean = rel_errors(out.features, of32)
+    assert mx <= 1e-2 and mean <= 1e-3, (mx, mean)
+
+
+def test_layer_bf16(ctx, oracle):
+    rng = np.random.default_rng(3)
+    xyz = random_cloud(rng, 5000, 30)
+    F = rng.random((len(xyz), 32), dtype=np.float32)
+    W = ((rng.random((27, 32, 32)) * 0.2 - 0.1)).astype(np.float32)
+    out = sc.sc_layer_forward(ctx, sc.PointCloud(xyz, F, False), W, 3, 1, sc.exec_cfg(compute_dtype=sc.BF16))
+    import torch
+    bf = lambda a: torch.from_numpy(a).to(torch.bfloat16).float().numpy()  # noqa: E731
+    _, of, _ = oracle.layer_forward(xyz, False, bf(F), bf(W), 3, 1, 1)
+    mx, _ = rel_errors(out.features, of)
+    assert mx <= 2e-6
+
+
+def test_tile_and_policy_invariance(ctx):
+    """Gather/scatter tiles and grouping policy never change results."""
+    rng = np.random.default_rng(9)
+    xyz = random_cloud(rng, 8000, 30)
+    F = rng.random((len(xyz), 48), dtype=np.float32)
+    W = ((rng.random((27, 48, 24)) * 0.2 - 0.1)).astype(np.float32)
+    m = sc.KernelMap.build(ctx, xyz, False, 3, 1, 1)
+    w = sc.Weights(ctx, W)
+    ref = sc.layer_forward(ctx, m, w, F)
+    for tg, ts in [(1, 1), (2, 3), (3, 4), (6, 6), (8, 8), (12, 12), (16, 24), (48, 24), (24, 2)]:
+        got = sc.layer_forward(ctx, m, w, F, sc.exec_cfg(gather_tile=tg, scatter_tile=ts))
+        np.testing.assert_array_equal(got, ref)
+    for pol, eps, mb in [(sc.GROUP_MAP_ORDER, 0.25, 16), (sc.GROUP_SORTED, 0.0, 1), (sc.GROUP_SORTED, 10.0, 27)]:
+        got = sc.layer_forward(ctx, m, w, F, sc.exec_cfg(policy=pol, epsilon=eps, max_batch=mb))
+        np.testing.assert_array_equal(got, ref)
+
+
+def test_map_determinism(ctx):
+    rng = np.random.default_rng(2)
+    xyz = random_cloud(rng, 50000, 80)
+    a = sc.KernelMap.build(ctx, xyz, False, 3, 1, 1).read()
+    b = sc.KernelMap.build(ctx, xyz, False, 3, 1, 1).read()
+    for x, y in zip(a, b):
+        np.testing.assert_array_equal(x, y)
+
+
+def test_c1_full_size_properties(ctx, oracle):
+    """BASELINE config 1 at full size: 100k voxels in 400^3, K=3, 32->32."""
+    xyz, F = sc.generate_synthetic(100000, 400, 32, 1)
+    W = sc.generate_weights(1, 1, 27, 32, 32)
+    m = sc.KernelMap.build(ctx, xyz, False, 3, 1, 1)
+    q, sizes, j, i = m.read()
+    ora = oracle.layer_map(xyz, False, 3, 1, 1)
+    assert_map_equal((q, sizes, j, i), ora)
+    np.testing.assert_array_equal(sizes, sizes[::-1])  # submanifold symmetry n_k = n_{26-k}
+    assert sizes[13] == len(xyz)
+    out = sc.layer_forward(ctx, m, sc.Weights(ctx, W), F)
+    _, of, _ = oracle.layer_forward(xyz, False, F, W, 3, 1, 1, workers=8)
+    mx, mean = rel_errors(out, of)
+    assert mx <= 1e-2 and mean <= 1e-3, (mx, mean)
