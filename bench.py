@@ -1,0 +1,320 @@
+#!/usr/bin/env python3
+"""Benchmark driver (contract: one JSON line on rank 0).
+
+Workload (default): BASELINE.json configs[0], the single submanifold 3x3x3 SC layer,
+C_in = C_out = 32, 100k synthetic voxels uniform in 400^3 (generate_synthetic seed 1,
+weights stream 1). A step = Map (pack, sort, backward/forward search) + GMaS (gather,
+tcgen05 grouped GEMM, scatter) on device-resident inputs. Inputs (12.8 MB) are smaller
+than L2, so L2 is flushed (256 MB memset) between timed steps, outside the events.
+
+metric/unit: input voxels processed per second through the layer (higher is better);
+ms_per_step is the SC-layer latency. Multi-GPU: every rank runs its own scene
+(seed 1 + rank), no data-path collective (scene sharding) -> weak scaling.
+
+--impl reference: the CPU oracle (oracle/liboracle.so, a port of the reference SPEC's
+Map/GMaS on top of a restatement of its geometry.hpp) on all host threads, same config.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SC layer latency (Map + GMaS, ms) and end-to-end network points/sec"
+WORKLOADS = {
+    "c1_submanifold_k3_32x32_100k": dict(N=100000, E=400, C_in=32, C_out=32, K=3, s=1, seed=1),
+}
+DEFAULT_WORKLOAD = "c1_submanifold_k3_32x32_100k"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=50)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(WORKLOADS))
+    p.add_argument("--dtype", default="f16", choices=["f16", "bf16"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), float(d["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+def load_traffic():
+    """Per-launch DRAM bytes of each kernel from the committed ncu --set full capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """NVML sampling of SM clock + throttle reasons during the timed region."""
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.stop_ev = [], set(), threading.Event()
+        self.ok = False
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            self.nv, self.h = nv, nv.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+        }
+        while not self.stop_ev.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in names.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self.stop_ev.set()
+            self.t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------- CPU oracle leg
+def cpu_run(wl, reps, workers):
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_lib import load_oracle  # CPU baseline only (test infrastructure)
+    o = load_oracle()
+    xyz, F = o.generate_synthetic(wl["N"], wl["E"], wl["C_in"], wl["seed"])
+    K3 = wl["K"] ** 3
+    W = o.generate_weights(wl["seed"], 1, K3, wl["C_in"], wl["C_out"])
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        o.layer_forward(xyz, False, F, W, wl["K"], wl["s"], wl["s"], workers=workers)
+        times.append(time.perf_counter() - t0)
+    return times
+
+
+def reference_arm(args, wl):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return  # rank 0 alone runs the CPU reference
+    workers = os.cpu_count() or 1
+    cpu_run(wl, max(0, args.warmup), workers) if args.warmup else None
+    times = cpu_run(wl, args.steps, workers)
+    total = sum(times)
+    pps = wl["N"] * len(times) / total
+    line = {
+        "metric": METRIC, "value": pps, "unit": "points/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64-acc", "data": "synthetic",
+        "config": {"workload": args.workload, **wl},
+        "impl": "reference",
+        "cpu_baseline": {"value": pps, "unit": "points/s", "cores": workers, "kind": "port",
+                         "sample": f"{args.steps} full C1 layers (Map+GMaS) on the oracle"},
+        "e2e": {"value": pps, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- GPU arm
+def main():
+    args = parse()
+    wl = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        return reference_arm(args, wl)
+
+    import torch
+    import paper_2401_06145_b200 as sc
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    ctx = sc.Context(local)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+    dtype = sc.F16 if args.dtype == "f16" else sc.BF16
+
+    # scene per rank (scene sharding): seed + rank
+    seed = wl["seed"] + rank
+    xyz, F = sc.generate_synthetic(wl["N"], wl["E"], wl["C_in"], seed)
+    K3 = wl["K"] ** 3
+    W = sc.generate_weights(wl["seed"], 1, K3, wl["C_in"], wl["C_out"])
+    w = sc.Weights(ctx, W, dtype)
+    xyz_d = torch.from_numpy(xyz).cuda()
+    F_d = torch.from_numpy(F).cuda()
+    out_d = torch.empty((wl["N"], wl["C_out"]), dtype=torch.float32, device="cuda")
+    torch.cuda.synchronize()
+
+    def step():
+        m = sc.KernelMap.build(ctx, None, False, wl["K"], wl["s"], wl["s"], device_ptr=xyz_d.data_ptr(), n=wl["N"])
+        sc.layer_forward_device(ctx, m, w, F_d.data_ptr(), sc.F32, out_d.data_ptr(), sc.F32,
+                                sc.exec_cfg(compute_dtype=dtype))
+        return m
+
+    # tile autotuning (Alg. 2) once, excluded from timing
+    m0 = step()
+    tg, ts, _ = sc.tune_layer(ctx, m0, w, F_d.data_ptr(), sc.F32, rounds=5)
+    info0 = m0.info()
+    m0.free()
+    for _ in range(args.warmup):
+        step().free()
+    torch.cuda.synchronize()
+
+    # ---- timed region: per-step CUDA events on the launching stream, L2 flushed between
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    ctx.set_profiling(True)
+    ctx.profile_reset()
+    launches0 = ctx.launch_count
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for a, b in ev:
+            ctx.flush_l2(256 << 20)
+            a.record(stream)
+            m = step()
+            b.record(stream)
+            m.free()
+        torch.cuda.synchronize()
+    launches = ctx.launch_count - launches0
+    prof = ctx.profile()
+    ctx.set_profiling(False)
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = sum(step_ms)
+    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+    max_total_ms = float(t.item())
+    pps = world * wl["N"] * args.steps / (max_total_ms / 1e3)
+
+    # ---- end-to-end through the reference-facing C ABI with host buffers
+    e2e_times = []
+    cfg = sc.exec_cfg(compute_dtype=dtype, gather_tile=tg, scatter_tile=ts)
+    cloud = sc.PointCloud(xyz, F, False)
+    for i in range(args.warmup + min(args.steps, 20)):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        out = sc.sc_layer_forward(ctx, cloud, W, wl["K"], wl["s"], cfg)
+        e2e_times.append(time.perf_counter() - t0)
+    e2e_times = e2e_times[args.warmup:]
+    e2e_ms = statistics.median(e2e_times) * 1e3
+    n_out = len(out.coords)
+    h2d = xyz.nbytes + F.nbytes + W.nbytes
+    d2h = n_out * (8 + 4 * wl["C_out"]) + 4 * (K3 + 1)
+    e2e_t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_pps = world * wl["N"] / (float(e2e_t.item()) / 1e3)
+
+    # ---- roofline of the dominant kernel (algorithmic bytes / measured duration)
+    hbm, tflops, peak_kind = load_peaks()
+    N, Cin, Cout = wl["N"], wl["C_in"], wl["C_out"]
+    M = info0.total_matches
+    R = info0.buffer_length
+    kpad = (Cin + 15) // 16 * 16
+    algo = {  # bytes per launch (with this path's dtypes)
+        "k_forward": 8 * N + 8 * info0.num_outputs + 8 * M + 12 * K3,
+        "k_gather": 4 * Cin * N + 2 * kpad * R + 4 * M,
+        "k_gemm_grouped": 2 * kpad * R + 4 * Cout * R + 2 * K3 * Cin * Cout,
+        "k_scatter": 4 * Cout * M + 4 * K3 * info0.num_outputs + 4 * Cout * info0.num_outputs,
+        "cub_radix_sort_pairs": 2 * (8 + 4) * N,
+        "k_pack_keys": 12 * N + 8 * N,
+        "k_backward": 8 * K3 * ((N + 255) // 256),
+    }
+    dominant = max(prof.items(), key=lambda kv: kv[1][1])[0] if prof else None
+    roofline = None
+    if dominant:
+        n_launch, tot = prof[dominant]
+        avg_ms = tot / n_launch
+        traffic = load_traffic().get(dominant)
+        if dominant == "k_gemm_grouped":
+            flops = 2 * Cin * Cout * M
+            ach = flops / (avg_ms / 1e3) / 1e12
+            roofline = {"kernel": dominant, "bound": "hbm", "achieved": algo[dominant] / (avg_ms / 1e3) / 1e9,
+                        "peak": hbm, "unit": "GB/s", "useful_tflops": ach, "traffic": traffic}
+        else:
+            ach = algo.get(dominant, 0) / (avg_ms / 1e3) / 1e9
+            roofline = {"kernel": dominant, "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
+                        "traffic": traffic}
+        roofline["frac"] = roofline["achieved"] / roofline["peak"]
+        roofline["peak_source"] = f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"
+        roofline["avg_launch_ms"] = avg_ms
+        roofline["algorithmic_bytes_per_launch"] = algo.get(dominant)
+
+    phases = {k: {"launches": n, "ms_per_step": ms / args.steps} for k, (n, ms) in sorted(prof.items())}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        workers = os.cpu_count() or 1
+        times = cpu_run(wl, 3, workers)
+        cpu = {"value": wl["N"] / statistics.median(times), "unit": "points/s", "cores": workers, "kind": "port",
+               "sample": "3 full C1 layers (Map+GMaS, fp64 accumulate) on oracle/liboracle.so, median"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": pps, "unit": "points/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": max_total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+            "config": {"workload": args.workload, **wl, "parallelism": f"scene-sharded x{world}",
+                       "l2": "flushed (256 MB memset) between timed steps", "gather_tile": tg, "scatter_tile": ts,
+                       "matches": M, "buffer_length": R, "groups": info0.groups,
+                       "padding_overhead": info0.padding_overhead},
+            "e2e": {"value": e2e_pps, "unit": "points/s", "ms": e2e_ms, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "api": "sconv_sc_layer_forward (host buffers)"},
+            "gpu_launches": launches,
+            "roofline": roofline,
+            "phases": phases,
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

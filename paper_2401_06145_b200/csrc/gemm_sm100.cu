@@ -281,7 +281,7 @@ void launch_kc(Ctx& ctx, const GemmArgs& a) {
                                   static_cast<uint32_t>(block_n), KC);
   const uint32_t fmt = a.dtype == SCONV_BF16 ? 1u : 0u;
   const uint32_t idesc_base = (1u << 4) | (fmt << 7) | (fmt << 10) | ((128u >> 4) << 24);
-  ctx.launch("k_gemm_grouped_tcgen05", [&] {
+  ctx.launch("k_gemm_grouped", [&] {
     kern<<<grid, kGemmThreads, smem, ctx.stream>>>(tA, tB, a.tiles, a.num_tiles, a.num_kb, block_n, a.n_pad, a.c_out,
                                                    a.out, stages, idesc_base, cols);
   });
