@@ -90,6 +90,8 @@ sconv_status sconv_ctx_synchronize(sconv_ctx* ctx);
 int64_t sconv_ctx_launch_count(const sconv_ctx* ctx);
 /* Per-kernel CUDA-event timing on the context stream (0 = off). */
 sconv_status sconv_ctx_set_profiling(sconv_ctx* ctx, int enabled);
+/* Restrict profiling events to launches with this label (NULL / "" = all). */
+sconv_status sconv_ctx_set_profile_filter(sconv_ctx* ctx, const char* kernel_label);
 /* Accumulated profile: kernel i -> name, launches, total ms. Returns count. */
 int sconv_ctx_profile_count(const sconv_ctx* ctx);
 sconv_status sconv_ctx_profile_entry(sconv_ctx* ctx, int i, const char** name, int64_t* launches, double* total_ms);

@@ -160,6 +160,11 @@ sconv_status sconv_ctx_create(int device, sconv_ctx** out) {
     SCONV_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
     uint64_t threshold = UINT64_MAX;
     SCONV_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
+    SCONV_CUDA(cudaMalloc(reinterpret_cast<void**>(&ctx->done), 64));
+    SCONV_CUDA(cudaMemset(ctx->done, 0, 64));
+    const size_t sort_bytes = sizeof(int) * (3 * 65536 + 8);
+    SCONV_CUDA(cudaMalloc(reinterpret_cast<void**>(&ctx->sort_state), sort_bytes));
+    SCONV_CUDA(cudaMemset(ctx->sort_state, 0, sort_bytes));
     SCONV_CUDA(cudaMallocHost(reinterpret_cast<void**>(&ctx->pinned),
                               Ctx::kPinFlagsBytes + Ctx::kPinReadbackBytes + Ctx::kPinPlanBytes));
   });
@@ -191,6 +196,8 @@ void sconv_ctx_destroy(sconv_ctx* ctx) {
   }
   for (auto e : ctx->event_pool) cudaEventDestroy(e);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  if (ctx->done) cudaFree(ctx->done);
+  if (ctx->sort_state) cudaFree(ctx->sort_state);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
 }
@@ -215,6 +222,12 @@ sconv_status sconv_ctx_set_profiling(sconv_ctx* ctx, int enabled) {
   return guarded(ctx, [&] {
     ctx->resolve_profile();
     ctx->profiling = enabled != 0;
+  });
+}
+sconv_status sconv_ctx_set_profile_filter(sconv_ctx* ctx, const char* kernel_label) {
+  return guarded(ctx, [&] {
+    ctx->resolve_profile();
+    ctx->profile_only = kernel_label ? kernel_label : "";
   });
 }
 int sconv_ctx_profile_count(const sconv_ctx* ctx) { return static_cast<int>(ctx->profile_names.size()); }

@@ -102,6 +102,7 @@ struct Ctx {
 
   // profiling (CUDA events around every launch on the context stream)
   bool profiling = false;
+  std::string profile_only;  // non-empty: time only launches with this label
   struct Pending {
     std::string name;
     cudaEvent_t a, b;
@@ -118,13 +119,18 @@ struct Ctx {
   // Pinned host staging, carved into fixed regions so an in-flight async copy from one
   // region is never overwritten by another purpose. Every map build ends with a stream
   // sync, so a region's next reuse always follows completion of its previous copy.
-  static constexpr size_t kPinFlagsBytes = 4096, kPinReadbackBytes = 16384, kPinPlanBytes = 1 << 20;
+  static constexpr size_t kPinFlagsBytes = 8192, kPinReadbackBytes = 16384, kPinPlanBytes = 1 << 20;
   unsigned char* pinned = nullptr;
   void* pin_flags() { return pinned; }
   void* pin_readback() { return pinned + kPinFlagsBytes; }
   void* pin_plan() { return pinned + kPinFlagsBytes + kPinReadbackBytes; }
 
   std::map<TuneKey, std::pair<int, int>> tuned;  // (T_g, T_s)
+  unsigned* done = nullptr;  // zero-initialised "last CTA" counter, reset by its user kernel
+  unsigned* done_counter() { return done; }
+  // bucket-sort state: histogram (kept zeroed by its scan kernel) + starts + cursors
+  int* sort_state = nullptr;
+  int* sort_hist() { return sort_state; }
 
   cudaEvent_t take_event();
   void resolve_profile();
@@ -132,7 +138,8 @@ struct Ctx {
   template <class F>
   void launch(const char* name, F&& f) {
     cudaEvent_t a = nullptr, b = nullptr;
-    if (profiling) {
+    const bool timed = profiling && (profile_only.empty() || profile_only == name);
+    if (timed) {
       a = take_event();
       b = take_event();
       SCONV_CUDA(cudaEventRecord(a, stream));
@@ -140,7 +147,7 @@ struct Ctx {
     f();
     SCONV_CUDA(cudaGetLastError());
     ++launches;
-    if (profiling) {
+    if (timed) {
       SCONV_CUDA(cudaEventRecord(b, stream));
       pending.push_back({name, a, b});
     }

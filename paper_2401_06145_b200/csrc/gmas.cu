@@ -177,22 +177,29 @@ __global__ void __launch_bounds__(256) k_scatter(const float* __restrict__ gemm_
   float acc[T];
 #pragma unroll
   for (int e = 0; e < T; ++e) acc[e] = 0.f;
-  for (int k = 0; k < K3; ++k) {
-    const int32_t m = __ldg(nbr_pos + int64_t{k} * n_out + i);
-    if (m < 0) continue;
-    const float* src = gemm_out + static_cast<int64_t>(m + s_delta[k]) * c_out + t * T;
-    if constexpr (T % 4 == 0) {
+  constexpr int kBatch = 9;  // independent index loads in flight per thread (27 = 3 x 9)
+  for (int k0 = 0; k0 < K3; k0 += kBatch) {
+    int32_t mk[kBatch];
 #pragma unroll
-      for (int e = 0; e < T; e += 4) {
-        const float4 x = __ldg(reinterpret_cast<const float4*>(src + e));
-        acc[e] += x.x;
-        acc[e + 1] += x.y;
-        acc[e + 2] += x.z;
-        acc[e + 3] += x.w;
+    for (int u = 0; u < kBatch; ++u)
+      mk[u] = k0 + u < K3 ? __ldg(nbr_pos + int64_t{k0 + u} * n_out + i) : -1;
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {  // ascending k: deterministic reduction order
+      if (mk[u] < 0) continue;
+      const float* src = gemm_out + static_cast<int64_t>(mk[u] + s_delta[k0 + u]) * c_out + t * T;
+      if constexpr (T % 4 == 0) {
+#pragma unroll
+        for (int e = 0; e < T; e += 4) {
+          const float4 x = __ldg(reinterpret_cast<const float4*>(src + e));
+          acc[e] += x.x;
+          acc[e + 1] += x.y;
+          acc[e + 2] += x.z;
+          acc[e + 3] += x.w;
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < T; ++e) acc[e] += __ldg(src + e);
       }
-    } else {
-#pragma unroll
-      for (int e = 0; e < T; ++e) acc[e] += __ldg(src + e);
     }
   }
   TOut* dst = f_out + i * c_out + t * T;

@@ -1,17 +1,15 @@
 // Map step on sm_100a: segmented query sorting + double-traversed binary search
 // (Minuet §5.1), producing the canonical kernel map without a hash table.
 //
-// Kernels (one launch each, all on the context stream):
-//   k_pack_keys      xyz -> packed u64 keys (+ range / sortedness checks)    geometry.hpp:59-67
-//   (CUB radix sort) unsorted P -> sorted source keys + original indices
-//   k_floor_keys     Eq. 1 floor-to-stride on sorted keys (then sort+unique) geometry.hpp:161-178
-//   k_backward       per (offset k, source block b): upper bound of pivot_b
-//                    in the virtual query segment {q_i + delta_k}
-//   k_plan           balance blocks into ranges of <= C queries, in canonical
-//                    (k, b) order, plus tail ranges for unmatched queries
-//   k_forward        one CTA per range: stage the source block in shared
-//                    memory, binary-search each query, warp-ballot compaction,
-//                    decoupled look-back for the canonical output position
+// Kernels (all on the context stream; file:line = the reference operation replaced):
+//   k_bbox / k_pack_compact / k_hist_scan / k_bucket_scatter / k_bucket_rank
+//                    unsorted P -> sorted source keys + original indices
+//                    (left-aligned compact keys, bucket sort; exact CUB 64-bit fallback)
+//   k_pack_keys      xyz -> packed u64 keys (+ range / sortedness checks)      geometry.hpp:59-67
+//   k_floor_keys     Eq. 1 floor-to-stride (then CUB sort + unique)            geometry.hpp:161-178
+//   k_search         double-traversed binary search: backward (pivot vs query
+//                    segment) + forward (query vs staged source block)
+//   k_emit           canonical positions (per offset k, ordered by i) and pairs SPEC.md:235-243
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -31,6 +29,9 @@ struct MapFlags {
   unsigned long long bad_floor;   // same for Eq. 1 floored coordinates (original index)
   int unsorted;                  // input flagged sorted but keys not strictly increasing
   int target_unsorted;
+  int bbox[6];                   // min x,y,z / max x,y,z of P (unsorted path)
+  int wide;                      // compact key needs > 32 bits: rebuild with the 64-bit CUB sort
+  int big_bucket;                // a sort bucket exceeds kMaxBucket: rebuild with the 64-bit CUB sort
 };
 
 // ---------------------------------------------------------------- key packing
@@ -64,6 +65,168 @@ __global__ void k_iota(int32_t* __restrict__ v, int64_t n) {
   if (i < n) v[i] = static_cast<int32_t>(i);
 }
 
+// ---- compact sort keys: (x-xmin, y-ymin, z-zmin) with the minimal bit widths preserve the
+// lexicographic order and usually fit 32 bits (KITTI at 5 cm: 12+12+8), so the radix sort
+// runs over 4 digits of a u32 key instead of 8 digits of the 63-bit packed key.
+__global__ void k_bbox(const int32_t* __restrict__ xyz, int64_t n, MapFlags* flags) {
+  int mn[3] = {INT_MAX, INT_MAX, INT_MAX}, mx[3] = {INT_MIN, INT_MIN, INT_MIN};
+  for (int64_t i = blockIdx.x * int64_t{blockDim.x} + threadIdx.x; i < n; i += int64_t{gridDim.x} * blockDim.x)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const int v = __ldg(xyz + 3 * i + a);
+      mn[a] = min(mn[a], v);
+      mx[a] = max(mx[a], v);
+    }
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      mn[a] = min(mn[a], __shfl_xor_sync(0xFFFFFFFFu, mn[a], o));
+      mx[a] = max(mx[a], __shfl_xor_sync(0xFFFFFFFFu, mx[a], o));
+    }
+  __shared__ int s_red[6][32];
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+  if (l == 0)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      s_red[a][w] = mn[a];
+      s_red[3 + a][w] = mx[a];
+    }
+  __syncthreads();
+  if (threadIdx.x < 6) {
+    const int a = threadIdx.x;
+    int v = s_red[a][0];
+    for (int q = 1; q < nw; ++q) v = a < 3 ? min(v, s_red[a][q]) : max(v, s_red[a][q]);
+    if (a < 3)
+      atomicMin(&flags->bbox[a], v);
+    else
+      atomicMax(&flags->bbox[a], v);
+  }
+}
+
+__device__ __forceinline__ int bits_for(int64_t extent) {  // bits to hold [0, extent]
+  return extent <= 0 ? 0 : 64 - __clzll(static_cast<unsigned long long>(extent));
+}
+
+// Left-aligned compact key: the T significant bits sit at the top of a u32, so the top
+// kBucketBits select a bucket independent of T.
+constexpr int kMaxBucketBits = 16, kBuckets = 1 << kMaxBucketBits, kMaxBucket = 4096;
+
+__device__ __forceinline__ int compact_bits(const MapFlags* f, int& by, int& bz) {
+  by = bits_for(int64_t{f->bbox[4]} - f->bbox[1]);
+  bz = bits_for(int64_t{f->bbox[5]} - f->bbox[2]);
+  return bits_for(int64_t{f->bbox[3]} - f->bbox[0]) + by + bz;
+}
+
+__global__ void k_pack_compact(const int32_t* __restrict__ xyz, int64_t n, MapFlags* flags,
+                               uint32_t* __restrict__ ck, int32_t* __restrict__ idx, int* __restrict__ hist, int H) {
+  const int64_t i = blockIdx.x * int64_t{blockDim.x} + threadIdx.x;
+  if (i >= n) return;
+  const int32_t x = xyz[3 * i], y = xyz[3 * i + 1], z = xyz[3 * i + 2];
+  idx[i] = static_cast<int32_t>(i);
+  if (!(in_range(x) && in_range(y) && in_range(z))) {
+    const int axis = !in_range(x) ? 0 : (!in_range(y) ? 1 : 2);
+    atomicMin(&flags->bad_coord, static_cast<unsigned long long>(i * 3 + axis));
+    ck[i] = 0;
+    return;
+  }
+  int by, bz;
+  const int T = compact_bits(flags, by, bz);
+  if (T > 32) {
+    if (i == 0) flags->wide = 1;
+    ck[i] = 0;
+    return;
+  }
+  const uint64_t c = (static_cast<uint64_t>(x - flags->bbox[0]) << (by + bz)) |
+                     (static_cast<uint64_t>(y - flags->bbox[1]) << bz) | static_cast<uint64_t>(z - flags->bbox[2]);
+  const uint32_t lk = static_cast<uint32_t>(c << (32 - T));
+  ck[i] = lk;
+  atomicAdd(hist + (lk >> (32 - H)), 1);
+}
+
+// One CTA: exclusive scan of the 2^H-bucket histogram into starts / cursors; resets the
+// histogram for the next build; flags oversized buckets. Warp w owns a contiguous slice of
+// buckets and walks it 32 at a time (coalesced), so no per-thread arrays are needed.
+constexpr int kScanThreads = 1024;
+__global__ void __launch_bounds__(kScanThreads) k_hist_scan(int* __restrict__ hist, int nbuckets,
+                                                             int* __restrict__ starts, int* __restrict__ cursor,
+                                                             MapFlags* flags) {
+  __shared__ int s_warp[kScanThreads / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int per_warp = nbuckets / (kScanThreads / 32);  // multiple of 32 (nbuckets >= 1024)
+  const int base = warp * per_warp;
+  int sum = 0;
+#pragma unroll 8
+  for (int r = 0; r < per_warp; r += 32) sum += hist[base + r + lane];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
+  if (lane == 0) s_warp[warp] = sum;
+  __syncthreads();
+  if (warp == 0) {
+    const int v = s_warp[lane];
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if (lane >= o) incl += u;
+    }
+    s_warp[lane] = incl - v;  // exclusive warp offsets
+    if (lane == 31) starts[nbuckets] = incl;
+  }
+  __syncthreads();
+  int carry = s_warp[warp];
+  int big = 0;
+  for (int r = 0; r < per_warp; r += 32) {
+    const int idx = base + r + lane;
+    const int v = hist[idx];
+    big |= v > kMaxBucket;
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if (lane >= o) incl += u;
+    }
+    starts[idx] = carry + incl - v;
+    cursor[idx] = carry + incl - v;
+    hist[idx] = 0;
+    carry += __shfl_sync(0xFFFFFFFFu, incl, 31);
+  }
+  if (__any_sync(0xFFFFFFFFu, big) && lane == 0) flags->big_bucket = 1;
+}
+
+__global__ void k_bucket_scatter(const uint32_t* __restrict__ ck, const int32_t* __restrict__ idx, int64_t n,
+                                 int* __restrict__ cursor, uint32_t* __restrict__ tk, int32_t* __restrict__ ti, int H) {
+  const int64_t i = blockIdx.x * int64_t{blockDim.x} + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t k = ck[i];
+  const int p = atomicAdd(cursor + (k >> (32 - H)), 1);
+  tk[p] = k;
+  ti[p] = idx[i];
+}
+
+// Sort inside each bucket by rank counting (keys are unique, so the result is exact and
+// independent of the scatter order); then expand to the packed 63-bit keys.
+__global__ void k_bucket_rank(const uint32_t* __restrict__ tk, const int32_t* __restrict__ ti, int64_t n,
+                              const int* __restrict__ starts, const MapFlags* flags, uint64_t* __restrict__ keys,
+                              int32_t* __restrict__ out_idx, int H) {
+  const int64_t p = blockIdx.x * int64_t{blockDim.x} + threadIdx.x;
+  if (p >= n) return;
+  const uint32_t k = tk[p];
+  const int b = k >> (32 - H);
+  const int s0 = __ldg(starts + b), s1 = __ldg(starts + b + 1);
+  if (s1 - s0 > kMaxBucket) return;  // flagged: the host rebuilds with the CUB sort
+  int rank = 0;
+  for (int q = s0; q < s1; ++q) rank += __ldg(tk + q) < k;
+  int by, bz;
+  const int T = compact_bits(flags, by, bz);
+  const uint64_t c = T ? (static_cast<uint64_t>(k) >> (32 - T)) : 0;
+  const int32_t x = static_cast<int32_t>(c >> (by + bz)) + flags->bbox[0];
+  const int32_t y = static_cast<int32_t>((c >> bz) & ((uint64_t{1} << by) - 1u)) + flags->bbox[1];
+  const int32_t z = static_cast<int32_t>(c & ((uint64_t{1} << bz) - 1u)) + flags->bbox[2];
+  keys[s0 + rank] = pack_key_unchecked(x, y, z);
+  out_idx[s0 + rank] = ti[p];
+}
+
 // Eq. 1 on sorted source keys; range failures recorded by ORIGINAL index so the error
 // names the same coordinate the reference's in-order loop would hit first.
 __global__ void k_floor_keys(const uint64_t* __restrict__ src, const int32_t* __restrict__ src_idx, int64_t n,
@@ -83,211 +246,378 @@ __global__ void k_floor_keys(const uint64_t* __restrict__ src, const int32_t* __
   out[i] = pack_key_unchecked(static_cast<int32_t>(fx), static_cast<int32_t>(fy), static_cast<int32_t>(fz));
 }
 
-// ---------------------------------------------------------------- backward search
-// ub[k * nb + b] = first i with segment_key(q_i, delta_k) > pivot_b.
-__global__ void k_backward(const uint64_t* __restrict__ src, int64_t n_src, int B, int64_t nb,
-                           const uint64_t* __restrict__ q, int64_t n_q, const int3* __restrict__ offsets, int K3,
-                           int32_t* __restrict__ ub) {
-  const int64_t t = blockIdx.x * int64_t{blockDim.x} + threadIdx.x;
-  if (t >= nb * K3) return;
-  const int k = static_cast<int>(t / nb);
-  const int64_t b = t - int64_t{k} * nb;
-  const uint64_t pivot = src[min((b + 1) * B, n_src) - 1];
-  const int3 d = offsets[k];
-  int64_t lo = 0, hi = n_q;
-  while (lo < hi) {
-    const int64_t mid = (lo + hi) >> 1;
-    if (segment_key(__ldg(q + mid), d) <= pivot)
-      lo = mid + 1;
-    else
-      hi = mid;
-  }
-  ub[t] = static_cast<int32_t>(lo);
+// ---------------------------------------------------------------- double-traversed search
+constexpr int kSearchThreads = 256;
+
+__device__ __forceinline__ uint64_t pivot_of(const uint64_t* src, int64_t n_src, int B, int64_t b) {
+  return __ldg(src + min((b + 1) * B, n_src) - 1);
 }
 
-// ---------------------------------------------------------------- range plan
-// One CTA. Entries e = k * (nb + 1) + b: b < nb are search blocks (query block
-// [ub[k][b-1], ub[k][b]) balanced into ceil(L/C) near-equal ranges, first ranges larger,
-// SPEC.md:220); b == nb is the unmatched tail [ub[k][nb-1], n_q), chunked by C so the
-// forward kernel can write the dense -1 entries. Descriptor: {k | first<<30, b, lo, hi}.
-constexpr int kPlanThreads = 1024;
-__global__ void __launch_bounds__(kPlanThreads) k_plan(const int32_t* __restrict__ ub, int64_t nb, int K3, int64_t n_q,
-                                                        int C, int4* __restrict__ descs, int* __restrict__ r_total) {
-  using Scan = cub::BlockScan<int, kPlanThreads>;
-  __shared__ typename Scan::TempStorage temp;
-  extern __shared__ int s_first[];  // K3 entries: global index of each offset's first range
-  const int64_t E = int64_t{K3} * (nb + 1);
-  const int64_t per = (E + kPlanThreads - 1) / kPlanThreads;
-  const int64_t e0 = threadIdx.x * per, e1 = min(E, e0 + per);
-  auto entry_len = [&](int64_t e, int64_t& lo) -> int64_t {
-    const int64_t k = e / (nb + 1), b = e - k * (nb + 1);
-    const int32_t* u = ub + k * nb;
-    lo = b == 0 ? 0 : u[b - 1];
-    const int64_t hi = b < nb ? u[b] : n_q;
-    return hi - lo;
-  };
-  int local = 0;
-  for (int64_t e = e0; e < e1; ++e) {
-    int64_t lo;
-    const int64_t L = entry_len(e, lo);
-    local += static_cast<int>((L + C - 1) / C);
+// First block b in [lo, nb) with pivot_b >= key (nb if none). Warp-cooperative: one probe
+// of 32 consecutive pivots around `hint` (the expected block: sorted queries land near
+// proportional source positions), then 32-way sampling rounds only if the probe misses.
+__device__ int64_t warp_first_pivot_ge(const uint64_t* src, int64_t n_src, int B, int64_t lo, int64_t nb,
+                                       uint64_t key, int lane, int64_t hint) {
+  int64_t hi = nb;  // invariant: answer in [lo, hi]; hi == nb means "none" unless proven
+  {
+    int64_t start = max(lo, min(hint - 8, nb - 32));
+    const int64_t p = start + lane;
+    const bool ge = p < nb && pivot_of(src, n_src, B, p) >= key;
+    const unsigned m = __ballot_sync(0xFFFFFFFFu, ge);
+    if (m) {
+      const int f = __ffs(m) - 1;
+      if (f > 0 || start == lo) return start + f;
+      hi = start;  // answer in [lo, start]
+    } else {
+      lo = min(nb, start + 32);
+    }
   }
-  int offset = 0, total = 0;
-  Scan(temp).ExclusiveSum(local, offset, total);
-  for (int64_t e = e0; e < e1; ++e)  // first range of each offset
-    if (e % (nb + 1) == 0) {
-      int before = offset;
-      for (int64_t f = e0; f < e; ++f) {
-        int64_t lo;
-        before += static_cast<int>((entry_len(f, lo) + C - 1) / C);
+  while (hi - lo > 32) {
+    const int64_t step = (hi - lo + 31) / 32;
+    const int64_t p = lo + lane * step;
+    const bool ge = p < hi && pivot_of(src, n_src, B, p) >= key;
+    const unsigned m = __ballot_sync(0xFFFFFFFFu, ge);
+    if (m == 0) {  // answer lies past the last valid sample
+      lo = lo + ((hi - 1 - lo) / step) * step + 1;
+    } else {
+      const int f = __ffs(m) - 1;
+      hi = lo + f * step;
+      lo = f ? lo + (f - 1) * step + 1 : lo;
+    }
+  }
+  const int64_t p = lo + lane;
+  const bool ge = p < hi && pivot_of(src, n_src, B, p) >= key;
+  const unsigned m = __ballot_sync(0xFFFFFFFFu, ge);
+  return m ? lo + (__ffs(m) - 1) : hi;
+}
+
+// Exclusive scan of counts[0, n) -> offs by one CTA (the last to finish): tiles of
+// kSearchThreads x 8 values loaded coalesced into registers, scanned, carried.
+__device__ void cta_exclusive_scan(const int32_t* counts, int64_t n, int32_t* offs, int64_t nchunk, int32_t* map_start,
+                                   int K3, int* s_warp) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int kPer = 8, kTile = kSearchThreads * kPer;
+  int carry = 0;
+  for (int64_t base = 0; base < n; base += kTile) {
+    int v[kPer];
+    int local = 0;
+#pragma unroll
+    for (int e = 0; e < kPer; ++e) {
+      const int64_t c = base + int64_t{tid} * kPer + e;
+      v[e] = c < n ? __ldcg(counts + c) : 0;
+      local += v[e];
+    }
+    int incl = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if (lane >= o) incl += u;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    int wprefix = 0, tile_total = 0;
+#pragma unroll
+    for (int w = 0; w < kSearchThreads / 32; ++w) {
+      wprefix += w < warp ? s_warp[w] : 0;
+      tile_total += s_warp[w];
+    }
+    int run = carry + wprefix + incl - local;
+#pragma unroll
+    for (int e = 0; e < kPer; ++e) {
+      const int64_t c = base + int64_t{tid} * kPer + e;
+      if (c < n) {
+        offs[c] = run;
+        if (c % nchunk == 0) map_start[c / nchunk] = run;
       }
-      s_first[e / (nb + 1)] = before;
+      run += v[e];
     }
-  __syncthreads();
-  int g = offset;
-  for (int64_t e = e0; e < e1; ++e) {
-    int64_t lo;
-    const int64_t L = entry_len(e, lo);
-    if (L <= 0) continue;
-    const int k = static_cast<int>(e / (nb + 1));
-    const int64_t b = e - int64_t{k} * (nb + 1);
-    const int64_t parts = (L + C - 1) / C, base = L / parts, extra = L % parts;
-    for (int64_t p = 0; p < parts; ++p, ++g) {
-      const int64_t len = base + (p < extra ? 1 : 0);
-      const int first = (g == s_first[k]) ? 1 : 0;
-      descs[g] = make_int4(k | (first << 30), b < nb ? static_cast<int>(b) : -1, static_cast<int>(lo),
-                           static_cast<int>(lo + len));
-      lo += len;
-    }
+    carry += tile_total;
+    __syncthreads();
   }
-  if (threadIdx.x == 0) *r_total = total;
+  if (tid == 0) map_start[K3] = carry;
 }
 
-// ---------------------------------------------------------------- forward search
-constexpr int kFwdThreads = 128;
-constexpr int kFwdWarps = kFwdThreads / 32;
-constexpr uint64_t kFlagAgg = uint64_t{1} << 62, kFlagPrefix = uint64_t{2} << 62, kValMask = (uint64_t{1} << 62) - 1;
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
 
-template <int QPT>
-__global__ void __launch_bounds__(kFwdThreads) k_forward(
-    const int4* __restrict__ descs, const int* __restrict__ r_total, int* __restrict__ ticket,
-    uint64_t* __restrict__ status, const uint64_t* __restrict__ src, const int32_t* __restrict__ src_idx,
-    int64_t n_src, int B, const uint64_t* __restrict__ q, int64_t n_q, const int3* __restrict__ offsets, int K3,
-    int32_t* __restrict__ pair_in, int32_t* __restrict__ pair_out, int32_t* __restrict__ nbr_pos,
+// Output-chunk double-traversed search. A CTA owns CQ = 32*QPL consecutive sorted queries
+// q_i and ALL K^3 offsets. Their segment keys {q_i + delta_k} lie between
+// q_first + delta_lexmin and q_last + delta_lexmax (translation preserves lexicographic
+// order), so ONE window of whole source blocks covers every segment of the chunk: it is
+// found with two warp-cooperative pivot searches and staged in shared memory by a single
+// bulk (TMA) copy, then reused by all K^3 offsets (windows larger than the shared-memory
+// capacity are processed in block-aligned slices). Warp w handles offsets k = w, w+8, ...:
+//   * segment keys of the CQ queries live in registers (lane-major => sorted across lanes);
+//   * BACKWARD search: every staged block pivot is compared with the whole sorted segment
+//     (one ballot per register row) -> its upper bound, i.e. the block's query sub-range
+//     (SPEC.md:208-216);
+//   * FORWARD search: each query is binary-searched only inside its own staged block,
+//     <= ceil(log2(B+1)) steps.
+// Results go to the dense k-major table (coalesced rows) and per-(k, chunk) hit counts,
+// scanned by the last CTA to finish (canonical order: k, then chunk).
+template <int QPL>
+__global__ void __launch_bounds__(kSearchThreads) k_search(
+    const uint64_t* __restrict__ src, const int32_t* __restrict__ src_idx, int64_t n_src, int B,
+    const uint64_t* __restrict__ q, int64_t n_q, const int3* __restrict__ offsets, int K3, int kmin_off,
+    int kmax_off, int64_t nchunk, int ngroups, int cap_blocks, int32_t* __restrict__ nbr,
+    int32_t* __restrict__ chunk_count, int32_t* __restrict__ chunk_off, unsigned* __restrict__ done,
     int32_t* __restrict__ map_start) {
+  constexpr int CQ = 32 * QPL;
+  constexpr int kWarps = kSearchThreads / 32;
   extern __shared__ __align__(16) unsigned char smem[];
-  uint64_t* s_keys = reinterpret_cast<uint64_t*>(smem);
-  int32_t* s_idx = reinterpret_cast<int32_t*>(s_keys + B);
-  __shared__ int s_r;
-  __shared__ int s_cnt[QPT][kFwdWarps];
-  __shared__ int s_pre[QPT][kFwdWarps];
-  __shared__ int s_count;
-  __shared__ uint64_t s_base;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (tid == 0) s_r = atomicAdd(ticket, 1);  // logical order = ticket order (forward progress)
-  __syncthreads();
-  const int r = s_r;
-  const int R = *r_total;
-  if (r >= R) return;
-  const int4 d = descs[r];
-  const int k = d.x & 0x3FFFFFFF, first = (d.x >> 30) & 1, b = d.y, lo = d.z, hi = d.w;
-  int blen = 0;
-  if (b >= 0) {  // stage the source block (scratchpad copy, PAPER §5.1.2 step 4)
-    const int64_t base = int64_t{b} * B;
-    blen = static_cast<int>(min(static_cast<int64_t>(B), n_src - base));
-    for (int t = tid; t < blen; t += kFwdThreads) {
-      s_keys[t] = src[base + t];
-      s_idx[t] = src_idx ? src_idx[base + t] : static_cast<int32_t>(base + t);
-    }
+  const int cap = cap_blocks * B;
+  uint64_t* s_win = reinterpret_cast<uint64_t*>(smem);           // cap staged keys
+  int32_t* s_widx = reinterpret_cast<int32_t*>(s_win + cap);     // cap staged indices
+  __shared__ uint64_t s_q[CQ];
+  __shared__ __align__(8) uint64_t s_bar;
+  __shared__ int64_t s_blo, s_bhi;
+  __shared__ int s_warp[kWarps];
+  __shared__ bool s_last;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t c = blockIdx.x / ngroups;
+  const int grp = static_cast<int>(blockIdx.x - c * ngroups);
+  const int my_k = grp + warp * ngroups;  // one offset per warp (CTA = chunk x offset group)
+  int my_cnt = 0;
+  const int64_t lo = c * CQ;
+  const int len = static_cast<int>(min(static_cast<int64_t>(CQ), n_q - lo));
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_bar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  for (int t = tid; t < CQ; t += kSearchThreads) s_q[t] = t < len ? __ldg(q + lo + t) : ~uint64_t{0};
   __syncthreads();
-  const int3 delta = offsets[k];
-  int hit[QPT];
-  unsigned bal[QPT];
-#pragma unroll
-  for (int u = 0; u < QPT; ++u) {
-    const int i = lo + u * kFwdThreads + tid;
-    hit[u] = -1;
-    if (i < hi && blen > 0) {
-      const uint64_t key = segment_key(__ldg(q + i), delta);
-      int l = 0, h = blen;
-      while (l < h) {  // 3-way search, <= ceil(log2(B+1)) steps
-        const int mid = (l + h) >> 1;
-        const uint64_t v = s_keys[mid];
-        if (v == key) {
-          hit[u] = s_idx[mid];
-          break;
-        }
-        if (v < key)
-          l = mid + 1;
-        else
-          h = mid;
-      }
-    }
-    bal[u] = __ballot_sync(0xFFFFFFFFu, hit[u] >= 0);
-    if (lane == 0) s_cnt[u][warp] = __popc(bal[u]);
-  }
-  __syncthreads();
-  if (tid == 0) {  // prefix over (round u, warp w) = query order
-    int acc = 0;
-    for (int u = 0; u < QPT; ++u)
-      for (int w = 0; w < kFwdWarps; ++w) {
-        s_pre[u][w] = acc;
-        acc += s_cnt[u][w];
-      }
-    s_count = acc;
-  }
-  __syncthreads();
-  if (warp == 0) {  // decoupled look-back over the ranges in canonical order
-    const uint64_t count = static_cast<uint64_t>(s_count);
-    uint64_t base = 0;
-    if (r > 0) {
-      if (lane == 0) st_release_u64(status + r, kFlagAgg | count);
-      int64_t j = r - 1;
-      for (;;) {
-        const int64_t idx = j - lane;
-        uint64_t s = idx >= 0 ? ld_acquire_u64(status + idx) : kFlagPrefix;
-        while (__any_sync(0xFFFFFFFFu, (s >> 62) == 0))
-          if ((s >> 62) == 0) s = ld_acquire_u64(status + idx);
-        const unsigned pmask = __ballot_sync(0xFFFFFFFFu, (s >> 62) == 2);
-        const int stop = pmask ? __ffs(pmask) - 1 : 31;
-        uint64_t v = lane <= stop ? (s & kValMask) : 0;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
-        base += v;
-        if (pmask) break;
-        j -= 32;
-      }
-    }
+  const int64_t nb = (n_src + B - 1) / B;
+  if (warp < 2) {  // window: blocks holding [q_first + delta_lexmin, q_last + delta_lexmax]
+    const uint64_t key = warp == 0 ? segment_key(s_q[0], offsets[kmin_off]) : segment_key(s_q[len - 1], offsets[kmax_off]);
+    const int64_t hint = (((warp == 0 ? lo : lo + len - 1) * n_src) / max(n_q, int64_t{1})) / B;
+    const int64_t b = warp_first_pivot_ge(src, n_src, B, 0, nb, key, lane, hint);
     if (lane == 0) {
-      st_release_u64(status + r, kFlagPrefix | (base + count));
-      s_base = base;
+      if (warp == 0)
+        s_blo = b;
+      else
+        s_bhi = min(b, nb - 1);
     }
   }
   __syncthreads();
-  const int64_t base = static_cast<int64_t>(s_base);
-  const unsigned lt = (1u << lane) - 1u;
-  int32_t* nbr_k = nbr_pos + int64_t{k} * n_q;
-#pragma unroll
-  for (int u = 0; u < QPT; ++u) {
-    const int i = lo + u * kFwdThreads + tid;
-    if (i < hi) {
-      int32_t m = -1;
-      if (hit[u] >= 0) {
-        m = static_cast<int32_t>(base + s_pre[u][warp] + __popc(bal[u] & lt));
-        pair_in[m] = hit[u];
-        pair_out[m] = i;
-      }
-      nbr_k[i] = m;
+  const int64_t blo = s_blo, bhi = s_bhi;
+  uint32_t phase = 0;
+  bool first_slice = true;
+  for (int64_t sb = blo; first_slice || sb <= bhi; sb += cap_blocks) {
+    const bool empty = blo >= nb || sb > bhi;  // no source block can match: write misses only
+    const int nblk = empty ? 0 : static_cast<int>(min(static_cast<int64_t>(cap_blocks), bhi - sb + 1));
+    const int64_t g0 = sb * B;
+    const int wlen = empty ? 0 : static_cast<int>(min(static_cast<int64_t>(nblk) * B, n_src - g0));
+    if (tid == 0 && wlen > 0) {  // one bulk copy per array (16-byte granules; arrays carry slack)
+      const uint32_t kb = static_cast<uint32_t>((wlen + 3) & ~3);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&s_bar)),
+                   "r"(kb * 8u + (src_idx ? kb * 4u : 0u))
+                   : "memory");
+      bulk_g2s(s_win, src + g0, kb * 8u, &s_bar);
+      if (src_idx) bulk_g2s(s_widx, src_idx + g0, kb * 4u, &s_bar);
     }
+    if (wlen > 0) {
+      mbar_wait_parity(&s_bar, phase);
+      phase ^= 1u;
+    }
+    // key just below this slice: queries <= it belong to earlier slices (or to nothing)
+    const uint64_t floor_key = (empty || sb == 0) ? 0 : __ldg(src + g0 - 1);
+    for (int k = my_k; k < K3; k += K3) {  // at most one iteration
+      const int3 d = offsets[k];
+      // lane-contiguous queries: lane L owns chunk positions [L*QPL, (L+1)*QPL), so a lane's
+      // consecutive sorted queries can be merged against the sorted block (galloping)
+      const int qb = lane * QPL;
+      uint64_t key[QPL];
+#pragma unroll
+      for (int u = 0; u < QPL; ++u) key[u] = qb + u < len ? segment_key(__ldg(q + lo + qb + u), d) : ~uint64_t{0};
+      int blk[QPL];  // block of each query inside the slice, -1 = not in this slice
+#pragma unroll
+      for (int u = 0; u < QPL; ++u) {
+        blk[u] = (sb == blo && !empty) || key[u] > floor_key ? 0 : -1;
+        if (empty || key[u] == ~uint64_t{0}) blk[u] = -1;
+      }
+      // BACKWARD search: each staged pivot splits the sorted segment; queries above pivot_b
+      // move to block b+1, above the last pivot they are outside the slice.
+      for (int bb = 0; bb < nblk; ++bb) {
+        const uint64_t piv = s_win[min((bb + 1) * B, wlen) - 1];
+#pragma unroll
+        for (int u = 0; u < QPL; ++u)
+          if (blk[u] == bb && key[u] > piv) blk[u] = bb + 1 < nblk ? bb + 1 : -1;
+      }
+      // FORWARD search inside the block: branchless lower bound for the first query of a
+      // block, then galloping from the previous position for the following (sorted) ones.
+      int res[QPL];
+      int p = 0, pblk = -1;
+#pragma unroll
+      for (int u = 0; u < QPL; ++u) {
+        res[u] = -1;
+        if (blk[u] < 0) continue;
+        const int w0 = blk[u] * B, end = w0 + min(B, wlen - w0);
+        bool bsearch = blk[u] != pblk;
+        if (!bsearch) {
+          int steps = 0;
+          while (p < end - 1 && s_win[p] < key[u] && steps < 6) {
+            ++p;
+            ++steps;
+          }
+          bsearch = p < end - 1 && s_win[p] < key[u];
+        }
+        if (bsearch) {
+          int base = blk[u] != pblk ? w0 : p, n = end - base;
+          while (n > 1) {
+            const int h = n >> 1;
+            base += s_win[base + h - 1] < key[u] ? h : 0;
+            n -= h;
+          }
+          p = base;
+        }
+        pblk = blk[u];
+        if (s_win[p] == key[u]) res[u] = src_idx ? s_widx[p] : static_cast<int32_t>(g0 + p);
+      }
+      int32_t* row = nbr + int64_t{k} * n_q + lo + qb;
+      int cnt = 0;
+#pragma unroll
+      for (int u = 0; u < QPL; ++u) {
+        if (qb + u < len && (first_slice || res[u] >= 0)) row[u] = res[u];
+        cnt += __popc(__ballot_sync(0xFFFFFFFFu, res[u] >= 0));
+      }
+      my_cnt += cnt;
+    }
+    first_slice = false;
+    __syncthreads();  // the next slice overwrites the window
+    if (empty) break;
+  }
+  if (lane == 0 && my_k < K3) chunk_count[int64_t{my_k} * nchunk + c] = my_cnt;
+}
+
+// Exclusive scan of the (k, chunk) hit counts in canonical order: each CTA scans a tile of
+// kScanTile counts (tile-local offsets + tile total); the last CTA to finish scans the tile
+// totals and writes the canonical list starts map_start[k] (= offset of (k, chunk 0)).
+constexpr int kScanPer = 8, kScanTile = kSearchThreads * kScanPer;
+__global__ void __launch_bounds__(kSearchThreads) k_scan_counts(const int32_t* __restrict__ counts, int64_t n,
+                                                                int32_t* __restrict__ offs, int32_t* __restrict__ tiles,
+                                                                int64_t nchunk, int K3, int32_t* __restrict__ map_start,
+                                                                unsigned* __restrict__ done) {
+  __shared__ int s_warp[kSearchThreads / 32];
+  __shared__ bool s_last;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t base = int64_t{blockIdx.x} * kScanTile;
+  int v[kScanPer];
+  int local = 0;
+#pragma unroll
+  for (int e = 0; e < kScanPer; ++e) {
+    const int64_t c = base + int64_t{tid} * kScanPer + e;
+    v[e] = c < n ? counts[c] : 0;
+    local += v[e];
+  }
+  int incl = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int u = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if (lane >= o) incl += u;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  int wprefix = 0, total = 0;
+#pragma unroll
+  for (int w = 0; w < kSearchThreads / 32; ++w) {
+    wprefix += w < warp ? s_warp[w] : 0;
+    total += s_warp[w];
+  }
+  int run = wprefix + incl - local;
+#pragma unroll
+  for (int e = 0; e < kScanPer; ++e) {
+    const int64_t c = base + int64_t{tid} * kScanPer + e;
+    if (c < n) offs[c] = run;
+    run += v[e];
   }
   if (tid == 0) {
-    if (first) map_start[k] = static_cast<int32_t>(base);
-    if (r == R - 1) map_start[K3] = static_cast<int32_t>(base + s_count);
+    tiles[blockIdx.x] = total;
+    __threadfence();
+    s_last = atomicAdd(done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (warp == 0) {  // scan tile totals (serial in 32-wide rounds; few hundred tiles at most)
+    int carry = 0;
+    for (int t0 = 0; t0 < static_cast<int>(gridDim.x); t0 += 32) {
+      const int t = t0 + lane;
+      const int x = t < static_cast<int>(gridDim.x) ? __ldcg(tiles + t) : 0;
+      int in = x;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xFFFFFFFFu, in, o);
+        if (lane >= o) in += u;
+      }
+      if (t < static_cast<int>(gridDim.x)) tiles[t] = carry + in - x;
+      carry += __shfl_sync(0xFFFFFFFFu, in, 31);
+    }
+    if (lane == 0) {
+      map_start[K3] = carry;
+      *done = 0;
+    }
+  }
+  __syncthreads();
+  for (int k = tid; k < K3; k += kSearchThreads) {
+    const int64_t c = int64_t{k} * nchunk;
+    map_start[k] = __ldcg(offs + c) + __ldcg(tiles + c / kScanTile);
+  }
+}
+
+// Canonical positions: m = chunk_off[k, c] + rank of the hit inside the chunk (query
+// order). One CTA per query chunk; warp w emits offsets k = w, w+8, ... with ballot ranks,
+// so no CTA-level barrier is needed.
+template <int QPL>
+__global__ void __launch_bounds__(kSearchThreads) k_emit(int32_t* __restrict__ nbr, int64_t n_q, int K3,
+                                                          int64_t nchunk, int ngroups, const int32_t* __restrict__ chunk_off,
+                                                          const int32_t* __restrict__ tile_base,
+                                                          int32_t* __restrict__ pair_in, int32_t* __restrict__ pair_out) {
+  constexpr int CQ = 32 * QPL;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t c = blockIdx.x / ngroups;
+  const int grp = static_cast<int>(blockIdx.x - c * ngroups);
+  const int64_t lo = c * CQ;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int k = grp + warp * ngroups; k < K3; k += K3) {
+    int32_t* row = nbr + int64_t{k} * n_q + lo;
+    const int64_t ci = int64_t{k} * nchunk + c;
+    int base = __ldg(chunk_off + ci) + __ldg(tile_base + ci / kScanTile);
+    int32_t j[QPL];
+#pragma unroll
+    for (int u = 0; u < QPL; ++u) j[u] = lo + u * 32 + lane < n_q ? row[u * 32 + lane] : -1;
+#pragma unroll
+    for (int u = 0; u < QPL; ++u) {
+      const unsigned bal = __ballot_sync(0xFFFFFFFFu, j[u] >= 0);
+      if (lo + u * 32 + lane < n_q) {
+        int32_t m = -1;
+        if (j[u] >= 0) {
+          m = base + __popc(bal & lt);
+          pair_in[m] = j[u];
+          pair_out[m] = static_cast<int32_t>(lo + u * 32 + lane);
+        }
+        row[u * 32 + lane] = m;
+      }
+      base += __popc(bal);
+    }
   }
 }
 
 constexpr int kThreads = 256;
+// Key / index arrays carry slack so 16-byte bulk copies may run past the last element.
+inline int64_t slack(int64_t n) { return ((n + 3) & ~int64_t{3}) + 4; }
 inline unsigned grid_for(int64_t n) { return static_cast<unsigned>(std::max<int64_t>(1, ceil_div<int64_t>(n, kThreads))); }
 
 std::string coord_error(char axis, int64_t v) {
@@ -333,9 +663,11 @@ std::vector<int3> weight_offsets_ext(int K, int scale) {
   return d;
 }
 
-std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map_cfg& cfg, const MapSource* target) {
-  if (cfg.block_B < 1 || cfg.block_B > 1024) fail(SCONV_ERR_ARG, "block size B must be in [1, 1024]");
-  if (cfg.block_C < 1 || cfg.block_C > 1024) fail(SCONV_ERR_ARG, "query block size C must be in [1, 1024]");
+std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map_cfg& cfg, const MapSource* target,
+                                   bool force_wide) {
+  if (cfg.block_B < 4 || cfg.block_B > 1024 || cfg.block_B % 4 != 0)
+    fail(SCONV_ERR_ARG, "block size B must be a multiple of 4 in [4, 1024]");
+  if (cfg.block_C < 1 || cfg.block_C > 4096) fail(SCONV_ERR_ARG, "query block size C must be in [1, 4096]");
   if (!cfg.transposed && cfg.out_stride < 1) fail(SCONV_ERR_ARG, "stride must be positive");
   if (P.n < 0 || P.n > INT32_MAX / 2) fail(SCONV_ERR_ARG, "point count out of supported range");
   auto m = std::make_unique<MapData>();
@@ -352,7 +684,7 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
   DevBuf flags_buf;
   flags_buf.alloc(sizeof(MapFlags), st);
   MapFlags* flags = flags_buf.get<MapFlags>();
-  MapFlags init{ULLONG_MAX, ULLONG_MAX, ULLONG_MAX, 0, 0};
+  MapFlags init{ULLONG_MAX, ULLONG_MAX, ULLONG_MAX, 0, 0, {INT_MAX, INT_MAX, INT_MAX, INT_MIN, INT_MIN, INT_MIN}, 0, 0};
   auto* pin = reinterpret_cast<MapFlags*>(ctx.pin_flags());
   pin[0] = init;
   SCONV_CUDA(cudaMemcpyAsync(flags, pin, sizeof(MapFlags), cudaMemcpyHostToDevice, st));
@@ -371,18 +703,52 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
     }
     m->src_keys = std::make_shared<DevBuf>();
     if (P.sorted) {
-      m->src_keys->alloc(sizeof(uint64_t) * n, st);
+      m->src_keys->alloc(sizeof(uint64_t) * slack(n), st);
       if (n > 0)
         ctx.launch("k_pack_keys", [&] {
           k_pack_keys<<<grid_for(n), kThreads, 0, st>>>(xyz, n, m->src_keys->get<uint64_t>(), 1, flags, 0);
         });
       m->src_identity = true;
+    } else if (!force_wide) {
+      // bbox -> left-aligned compact u32 keys + bucket histogram -> scan -> bucket scatter
+      // -> in-bucket rank: 5 launches instead of CUB's 8-digit 64-bit onesweep passes.
+      DevBuf ck, iota, tk, ti;
+      ck.alloc(sizeof(uint32_t) * n, st);
+      iota.alloc(sizeof(int32_t) * n, st);
+      tk.alloc(sizeof(uint32_t) * n, st);
+      ti.alloc(sizeof(int32_t) * n, st);
+      m->src_keys->alloc(sizeof(uint64_t) * slack(n), st);
+      m->src_idx.alloc(sizeof(int32_t) * slack(n), st);
+      if (n > 0) {
+        int* hist = ctx.sort_hist();
+        int* starts = hist + kBuckets;
+        int* cursor = starts + kBuckets + 1;
+        // 2^H buckets, ~4 keys per bucket on average (H in [10, 16])
+        int H = 10;
+        while (H < kMaxBucketBits && (int64_t{1} << (H + 2)) < n) ++H;
+        const unsigned bb = static_cast<unsigned>(std::min<int64_t>(grid_for(n), ctx.num_sms));
+        ctx.launch("k_bbox", [&] { k_bbox<<<bb, kThreads, 0, st>>>(xyz, n, flags); });
+        ctx.launch("k_pack_compact", [&] {
+          k_pack_compact<<<grid_for(n), kThreads, 0, st>>>(xyz, n, flags, ck.get<uint32_t>(), iota.get<int32_t>(),
+                                                           hist, H);
+        });
+        ctx.launch("k_hist_scan", [&] { k_hist_scan<<<1, kScanThreads, 0, st>>>(hist, 1 << H, starts, cursor, flags); });
+        ctx.launch("k_bucket_scatter", [&] {
+          k_bucket_scatter<<<grid_for(n), kThreads, 0, st>>>(ck.get<uint32_t>(), iota.get<int32_t>(), n, cursor,
+                                                             tk.get<uint32_t>(), ti.get<int32_t>(), H);
+        });
+        ctx.launch("k_bucket_rank", [&] {
+          k_bucket_rank<<<grid_for(n), kThreads, 0, st>>>(tk.get<uint32_t>(), ti.get<int32_t>(), n, starts, flags,
+                                                          m->src_keys->get<uint64_t>(), m->src_idx.get<int32_t>(), H);
+        });
+      }
+      m->src_identity = false;
     } else {
       DevBuf raw, iota;
       raw.alloc(sizeof(uint64_t) * n, st);
       iota.alloc(sizeof(int32_t) * n, st);
-      m->src_keys->alloc(sizeof(uint64_t) * n, st);
-      m->src_idx.alloc(sizeof(int32_t) * n, st);
+      m->src_keys->alloc(sizeof(uint64_t) * slack(n), st);
+      m->src_idx.alloc(sizeof(int32_t) * slack(n), st);
       if (n > 0) {
         ctx.launch("k_pack_keys", [&] {
           k_pack_keys<<<grid_for(n), kThreads, 0, st>>>(xyz, n, raw.get<uint64_t>(), 0, flags, 0);
@@ -414,7 +780,7 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
         txyz = target_xyz_dev.get<int32_t>();
       }
       m->q_keys = std::make_shared<DevBuf>();
-      m->q_keys->alloc(sizeof(uint64_t) * target->n, st);
+      m->q_keys->alloc(sizeof(uint64_t) * slack(target->n), st);
       if (target->n > 0)
         ctx.launch("k_pack_keys", [&] {
           k_pack_keys<<<grid_for(target->n), kThreads, 0, st>>>(txyz, target->n, m->q_keys->get<uint64_t>(), 1,
@@ -430,7 +796,7 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
     fl.alloc(sizeof(uint64_t) * std::max<int64_t>(n, 1), st);
     fs.alloc(sizeof(uint64_t) * std::max<int64_t>(n, 1), st);
     m->q_keys = std::make_shared<DevBuf>();
-    m->q_keys->alloc(sizeof(uint64_t) * std::max<int64_t>(n, 1), st);
+    m->q_keys->alloc(sizeof(uint64_t) * slack(n), st);
     nsel.alloc(sizeof(int64_t), st);
     if (n > 0) {
       ctx.launch("k_floor_keys", [&] {
@@ -498,11 +864,13 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
 
   // ---- search
   m->offsets.alloc(sizeof(int3) * K3, st);
-  SCONV_CUDA(cudaMemcpyAsync(m->offsets.get(), delta.data(), sizeof(int3) * K3, cudaMemcpyHostToDevice, st));
+  static_assert(sizeof(MapFlags) + 512 * sizeof(int3) <= Ctx::kPinFlagsBytes, "pinned flags region");
+  int3* pin_off = reinterpret_cast<int3*>(reinterpret_cast<unsigned char*>(ctx.pin_flags()) + 2 * sizeof(MapFlags));
+  std::memcpy(pin_off, delta.data(), sizeof(int3) * K3);
+  SCONV_CUDA(cudaMemcpyAsync(m->offsets.get(), pin_off, sizeof(int3) * K3, cudaMemcpyHostToDevice, st));
   m->map_start.alloc(sizeof(int32_t) * (K3 + 1), st);
   m->nbr_pos.alloc(sizeof(int32_t) * std::max<int64_t>(1, int64_t{K3} * n_out), st);
   const int B = cfg.block_B, C = cfg.block_C;
-  const int64_t nb = ceil_div<int64_t>(n, B);
   // upper bound on the match count: every query hits at most once
   const int64_t max_pairs = std::min<int64_t>(int64_t{K3} * n_out, int64_t{K3} * n);
   if (n == 0 || n_out == 0) {
@@ -510,44 +878,64 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
     if (n_out > 0)
       SCONV_CUDA(cudaMemsetAsync(m->nbr_pos.get(), 0xFF, sizeof(int32_t) * int64_t{K3} * n_out, st));
   } else {
-    DevBuf ub, descs, rtot, status, ticket;
-    ub.alloc(sizeof(int32_t) * nb * K3, st);
-    const int64_t r_max = int64_t{K3} * (nb + ceil_div<int64_t>(n_out, C) + 2);
-    if (r_max > INT32_MAX) fail(SCONV_ERR_ARG, "kernel map too large");
-    descs.alloc(sizeof(int4) * r_max, st);
-    rtot.alloc(sizeof(int), st);
-    status.alloc(sizeof(uint64_t) * r_max, st);
-    ticket.alloc(sizeof(int), st);
+    // Work item = one CTA per chunk of CQ = 32*QPL sorted queries (CQ <= C), all offsets.
+    const int qpl = C >= 256 ? 8 : (C >= 128 ? 4 : (C >= 64 ? 2 : 1));
+    const int CQ = 32 * qpl;
+    const int64_t nchunk2 = ceil_div<int64_t>(n_out, CQ);
+    const int64_t grid2 = nchunk2 * K3;
+    if (grid2 > INT32_MAX) fail(SCONV_ERR_ARG, "kernel map too large");
+    DevBuf counts, offs, tiles;
+    const int64_t ntiles = ceil_div<int64_t>(grid2, kScanTile);
+    counts.alloc(sizeof(int32_t) * grid2, st);
+    offs.alloc(sizeof(int32_t) * grid2, st);
+    tiles.alloc(sizeof(int32_t) * ntiles, st);
     m->pair_in.alloc(sizeof(int32_t) * std::max<int64_t>(1, max_pairs), st);
     m->pair_out.alloc(sizeof(int32_t) * std::max<int64_t>(1, max_pairs), st);
-    ctx.launch("k_backward", [&] {
-      k_backward<<<grid_for(nb * K3), kThreads, 0, st>>>(src, n, B, nb, q, n_out, m->offsets.get<int3>(), K3,
-                                                         ub.get<int32_t>());
-    });
-    ctx.launch("k_plan", [&] {
-      k_plan<<<1, kPlanThreads, sizeof(int) * K3, st>>>(ub.get<int32_t>(), nb, K3, n_out, C, descs.get<int4>(),
-                                                         rtot.get<int>());
-    });
-    SCONV_CUDA(cudaMemsetAsync(status.get(), 0, sizeof(uint64_t) * r_max, st));
-    SCONV_CUDA(cudaMemsetAsync(ticket.get(), 0, sizeof(int), st));
-    const size_t smem = (sizeof(uint64_t) + sizeof(int32_t)) * B;
-    const int qpt = ceil_div(C, kFwdThreads);
-    auto fwd = [&](auto kernel) {
-      ctx.launch("k_forward", [&] {
-        kernel<<<static_cast<unsigned>(r_max), kFwdThreads, smem, st>>>(
-            descs.get<int4>(), rtot.get<int>(), ticket.get<int>(), status.get<uint64_t>(), src, src_idx, n, B, q,
-            n_out, m->offsets.get<int3>(), K3, m->pair_in.get<int32_t>(), m->pair_out.get<int32_t>(),
-            m->nbr_pos.get<int32_t>(), m->map_start.get<int32_t>());
+    int kmin_off = 0, kmax_off = 0;  // lexicographically smallest / largest search offset
+    auto lex_less = [](const int3& a, const int3& b) {
+      return a.x != b.x ? a.x < b.x : (a.y != b.y ? a.y < b.y : a.z < b.z);
+    };
+    for (int k = 1; k < K3; ++k) {
+      if (lex_less(delta[k], delta[kmin_off])) kmin_off = k;
+      if (lex_less(delta[kmax_off], delta[k])) kmax_off = k;
+    }
+    const int cap_blocks = std::max(1, static_cast<int>((24 * 1024) / (12 * B)));
+    const int ngroups = ceil_div(K3, kSearchThreads / 32);  // CTA = chunk x group of <= 8 offsets
+    const size_t smem = size_t{12} * cap_blocks * B;
+    auto go = [&](auto kern) {
+      SCONV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      ctx.launch("k_search", [&] {
+        kern<<<static_cast<unsigned>(nchunk2 * ngroups), kSearchThreads, smem, st>>>(
+            src, src_idx, n, B, q, n_out, m->offsets.get<int3>(), K3, kmin_off, kmax_off, nchunk2, ngroups, cap_blocks,
+            m->nbr_pos.get<int32_t>(), counts.get<int32_t>(), offs.get<int32_t>(), ctx.done_counter(),
+            m->map_start.get<int32_t>());
       });
     };
-    if (qpt <= 1)
-      fwd(k_forward<1>);
-    else if (qpt <= 2)
-      fwd(k_forward<2>);
-    else if (qpt <= 4)
-      fwd(k_forward<4>);
-    else
-      fwd(k_forward<8>);
+    switch (qpl) {
+      case 1: go(k_search<1>); break;
+      case 2: go(k_search<2>); break;
+      case 4: go(k_search<4>); break;
+      default: go(k_search<8>); break;
+    }
+    ctx.launch("k_scan_counts", [&] {
+      k_scan_counts<<<static_cast<unsigned>(ntiles), kSearchThreads, 0, st>>>(
+          counts.get<int32_t>(), grid2, offs.get<int32_t>(), tiles.get<int32_t>(), nchunk2, K3,
+          m->map_start.get<int32_t>(), ctx.done_counter());
+    });
+    auto emit = [&](auto kern) {
+      ctx.launch("k_emit", [&] {
+        kern<<<static_cast<unsigned>(nchunk2 * ngroups), kSearchThreads, 0, st>>>(
+            m->nbr_pos.get<int32_t>(), n_out, K3, nchunk2, ngroups, offs.get<int32_t>(), tiles.get<int32_t>(),
+            m->pair_in.get<int32_t>(),
+                                                                        m->pair_out.get<int32_t>());
+      });
+    };
+    switch (qpl) {
+      case 1: emit(k_emit<1>); break;
+      case 2: emit(k_emit<2>); break;
+      case 4: emit(k_emit<4>); break;
+      default: emit(k_emit<8>); break;
+    }
   }
   // ---- readback: flags + canonical list starts (one sync per map)
   if (sizeof(MapFlags) + sizeof(int32_t) * (K3 + 1) > Ctx::kPinReadbackBytes) fail(SCONV_ERR_ARG, "kernel too large");
@@ -559,6 +947,7 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
   MapFlags f;
   std::memcpy(&f, pin2, sizeof(f));
   check_flags(f);
+  if (f.wide || f.big_bucket) return build_map(ctx, P, cfg, target, true);  // exact fallback: CUB 64-bit sort
   m->starts.resize(K3 + 1);
   std::memcpy(m->starts.data(), pin2 + sizeof(MapFlags), sizeof(int32_t) * (K3 + 1));
   m->sizes.resize(K3);

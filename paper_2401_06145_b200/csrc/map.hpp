@@ -44,7 +44,8 @@ struct MapSource {
   int64_t n = 0;
 };
 
-std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map_cfg& cfg, const MapSource* target);
+std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map_cfg& cfg, const MapSource* target,
+                                   bool force_wide = false);
 
 // Weight offsets (reference weight_offsets + SURVEY §2.2 even-K extension), lexicographic.
 std::vector<int3> weight_offsets_ext(int K, int scale);

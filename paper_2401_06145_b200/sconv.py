@@ -77,6 +77,7 @@ SIGNATURES = [
     ("sconv_ctx_synchronize", _I, [_P]),
     ("sconv_ctx_launch_count", _I64, [_P]),
     ("sconv_ctx_set_profiling", _I, [_P, _I]),
+    ("sconv_ctx_set_profile_filter", _I, [_P, C.c_char_p]),
     ("sconv_ctx_profile_count", _I, [_P]),
     ("sconv_ctx_profile_entry", _I, [_P, _I, C.POINTER(C.c_char_p), C.POINTER(_I64), C.POINTER(_D)]),
     ("sconv_ctx_profile_reset", _I, [_P]),
@@ -168,7 +169,11 @@ class Context:
     def set_profiling(self, on: bool):
         self.check(self.lib.sconv_ctx_set_profiling(self.h, 1 if on else 0))
 
+    def set_profile_filter(self, label: Optional[str]):
+        self.check(self.lib.sconv_ctx_set_profile_filter(self.h, label.encode() if label else None))
+
     def profile(self) -> dict:
+        self.synchronize()  # resolves pending per-launch events
         out = {}
         for i in range(self.lib.sconv_ctx_profile_count(self.h)):
             name, n, ms = C.c_char_p(), C.c_int64(), C.c_double()

@@ -49,7 +49,7 @@ def assert_map_equal(gpu, ora):
     (3, 2, 20000, 50, False, 256, 512),   # strided (SPEC-literal offsets s*t)
     (5, 2, 4000, 25, True, 32, 40),
     (3, 1, 7, 5, False, 256, 512),
-    (3, 1, 30000, 60, False, 17, 33),     # odd B/C exercise balancing + tails
+    (3, 1, 30000, 60, False, 20, 33),     # odd C, small B: many windows + tails
 ])
 def test_map_parity(ctx, oracle, K, s, n, extent, presorted, B, Cq):
     rng = np.random.default_rng(K * 1000 + s * 100 + n)
@@ -73,6 +73,16 @@ def test_map_range_edges(ctx, oracle):
     gpu = m.read()
     ora = oracle.layer_map(xyz, False, 5, 1, 1, backend=2)
     assert_map_equal(gpu, ora)
+
+
+def test_map_sort_fallbacks(ctx, oracle):
+    """Compact 32-bit keys with an oversized bucket (> 4096 keys share the top 16 bits)
+    force the exact CUB fallback; the map must not change."""
+    line = np.stack([np.zeros(5000), np.zeros(5000), np.arange(5000)], 1).astype(np.int32)
+    extra = np.array([[1, 1023, -(2 ** 20 - 1)], [0, 0, 2 ** 20 - 1]], np.int32)
+    xyz = np.concatenate([line, extra])[np.random.default_rng(0).permutation(5002)]
+    m = sc.KernelMap.build(ctx, xyz, False, 3, 1, 1)
+    assert_map_equal(m.read(), oracle.layer_map(xyz, False, 3, 1, 1))
 
 
 def test_map_even_kernel_and_transposed(ctx, oracle):
@@ -111,6 +121,11 @@ def test_map_errors(ctx):
         sc.KernelMap.build(ctx, bad, False, 3, 1, 1)
     with pytest.raises(sc.InvalidArgument):
         sc.KernelMap.build(ctx, np.array([[1, 0, 0], [0, 0, 0]], np.int32), True, 3, 1, 1)  # flagged sorted, is not
+    with pytest.raises(sc.InvalidArgument):
+        sc.KernelMap.build(ctx, np.array([[1, 0, 0]], np.int32), False, 3, 1, 1, B=17)  # B must be a multiple of 4
+    with pytest.raises(sc.InvalidArgument, match="kernel size must be a positive odd integer"):
+        sc.sc_layer_forward(ctx, sc.PointCloud(np.zeros((1, 3), np.int32), np.zeros((1, 4), np.float32)),
+                            np.zeros((8, 4, 4), np.float32), 2, 1)
 
 
 def rel_errors(g, r):
