@@ -10,6 +10,7 @@ OBJ      := $(patsubst $(SRC)/%.cu,build/%.o,$(CU))
 LIB      := $(PKG)/libsconv_b200.so
 
 all: $(LIB) oracle
+	@if [ -d $(REF_INC) ]; then $(MAKE) tests/cpp/test_adapter; fi
 
 build/%.o: $(SRC)/%.cu $(HDR)
 	@mkdir -p build
@@ -27,3 +28,11 @@ clean:
 	$(MAKE) -C oracle clean
 
 .PHONY: all oracle clean
+
+# Reference-typed adapter test (needs the reference headers at build time; the binary travels)
+REF_INC ?= /root/reference/proj/include
+tests/cpp/test_adapter: tests/cpp/test_adapter.cpp include/sconv_b200.hpp include/sconv_b200.h $(LIB)
+	g++ -std=c++20 -O2 -I$(REF_INC) -Iinclude -o $@ $< -L$(PKG) -lsconv_b200 -Wl,-rpath,'$$ORIGIN/../../$(PKG)'
+
+adapter: tests/cpp/test_adapter
+.PHONY: adapter

@@ -159,6 +159,15 @@ sconv_status sconv_sc_layer_forward(sconv_ctx* ctx, const int32_t* xyz, int64_t 
                                     int c_in, const float* w, int c_out, int K, int s, const sconv_exec_cfg* cfg,
                                     int32_t* out_xyz, int64_t* n_out, float* f_out);
 
+/* GEMM grouping on host (replaces group_gemms + padding_overhead):
+ * sizes[n] -> order (non-empty offsets in the chosen order, *n_order entries), groups as
+ * [group_begin[g], group_end[g]) over `order` with padded heights[g] (*n_groups), per-offset
+ * buffer_offsets[n] (-1 when n_k = 0), *buffer_length, *overhead (x / y; -1 when y = 0).
+ * Output arrays hold n entries. */
+sconv_status sconv_plan_groups(const int64_t* sizes, int n, int policy, double epsilon, int max_batch, int* order,
+                               int* n_order, int* group_begin, int* group_end, int64_t* heights, int* n_groups,
+                               int64_t* buffer_offsets, int64_t* buffer_length, double* overhead);
+
 /* ---------------- utilities (cli gen) ----------------
  * N unique coordinates uniform in [0,E)^3 from Rng(stream_seed(seed,0)) (x,y,z order,
  * duplicates rejected), then N x C features U[0,1) from the same stream. Host buffers. */

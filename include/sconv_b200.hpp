@@ -1,0 +1,135 @@
+// sconv_b200.hpp — header-only C++ adapter: the reference's SC-layer API on the B200 engine.
+//
+// Include AFTER the reference's own headers (<sconv/geometry.hpp>, proj/include/sconv/
+// geometry.hpp:16-257): the functions take and return the reference types (PointCloud,
+// Matrix, OffsetSet, Coordinate) and rethrow the reference exception types with the same
+// messages (geometry.hpp:53 std::out_of_range "coordinate x out of range: v",
+// std::invalid_argument for arguments, std::logic_error for invariant violations).
+//
+//   sconv::gpu::Context ctx(0);
+//   auto [Q, map] = sconv::gpu::build_kernel_map_sorted(ctx, P, K, s);
+//   sconv::PointCloud out = sconv::gpu::sc_layer_forward(ctx, P, W, K, s);
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "sconv_b200.h"
+
+namespace sconv::gpu {
+
+inline void check(sconv_status st, const char* msg) {
+  switch (st) {
+    case SCONV_OK:
+      return;
+    case SCONV_ERR_ARG:
+      throw std::invalid_argument(msg);
+    case SCONV_ERR_RANGE:
+      throw std::out_of_range(msg);
+    case SCONV_ERR_STATE:
+      throw std::logic_error(msg);
+    default:
+      throw std::runtime_error(msg);
+  }
+}
+
+class Context {
+ public:
+  explicit Context(int device = 0) { check(sconv_ctx_create(device, &h_), sconv_global_last_error()); }
+  ~Context() { sconv_ctx_destroy(h_); }
+  Context(const Context&) = delete;
+  Context& operator=(const Context&) = delete;
+  sconv_ctx* get() const { return h_; }
+  void check_status(sconv_status st) const { check(st, sconv_last_error(h_)); }
+
+ private:
+  sconv_ctx* h_ = nullptr;
+};
+
+// KernelMap: per offset k, (input j, output i) pairs sorted by i.
+struct KernelMap {
+  OffsetSet offsets;
+  std::vector<std::vector<std::pair<std::int32_t, std::int32_t>>> matches;
+  std::int64_t total() const {
+    std::int64_t t = 0;
+    for (const auto& m : matches) t += static_cast<std::int64_t>(m.size());
+    return t;
+  }
+};
+
+struct LayerConfig {  // SPEC.md:359 config{grouping policy, eps, max_batch, tiles T_g/T_s, B, C}
+  int policy = SCONV_GROUP_SORTED;
+  double epsilon = 0.25;
+  int max_batch = 16;
+  int gather_tile = 0, scatter_tile = 0;  // 0 = tuned / heuristic
+  int B = 256, C = 512;
+  int compute_dtype = SCONV_F16;
+};
+
+namespace detail {
+inline std::vector<std::int32_t> flatten(const CoordList& c) {
+  std::vector<std::int32_t> v(c.size() * 3);
+  for (std::size_t i = 0; i < c.size(); ++i) {
+    v[3 * i] = c[i].x;
+    v[3 * i + 1] = c[i].y;
+    v[3 * i + 2] = c[i].z;
+  }
+  return v;
+}
+inline CoordList unflatten(const std::vector<std::int32_t>& v, std::int64_t n) {
+  CoordList c(static_cast<std::size_t>(n));
+  for (std::int64_t i = 0; i < n; ++i) c[i] = {v[3 * i], v[3 * i + 1], v[3 * i + 2]};
+  return c;
+}
+}  // namespace detail
+
+// build_kernel_map_sorted for a SPEC-literal layer: Q = Eq. 1 coordinates of P with stride
+// s (sorted; for s == 1 and sorted P they alias P), offsets = weight_offsets(K, s).
+inline std::pair<CoordsPtr, KernelMap> build_kernel_map_sorted(Context& ctx, const PointCloud& P, int K, int s,
+                                                               int B = 256, int C = 512) {
+  const auto xyz = detail::flatten(*P.coords);
+  sconv_map_cfg cfg{K, s, s, 0, B, C};
+  sconv_map* m = nullptr;
+  ctx.check_status(sconv_map_build(ctx.get(), xyz.data(), P.size(), SCONV_MEM_HOST, P.sorted ? 1 : 0, &cfg, nullptr,
+                                   0, SCONV_MEM_HOST, &m));
+  sconv_map_info info;
+  ctx.check_status(sconv_map_get_info(ctx.get(), m, &info));
+  std::vector<std::int32_t> q(static_cast<std::size_t>(info.num_outputs) * 3), in(info.total_matches),
+      out(info.total_matches);
+  std::vector<std::int64_t> sizes(info.num_offsets);
+  const sconv_status st = sconv_map_read(ctx.get(), m, q.data(), sizes.data(), in.data(), out.data());
+  sconv_map_free(ctx.get(), m);
+  ctx.check_status(st);
+  KernelMap km;
+  km.offsets = weight_offsets(K, s);
+  km.matches.resize(static_cast<std::size_t>(info.num_offsets));
+  std::size_t pos = 0;
+  for (int k = 0; k < info.num_offsets; ++k)
+    for (std::int64_t r = 0; r < sizes[k]; ++r, ++pos) km.matches[k].emplace_back(in[pos], out[pos]);
+  CoordsPtr Q = (s == 1 && P.sorted) ? P.coords : make_coords(detail::unflatten(q, info.num_outputs));
+  return {Q, std::move(km)};
+}
+
+// sc_layer_forward. W: K^3 matrices C_in x C_out, flattened [k][cin][cout].
+inline PointCloud sc_layer_forward(Context& ctx, const PointCloud& cloud, const std::vector<float>& W, int c_out,
+                                   int K, int s, const LayerConfig& cfg = {}) {
+  const auto xyz = detail::flatten(*cloud.coords);
+  const int c_in = static_cast<int>(cloud.channels());
+  sconv_exec_cfg ec{cfg.policy, cfg.epsilon, cfg.max_batch, cfg.gather_tile, cfg.scatter_tile, cfg.compute_dtype};
+  std::vector<std::int32_t> oxyz(xyz.size());
+  Matrix out(cloud.size(), c_out);
+  std::int64_t n_out = 0;
+  ctx.check_status(sconv_sc_layer_forward(ctx.get(), xyz.data(), cloud.size(), cloud.sorted ? 1 : 0,
+                                          cloud.size() ? cloud.features.row(0) : nullptr, c_in, W.data(), c_out, K,
+                                          s, &ec, oxyz.data(), &n_out, cloud.size() ? out.row(0) : nullptr));
+  Matrix trimmed(n_out, c_out);
+  for (std::int64_t r = 0; r < n_out; ++r)
+    for (int c = 0; c < c_out; ++c) trimmed(r, c) = out(r, c);
+  CoordsPtr Q = (s == 1 && cloud.sorted) ? cloud.coords : make_coords(detail::unflatten(oxyz, n_out));
+  return PointCloud{Q, std::move(trimmed), true};
+}
+
+}  // namespace sconv::gpu

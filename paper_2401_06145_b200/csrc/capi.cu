@@ -470,6 +470,26 @@ sconv_status sconv_sc_layer_forward(sconv_ctx* ctx, const int32_t* xyz, int64_t 
   });
 }
 
+sconv_status sconv_plan_groups(const int64_t* sizes, int n, int policy, double epsilon, int max_batch, int* order,
+                               int* n_order, int* group_begin, int* group_end, int64_t* heights, int* n_groups,
+                               int64_t* buffer_offsets, int64_t* buffer_length, double* overhead) {
+  return guarded(nullptr, [&] {
+    if (n < 0 || (n > 0 && !sizes)) fail(SCONV_ERR_ARG, "invalid sizes");
+    const GroupPlan p = group_gemms(std::vector<int64_t>(sizes, sizes + n), policy, epsilon, max_batch);
+    *n_order = static_cast<int>(p.order.size());
+    for (size_t i = 0; i < p.order.size(); ++i) order[i] = p.order[i];
+    *n_groups = static_cast<int>(p.groups.size());
+    for (size_t g = 0; g < p.groups.size(); ++g) {
+      group_begin[g] = p.groups[g].begin;
+      group_end[g] = p.groups[g].end;
+      heights[g] = p.groups[g].height;
+    }
+    for (int k = 0; k < n; ++k) buffer_offsets[k] = p.buffer_offsets[k];
+    *buffer_length = p.buffer_length;
+    *overhead = p.real_rows > 0 ? static_cast<double>(p.buffer_length - p.real_rows) / p.real_rows : -1.0;
+  });
+}
+
 sconv_status sconv_generate_synthetic(int64_t N, int64_t E, int64_t C, uint64_t seed, int32_t* xyz, float* feats) {
   return guarded(nullptr, [&] {
     if (N < 0 || E < 1 || C < 0) fail(SCONV_ERR_ARG, "invalid synthetic cloud parameters");

@@ -97,6 +97,8 @@ SIGNATURES = [
     ("sconv_tune_layer", _I, [_P, _P, _P, _P, _I, _I, C.POINTER(_I), C.POINTER(_I), _P, C.POINTER(_I)]),
     ("sconv_sc_layer_forward", _I, [_P, _P, _I64, _I, _P, _I, _P, _I, _I, _I, C.POINTER(ExecCfg), _P,
                                     C.POINTER(_I64), _P]),
+    ("sconv_plan_groups", _I, [_P, _I, _I, _D, _I, _P, C.POINTER(_I), _P, _P, _P, C.POINTER(_I), _P,
+                               C.POINTER(_I64), C.POINTER(_D)]),
     ("sconv_generate_synthetic", _I, [_I64, _I64, _I64, _U64, _P, _P]),
     ("sconv_generate_weights", _I, [_U64, _U64, _I, _I, _I, _P]),
     ("sconv_global_last_error", C.c_char_p, []),
@@ -361,6 +363,22 @@ def sc_layer_forward(ctx: Context, cloud: PointCloud, W: np.ndarray, K: int, s: 
                                              c_out, K, s, C.byref(cfg), _ptr(out_xyz), C.byref(n_out), _ptr(out_f)))
     n = n_out.value
     return PointCloud(out_xyz[:n].copy(), out_f[:n].copy(), True)
+
+
+def plan_groups(sizes, policy=GROUP_SORTED, epsilon=0.25, max_batch=16) -> dict:
+    """SPEC group_gemms + padding_overhead through the library's planner."""
+    lib = load()
+    s = np.ascontiguousarray(sizes, np.int64)
+    n = len(s)
+    order, gb, ge = np.empty(n, np.int32), np.empty(n, np.int32), np.empty(n, np.int32)
+    heights, boff = np.empty(n, np.int64), np.empty(n, np.int64)
+    no, ng, blen, ovh = C.c_int(), C.c_int(), C.c_int64(), C.c_double()
+    st = lib.sconv_plan_groups(_ptr(s), n, policy, epsilon, max_batch, _ptr(order), C.byref(no), _ptr(gb), _ptr(ge),
+                               _ptr(heights), C.byref(ng), _ptr(boff), C.byref(blen), C.byref(ovh))
+    if st != OK:
+        _raise(st, lib.sconv_global_last_error().decode())
+    return dict(order=order[: no.value], groups=list(zip(gb[: ng.value], ge[: ng.value], heights[: ng.value])),
+                buffer_offsets=boff, buffer_length=blen.value, overhead=ovh.value)
 
 
 def generate_synthetic(N: int, E: int, Cch: int, seed: int):
