@@ -168,6 +168,34 @@ sconv_status sconv_plan_groups(const int64_t* sizes, int n, int policy, double e
                                int* n_order, int* group_begin, int* group_end, int64_t* heights, int* n_groups,
                                int64_t* buffer_offsets, int64_t* buffer_length, double* overhead);
 
+/* ---------------- network driver (SPEC netdef) ----------------
+ * An op list over tensor ids, 12 int32 fields per op:
+ *   {kind, out, in, b_or_target, K, offset_scale, out_stride, transposed, c_in, c_out, weight_id, relu}
+ * kind 1 = CONV (SC layer; transposed convs take the target tensor's coordinates),
+ * kind 2 = ADD (out = [relu](in + b)), kind 3 = CONCAT (out = [in | b] along channels).
+ * forward_network's sequential chain is the special case of CONV-only ops;
+ * U-Net skips / residual blocks (BASELINE configs 2-5) use ADD and CONCAT. Kernel maps are
+ * cached per (input coordinates, K, offset scale, stride, transposed, target) within a forward. */
+typedef struct sconv_net sconv_net;
+sconv_status sconv_net_create(sconv_ctx* ctx, const int32_t* ops, int n_ops, int num_tensors, int input_tensor,
+                              int output_tensor, const sconv_exec_cfg* cfg, int block_B, int block_C,
+                              sconv_net** out);
+/* Weights of CONV ops with this weight_id: fp32 [num_offsets][c_in][c_out] in `mem`. */
+sconv_status sconv_net_set_weights(sconv_ctx* ctx, sconv_net* net, int weight_id, const float* w, int mem,
+                                   int num_offsets, int c_in, int c_out);
+/* Runs the graph on a cloud (xyz n x 3 int32 + fp32 features n x c_in). Asynchronous apart
+ * from one sync per distinct kernel map. */
+sconv_status sconv_net_forward(sconv_ctx* ctx, sconv_net* net, const int32_t* xyz, int64_t n, int mem, int in_sorted,
+                               const float* feats, int f_mem, int c_in);
+sconv_status sconv_net_tensor_info(sconv_ctx* ctx, const sconv_net* net, int tensor, int64_t* n, int* channels,
+                                   int* coordset);
+/* Host readback: coordinates (n x 3, sorted unless the tensor is the unsorted raw input) and fp32 features. */
+sconv_status sconv_net_read_tensor(sconv_ctx* ctx, const sconv_net* net, int tensor, int32_t* xyz, float* feats);
+/* Device view of a tensor's fp32 features (valid until the next forward). */
+sconv_status sconv_net_tensor_device(const sconv_net* net, int tensor, const float** feats);
+sconv_status sconv_net_stats(const sconv_net* net, int* maps_built, int* convs);
+void sconv_net_free(sconv_ctx* ctx, sconv_net* net);
+
 /* ---------------- utilities (cli gen) ----------------
  * N unique coordinates uniform in [0,E)^3 from Rng(stream_seed(seed,0)) (x,y,z order,
  * duplicates rejected), then N x C features U[0,1) from the same stream. Host buffers. */

@@ -13,6 +13,7 @@
 #include "ctx.hpp"
 #include "gmas.hpp"
 #include "map.hpp"
+#include "net.hpp"
 
 namespace sconvb {
 
@@ -488,6 +489,129 @@ sconv_status sconv_plan_groups(const int64_t* sizes, int n, int policy, double e
     *buffer_length = p.buffer_length;
     *overhead = p.real_rows > 0 ? static_cast<double>(p.buffer_length - p.real_rows) / p.real_rows : -1.0;
   });
+}
+
+sconv_status sconv_net_create(sconv_ctx* ctx, const int32_t* ops, int n_ops, int num_tensors, int input_tensor,
+                              int output_tensor, const sconv_exec_cfg* cfg, int block_B, int block_C,
+                              sconv_net** out) {
+  return guarded(ctx, [&] {
+    if (!out || (n_ops > 0 && !ops)) fail(SCONV_ERR_ARG, "null argument");
+    auto n = std::make_unique<sconv_net>();
+    n->num_tensors = num_tensors;
+    n->input_tensor = input_tensor;
+    n->output_tensor = output_tensor;
+    n->block_B = block_B > 0 ? block_B : 256;
+    n->block_C = block_C > 0 ? block_C : 512;
+    n->cfg = normalize(cfg);
+    if (input_tensor < 0 || input_tensor >= num_tensors || output_tensor < 0 || output_tensor >= num_tensors)
+      fail(SCONV_ERR_ARG, "tensor id out of range");
+    for (int i = 0; i < n_ops; ++i) {
+      const int32_t* r = ops + static_cast<size_t>(i) * kOpFields;
+      NetOp o;
+      o.kind = r[0];
+      o.out = r[1];
+      o.in = r[2];
+      o.b = r[3];
+      o.target = r[3];
+      o.K = r[4];
+      o.offset_scale = r[5];
+      o.out_stride = r[6];
+      o.transposed = r[7];
+      o.c_in = r[8];
+      o.c_out = r[9];
+      o.weight = r[10];
+      o.relu = r[11];
+      n->ops.push_back(o);
+    }
+    n->check_ops();
+    *out = n.release();
+  });
+}
+
+sconv_status sconv_net_set_weights(sconv_ctx* ctx, sconv_net* net, int weight_id, const float* w, int mem,
+                                   int num_offsets, int c_in, int c_out) {
+  return guarded(ctx, [&] {
+    if (!net || !w) fail(SCONV_ERR_ARG, "null argument");
+    net->weights[weight_id] = create_weights(*ctx, w, mem, num_offsets, c_in, c_out, net->cfg.compute_dtype);
+  });
+}
+
+sconv_status sconv_net_forward(sconv_ctx* ctx, sconv_net* net, const int32_t* xyz, int64_t n, int mem, int in_sorted,
+                               const float* feats, int f_mem, int c_in) {
+  return guarded(ctx, [&] {
+    if (!net || (n > 0 && (!xyz || !feats))) fail(SCONV_ERR_ARG, "null argument");
+    MapSource P;
+    P.xyz = xyz;
+    P.n = n;
+    P.mem = mem;
+    P.sorted = in_sorted != 0;
+    // host coordinates must outlive the asynchronous forward: stage them on device
+    DevBuf staged;
+    if (mem == SCONV_MEM_HOST && n > 0) {
+      staged.alloc(sizeof(int32_t) * 3 * n, ctx->stream);
+      SCONV_CUDA(cudaMemcpyAsync(staged.get(), xyz, sizeof(int32_t) * 3 * n, cudaMemcpyHostToDevice, ctx->stream));
+      net->input_xyz = std::move(staged);
+      P.xyz = net->input_xyz.get<int32_t>();
+      P.mem = SCONV_MEM_DEVICE;
+    }
+    net->forward(*ctx, P, feats, SCONV_F32, f_mem, c_in);
+  });
+}
+
+sconv_status sconv_net_tensor_info(sconv_ctx* ctx, const sconv_net* net, int tensor, int64_t* n, int* channels,
+                                   int* coordset) {
+  return guarded(ctx, [&] {
+    if (!net || tensor < 0 || tensor >= static_cast<int>(net->tensors.size())) fail(SCONV_ERR_ARG, "bad tensor");
+    const NetTensor& t = net->tensors[tensor];
+    if (n) *n = t.n;
+    if (channels) *channels = t.channels;
+    if (coordset) *coordset = t.coordset;
+  });
+}
+
+sconv_status sconv_net_read_tensor(sconv_ctx* ctx, const sconv_net* net, int tensor, int32_t* xyz, float* feats) {
+  return guarded(ctx, [&] {
+    if (!net || tensor < 0 || tensor >= static_cast<int>(net->tensors.size())) fail(SCONV_ERR_ARG, "bad tensor");
+    const NetTensor& t = net->tensors[tensor];
+    if (t.coordset < 0) fail(SCONV_ERR_STATE, "tensor not produced");
+    if (feats && t.n > 0)
+      SCONV_CUDA(cudaMemcpyAsync(feats, t.feats.get(), sizeof(float) * t.n * t.channels, cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+    if (xyz && t.n > 0) {
+      const CoordSet& cs = net->coordsets[t.coordset];
+      if (cs.keys) {
+        std::vector<uint64_t> keys(t.n);
+        SCONV_CUDA(cudaMemcpyAsync(keys.data(), cs.keys->get(), 8 * t.n, cudaMemcpyDeviceToHost, ctx->stream));
+        ctx->sync();
+        for (int64_t i = 0; i < t.n; ++i) unpack_key(keys[i], xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2]);
+      } else {
+        SCONV_CUDA(cudaMemcpyAsync(xyz, net->raw_input.xyz, 12 * t.n, cudaMemcpyDeviceToHost, ctx->stream));
+      }
+    }
+    ctx->sync();
+  });
+}
+
+sconv_status sconv_net_tensor_device(const sconv_net* net, int tensor, const float** feats) {
+  if (!net || tensor < 0 || tensor >= static_cast<int>(net->tensors.size()) || !feats) return SCONV_ERR_ARG;
+  *feats = net->tensors[tensor].feats.get<float>();
+  return SCONV_OK;
+}
+
+sconv_status sconv_net_stats(const sconv_net* net, int* maps_built, int* convs) {
+  if (!net) return SCONV_ERR_ARG;
+  if (maps_built) *maps_built = net->maps_built;
+  if (convs) {
+    int c = 0;
+    for (const auto& o : net->ops) c += o.kind == kOpConv;
+    *convs = c;
+  }
+  return SCONV_OK;
+}
+
+void sconv_net_free(sconv_ctx* ctx, sconv_net* net) {
+  if (ctx) cudaStreamSynchronize(ctx->stream);
+  delete net;
 }
 
 sconv_status sconv_generate_synthetic(int64_t N, int64_t E, int64_t C, uint64_t seed, int32_t* xyz, float* feats) {

@@ -84,10 +84,26 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
 
 constexpr int kGemmThreads = 192;
 
+// tile t -> {first buffer row, rows, offset k, first output channel}
+__device__ __forceinline__ int4 decode_tile(const LayerPlan& p, int t) {
+  int lo = 0, hi = p.nm - 1;  // last member with tile_start <= t
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (p.tile_start[mid] <= t)
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  const int4 mb = p.members[lo];
+  const int local = t - p.tile_start[lo];
+  const int rb = local / p.n_blocks, nbk = local - rb * p.n_blocks;
+  return make_int4(mb.y + rb * 128, min(128, mb.w - rb * 128), mb.x, nbk * p.block_n);
+}
+
 template <int KC>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_gemm_grouped(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const int4* __restrict__ tiles, int num_tiles, int num_kb, int block_n, int n_pad, int c_out,
+                   const __grid_constant__ LayerPlan plan, int num_tiles, int num_kb, int block_n, int n_pad, int c_out,
                    float* __restrict__ out, int stages, uint32_t idesc_base, uint32_t tmem_cols) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t{1023});
@@ -130,7 +146,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        const int4 td = tiles[t];
+        const int4 td = decode_tile(plan, t);
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1u);
           uint8_t* sa = smem + stage * stage_bytes;
@@ -149,7 +165,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       int stage = 0, acc = 0;
       uint32_t phase = 0, acc_phase = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        const int4 td = tiles[t];
+        const int4 td = decode_tile(plan, t);
         const int n_tile = min(block_n, n_pad - td.w);
         const uint32_t idesc = idesc_base | (static_cast<uint32_t>(n_tile >> 3) << 17);
         mbar_wait(&tempty[acc], acc_phase ^ 1u);
@@ -182,7 +198,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     uint32_t acc_phase = 0;
     const bool vec4 = (c_out & 3) == 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-      const int4 td = tiles[t];
+      const int4 td = decode_tile(plan, t);
       const int n_tile = min(block_n, n_pad - td.w);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
@@ -282,7 +298,7 @@ void launch_kc(Ctx& ctx, const GemmArgs& a) {
   const uint32_t fmt = a.dtype == SCONV_BF16 ? 1u : 0u;
   const uint32_t idesc_base = (1u << 4) | (fmt << 7) | (fmt << 10) | ((128u >> 4) << 24);
   ctx.launch("k_gemm_grouped", [&] {
-    kern<<<grid, kGemmThreads, smem, ctx.stream>>>(tA, tB, a.tiles, a.num_tiles, a.num_kb, block_n, a.n_pad, a.c_out,
+    kern<<<grid, kGemmThreads, smem, ctx.stream>>>(tA, tB, *a.plan, a.num_tiles, a.num_kb, block_n, a.n_pad, a.c_out,
                                                    a.out, stages, idesc_base, cols);
   });
 }

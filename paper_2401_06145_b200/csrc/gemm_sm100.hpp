@@ -2,13 +2,14 @@
 #pragma once
 
 #include "ctx.hpp"
+#include "gmas.hpp"
 
 namespace sconvb {
 
 struct GemmArgs {
   const void* a = nullptr;   // gather buffer [rows x k_pad], f16/bf16
   const void* b = nullptr;   // weights [num_offsets * n_pad x k_pad], K-major
-  const int4* tiles = nullptr;  // device tile list {row0, nrows, k, n0}
+  const LayerPlan* plan = nullptr;  // tiles decoded from the member table (kernel parameter)
   int num_tiles = 0;
   int64_t rows = 0;
   int k_pad = 0, num_kb = 0;

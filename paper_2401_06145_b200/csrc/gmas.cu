@@ -88,12 +88,14 @@ struct Cvt<float> {
 // k_gather: slot s -> member (binary search over row0 in shared memory) -> canonical
 // pair m = map_start[k] + r -> input row j = pair_in[m].
 template <int T, class TIn, class TOp>
-__global__ void __launch_bounds__(256) k_gather(const TIn* __restrict__ f_in, int c_in, const int4* __restrict__ members,
-                                                int num_members, const int32_t* __restrict__ map_start,
+__global__ void __launch_bounds__(256) k_gather(const TIn* __restrict__ f_in, int c_in,
+                                                const __grid_constant__ LayerPlan plan,
+                                                const int32_t* __restrict__ map_start,
                                                 const int32_t* __restrict__ pair_in, int64_t rows, int k_pad,
                                                 TOp* __restrict__ buf) {
   __shared__ int4 s_mem[kMaxOffsets];
-  for (int t = threadIdx.x; t < num_members; t += blockDim.x) s_mem[t] = members[t];
+  const int num_members = plan.nm;
+  for (int t = threadIdx.x; t < num_members; t += blockDim.x) s_mem[t] = plan.members[t];
   __syncthreads();
   const int tiles = c_in / T;
   const int64_t gid = blockIdx.x * int64_t{blockDim.x} + threadIdx.x;
@@ -165,9 +167,10 @@ __global__ void __launch_bounds__(256) k_gather(const TIn* __restrict__ f_in, in
 template <int T, class TOut>
 __global__ void __launch_bounds__(256) k_scatter(const float* __restrict__ gemm_out, int c_out,
                                                  const int32_t* __restrict__ nbr_pos, int64_t n_out, int K3,
-                                                 const int32_t* __restrict__ delta, TOut* __restrict__ f_out) {
+                                                 const __grid_constant__ LayerPlan plan, TOut* __restrict__ f_out,
+                                                 int relu) {
   __shared__ int32_t s_delta[kMaxOffsets];
-  for (int t = threadIdx.x; t < K3; t += blockDim.x) s_delta[t] = delta[t];
+  for (int t = threadIdx.x; t < K3; t += blockDim.x) s_delta[t] = plan.delta[t];
   __syncthreads();
   const int tiles = c_out / T;
   const int64_t gid = blockIdx.x * int64_t{blockDim.x} + threadIdx.x;
@@ -202,6 +205,9 @@ __global__ void __launch_bounds__(256) k_scatter(const float* __restrict__ gemm_
       }
     }
   }
+  if (relu)
+#pragma unroll
+    for (int e = 0; e < T; ++e) acc[e] = fmaxf(acc[e], 0.f);  // fused ReLU epilogue (network driver)
   TOut* dst = f_out + i * c_out + t * T;
   if constexpr (std::is_same<TOut, float>::value && T % 4 == 0) {
 #pragma unroll
@@ -216,13 +222,13 @@ constexpr int kBlock = 256;
 inline unsigned blocks_for(int64_t n) { return static_cast<unsigned>(std::max<int64_t>(1, ceil_div<int64_t>(n, kBlock))); }
 
 template <class TIn, class TOp>
-void gather_dispatch(Ctx& ctx, int T, const void* f_in, int c_in, const int4* members, int nm, const int32_t* starts,
+void gather_dispatch(Ctx& ctx, int T, const void* f_in, int c_in, const LayerPlan& plan, const int32_t* starts,
                      const int32_t* pair_in, int64_t rows, int k_pad, void* buf) {
   const int64_t work = rows * (c_in / T);
   auto go = [&](auto kern) {
     ctx.launch("k_gather", [&] {
-      kern<<<blocks_for(work), kBlock, 0, ctx.stream>>>(static_cast<const TIn*>(f_in), c_in, members, nm, starts,
-                                                        pair_in, rows, k_pad, static_cast<TOp*>(buf));
+      kern<<<blocks_for(work), kBlock, 0, ctx.stream>>>(static_cast<const TIn*>(f_in), c_in, plan, starts, pair_in,
+                                                        rows, k_pad, static_cast<TOp*>(buf));
     });
   };
   switch (T) {
@@ -244,12 +250,12 @@ void gather_dispatch(Ctx& ctx, int T, const void* f_in, int c_in, const int4* me
 
 template <class TOut>
 void scatter_dispatch(Ctx& ctx, int T, const float* gemm_out, int c_out, const int32_t* nbr, int64_t n_out, int K3,
-                      const int32_t* delta, void* f_out) {
+                      const LayerPlan& plan, void* f_out, int relu) {
   const int64_t work = n_out * (c_out / T);
   auto go = [&](auto kern) {
     ctx.launch("k_scatter", [&] {
-      kern<<<blocks_for(work), kBlock, 0, ctx.stream>>>(gemm_out, c_out, nbr, n_out, K3, delta,
-                                                        static_cast<TOut*>(f_out));
+      kern<<<blocks_for(work), kBlock, 0, ctx.stream>>>(gemm_out, c_out, nbr, n_out, K3, plan,
+                                                        static_cast<TOut*>(f_out), relu);
     });
   };
   switch (T) {
@@ -341,7 +347,7 @@ std::unique_ptr<WeightData> create_weights(Ctx& ctx, const float* w, int mem, in
 
 // ---------------------------------------------------------------- layer forward
 void layer_forward(Ctx& ctx, MapData& m, const WeightData& w, const void* f_in, int f_in_dtype, int f_in_mem,
-                   const sconv_exec_cfg& cfg, void* f_out, int f_out_dtype, int f_out_mem) {
+                   const sconv_exec_cfg& cfg, void* f_out, int f_out_dtype, int f_out_mem, int relu) {
   if (w.K3 != m.K3) fail(SCONV_ERR_ARG, "weight count does not match the kernel volume");
   if (f_in_dtype != SCONV_F32 && f_in_dtype != SCONV_F16 && f_in_dtype != SCONV_BF16)
     fail(SCONV_ERR_ARG, "unsupported input dtype");
@@ -385,55 +391,44 @@ void layer_forward(Ctx& ctx, MapData& m, const WeightData& w, const void* f_in, 
   if (m.n_out > 0 && (R == 0 || m.n_in == 0)) {
     SCONV_CUDA(cudaMemsetAsync(fout, 0, out_bytes, st));
   } else if (m.n_out > 0) {
-    // ---- plan tables -> device (members, GEMM tiles, scatter deltas)
-    std::vector<int4> members;
+    // ---- plan (members in buffer order, GEMM tile prefix, scatter deltas): a kernel
+    // parameter, so consecutive layers never race on a staging buffer.
+    if (plan.order.size() > static_cast<size_t>(kMaxOffsets)) fail(SCONV_ERR_ARG, "too many offsets");
+    auto lp = std::make_unique<LayerPlan>();
+    const int block_n = std::min(w.n_pad, 256);
+    lp->block_n = block_n;
+    lp->n_blocks = ceil_div(w.n_pad, block_n);
+    lp->nm = 0;
+    lp->tile_start[0] = 0;
     for (const auto& g : plan.groups)
       for (int q = g.begin; q < g.end; ++q) {
         const int k = plan.order[q];
-        members.push_back(make_int4(k, static_cast<int>(plan.buffer_offsets[k]), static_cast<int>(m.sizes[k]),
-                                    static_cast<int>(g.height)));
+        lp->members[lp->nm] = make_int4(k, static_cast<int>(plan.buffer_offsets[k]), static_cast<int>(m.sizes[k]),
+                                        static_cast<int>(g.height));
+        lp->tile_start[lp->nm + 1] = lp->tile_start[lp->nm] + ceil_div(static_cast<int>(g.height), 128) * lp->n_blocks;
+        ++lp->nm;
       }
-    const int block_n = std::min(w.n_pad, 256);
-    std::vector<int4> tiles;
-    for (const auto& mb : members)
-      for (int r0 = 0; r0 < mb.w; r0 += 128)
-        for (int n0 = 0; n0 < w.n_pad; n0 += block_n)
-          tiles.push_back(make_int4(mb.y + r0, std::min(128, mb.w - r0), mb.x, n0));
-    std::vector<int32_t> delta(K3, 0);
+    lp->num_tiles = lp->tile_start[lp->nm];
     for (int k = 0; k < K3; ++k)
-      if (plan.buffer_offsets[k] >= 0) delta[k] = static_cast<int32_t>(plan.buffer_offsets[k] - m.starts[k]);
-    const size_t bytes_members = members.size() * sizeof(int4), bytes_tiles = tiles.size() * sizeof(int4),
-                 bytes_delta = delta.size() * sizeof(int32_t);
-    const size_t total = bytes_members + bytes_tiles + bytes_delta;
-    if (total > Ctx::kPinPlanBytes) fail(SCONV_ERR_ARG, "layer plan too large");
-    auto* pin = static_cast<unsigned char*>(ctx.pin_plan());
-    std::memcpy(pin, members.data(), bytes_members);
-    std::memcpy(pin + bytes_members, tiles.data(), bytes_tiles);
-    std::memcpy(pin + bytes_members + bytes_tiles, delta.data(), bytes_delta);
-    ctx.plan_dev.reserve(total, st);
-    SCONV_CUDA(cudaMemcpyAsync(ctx.plan_dev.get(), pin, total, cudaMemcpyHostToDevice, st));
-    const auto* d_members = reinterpret_cast<const int4*>(ctx.plan_dev.get<unsigned char>());
-    const auto* d_tiles = reinterpret_cast<const int4*>(ctx.plan_dev.get<unsigned char>() + bytes_members);
-    const auto* d_delta = reinterpret_cast<const int32_t*>(ctx.plan_dev.get<unsigned char>() + bytes_members + bytes_tiles);
+      lp->delta[k] = plan.buffer_offsets[k] >= 0 ? static_cast<int32_t>(plan.buffer_offsets[k] - m.starts[k]) : 0;
 
     // ---- gather
     const int k_pad = w.k_pad;
     ctx.gather_buf.reserve(static_cast<size_t>(R) * k_pad * 2, st);
     if (k_pad != c_in) SCONV_CUDA(cudaMemsetAsync(ctx.gather_buf.get(), 0, static_cast<size_t>(R) * k_pad * 2, st));
-    const int nm = static_cast<int>(members.size());
     const int32_t* starts = m.map_start.get<int32_t>();
     const int32_t* pin_idx = m.pair_in.get<int32_t>();
     if (w.dtype == SCONV_F16) {
       if (f_in_dtype == SCONV_F32)
-        gather_dispatch<float, __half>(ctx, Tg, fin, c_in, d_members, nm, starts, pin_idx, R, k_pad, ctx.gather_buf.get());
+        gather_dispatch<float, __half>(ctx, Tg, fin, c_in, *lp, starts, pin_idx, R, k_pad, ctx.gather_buf.get());
       else
-        gather_dispatch<__half, __half>(ctx, Tg, fin, c_in, d_members, nm, starts, pin_idx, R, k_pad, ctx.gather_buf.get());
+        gather_dispatch<__half, __half>(ctx, Tg, fin, c_in, *lp, starts, pin_idx, R, k_pad, ctx.gather_buf.get());
     } else {
       if (f_in_dtype == SCONV_F32)
-        gather_dispatch<float, __nv_bfloat16>(ctx, Tg, fin, c_in, d_members, nm, starts, pin_idx, R, k_pad,
+        gather_dispatch<float, __nv_bfloat16>(ctx, Tg, fin, c_in, *lp, starts, pin_idx, R, k_pad,
                                               ctx.gather_buf.get());
       else
-        gather_dispatch<__nv_bfloat16, __nv_bfloat16>(ctx, Tg, fin, c_in, d_members, nm, starts, pin_idx, R, k_pad,
+        gather_dispatch<__nv_bfloat16, __nv_bfloat16>(ctx, Tg, fin, c_in, *lp, starts, pin_idx, R, k_pad,
                                                       ctx.gather_buf.get());
     }
     // ---- grouped GEMM
@@ -441,8 +436,8 @@ void layer_forward(Ctx& ctx, MapData& m, const WeightData& w, const void* f_in, 
     GemmArgs ga;
     ga.a = ctx.gather_buf.get();
     ga.b = w.buf.get();
-    ga.tiles = d_tiles;
-    ga.num_tiles = static_cast<int>(tiles.size());
+    ga.plan = lp.get();
+    ga.num_tiles = lp->num_tiles;
     ga.rows = R;
     ga.k_pad = k_pad;
     ga.num_kb = k_pad / gemm_chunk(k_pad);
@@ -456,11 +451,11 @@ void layer_forward(Ctx& ctx, MapData& m, const WeightData& w, const void* f_in, 
     // ---- scatter
     const int32_t* nbr = m.nbr_pos.get<int32_t>();
     if (f_out_dtype == SCONV_F32)
-      scatter_dispatch<float>(ctx, Ts, ctx.gemm_out.get<float>(), c_out, nbr, m.n_out, K3, d_delta, fout);
+      scatter_dispatch<float>(ctx, Ts, ctx.gemm_out.get<float>(), c_out, nbr, m.n_out, K3, *lp, fout, relu);
     else if (f_out_dtype == SCONV_F16)
-      scatter_dispatch<__half>(ctx, Ts, ctx.gemm_out.get<float>(), c_out, nbr, m.n_out, K3, d_delta, fout);
+      scatter_dispatch<__half>(ctx, Ts, ctx.gemm_out.get<float>(), c_out, nbr, m.n_out, K3, *lp, fout, relu);
     else
-      scatter_dispatch<__nv_bfloat16>(ctx, Ts, ctx.gemm_out.get<float>(), c_out, nbr, m.n_out, K3, d_delta, fout);
+      scatter_dispatch<__nv_bfloat16>(ctx, Ts, ctx.gemm_out.get<float>(), c_out, nbr, m.n_out, K3, *lp, fout, relu);
   }
   if (f_out_mem == SCONV_MEM_HOST && m.n_out > 0) {
     SCONV_CUDA(cudaMemcpyAsync(f_out, fout, out_bytes, cudaMemcpyDeviceToHost, st));

@@ -10,6 +10,18 @@ namespace sconvb {
 
 constexpr int kMaxOffsets = 512;  // K <= 8
 
+// Per-layer GMaS plan, passed BY VALUE as a kernel parameter (CUDA >= 12.1 allows 32 KB of
+// parameters), so no host->device copy (and no pinned staging) is needed between layers.
+struct LayerPlan {
+  int nm;         // group members in buffer order
+  int num_tiles;  // GEMM tiles = sum over members of ceil(height / 128) * n_blocks
+  int n_blocks;   // output-channel blocks per row block
+  int block_n;
+  int4 members[kMaxOffsets];         // {offset k, first buffer row, n_k, padded height}
+  int tile_start[kMaxOffsets + 1];   // tile prefix per member
+  int delta[kMaxOffsets];            // scatter: buffer slot = canonical position + delta[k]
+};
+
 struct MapData;
 
 // GemmGroupPlan: order = chosen offset order without empty offsets.
@@ -40,7 +52,7 @@ int default_tile(int channels, bool gather);
 int padded_k(int c_in);
 
 void layer_forward(Ctx& ctx, MapData& m, const WeightData& w, const void* f_in, int f_in_dtype, int f_in_mem,
-                   const sconv_exec_cfg& cfg, void* f_out, int f_out_dtype, int f_out_mem);
+                   const sconv_exec_cfg& cfg, void* f_out, int f_out_dtype, int f_out_mem, int relu = 0);
 
 }  // namespace sconvb
 

@@ -1,0 +1,63 @@
+// Network driver types (net.cu).
+#pragma once
+
+#include <map>
+#include <memory>
+#include <tuple>
+#include <vector>
+
+#include "gmas.hpp"
+#include "map.hpp"
+
+namespace sconvb {
+
+enum { kOpConv = 1, kOpAdd = 2, kOpConcat = 3 };
+constexpr int kOpFields = 12;
+
+// Op record (12 int32 fields on the ABI): kind, out, in, b (second operand) | target,
+// K, offset_scale, out_stride, transposed, c_in, c_out, weight id, relu.
+struct NetOp {
+  int kind = 0, out = 0, in = 0, b = -1, target = -1;
+  int K = 3, offset_scale = 1, out_stride = 1, transposed = 0, c_in = 0, c_out = 0, weight = -1, relu = 0;
+};
+
+struct NetTensor {
+  int coordset = -1;
+  int64_t n = 0;
+  int channels = 0;
+  DevBuf feats;  // fp32 [n][channels], rows in the coordinate set's order
+};
+
+struct CoordSet {
+  std::shared_ptr<DevBuf> keys;  // sorted packed keys (null: raw input not yet packed)
+  int64_t n = 0;
+  bool sorted = true;
+  bool raw = false;
+};
+
+using MapKey = std::tuple<int, int, int, int, int, int>;
+struct MapEntry {
+  std::unique_ptr<MapData> map;
+  int out_cs = -1;
+};
+
+struct NetData {
+  std::vector<NetOp> ops;
+  int num_tensors = 0, input_tensor = 0, output_tensor = 0;
+  int block_B = 256, block_C = 512;
+  sconv_exec_cfg cfg{};
+  std::map<int, std::unique_ptr<WeightData>> weights;
+  std::vector<NetTensor> tensors;
+  std::vector<CoordSet> coordsets;
+  std::map<MapKey, MapEntry> maps;
+  MapSource raw_input;
+  DevBuf input_xyz;  // device copy of host input coordinates
+  int maps_built = 0;
+
+  void check_ops() const;
+  void forward(Ctx& ctx, const MapSource& input, const void* feats, int f_dtype, int f_mem, int c_in);
+};
+
+}  // namespace sconvb
+
+struct sconv_net : sconvb::NetData {};

@@ -99,6 +99,14 @@ SIGNATURES = [
                                     C.POINTER(_I64), _P]),
     ("sconv_plan_groups", _I, [_P, _I, _I, _D, _I, _P, C.POINTER(_I), _P, _P, _P, C.POINTER(_I), _P,
                                C.POINTER(_I64), C.POINTER(_D)]),
+    ("sconv_net_create", _I, [_P, _P, _I, _I, _I, _I, C.POINTER(ExecCfg), _I, _I, C.POINTER(_P)]),
+    ("sconv_net_set_weights", _I, [_P, _P, _I, _P, _I, _I, _I, _I]),
+    ("sconv_net_forward", _I, [_P, _P, _P, _I64, _I, _I, _P, _I, _I]),
+    ("sconv_net_tensor_info", _I, [_P, _P, _I, C.POINTER(_I64), C.POINTER(_I), C.POINTER(_I)]),
+    ("sconv_net_read_tensor", _I, [_P, _P, _I, _P, _P]),
+    ("sconv_net_tensor_device", _I, [_P, _I, C.POINTER(_P)]),
+    ("sconv_net_stats", _I, [_P, C.POINTER(_I), C.POINTER(_I)]),
+    ("sconv_net_free", None, [_P, _P]),
     ("sconv_generate_synthetic", _I, [_I64, _I64, _I64, _U64, _P, _P]),
     ("sconv_generate_weights", _I, [_U64, _U64, _I, _I, _I, _P]),
     ("sconv_global_last_error", C.c_char_p, []),
