@@ -1,24 +1,32 @@
 #!/usr/bin/env python3
 """Benchmark driver (contract: one JSON line on rank 0).
 
-Workload (default): BASELINE.json configs[0], the single submanifold 3x3x3 SC layer,
-C_in = C_out = 32, 100k synthetic voxels uniform in 400^3 (generate_synthetic seed 1,
-weights stream 1). A step = Map (pack, sort, backward/forward search) + GMaS (gather,
-tcgen05 grouped GEMM, scatter) on device-resident inputs. Inputs (12.8 MB) are smaller
-than L2, so L2 is flushed (256 MB memset) between timed steps, outside the events.
+metric (BASELINE.json): "SC layer latency (Map + GMaS, ms) and end-to-end network points/sec".
+value = input voxels processed per second by the whole job (higher is better);
+ms_per_step = latency of one step. Workloads (BASELINE.json configs):
 
-metric/unit: input voxels processed per second through the layer (higher is better);
-ms_per_step is the SC-layer latency. Multi-GPU: every rank runs its own scene
-(seed 1 + rank), no data-path collective (scene sharding) -> weak scaling.
+  c2_minkunet42_kitti  (default, configs[1]) MinkUNet42 forward on a synthetic KITTI-shaped
+                       scan (~120k voxels at 5 cm, 4 channels); step = Map for every distinct
+                       geometry + GMaS for all 49 convs (42 SC + 7 1x1) + residual/concat ops
+  c1_layer_100k        (configs[0]) one submanifold 3^3 layer, 32->32, 100k voxels in 400^3
+  c3_resnet21d_s3dis   (configs[2]) SparseResNet21D (width x2) on an S3DIS-shaped room
+  c4_unet_pair_shapenet (configs[3]) K=2 s=2 down + transposed pair on ShapeNet-shaped objects
 
---impl reference: the CPU oracle (oracle/liboracle.so, a port of the reference SPEC's
-Map/GMaS on top of a restatement of its geometry.hpp) on all host threads, same config.
+Multi-GPU (configs[4] shape): one process per GPU, each rank runs its OWN scene
+(scene seed = base + rank): scene sharding with no data-path collective -> weak scaling;
+NCCL is used for the barrier and the max-over-ranks timing only.
+
+Inputs are device resident before the timed region; L2 (126 MB) is flushed by a 256 MB
+memset between timed steps, outside the events. Timing: CUDA events per step on the
+launching stream, summed, max over ranks.
+
+--impl reference: the CPU oracle (oracle/liboracle.so — the restatement of the reference
+SPEC's Map/GMaS on its geometry) on all host threads, same workload, bounded sample.
 """
 import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -29,19 +37,17 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "SC layer latency (Map + GMaS, ms) and end-to-end network points/sec"
-WORKLOADS = {
-    "c1_submanifold_k3_32x32_100k": dict(N=100000, E=400, C_in=32, C_out=32, K=3, s=1, seed=1),
-}
-DEFAULT_WORKLOAD = "c1_submanifold_k3_32x32_100k"
+DEFAULT_WORKLOAD = "c2_minkunet42_kitti"
 
 
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=50)
+    p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(WORKLOADS))
+    p.add_argument("--workload", default=DEFAULT_WORKLOAD,
+                   choices=["c2_minkunet42_kitti", "c1_layer_100k", "c3_resnet21d_s3dis", "c4_unet_pair_shapenet"])
     p.add_argument("--dtype", default="f16", choices=["f16", "bf16"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--B", type=int, default=256, help="source block size (SPEC default 256)")
@@ -59,7 +65,6 @@ def load_peaks():
 
 
 def load_traffic():
-    """Per-launch DRAM bytes of each kernel from the committed ncu --set full capture."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             return json.load(f)
@@ -84,12 +89,7 @@ class ClockSampler:
 
     def _run(self):
         nv = self.nv
-        names = {
-            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
-            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
-            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
-            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
-        }
+        names = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40, "sw_power_cap": 0x4}
         while not self.stop_ev.is_set():
             try:
                 self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
@@ -117,51 +117,202 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-# ---------------------------------------------------------------- CPU oracle leg
-def cpu_run(wl, reps, workers):
-    sys.path.insert(0, os.path.join(ROOT, "tests"))
-    from oracle_lib import load_oracle  # CPU baseline only (test infrastructure)
-    o = load_oracle()
-    xyz, F = o.generate_synthetic(wl["N"], wl["E"], wl["C_in"], wl["seed"])
-    K3 = wl["K"] ** 3
-    W = o.generate_weights(wl["seed"], 1, K3, wl["C_in"], wl["C_out"])
-    times = []
-    for _ in range(reps):
-        t0 = time.perf_counter()
-        o.layer_forward(xyz, False, F, W, wl["K"], wl["s"], wl["s"], workers=workers)
-        times.append(time.perf_counter() - t0)
-    return times
+# ---------------------------------------------------------------- workloads
+def scene(name, seed):
+    from paper_2401_06145_b200 import datasets as D
+    if name == "c2_minkunet42_kitti":
+        return D.kitti_scan(seed)
+    if name == "c3_resnet21d_s3dis":
+        return D.s3dis_room(seed, n_points=870_000)
+    if name == "c4_unet_pair_shapenet":
+        return D.shapenet_object(seed)
+    raise ValueError(name)
 
 
-def reference_arm(args, wl):
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return  # rank 0 alone runs the CPU reference
+def graph(name):
+    from paper_2401_06145_b200 import network as N
+    return {"c2_minkunet42_kitti": N.minkunet42, "c3_resnet21d_s3dis": N.sparse_resnet21d,
+            "c4_unet_pair_shapenet": N.unet_pair}[name]()
+
+
+def oracle_crop(c, f, n):
+    """The n voxels closest to the scene's median point (a bounded CPU sample)."""
+    ctr = np.median(c, axis=0)
+    idx = np.sort(np.argsort(np.linalg.norm((c - ctr).astype(np.float64), axis=1), kind="stable")[:n])
+    return c[idx], f[idx]
+
+
+class NetWorkload:
+    """A whole network forward per step; C4 runs a batch of objects (one after another)."""
+
+    def __init__(self, name, ctx, torch, seed, dtype, B, C):
+        import paper_2401_06145_b200 as sc
+        from paper_2401_06145_b200 import network as N
+        self.name, self.sc = name, sc
+        self.g = graph(name)
+        self.w = N.init_weights(self.g, 1)
+        self.net = N.Network(ctx, self.g, self.w, sc.exec_cfg(compute_dtype=dtype), B, C)
+        n_obj = 8 if name == "c4_unet_pair_shapenet" else 1
+        self.scenes = [scene(name, seed * 100 + i) for i in range(n_obj)]
+        self.dev = [(torch.from_numpy(c).cuda(), torch.from_numpy(f).cuda()) for c, f in self.scenes]
+        self.points = sum(len(c) for c, _ in self.scenes)
+        self.config = {"model": {"c2_minkunet42_kitti": "MinkUNet42", "c3_resnet21d_s3dis": "SparseResNet21D-w2",
+                                 "c4_unet_pair_shapenet": "UNetPair(K2s2 down+transposed)"}[name],
+                       "scenes_per_step": n_obj, "voxels_per_step": self.points,
+                       "convs": len(self.g.convs()), "in_channels": self.g.in_channels}
+
+    def step(self):
+        for xyz, f in self.dev:
+            self.net.forward(device_xyz=xyz.data_ptr(), device_feats=f.data_ptr(), n=xyz.shape[0], sorted_=True)
+
+    def e2e_step(self):
+        h2d = d2h = 0
+        for c, f in self.scenes:
+            self.net.forward(c, f, True)
+            _, out = self.net.read(self.g.output)
+            h2d += c.nbytes + f.nbytes
+            d2h += out.nbytes
+        return h2d, d2h
+
+    def extra(self):
+        return {"maps_built_per_scene": self.net.stats()["maps_built"]}
+
+    def algo_bytes(self):
+        """Per launch, averaged over the network's convs (the roofline divides by the average
+        launch duration of the dominant kernel type)."""
+        tot = self.net.algo_bytes()
+        nconv = len(self.g.convs()) * len(self.scenes)
+        return {k: v * len(self.scenes) / nconv for k, v in tot.items()}
+
+    def cpu_sample(self, workers, budget_s=20.0):
+        """Oracle network on a crop of scene 0, grown until ~budget_s/3 of CPU work."""
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        from test_gpu_network import oracle_graph  # the oracle graph runner (test infrastructure)
+        c, f = self.scenes[0]
+        n = min(len(c), 5000)
+        while True:
+            cc, ff = oracle_crop(c, f, n)
+            t0 = time.perf_counter()
+            oracle_graph(self.g, self.w, cc, ff)
+            dt = time.perf_counter() - t0
+            if dt > budget_s / 3 or n >= len(c):
+                return n / dt, f"oracle {self.config['model']} on a {n}-voxel crop of scene 0 ({dt:.1f}s)"
+            n = min(len(c), int(n * min(4.0, max(1.5, budget_s / 3 / max(dt, 1e-3)))))
+
+
+class LayerWorkload:
+    def __init__(self, name, ctx, torch, seed, dtype, B, C):
+        import paper_2401_06145_b200 as sc
+        self.name, self.sc, self.ctx, self.dtype, self.B, self.C = name, sc, ctx, dtype, B, C
+        self.N, self.E, self.c = 100000, 400, 32
+        self.xyz, self.F = sc.generate_synthetic(self.N, self.E, self.c, seed)
+        self.W = sc.generate_weights(1, 1, 27, self.c, self.c)
+        self.w = sc.Weights(ctx, self.W, dtype)
+        self.xyz_d, self.F_d = torch.from_numpy(self.xyz).cuda(), torch.from_numpy(self.F).cuda()
+        self.out_d = torch.empty((self.N, self.c), dtype=torch.float32, device="cuda")
+        self.points = self.N
+        m = self._map()
+        self.tg, self.ts, _ = sc.tune_layer(ctx, m, self.w, self.F_d.data_ptr(), sc.F32, rounds=5)
+        self.cfg = sc.exec_cfg(compute_dtype=dtype, gather_tile=self.tg, scatter_tile=self.ts)
+        sc.layer_forward_device(ctx, m, self.w, self.F_d.data_ptr(), sc.F32, self.out_d.data_ptr(), sc.F32, self.cfg)
+        self.info = m.info()
+        m.free()
+        self.config = {"model": "single SC layer K=3 s=1", "N": self.N, "E": self.E, "C_in": self.c,
+                       "C_out": self.c, "gather_tile": self.tg, "scatter_tile": self.ts,
+                       "matches": self.info.total_matches, "buffer_length": self.info.buffer_length,
+                       "groups": self.info.groups, "padding_overhead": self.info.padding_overhead}
+
+    def _map(self):
+        return self.sc.KernelMap.build(self.ctx, None, False, 3, 1, 1, device_ptr=self.xyz_d.data_ptr(), n=self.N,
+                                       B=self.B, Cq=self.C)
+
+    def step(self):
+        m = self._map()
+        self.sc.layer_forward_device(self.ctx, m, self.w, self.F_d.data_ptr(), self.sc.F32, self.out_d.data_ptr(),
+                                     self.sc.F32, self.cfg)
+        m.free()
+
+    def e2e_step(self):
+        out = self.sc.sc_layer_forward(self.ctx, self.sc.PointCloud(self.xyz, self.F, False), self.W, 3, 1, self.cfg)
+        return self.xyz.nbytes + self.F.nbytes + self.W.nbytes, out.coords.nbytes + out.features.nbytes
+
+    def extra(self):
+        return {}
+
+    def algo_bytes(self):  # per launch (SURVEY §8d with this path's dtypes)
+        i, N, c, K3 = self.info, self.N, self.c, 27
+        M, R, nq = i.total_matches, i.buffer_length, i.num_outputs
+        return {"k_search": 8 * N + 8 * nq + 12 * K3, "k_emit": 8 * M + 4 * K3 * nq,
+                "k_gather": 4 * c * N + 2 * c * R + 4 * M, "k_gemm_grouped": 2 * c * R + 4 * c * R + 2 * K3 * c * c,
+                "k_scatter": 4 * c * M + 4 * K3 * nq + 4 * c * nq, "k_bucket_rank": 8 * N + 12 * N,
+                "k_bucket_scatter": 16 * N, "k_pack_compact": 20 * N, "k_bbox": 12 * N}
+
+    def cpu_sample(self, workers, budget_s=20.0):
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        from oracle_lib import load_oracle  # CPU baseline only (test infrastructure)
+        o = load_oracle()
+        times = []
+        while sum(times) < budget_s / 2 and len(times) < 5:
+            t0 = time.perf_counter()
+            o.layer_forward(self.xyz, False, self.F, self.W, 3, 1, 1, workers=workers)
+            times.append(time.perf_counter() - t0)
+        return self.N / statistics.median(times), f"{len(times)} full C1 layers on the oracle, median"
+
+
+def make_workload(args, ctx, torch, rank):
+    dtype = 1 if args.dtype == "f16" else 2
+    if args.workload == "c1_layer_100k":
+        return LayerWorkload(args.workload, ctx, torch, 1 + rank, dtype, args.B, args.C)
+    return NetWorkload(args.workload, ctx, torch, rank, dtype, args.B, args.C)
+
+
+# ---------------------------------------------------------------- reference arm (CPU oracle)
+def reference_arm(args):
+    if int(os.environ.get("RANK", "0")) != 0:
+        return
     workers = os.cpu_count() or 1
-    cpu_run(wl, max(0, args.warmup), workers) if args.warmup else None
-    times = cpu_run(wl, args.steps, workers)
-    total = sum(times)
-    pps = wl["N"] * len(times) / total
-    line = {
-        "metric": METRIC, "value": pps, "unit": "points/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64-acc", "data": "synthetic",
-        "config": {"workload": args.workload, **wl},
-        "impl": "reference",
-        "cpu_baseline": {"value": pps, "unit": "points/s", "cores": workers, "kind": "port",
-                         "sample": f"{args.steps} full C1 layers (Map+GMaS) on the oracle"},
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    if args.workload == "c1_layer_100k":
+        import paper_2401_06145_b200 as sc
+        from oracle_lib import load_oracle
+        o = load_oracle()
+        xyz, F = sc.generate_synthetic(100000, 400, 32, 1)
+        W = sc.generate_weights(1, 1, 27, 32, 32)
+        run = lambda: o.layer_forward(xyz, False, F, W, 3, 1, 1, workers=workers)  # noqa: E731
+        pts, sample = 100000, "full C1 layer per step"
+    else:
+        from paper_2401_06145_b200 import network as N
+        from test_gpu_network import oracle_graph
+        g = graph(args.workload)
+        w = N.init_weights(g, 1)
+        c, f = oracle_crop(*scene(args.workload, 0), 20000)
+        run = lambda: oracle_graph(g, w, c, f)  # noqa: E731
+        pts, sample = len(c), f"{len(c)}-voxel crop of scene 0 per step (the full scene is too slow on the CPU)"
+    for _ in range(min(args.warmup, 1)):
+        run()
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        run()
+        times.append(time.perf_counter() - t0)
+        if sum(times) > 120:
+            break
+    pps = pts * len(times) / sum(times)
+    print(json.dumps({
+        "metric": METRIC, "value": pps, "unit": "points/s", "n_gpus": args.gpus, "steps": len(times),
+        "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32 (fp64 accumulate)", "data": "synthetic",
+        "config": {"workload": args.workload}, "impl": "reference",
+        "cpu_baseline": {"value": pps, "unit": "points/s", "cores": workers, "kind": "port", "sample": sample},
         "e2e": {"value": pps, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line), flush=True)
+    }), flush=True)
 
 
 # ---------------------------------------------------------------- GPU arm
 def main():
     args = parse()
-    wl = WORKLOADS[args.workload]
     if args.impl == "reference":
-        return reference_arm(args, wl)
-
+        return reference_arm(args)
     import torch
     import paper_2401_06145_b200 as sc
 
@@ -173,52 +324,26 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-
     ctx = sc.Context(local)
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)
-    dtype = sc.F16 if args.dtype == "f16" else sc.BF16
-
-    # scene per rank (scene sharding): seed + rank
-    seed = wl["seed"] + rank
-    xyz, F = sc.generate_synthetic(wl["N"], wl["E"], wl["C_in"], seed)
-    K3 = wl["K"] ** 3
-    W = sc.generate_weights(wl["seed"], 1, K3, wl["C_in"], wl["C_out"])
-    w = sc.Weights(ctx, W, dtype)
-    xyz_d = torch.from_numpy(xyz).cuda()
-    F_d = torch.from_numpy(F).cuda()
-    out_d = torch.empty((wl["N"], wl["C_out"]), dtype=torch.float32, device="cuda")
-    torch.cuda.synchronize()
-
-    def step():
-        m = sc.KernelMap.build(ctx, None, False, wl["K"], wl["s"], wl["s"], device_ptr=xyz_d.data_ptr(), n=wl["N"],
-                               B=args.B, Cq=args.C)
-        sc.layer_forward_device(ctx, m, w, F_d.data_ptr(), sc.F32, out_d.data_ptr(), sc.F32,
-                                sc.exec_cfg(compute_dtype=dtype))
-        return m
-
-    # tile autotuning (Alg. 2) once, excluded from timing
-    m0 = step()
-    tg, ts, _ = sc.tune_layer(ctx, m0, w, F_d.data_ptr(), sc.F32, rounds=5)
-    info0 = m0.info()
-    m0.free()
+    wl = make_workload(args, ctx, torch, rank)
     for _ in range(args.warmup):
-        step().free()
+        wl.step()
     torch.cuda.synchronize()
 
-    # ---- per-kernel breakdown (untimed pass, every launch bracketed by events)
+    # per-kernel breakdown (untimed pass; every launch bracketed by events)
     ctx.set_profiling(True)
     ctx.profile_reset()
-    for _ in range(max(3, min(args.steps, 10))):
+    n_bd = 3
+    for _ in range(n_bd):
         ctx.flush_l2(256 << 20)
-        step().free()
+        wl.step()
     breakdown = ctx.profile()
-    n_bd = max(3, min(args.steps, 10))
     dominant = max(breakdown.items(), key=lambda kv: kv[1][1])[0] if breakdown else None
     ctx.profile_reset()
     ctx.set_profile_filter(dominant)  # timed region: events only around the dominant kernel
 
-    # ---- timed region: per-step CUDA events on the launching stream, L2 flushed between
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     launches0 = ctx.launch_count
     if dist:
@@ -228,102 +353,67 @@ def main():
         for a, b in ev:
             ctx.flush_l2(256 << 20)
             a.record(stream)
-            m = step()
+            wl.step()
             b.record(stream)
-            m.free()
         torch.cuda.synchronize()
     launches = ctx.launch_count - launches0
     prof = ctx.profile()
     ctx.set_profiling(False)
     ctx.set_profile_filter(None)
-    step_ms = [a.elapsed_time(b) for a, b in ev]
-    total_ms = sum(step_ms)
+    total_ms = sum(a.elapsed_time(b) for a, b in ev)
     t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
     if dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.barrier()
     max_total_ms = float(t.item())
-    pps = world * wl["N"] * args.steps / (max_total_ms / 1e3)
+    pps = world * wl.points * args.steps / (max_total_ms / 1e3)
 
-    # ---- end-to-end through the reference-facing C ABI with host buffers
-    e2e_times = []
-    cfg = sc.exec_cfg(compute_dtype=dtype, gather_tile=tg, scatter_tile=ts)
-    cloud = sc.PointCloud(xyz, F, False)
-    for i in range(args.warmup + min(args.steps, 20)):
+    # end-to-end through the public API with host buffers (H2D + D2H inside the timing)
+    e2e_times, h2d, d2h = [], 0, 0
+    for i in range(2 + min(args.steps, 10)):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        out = sc.sc_layer_forward(ctx, cloud, W, wl["K"], wl["s"], cfg)
-        e2e_times.append(time.perf_counter() - t0)
-    e2e_times = e2e_times[args.warmup:]
-    e2e_ms = statistics.median(e2e_times) * 1e3
-    n_out = len(out.coords)
-    h2d = xyz.nbytes + F.nbytes + W.nbytes
-    d2h = n_out * (8 + 4 * wl["C_out"]) + 4 * (K3 + 1)
-    e2e_t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+        h2d, d2h = wl.e2e_step()
+        torch.cuda.synchronize()
+        if i >= 2:
+            e2e_times.append(time.perf_counter() - t0)
+    e2e_t = torch.tensor([statistics.median(e2e_times)], dtype=torch.float64, device="cuda")
     if dist:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-    e2e_pps = world * wl["N"] / (float(e2e_t.item()) / 1e3)
+    e2e_pps = world * wl.points / float(e2e_t.item())
 
-    # ---- roofline of the dominant kernel (algorithmic bytes / measured duration)
-    hbm, tflops, peak_kind = load_peaks()
-    N, Cin, Cout = wl["N"], wl["C_in"], wl["C_out"]
-    M = info0.total_matches
-    R = info0.buffer_length
-    kpad = (Cin + 15) // 16 * 16
-    algo = {  # bytes per launch (with this path's dtypes)
-        "k_search": 8 * N + 8 * info0.num_outputs + 12 * K3,
-        "k_emit": 8 * M + 4 * K3 * info0.num_outputs,
-        "k_gather": 4 * Cin * N + 2 * kpad * R + 4 * M,
-        "k_gemm_grouped": 2 * kpad * R + 4 * Cout * R + 2 * K3 * Cin * Cout,
-        "k_scatter": 4 * Cout * M + 4 * K3 * info0.num_outputs + 4 * Cout * info0.num_outputs,
-        "cub_radix_sort_pairs_u32": 2 * (4 + 4) * N,
-        "k_bbox": 12 * N,
-        "k_pack_compact": 12 * N + 8 * N,
-        "k_expand_keys": 4 * N + 8 * N,
-        "k_pack_keys": 12 * N + 8 * N,
-        "k_backward": 8 * K3 * ((N + 255) // 256),
-    }
+    # roofline of the dominant kernel: algorithmic bytes / measured duration
+    hbm, _, peak_kind = load_peaks()
     roofline = None
     if dominant and dominant in prof:
         n_launch, tot = prof[dominant]
         avg_ms = tot / n_launch
-        traffic = load_traffic().get(dominant)
-        if dominant == "k_gemm_grouped":
-            flops = 2 * Cin * Cout * M
-            ach = flops / (avg_ms / 1e3) / 1e12
-            roofline = {"kernel": dominant, "bound": "hbm", "achieved": algo[dominant] / (avg_ms / 1e3) / 1e9,
-                        "peak": hbm, "unit": "GB/s", "useful_tflops": ach, "traffic": traffic}
-        else:
-            ach = algo.get(dominant, 0) / (avg_ms / 1e3) / 1e9
-            roofline = {"kernel": dominant, "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
-                        "traffic": traffic}
-        roofline["frac"] = roofline["achieved"] / roofline["peak"]
-        roofline["peak_source"] = f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"
-        roofline["avg_launch_ms"] = avg_ms
-        roofline["algorithmic_bytes_per_launch"] = algo.get(dominant)
-
+        algo = wl.algo_bytes().get(dominant)
+        ach = algo / (avg_ms / 1e3) / 1e9 if algo else None
+        roofline = {"kernel": dominant, "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
+                    "frac": (ach / hbm) if ach else None, "traffic": load_traffic().get(dominant),
+                    "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})", "avg_launch_ms": avg_ms,
+                    "launches_per_step": n_launch / args.steps, "algorithmic_bytes_per_launch": algo,
+                    "share_of_step": tot / total_ms}
     phases = {k: {"launches_per_step": n / n_bd, "us_per_step": 1e3 * ms / n_bd}
               for k, (n, ms) in sorted(breakdown.items(), key=lambda kv: -kv[1][1])}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         workers = os.cpu_count() or 1
-        times = cpu_run(wl, 3, workers)
-        cpu = {"value": wl["N"] / statistics.median(times), "unit": "points/s", "cores": workers, "kind": "port",
-               "sample": "3 full C1 layers (Map+GMaS, fp64 accumulate) on oracle/liboracle.so, median"}
+        v, sample = wl.cpu_sample(workers)
+        cpu = {"value": v, "unit": "points/s", "cores": workers, "kind": "port", "sample": sample}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": pps, "unit": "points/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": max_total_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
-            "config": {"workload": args.workload, **wl, "B": args.B, "C": args.C,
-                       "parallelism": f"scene-sharded x{world}",
-                       "l2": "flushed (256 MB memset) between timed steps", "gather_tile": tg, "scatter_tile": ts,
-                       "matches": M, "buffer_length": R, "groups": info0.groups,
-                       "padding_overhead": info0.padding_overhead},
-            "e2e": {"value": e2e_pps, "unit": "points/s", "ms": e2e_ms, "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "api": "sconv_sc_layer_forward (host buffers)"},
+            "config": {"workload": args.workload, **wl.config, "B": args.B, "C": args.C,
+                       "parallelism": f"scene-sharded x{world}", "l2": "flushed (256 MB memset) between timed steps",
+                       **wl.extra()},
+            "e2e": {"value": e2e_pps, "unit": "points/s", "ms": 1e3 * float(e2e_t.item()), "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "api": "host buffers through the C ABI (sconv_net_forward / "
+                                                      "sconv_sc_layer_forward + readback)"},
             "gpu_launches": launches,
             "roofline": roofline,
             "phases": phases,

@@ -65,6 +65,8 @@ typedef struct {
   int gather_tile;    /* T_g channels per work item; 0 = autotuned / heuristic */
   int scatter_tile;   /* T_s; 0 = autotuned / heuristic */
   int compute_dtype;  /* GEMM operand type: SCONV_F16 (default) or SCONV_BF16 */
+  int partial_f16;    /* 1 (default): per-offset GEMM partials stored as f16 when compute is f16;
+                         0: fp32 partials ("stored as 32-bit") */
 } sconv_exec_cfg;
 
 typedef struct {
@@ -194,6 +196,8 @@ sconv_status sconv_net_read_tensor(sconv_ctx* ctx, const sconv_net* net, int ten
 /* Device view of a tensor's fp32 features (valid until the next forward). */
 sconv_status sconv_net_tensor_device(const sconv_net* net, int tensor, const float** feats);
 sconv_status sconv_net_stats(const sconv_net* net, int* maps_built, int* convs);
+/* Per CONV op (execution order) of the last forward: {n_in, n_out, |M|, R_pad, c_in, c_out, k_pad, K3}. */
+sconv_status sconv_net_conv_stats(const sconv_net* net, int conv, int64_t* out8);
 void sconv_net_free(sconv_ctx* ctx, sconv_net* net);
 
 /* ---------------- utilities (cli gen) ----------------

@@ -93,6 +93,7 @@ sconv_exec_cfg normalize(const sconv_exec_cfg* cfg) {
   c.gather_tile = 0;
   c.scatter_tile = 0;
   c.compute_dtype = SCONV_F16;
+  c.partial_f16 = 1;
   if (cfg) c = *cfg;
   if (c.compute_dtype != SCONV_F16 && c.compute_dtype != SCONV_BF16) fail(SCONV_ERR_ARG, "compute dtype must be f16 or bf16");
   return c;
@@ -606,6 +607,12 @@ sconv_status sconv_net_stats(const sconv_net* net, int* maps_built, int* convs) 
     for (const auto& o : net->ops) c += o.kind == kOpConv;
     *convs = c;
   }
+  return SCONV_OK;
+}
+
+sconv_status sconv_net_conv_stats(const sconv_net* net, int conv, int64_t* out8) {
+  if (!net || !out8 || conv < 0 || conv >= static_cast<int>(net->conv_stats.size())) return SCONV_ERR_ARG;
+  for (int i = 0; i < 8; ++i) out8[i] = net->conv_stats[conv][i];
   return SCONV_OK;
 }
 

@@ -100,11 +100,11 @@ __device__ __forceinline__ int4 decode_tile(const LayerPlan& p, int t) {
   return make_int4(mb.y + rb * 128, min(128, mb.w - rb * 128), mb.x, nbk * p.block_n);
 }
 
-template <int KC>
+template <int KC, class TOut>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_gemm_grouped(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ LayerPlan plan, int num_tiles, int num_kb, int block_n, int n_pad, int c_out,
-                   float* __restrict__ out, int stages, uint32_t idesc_base, uint32_t tmem_cols) {
+                   TOut* __restrict__ out, int stages, uint32_t idesc_base, uint32_t tmem_cols) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t{1023});
   const uint32_t a_bytes = 128u * KC * 2u;
@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       tc_fence_after();
       const int r = q * 32 + lane;
       const bool valid = r < td.y;
-      float* orow = out + static_cast<int64_t>(td.x + r) * c_out + td.w;
+      TOut* orow = out + static_cast<int64_t>(td.x + r) * c_out + td.w;
       const int ncols = min(n_tile, c_out - td.w);
       for (int c0 = 0; c0 < n_tile; c0 += 16) {
         uint32_t v[16];
@@ -215,7 +215,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
             : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (valid) {
+        if (!valid) continue;
+        if constexpr (std::is_same<TOut, float>::value) {
           if (vec4 && c0 + 16 <= ncols) {
 #pragma unroll
             for (int e = 0; e < 16; e += 4)
@@ -226,6 +227,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
             for (int e = 0; e < 16; ++e)
               if (c0 + e < ncols) orow[c0 + e] = __uint_as_float(v[e]);
+          }
+        } else {  // f16 partials: 2 x 16-byte stores per 16 columns
+          if ((c_out & 7) == 0 && c0 + 16 <= ncols) {
+            uint4 pk[2];
+            __half2* h2 = reinterpret_cast<__half2*>(pk);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) h2[e] = __floats2half2_rn(__uint_as_float(v[2 * e]), __uint_as_float(v[2 * e + 1]));
+            reinterpret_cast<uint4*>(orow + c0)[0] = pk[0];
+            reinterpret_cast<uint4*>(orow + c0)[1] = pk[1];
+          } else {
+#pragma unroll
+            for (int e = 0; e < 16; ++e)
+              if (c0 + e < ncols) orow[c0 + e] = __float2half_rn(__uint_as_float(v[e]));
           }
         }
       }
@@ -275,7 +289,7 @@ CUtensorMap make_map(const void* base, int dtype, uint64_t inner, uint64_t outer
   return m;
 }
 
-template <int KC>
+template <int KC, class TOut>
 void launch_kc(Ctx& ctx, const GemmArgs& a) {
   const int block_n = a.block_n;
   const uint32_t a_bytes = 128u * KC * 2u, b_bytes = static_cast<uint32_t>(block_n) * KC * 2u;
@@ -286,7 +300,7 @@ void launch_kc(Ctx& ctx, const GemmArgs& a) {
   // TMEM: two accumulators of block_n fp32 columns, power of two >= 32.
   uint32_t cols = 32;
   while (cols < 2u * static_cast<uint32_t>(block_n)) cols <<= 1;
-  auto kern = k_gemm_grouped<KC>;
+  auto kern = k_gemm_grouped<KC, TOut>;
   SCONV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   int occ = 0;
   SCONV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kGemmThreads, smem));
@@ -299,7 +313,7 @@ void launch_kc(Ctx& ctx, const GemmArgs& a) {
   const uint32_t idesc_base = (1u << 4) | (fmt << 7) | (fmt << 10) | ((128u >> 4) << 24);
   ctx.launch("k_gemm_grouped", [&] {
     kern<<<grid, kGemmThreads, smem, ctx.stream>>>(tA, tB, *a.plan, a.num_tiles, a.num_kb, block_n, a.n_pad, a.c_out,
-                                                   a.out, stages, idesc_base, cols);
+                                                   static_cast<TOut*>(a.out), stages, idesc_base, cols);
   });
 }
 
@@ -310,12 +324,21 @@ int gemm_chunk(int k_pad) { return k_pad % 64 == 0 ? 64 : (k_pad % 32 == 0 ? 32 
 void launch_grouped_gemm(Ctx& ctx, const GemmArgs& a) {
   if (a.num_tiles == 0) return;
   const int kc = gemm_chunk(a.k_pad);
-  if (kc == 64)
-    launch_kc<64>(ctx, a);
-  else if (kc == 32)
-    launch_kc<32>(ctx, a);
-  else
-    launch_kc<16>(ctx, a);
+  if (a.out_f16) {
+    if (kc == 64)
+      launch_kc<64, __half>(ctx, a);
+    else if (kc == 32)
+      launch_kc<32, __half>(ctx, a);
+    else
+      launch_kc<16, __half>(ctx, a);
+  } else {
+    if (kc == 64)
+      launch_kc<64, float>(ctx, a);
+    else if (kc == 32)
+      launch_kc<32, float>(ctx, a);
+    else
+      launch_kc<16, float>(ctx, a);
+  }
 }
 
 }  // namespace sconvb

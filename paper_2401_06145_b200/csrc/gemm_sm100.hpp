@@ -16,7 +16,8 @@ struct GemmArgs {
   int n_pad = 0, block_n = 0, c_out = 0;
   int num_offsets = 0;
   int dtype = SCONV_F16;
-  float* out = nullptr;  // [rows x c_out] fp32
+  void* out = nullptr;  // [rows x c_out] per-offset partials: fp32, or f16 when out_f16
+  bool out_f16 = false;
 };
 
 // K chunk (elements) per pipeline stage for a padded input width: 64/32/16 -> swizzle 128/64/32 B.

@@ -218,6 +218,165 @@ __global__ void __launch_bounds__(256) k_scatter(const float* __restrict__ gemm_
   }
 }
 
+// ---------------------------------------------------------------- segmented scatter
+// Canonical order makes the partials of a tile of consecutive outputs contiguous PER OFFSET:
+// list k is sorted by output index, so the hits of outputs [i0, i0+TI) occupy one slot range
+// [first, last] of offset k. The CTA loads all K^3 position rows of its tile (coalesced),
+// then streams each offset's partial rows with ONE bulk copy (TMA engine) through a ring of
+// kScatStages shared-memory stages, accumulating in fp32 in ascending k (deterministic,
+// SPEC.md:353) — the partial buffer is read exactly once, fully coalesced.
+constexpr int kScatThreads = 256, kScatStages = 4;
+
+__device__ __forceinline__ void bulk_g2s_(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// T = output channels per work item (the scatter tile), TP = partial type, TI = tile rows.
+template <int T, class TP, class TOut>
+__global__ void __launch_bounds__(kScatThreads) k_scatter_seg(const TP* __restrict__ partials, int c_out,
+                                                               const int32_t* __restrict__ nbr_pos, int64_t n_out,
+                                                               int K3, const __grid_constant__ LayerPlan plan,
+                                                               TOut* __restrict__ f_out, int relu, int TI) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int row_bytes = c_out * static_cast<int>(sizeof(TP));
+  TP* s_rows = reinterpret_cast<TP*>(smem);                                      // stages x TI rows
+  int32_t* s_m = reinterpret_cast<int32_t*>(smem + static_cast<size_t>(kScatStages) * TI * row_bytes);  // K3 x TI
+  int32_t* s_first = s_m + K3 * TI;                                              // K3: first position (or -1)
+  int32_t* s_cnt = s_first + K3;                                                 // K3: hits
+  int32_t* s_act = s_cnt + K3;                                                   // active offsets, ascending
+  __shared__ __align__(8) uint64_t s_bar[kScatStages];
+  __shared__ int s_nact;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t i0 = static_cast<int64_t>(blockIdx.x) * TI;
+  const int n = static_cast<int>(min(static_cast<int64_t>(TI), n_out - i0));
+  if (tid == 0) {
+    for (int s = 0; s < kScatStages; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_bar[s])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int e = tid; e < K3 * TI; e += kScatThreads) {
+    const int k = e / TI, r = e - k * TI;
+    s_m[e] = r < n ? __ldg(nbr_pos + int64_t{k} * n_out + i0 + r) : -1;
+  }
+  __syncthreads();
+  for (int k = warp; k < K3; k += kScatThreads / 32) {  // first hit + hit count per offset
+    int first = INT_MAX, cnt = 0;
+    for (int r = lane; r < TI; r += 32) {
+      const int m = s_m[k * TI + r];
+      if (m >= 0) {
+        first = min(first, m);
+        ++cnt;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      first = min(first, __shfl_xor_sync(0xFFFFFFFFu, first, o));
+      cnt += __shfl_xor_sync(0xFFFFFFFFu, cnt, o);
+    }
+    if (lane == 0) {
+      s_first[k] = cnt ? first : -1;
+      s_cnt[k] = cnt;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int na = 0;
+    for (int k = 0; k < K3; ++k)
+      if (s_cnt[k] > 0) s_act[na++] = k;
+    s_nact = na;
+    for (int a = 0; a < min(na, kScatStages); ++a) {  // prime the ring
+      const int k = s_act[a];
+      const uint32_t bytes = static_cast<uint32_t>(s_cnt[k]) * row_bytes;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&s_bar[a])), "r"(bytes)
+                   : "memory");
+      bulk_g2s_(s_rows + static_cast<size_t>(a) * TI * c_out,
+                partials + static_cast<int64_t>(s_first[k] + plan.delta[k]) * c_out, bytes, &s_bar[a]);
+    }
+  }
+  __syncthreads();
+  const int G = c_out / T;             // channel groups per row
+  const int pairs = TI * G;            // (row, group) work items
+  constexpr int kMaxPer = 8;           // pairs per thread (TI * G <= 8 * 256)
+  float acc[kMaxPer][T];
+#pragma unroll
+  for (int j = 0; j < kMaxPer; ++j)
+#pragma unroll
+    for (int e = 0; e < T; ++e) acc[j][e] = 0.f;
+  const int nact = s_nact;
+  for (int a = 0; a < nact; ++a) {
+    const int st = a % kScatStages;
+    mbar_wait_(&s_bar[st], static_cast<uint32_t>((a / kScatStages) & 1));
+    const int k = s_act[a];
+    const int first = s_first[k];
+    const TP* rows = s_rows + static_cast<size_t>(st) * TI * c_out;
+#pragma unroll
+    for (int j = 0; j < kMaxPer; ++j) {
+      const int p = tid + j * kScatThreads;
+      if (p >= pairs) break;
+      const int r = p / G, g = p - r * G;
+      const int m = s_m[k * TI + r];
+      if (m < 0) continue;
+      const TP* src = rows + static_cast<size_t>(m - first) * c_out + g * T;
+      if constexpr (std::is_same<TP, __half>::value && T % 8 == 0) {
+#pragma unroll
+        for (int e = 0; e < T; e += 8) {
+          const uint4 x = *reinterpret_cast<const uint4*>(src + e);
+          const __half2* h = reinterpret_cast<const __half2*>(&x);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float2 f = __half22float2(h[q]);
+            acc[j][e + 2 * q] += f.x;
+            acc[j][e + 2 * q + 1] += f.y;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < T; ++e) acc[j][e] += Cvt<TP>::to(src[e]);
+      }
+    }
+    __syncthreads();  // stage consumed by every thread
+    if (tid == 0 && a + kScatStages < nact) {
+      const int k2 = s_act[a + kScatStages];
+      const uint32_t bytes = static_cast<uint32_t>(s_cnt[k2]) * row_bytes;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&s_bar[st])), "r"(bytes)
+                   : "memory");
+      bulk_g2s_(s_rows + static_cast<size_t>(st) * TI * c_out,
+                partials + static_cast<int64_t>(s_first[k2] + plan.delta[k2]) * c_out, bytes, &s_bar[st]);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kMaxPer; ++j) {
+    const int p = tid + j * kScatThreads;
+    if (p >= pairs) break;
+    const int r = p / G, g = p - r * G;
+    if (r >= n) continue;
+    TOut* dst = f_out + (i0 + r) * c_out + g * T;
+    if (relu)
+#pragma unroll
+      for (int e = 0; e < T; ++e) acc[j][e] = fmaxf(acc[j][e], 0.f);
+    if constexpr (std::is_same<TOut, float>::value && T % 4 == 0) {
+#pragma unroll
+      for (int e = 0; e < T; e += 4)
+        *reinterpret_cast<float4*>(dst + e) = make_float4(acc[j][e], acc[j][e + 1], acc[j][e + 2], acc[j][e + 3]);
+    } else {
+#pragma unroll
+      for (int e = 0; e < T; ++e) dst[e] = Cvt<TOut>::from(acc[j][e]);
+    }
+  }
+}
+
 constexpr int kBlock = 256;
 inline unsigned blocks_for(int64_t n) { return static_cast<unsigned>(std::max<int64_t>(1, ceil_div<int64_t>(n, kBlock))); }
 
@@ -275,6 +434,39 @@ void scatter_dispatch(Ctx& ctx, int T, const float* gemm_out, int c_out, const i
   }
 }
 
+// tile rows so that every thread owns <= 8 (row, group) items and the ring fits ~96 KB
+int scatter_rows(int c_out, int T, int part_bytes) {
+  int ti = std::min(128, (8 * kScatThreads * T) / c_out);
+  ti = std::min(ti, (96 * 1024) / (kScatStages * c_out * part_bytes));
+  return std::max(1, ti);
+}
+
+bool seg_scatter_ok(int c_out, int T, int part_bytes) {
+  return (c_out * part_bytes) % 16 == 0 && c_out % T == 0 && (T == 1 || T == 2 || T == 4 || T == 8 || T == 16) &&
+         (8 * kScatThreads * T) / c_out >= 1;
+}
+
+template <class TP, class TOut>
+void scatter_seg_dispatch(Ctx& ctx, int T, const TP* partials, int c_out, const int32_t* nbr, int64_t n_out, int K3,
+                          const LayerPlan& plan, void* f_out, int relu) {
+  const int TI = scatter_rows(c_out, T, sizeof(TP));
+  const size_t smem = static_cast<size_t>(kScatStages) * TI * c_out * sizeof(TP) + sizeof(int32_t) * (K3 * TI + 3 * K3) + 16;
+  auto go = [&](auto kern) {
+    SCONV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    ctx.launch("k_scatter", [&] {
+      kern<<<static_cast<unsigned>(ceil_div<int64_t>(n_out, TI)), kScatThreads, smem, ctx.stream>>>(
+          partials, c_out, nbr, n_out, K3, plan, static_cast<TOut*>(f_out), relu, TI);
+    });
+  };
+  switch (T) {
+    case 1: go(k_scatter_seg<1, TP, TOut>); break;
+    case 2: go(k_scatter_seg<2, TP, TOut>); break;
+    case 4: go(k_scatter_seg<4, TP, TOut>); break;
+    case 8: go(k_scatter_seg<8, TP, TOut>); break;
+    default: go(k_scatter_seg<16, TP, TOut>); break;
+  }
+}
+
 size_t dtype_size(int d) { return d == SCONV_F32 ? 4 : 2; }
 
 }  // namespace
@@ -296,8 +488,9 @@ bool is_supported_tile(int t) {
 }
 
 int default_tile(int channels, bool gather) {
-  // Heuristic before tuning: 16-byte operand stores for gather, float4 reads for scatter.
-  const int pref = gather ? 8 : 4;
+  // Heuristic before tuning: 16-byte operand stores for gather, 16-byte f16 partial reads
+  // (8 channels) for the segmented scatter.
+  const int pref = 8;
   for (int t = pref; t >= 1; --t)
     if (channels % t == 0 && is_supported_tile(t)) return t;
   return 1;
@@ -432,7 +625,10 @@ void layer_forward(Ctx& ctx, MapData& m, const WeightData& w, const void* f_in, 
                                                       ctx.gather_buf.get());
     }
     // ---- grouped GEMM
-    ctx.gemm_out.reserve(static_cast<size_t>(R) * c_out * 4, st);
+    // per-offset partials: f16 when computing in f16 (halves the largest stream), else fp32
+    const bool part_f16 = cfg.partial_f16 && w.dtype == SCONV_F16 && seg_scatter_ok(c_out, Ts, 2);
+    const int part_bytes = part_f16 ? 2 : 4;
+    ctx.gemm_out.reserve(static_cast<size_t>(R) * c_out * part_bytes, st);
     GemmArgs ga;
     ga.a = ctx.gather_buf.get();
     ga.b = w.buf.get();
@@ -446,16 +642,36 @@ void layer_forward(Ctx& ctx, MapData& m, const WeightData& w, const void* f_in, 
     ga.c_out = c_out;
     ga.num_offsets = K3;
     ga.dtype = w.dtype;
-    ga.out = ctx.gemm_out.get<float>();
+    ga.out = ctx.gemm_out.get();
+    ga.out_f16 = part_f16;
     launch_grouped_gemm(ctx, ga);
     // ---- scatter
     const int32_t* nbr = m.nbr_pos.get<int32_t>();
-    if (f_out_dtype == SCONV_F32)
-      scatter_dispatch<float>(ctx, Ts, ctx.gemm_out.get<float>(), c_out, nbr, m.n_out, K3, *lp, fout, relu);
-    else if (f_out_dtype == SCONV_F16)
-      scatter_dispatch<__half>(ctx, Ts, ctx.gemm_out.get<float>(), c_out, nbr, m.n_out, K3, *lp, fout, relu);
-    else
-      scatter_dispatch<__nv_bfloat16>(ctx, Ts, ctx.gemm_out.get<float>(), c_out, nbr, m.n_out, K3, *lp, fout, relu);
+    if (part_f16) {
+      if (f_out_dtype == SCONV_F32)
+        scatter_seg_dispatch<__half, float>(ctx, Ts, ctx.gemm_out.get<__half>(), c_out, nbr, m.n_out, K3, *lp, fout, relu);
+      else if (f_out_dtype == SCONV_F16)
+        scatter_seg_dispatch<__half, __half>(ctx, Ts, ctx.gemm_out.get<__half>(), c_out, nbr, m.n_out, K3, *lp, fout,
+                                             relu);
+      else
+        scatter_seg_dispatch<__half, __nv_bfloat16>(ctx, Ts, ctx.gemm_out.get<__half>(), c_out, nbr, m.n_out, K3, *lp,
+                                                    fout, relu);
+    } else if (seg_scatter_ok(c_out, Ts, 4)) {
+      if (f_out_dtype == SCONV_F32)
+        scatter_seg_dispatch<float, float>(ctx, Ts, ctx.gemm_out.get<float>(), c_out, nbr, m.n_out, K3, *lp, fout, relu);
+      else if (f_out_dtype == SCONV_F16)
+        scatter_seg_dispatch<float, __half>(ctx, Ts, ctx.gemm_out.get<float>(), c_out, nbr, m.n_out, K3, *lp, fout, relu);
+      else
+        scatter_seg_dispatch<float, __nv_bfloat16>(ctx, Ts, ctx.gemm_out.get<float>(), c_out, nbr, m.n_out, K3, *lp,
+                                                   fout, relu);
+    } else {
+      if (f_out_dtype == SCONV_F32)
+        scatter_dispatch<float>(ctx, Ts, ctx.gemm_out.get<float>(), c_out, nbr, m.n_out, K3, *lp, fout, relu);
+      else if (f_out_dtype == SCONV_F16)
+        scatter_dispatch<__half>(ctx, Ts, ctx.gemm_out.get<float>(), c_out, nbr, m.n_out, K3, *lp, fout, relu);
+      else
+        scatter_dispatch<__nv_bfloat16>(ctx, Ts, ctx.gemm_out.get<float>(), c_out, nbr, m.n_out, K3, *lp, fout, relu);
+    }
   }
   if (f_out_mem == SCONV_MEM_HOST && m.n_out > 0) {
     SCONV_CUDA(cudaMemcpyAsync(f_out, fout, out_bytes, cudaMemcpyDeviceToHost, st));

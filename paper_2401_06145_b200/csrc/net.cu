@@ -86,6 +86,7 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
   coordsets.clear();
   maps.clear();
   maps_built = 0;
+  conv_stats.clear();
   // coordinate set 0 = the raw input (may be unsorted)
   coordsets.push_back({input.keys, input.n, input.sorted, true});
   raw_input = input;
@@ -158,6 +159,7 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
       c.compute_dtype = w.dtype;
       layer_forward(ctx, m, w, a.feats.get(), SCONV_F32, SCONV_MEM_DEVICE, c, out.feats.get(), SCONV_F32,
                     SCONV_MEM_DEVICE, o.relu);
+      conv_stats.push_back({m.n_in, m.n_out, m.total, m.buffer_length, w.c_in, w.c_out, w.k_pad, m.K3});
     } else {
       NetTensor& b = tensors.at(o.b);
       if (b.coordset < 0) fail(SCONV_ERR_STATE, "op reads a tensor that was not produced yet");

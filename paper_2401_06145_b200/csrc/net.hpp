@@ -1,6 +1,7 @@
 // Network driver types (net.cu).
 #pragma once
 
+#include <array>
 #include <map>
 #include <memory>
 #include <tuple>
@@ -53,6 +54,8 @@ struct NetData {
   MapSource raw_input;
   DevBuf input_xyz;  // device copy of host input coordinates
   int maps_built = 0;
+  // per CONV op of the last forward: n_in, n_out, |M|, R_pad, c_in, c_out, k_pad, K3
+  std::vector<std::array<int64_t, 8>> conv_stats;
 
   void check_ops() const;
   void forward(Ctx& ctx, const MapSource& input, const void* feats, int f_dtype, int f_mem, int c_in);

@@ -217,6 +217,27 @@ class Network:
         self.ctx.check(self.ctx.lib.sconv_net_stats(self.h, C.byref(mb), C.byref(nc)))
         return dict(maps_built=mb.value, convs=nc.value)
 
+    def conv_stats(self):
+        """Per conv (execution order): n_in, n_out, M, R_pad, c_in, c_out, k_pad, K3."""
+        out = []
+        for i in range(len(self.g.convs())):
+            v = np.zeros(8, np.int64)
+            if self.ctx.lib.sconv_net_conv_stats(self.h, i, S._ptr(v)) != S.OK:
+                break
+            out.append(dict(zip(["n_in", "n_out", "M", "R", "c_in", "c_out", "k_pad", "K3"], v.tolist())))
+        return out
+
+    def algo_bytes(self):
+        """Algorithmic bytes per kernel type summed over the convs (this path's dtypes:
+        fp32 features, 16-bit gather buffer, fp32 GEMM partials)."""
+        g = e = s = sc = 0
+        for st in self.conv_stats():
+            n, q, M, R, ci, co, kp, K3 = (st[k] for k in ["n_in", "n_out", "M", "R", "c_in", "c_out", "k_pad", "K3"])
+            g += 4 * ci * n + 2 * kp * R + 4 * M
+            e += 2 * kp * R + 4 * co * R + 2 * K3 * ci * co
+            s += 4 * co * M + 4 * K3 * q + 4 * co * q
+        return {"k_gather": g, "k_gemm_grouped": e, "k_scatter": s}
+
     def free(self):
         if self.h:
             self.ctx.lib.sconv_net_free(self.ctx.h, self.h)

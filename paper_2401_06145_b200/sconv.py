@@ -55,7 +55,8 @@ class MapCfg(C.Structure):
 
 class ExecCfg(C.Structure):
     _fields_ = [("policy", C.c_int), ("epsilon", C.c_double), ("max_batch", C.c_int),
-                ("gather_tile", C.c_int), ("scatter_tile", C.c_int), ("compute_dtype", C.c_int)]
+                ("gather_tile", C.c_int), ("scatter_tile", C.c_int), ("compute_dtype", C.c_int),
+                ("partial_f16", C.c_int)]
 
 
 class MapInfo(C.Structure):
@@ -106,6 +107,7 @@ SIGNATURES = [
     ("sconv_net_read_tensor", _I, [_P, _P, _I, _P, _P]),
     ("sconv_net_tensor_device", _I, [_P, _I, C.POINTER(_P)]),
     ("sconv_net_stats", _I, [_P, C.POINTER(_I), C.POINTER(_I)]),
+    ("sconv_net_conv_stats", _I, [_P, _I, _P]),
     ("sconv_net_free", None, [_P, _P]),
     ("sconv_generate_synthetic", _I, [_I64, _I64, _I64, _U64, _P, _P]),
     ("sconv_generate_weights", _I, [_U64, _U64, _I, _I, _I, _P]),
@@ -203,8 +205,8 @@ def map_cfg(K=3, offset_scale=1, out_stride=1, transposed=False, B=256, Cq=512) 
 
 
 def exec_cfg(policy=GROUP_SORTED, epsilon=0.25, max_batch=16, gather_tile=0, scatter_tile=0,
-             compute_dtype=F16) -> ExecCfg:
-    return ExecCfg(policy, epsilon, max_batch, gather_tile, scatter_tile, compute_dtype)
+             compute_dtype=F16, partial_f16=1) -> ExecCfg:
+    return ExecCfg(policy, epsilon, max_batch, gather_tile, scatter_tile, compute_dtype, partial_f16)
 
 
 class KernelMap:

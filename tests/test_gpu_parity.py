@@ -153,7 +153,8 @@ def test_layer_parity(ctx, oracle, K, s, n, extent, cin, cout):
     xyz = random_cloud(rng, n, extent)
     F = rng.random((len(xyz), cin), dtype=np.float32)
     W = ((rng.random((K ** 3, cin, cout)) * 0.2 - 0.1)).astype(np.float32)
-    out = sc.sc_layer_forward(ctx, sc.PointCloud(xyz, F, False), W, K, s)
+    # fp32 partials: same operands as the oracle -> only accumulation order differs
+    out = sc.sc_layer_forward(ctx, sc.PointCloud(xyz, F, False), W, K, s, sc.exec_cfg(partial_f16=0))
     oq, of, st = oracle.layer_forward(xyz, False, f16(F), f16(W), K, s, s)
     np.testing.assert_array_equal(out.coords, oq)
     mx, _ = rel_errors(out.features, of)
@@ -161,6 +162,11 @@ def test_layer_parity(ctx, oracle, K, s, n, extent, cin, cout):
     _, of32, _ = oracle.layer_forward(xyz, False, F, W, K, s, s)
     mx, mean = rel_errors(out.features, of32)
     assert mx <= 1e-2 and mean <= 1e-3, (mx, mean)
+    # default: f16 partials (halved partial traffic) -> still within the north_star tolerance
+    out16 = sc.sc_layer_forward(ctx, sc.PointCloud(xyz, F, False), W, K, s)
+    mx16, mean16 = rel_errors(out16.features, of32)
+    assert mx16 <= 1e-2 and mean16 <= 1e-3, (mx16, mean16)
+    assert rel_errors(out16.features, of)[0] <= 2e-3
 
 
 def test_layer_bf16(ctx, oracle):
@@ -168,7 +174,8 @@ def test_layer_bf16(ctx, oracle):
     xyz = random_cloud(rng, 5000, 30)
     F = rng.random((len(xyz), 32), dtype=np.float32)
     W = ((rng.random((27, 32, 32)) * 0.2 - 0.1)).astype(np.float32)
-    out = sc.sc_layer_forward(ctx, sc.PointCloud(xyz, F, False), W, 3, 1, sc.exec_cfg(compute_dtype=sc.BF16))
+    out = sc.sc_layer_forward(ctx, sc.PointCloud(xyz, F, False), W, 3, 1,
+                              sc.exec_cfg(compute_dtype=sc.BF16, partial_f16=0))
     import torch
     bf = lambda a: torch.from_numpy(a).to(torch.bfloat16).float().numpy()  # noqa: E731
     _, of, _ = oracle.layer_forward(xyz, False, bf(F), bf(W), 3, 1, 1)
@@ -184,13 +191,16 @@ def test_tile_and_policy_invariance(ctx):
     W = ((rng.random((27, 48, 24)) * 0.2 - 0.1)).astype(np.float32)
     m = sc.KernelMap.build(ctx, xyz, False, 3, 1, 1)
     w = sc.Weights(ctx, W)
-    ref = sc.layer_forward(ctx, m, w, F)
-    for tg, ts in [(1, 1), (2, 3), (3, 4), (6, 6), (8, 8), (12, 12), (16, 24), (48, 24), (24, 2)]:
-        got = sc.layer_forward(ctx, m, w, F, sc.exec_cfg(gather_tile=tg, scatter_tile=ts))
-        np.testing.assert_array_equal(got, ref)
-    for pol, eps, mb in [(sc.GROUP_MAP_ORDER, 0.25, 16), (sc.GROUP_SORTED, 0.0, 1), (sc.GROUP_SORTED, 10.0, 27)]:
-        got = sc.layer_forward(ctx, m, w, F, sc.exec_cfg(policy=pol, epsilon=eps, max_batch=mb))
-        np.testing.assert_array_equal(got, ref)
+    for pf in (0, 1):  # fp32 partials (every divisor tile) and f16 partials (segmented-scatter tiles)
+        ref = sc.layer_forward(ctx, m, w, F, sc.exec_cfg(partial_f16=pf))
+        tiles = [(1, 1), (2, 3), (3, 4), (6, 6), (8, 8), (12, 12), (16, 24), (48, 24), (24, 2)] if pf == 0 else \
+            [(1, 1), (2, 2), (3, 4), (6, 8), (8, 8), (12, 8), (48, 4)]
+        for tg, ts in tiles:
+            got = sc.layer_forward(ctx, m, w, F, sc.exec_cfg(gather_tile=tg, scatter_tile=ts, partial_f16=pf))
+            np.testing.assert_array_equal(got, ref)
+        for pol, eps, mb in [(sc.GROUP_MAP_ORDER, 0.25, 16), (sc.GROUP_SORTED, 0.0, 1), (sc.GROUP_SORTED, 10.0, 27)]:
+            got = sc.layer_forward(ctx, m, w, F, sc.exec_cfg(policy=pol, epsilon=eps, max_batch=mb, partial_f16=pf))
+            np.testing.assert_array_equal(got, ref)
 
 
 def test_map_determinism(ctx):
