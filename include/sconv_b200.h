@@ -38,6 +38,12 @@ typedef enum {
 typedef enum { SCONV_MEM_HOST = 0, SCONV_MEM_DEVICE = 1 } sconv_mem;
 typedef enum { SCONV_F32 = 0, SCONV_F16 = 1, SCONV_BF16 = 2 } sconv_dtype;
 typedef enum { SCONV_GROUP_MAP_ORDER = 0, SCONV_GROUP_SORTED = 1 } sconv_group_policy;
+/* GMaS dataflow. GMAS: Minuet's gather -> grouped GEMM -> scatter with materialised
+ * buffers. FUSED: output-stationary gather -> tcgen05 GEMM -> in-TMEM
+ * ascending-k reduction in one kernel; same arithmetic (fp32
+ * accumulation of 16-bit operand products, ascending k). AUTO (network driver only):
+ * each conv is timed once with both dataflows and the faster is kept (Alg. 2 style). */
+typedef enum { SCONV_DATAFLOW_GMAS = 0, SCONV_DATAFLOW_FUSED = 1, SCONV_DATAFLOW_AUTO = 2 } sconv_dataflow;
 
 typedef struct sconv_ctx sconv_ctx;
 typedef struct sconv_map sconv_map;
@@ -67,6 +73,8 @@ typedef struct {
   int compute_dtype;  /* GEMM operand type: SCONV_F16 (default) or SCONV_BF16 */
   int partial_f16;    /* 1 (default): per-offset GEMM partials stored as f16 when compute is f16;
                          0: fp32 partials ("stored as 32-bit") */
+  int dataflow;       /* sconv_dataflow, default GMAS for layers, AUTO for networks */
+  int fuse_residual;  /* network driver: fold ADD (+ReLU) into the producing conv's epilogue (default 1) */
 } sconv_exec_cfg;
 
 typedef struct {

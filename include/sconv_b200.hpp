@@ -68,6 +68,7 @@ struct LayerConfig {  // SPEC.md:359 config{grouping policy, eps, max_batch, til
   int B = 256, C = 512;
   int compute_dtype = SCONV_F16;
   int partial_f16 = 1;
+  int dataflow = SCONV_DATAFLOW_GMAS;  // SCONV_DATAFLOW_FUSED: one output-stationary kernel
 };
 
 namespace detail {
@@ -120,7 +121,7 @@ inline PointCloud sc_layer_forward(Context& ctx, const PointCloud& cloud, const 
   const auto xyz = detail::flatten(*cloud.coords);
   const int c_in = static_cast<int>(cloud.channels());
   sconv_exec_cfg ec{cfg.policy,       cfg.epsilon,      cfg.max_batch,   cfg.gather_tile,
-                    cfg.scatter_tile, cfg.compute_dtype, cfg.partial_f16};
+                    cfg.scatter_tile, cfg.compute_dtype, cfg.partial_f16, cfg.dataflow, 1};
   std::vector<std::int32_t> oxyz(xyz.size());
   Matrix out(cloud.size(), c_out);
   std::int64_t n_out = 0;

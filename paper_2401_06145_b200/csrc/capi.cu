@@ -85,7 +85,7 @@ sconv_map_cfg default_map_cfg(int K, int s) {
   return c;
 }
 
-sconv_exec_cfg normalize(const sconv_exec_cfg* cfg) {
+sconv_exec_cfg normalize(const sconv_exec_cfg* cfg, int default_dataflow = SCONV_DATAFLOW_GMAS) {
   sconv_exec_cfg c;
   c.policy = SCONV_GROUP_SORTED;
   c.epsilon = 0.25;
@@ -94,7 +94,11 @@ sconv_exec_cfg normalize(const sconv_exec_cfg* cfg) {
   c.scatter_tile = 0;
   c.compute_dtype = SCONV_F16;
   c.partial_f16 = 1;
+  c.dataflow = default_dataflow;
+  c.fuse_residual = 1;
   if (cfg) c = *cfg;
+  if (c.dataflow < 0) c.dataflow = default_dataflow;
+  if (c.dataflow < SCONV_DATAFLOW_GMAS || c.dataflow > SCONV_DATAFLOW_AUTO) fail(SCONV_ERR_ARG, "unknown dataflow");
   if (c.compute_dtype != SCONV_F16 && c.compute_dtype != SCONV_BF16) fail(SCONV_ERR_ARG, "compute dtype must be f16 or bf16");
   return c;
 }
@@ -503,7 +507,7 @@ sconv_status sconv_net_create(sconv_ctx* ctx, const int32_t* ops, int n_ops, int
     n->output_tensor = output_tensor;
     n->block_B = block_B > 0 ? block_B : 256;
     n->block_C = block_C > 0 ? block_C : 512;
-    n->cfg = normalize(cfg);
+    n->cfg = normalize(cfg, SCONV_DATAFLOW_AUTO);
     if (input_tensor < 0 || input_tensor >= num_tensors || output_tensor < 0 || output_tensor >= num_tensors)
       fail(SCONV_ERR_ARG, "tensor id out of range");
     for (int i = 0; i < n_ops; ++i) {

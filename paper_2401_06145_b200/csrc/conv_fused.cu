@@ -1,0 +1,498 @@
+// Fused output-stationary SC layer on sm_100a ("fused gather -> tcgen05
+// GEMM -> scatter"). Same result as Minuet's GMaS (gather, per-offset GEMM,
+// ascending-k scatter-sum) without materialising the gather buffer or the per-offset
+// partials: for a tile of 128 output rows (sorted Q order) the kernel walks the offsets
+// k = 0..K3-1 in ascending order, gathers the 128 input rows nbr_in[k][i] into shared
+// memory and accumulates A_k . W_k into one fp32 TMEM accumulator, so the reduction over k
+// happens inside the tensor core in ascending k (SPEC.md:353 order) and the output row is
+// written once. Offsets with no neighbour anywhere in the tile are skipped.
+//
+// HBM/L2 traffic per layer: input rows |M| x C_in x 2 B (L2-resident at these sizes) +
+// nbr table K3 x |Q| x 4 B + output |Q| x C_out x {2,4} B (+ residual read). No |M|-sized
+// intermediate is written.
+//
+// Warp roles (288 threads, persistent CTAs over (row block, n block) tiles):
+//   warps 0-3  gather producers: index rows of the tile (prefetched one tile ahead into
+//              registers, published in shared memory), cp.async 16-byte chunks with the
+//              UMMA 128/64/32-byte XOR swizzle, zero-fill for missing neighbours; thread 0
+//              also TMA-loads the weight tile W_k^T. Completion: cp.async.wait_group ->
+//              fence.proxy.async -> mbarrier arrive (129 arrivals incl. the TMA expect_tx).
+//   warps 4-7  epilogue: tcgen05.ld (32 lanes x 16 columns) -> + residual -> ReLU -> store
+//   warp 8     TMEM owner; lane 0 issues tcgen05.mma (M=128, N=block_n, K=16) and commits
+// Two TMEM accumulators let the epilogue of tile t overlap the MMAs of tile t+1.
+#include <algorithm>
+#include <string>
+
+#include "common.cuh"
+#include "conv_fused.hpp"
+#include "sm100.cuh"
+
+namespace sconvb {
+namespace {
+
+using namespace sm100;
+
+constexpr int kProducers = 128, kEpiWarps = 4;
+constexpr int kThreads = kProducers + 32 * kEpiWarps + 32;  // 288
+constexpr int kStages = 4, kLook = kStages - 1;             // cp.async stages in flight per thread
+
+template <class T>
+struct OutCvt;
+template <>
+struct OutCvt<float> {
+  static __device__ __forceinline__ void load16(const float* p, float (&x)[16]) {
+#pragma unroll
+    for (int e = 0; e < 16; e += 4) {
+      const float4 v = *reinterpret_cast<const float4*>(p + e);
+      x[e] = v.x;
+      x[e + 1] = v.y;
+      x[e + 2] = v.z;
+      x[e + 3] = v.w;
+    }
+  }
+  static __device__ __forceinline__ void store16(float* p, const float (&x)[16]) {
+#pragma unroll
+    for (int e = 0; e < 16; e += 4) *reinterpret_cast<float4*>(p + e) = make_float4(x[e], x[e + 1], x[e + 2], x[e + 3]);
+  }
+  static __device__ __forceinline__ float to(float v) { return v; }
+  static __device__ __forceinline__ float from(float v) { return v; }
+};
+template <>
+struct OutCvt<__half> {
+  static __device__ __forceinline__ void load16(const __half* p, float (&x)[16]) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint4 v = *reinterpret_cast<const uint4*>(p + 8 * h);
+      const __half2* q = reinterpret_cast<const __half2*>(&v);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = __half22float2(q[e]);
+        x[8 * h + 2 * e] = f.x;
+        x[8 * h + 2 * e + 1] = f.y;
+      }
+    }
+  }
+  static __device__ __forceinline__ void store16(__half* p, const float (&x)[16]) {
+    uint4 v[2];
+    __half2* q = reinterpret_cast<__half2*>(v);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) q[e] = __floats2half2_rn(x[2 * e], x[2 * e + 1]);
+    reinterpret_cast<uint4*>(p)[0] = v[0];
+    reinterpret_cast<uint4*>(p)[1] = v[1];
+  }
+  static __device__ __forceinline__ float to(__half v) { return __half2float(v); }
+  static __device__ __forceinline__ __half from(float v) { return __float2half_rn(v); }
+};
+template <>
+struct OutCvt<__nv_bfloat16> {
+  static __device__ __forceinline__ void load16(const __nv_bfloat16* p, float (&x)[16]) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint4 v = *reinterpret_cast<const uint4*>(p + 8 * h);
+      const __nv_bfloat162* q = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = __bfloat1622float2(q[e]);
+        x[8 * h + 2 * e] = f.x;
+        x[8 * h + 2 * e + 1] = f.y;
+      }
+    }
+  }
+  static __device__ __forceinline__ void store16(__nv_bfloat16* p, const float (&x)[16]) {
+    uint4 v[2];
+    __nv_bfloat162* q = reinterpret_cast<__nv_bfloat162*>(v);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) q[e] = __floats2bfloat162_rn(x[2 * e], x[2 * e + 1]);
+    reinterpret_cast<uint4*>(p)[0] = v[0];
+    reinterpret_cast<uint4*>(p)[1] = v[1];
+  }
+  static __device__ __forceinline__ float to(__nv_bfloat16 v) { return __bfloat162float(v); }
+  static __device__ __forceinline__ __nv_bfloat16 from(float v) { return __float2bfloat16_rn(v); }
+};
+
+struct FusedParams {
+  const unsigned char* f_in;
+  int64_t ld_in_bytes;
+  const int32_t* nbr;
+  int64_t n_out;
+  int K3, num_kb, block_n, n_pad, n_blocks, num_tiles, c_out;
+  void* out;
+  int64_t ld_out;
+  const void* res;
+  int64_t ld_res;
+  int relu;
+  int vec;  // 16-byte aligned output / residual rows
+  uint32_t stage_bytes, a_bytes, b_bytes, idx_off, bar_off;
+  uint32_t tmem_cols;
+  int bf16;
+};
+
+// NK = compile-time offset count (registers prefetch the next tile's index rows), 0 = runtime
+template <int NK, int KC, class TOut>
+__global__ void __launch_bounds__(kThreads, 1) k_conv_fused(const __grid_constant__ CUtensorMap tmB,
+                                                           const __grid_constant__ FusedParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t{1023});
+  int32_t* s_idx = reinterpret_cast<int32_t*>(smem + p.idx_off);  // [2][K3][128]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.bar_off);
+  uint64_t* empty = full + kStages;
+  uint64_t* tfull = empty + kStages;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* ifull = tempty + 2;
+  uint64_t* iempty = ifull + 2;
+  uint64_t* s_mask = iempty + 2;       // [2] active-offset mask per tile slot
+  uint64_t* s_part = s_mask + 2;       // [2][4] per-producer-warp partial masks
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_part + 8);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int K3 = p.K3;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], kProducers + 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], kEpiWarps);
+      mbar_init(&ifull[a], 1);
+      mbar_init(&iempty[a], 1);
+    }
+    mbar_fence_init();
+  }
+  if (warp == 8) tmem_alloc(tmem_slot, p.tmem_cols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp < 4) {
+    // ------------------------------------------------------------ gather producers
+    const int tid = threadIdx.x;
+    constexpr int CPR = KC / 8;      // 16-byte chunks per row
+    constexpr int RPP = 128 / CPR;   // rows per pass
+    const int chunk = tid % CPR, rbase = tid / CPR;
+    uint32_t a_off[CPR];
+#pragma unroll
+    for (int q = 0; q < CPR; ++q) a_off[q] = swizzled_offset<KC>(rbase + q * RPP, chunk);
+    const unsigned char* src_col = p.f_in + chunk * 16;
+    if (tid == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+
+    constexpr int NR = NK > 0 ? NK : 1;
+    int jn[NR];
+    auto load_rows = [&](int t) {
+      const int64_t i = static_cast<int64_t>(t / p.n_blocks) * 128 + tid;
+      const bool ok = i < p.n_out;
+#pragma unroll
+      for (int k = 0; k < NR; ++k) jn[k] = ok ? __ldg(p.nbr + int64_t{k} * p.n_out + i) : -1;
+    };
+    if (NK > 0) load_rows(blockIdx.x);
+    uint32_t issued = 0, arrived = 0;  // sequential stage counters
+    int it = 0;
+    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
+      const int buf = it & 1;
+      const int nb = t % p.n_blocks;
+      int32_t* srow = s_idx + buf * K3 * 128;
+      uint64_t mine = 0;
+      if constexpr (NK > 0) {
+#pragma unroll
+        for (int k = 0; k < NK; ++k) {
+          srow[k * 128 + tid] = jn[k];
+          mine |= static_cast<uint64_t>(jn[k] >= 0) << k;
+        }
+        if (t + static_cast<int>(gridDim.x) < p.num_tiles) load_rows(t + gridDim.x);  // next tile, in flight
+      } else {
+        const int64_t i = static_cast<int64_t>(t / p.n_blocks) * 128 + tid;
+        for (int k = 0; k < K3; ++k) {
+          const int32_t j = i < p.n_out ? __ldg(p.nbr + int64_t{k} * p.n_out + i) : -1;
+          srow[k * 128 + tid] = j;
+          mine |= static_cast<uint64_t>(j >= 0) << k;
+        }
+      }
+      const uint32_t lo = __reduce_or_sync(0xFFFFFFFFu, static_cast<uint32_t>(mine));
+      const uint32_t hi = __reduce_or_sync(0xFFFFFFFFu, static_cast<uint32_t>(mine >> 32));
+      if (lane == 0) s_part[buf * 4 + warp] = (static_cast<uint64_t>(hi) << 32) | lo;
+      named_bar(1, kProducers);  // index rows + partial masks of this tile are published
+      uint64_t mask = s_part[buf * 4] | s_part[buf * 4 + 1] | s_part[buf * 4 + 2] | s_part[buf * 4 + 3];
+      if (mask == 0) mask = 1;  // no neighbour at all: one all-zero stage keeps the accumulator defined
+      if (tid == 0) {
+        mbar_wait(&iempty[buf], ((it >> 1) & 1) ^ 1);
+        s_mask[buf] = mask;
+        mbar_arrive(&ifull[buf]);
+      }
+      for (uint64_t m = mask; m; m &= m - 1) {
+        const int k = __ffsll(static_cast<long long>(m)) - 1;
+        const int32_t* sk = srow + k * 128;
+        int32_t j[CPR];
+#pragma unroll
+        for (int q = 0; q < CPR; ++q) j[q] = sk[rbase + q * RPP];
+        for (int kb = 0; kb < p.num_kb; ++kb) {
+          const int stage = static_cast<int>(issued % kStages);
+          mbar_wait(&empty[stage], ((issued / kStages) & 1) ^ 1);
+          uint8_t* sa = smem + stage * p.stage_bytes;
+          if (tid == 0) {
+            mbar_expect_tx(&full[stage], p.b_bytes);
+            tma_load_2d(sa + p.a_bytes, &tmB, kb * KC, k * p.n_pad + nb * p.block_n, &full[stage]);
+          }
+          const uint32_t sa32 = smem_u32(sa);
+          const unsigned char* col = src_col + kb * (KC * 2);
+#pragma unroll
+          for (int q = 0; q < CPR; ++q) {
+            const unsigned char* src = col + static_cast<int64_t>(j[q] >= 0 ? j[q] : 0) * p.ld_in_bytes;
+            cp_async16(sa32 + a_off[q], src, j[q] >= 0 ? 16u : 0u);
+          }
+          cp_async_commit();
+          ++issued;
+          if (issued - arrived > static_cast<uint32_t>(kLook)) {
+            cp_async_wait<kLook>();
+            fence_proxy_async_smem();
+            mbar_arrive(&full[arrived % kStages]);
+            ++arrived;
+          }
+        }
+      }
+    }
+    cp_async_wait<0>();
+    fence_proxy_async_smem();
+    for (; arrived < issued; ++arrived) mbar_arrive(&full[arrived % kStages]);
+  } else if (warp == 8) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      uint32_t consumed = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      int it = 0;
+      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
+        const int buf = it & 1;
+        const int nb = t % p.n_blocks;
+        const int n_tile = min(p.block_n, p.n_pad - nb * p.block_n);
+        const uint32_t idesc = idesc_f16(p.bf16, n_tile);
+        mbar_wait(&ifull[buf], (it >> 1) & 1);
+        const uint64_t mask = s_mask[buf];
+        mbar_arrive(&iempty[buf]);
+        mbar_wait(&tempty[acc], acc_phase ^ 1u);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * p.block_n);
+        uint32_t accumulate = 0;
+        for (uint64_t m = mask; m; m &= m - 1) {
+          for (int kb = 0; kb < p.num_kb; ++kb) {
+            const int stage = static_cast<int>(consumed % kStages);
+            mbar_wait(&full[stage], (consumed / kStages) & 1);
+            tc_fence_after();
+            const uint32_t sa = smem_u32(smem + stage * p.stage_bytes);
+            const uint32_t sb = sa + p.a_bytes;
+#pragma unroll
+            for (int kk = 0; kk < KC / 16; ++kk) {
+              tc_mma(d_tmem, smem_desc<KC>(sa + kk * 32), smem_desc<KC>(sb + kk * 32), idesc, accumulate);
+              accumulate = 1;
+            }
+            tc_commit(&empty[stage]);  // frees the stage once these MMAs retire
+            ++consumed;
+          }
+        }
+        tc_commit(&tfull[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1u;
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int q = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    TOut* out = static_cast<TOut*>(p.out);
+    const TOut* res = static_cast<const TOut*>(p.res);
+    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+      const int nb = t % p.n_blocks;
+      const int n0 = nb * p.block_n;
+      const int n_tile = min(p.block_n, p.n_pad - n0);
+      const int64_t i = static_cast<int64_t>(t / p.n_blocks) * 128 + q * 32 + lane;
+      const bool valid = i < p.n_out;
+      const int ncols = min(n_tile, p.c_out - n0);
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      TOut* orow = out + i * p.ld_out + n0;
+      const TOut* rrow = res ? res + i * p.ld_res + n0 : nullptr;
+      for (int c0 = 0; c0 < n_tile; c0 += 16) {
+        uint32_t v[16];
+        tmem_ld16(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * p.block_n + c0), v);
+        if (!valid || c0 >= ncols) continue;
+        float x[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) x[e] = __uint_as_float(v[e]);
+        const bool full16 = p.vec && c0 + 16 <= ncols;
+        if (rrow) {
+          if (full16) {
+            float r[16];
+            OutCvt<TOut>::load16(rrow + c0, r);
+#pragma unroll
+            for (int e = 0; e < 16; ++e) x[e] += r[e];
+          } else {
+#pragma unroll
+            for (int e = 0; e < 16; ++e)
+              if (e < ncols - c0) x[e] += OutCvt<TOut>::to(rrow[c0 + e]);
+          }
+        }
+        if (p.relu)
+#pragma unroll
+          for (int e = 0; e < 16; ++e) x[e] = fmaxf(x[e], 0.f);
+        if (full16)
+          OutCvt<TOut>::store16(orow + c0, x);
+        else
+#pragma unroll
+          for (int e = 0; e < 16; ++e)
+            if (e < ncols - c0) orow[c0 + e] = OutCvt<TOut>::from(x[e]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1u;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 8) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, p.tmem_cols);
+  }
+}
+
+template <class TS, class TD>
+__global__ void k_convert_rows(const TS* __restrict__ src, int64_t n, int c, int64_t ld_src, TD* __restrict__ dst,
+                               int64_t ld_dst) {
+  const int64_t g = blockIdx.x * int64_t{blockDim.x} + threadIdx.x;
+  if (g >= n * ld_dst) return;
+  const int64_t r = g / ld_dst;
+  const int col = static_cast<int>(g - r * ld_dst);
+  const float v = col < c ? OutCvt<TS>::to(src[r * ld_src + col]) : 0.f;
+  dst[g] = OutCvt<TD>::from(v);
+}
+
+template <int NK, int KC, class TOut>
+void launch_t(Ctx& ctx, const FusedArgs& a, const FusedParams& prm, size_t smem, const CUtensorMap& tB) {
+  auto kern = k_conv_fused<NK, KC, TOut>;
+  SCONV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  int occ = 0;
+  SCONV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem));
+  occ = std::max(1, std::min<int>(occ, static_cast<int>(512u / prm.tmem_cols)));  // never oversubscribe TMEM
+  const int grid = std::max(1, std::min(prm.num_tiles, ctx.num_sms * occ));
+  ctx.launch("k_conv_fused", [&] { kern<<<grid, kThreads, smem, ctx.stream>>>(tB, prm); });
+}
+
+template <int KC, class TOut>
+void launch_nk(Ctx& ctx, const FusedArgs& a, const FusedParams& prm, size_t smem, const CUtensorMap& tB) {
+  switch (prm.K3) {
+    case 27: launch_t<27, KC, TOut>(ctx, a, prm, smem, tB); break;
+    case 8: launch_t<8, KC, TOut>(ctx, a, prm, smem, tB); break;
+    case 1: launch_t<1, KC, TOut>(ctx, a, prm, smem, tB); break;
+    default: launch_t<0, KC, TOut>(ctx, a, prm, smem, tB); break;
+  }
+}
+
+template <class TOut>
+void launch_kc(Ctx& ctx, const FusedArgs& a, const FusedParams& prm, size_t smem, const CUtensorMap& tB, int kc) {
+  if (kc == 64)
+    launch_nk<64, TOut>(ctx, a, prm, smem, tB);
+  else if (kc == 32)
+    launch_nk<32, TOut>(ctx, a, prm, smem, tB);
+  else
+    launch_nk<16, TOut>(ctx, a, prm, smem, tB);
+}
+
+}  // namespace
+
+bool fused_supported(int K3, int c_in, int c_out) { return K3 >= 1 && K3 <= 64 && c_in >= 1 && c_out >= 1; }
+
+void launch_conv_fused(Ctx& ctx, const FusedArgs& a) {
+  const WeightData& w = *a.w;
+  if (!fused_supported(w.K3, w.c_in, w.c_out)) fail(SCONV_ERR_ARG, "fused dataflow supports at most 64 offsets");
+  if (a.n_out == 0) return;
+  if (a.ld_in < w.k_pad || a.ld_in % 8 != 0) fail(SCONV_ERR_ARG, "fused input row stride must be >= k_pad and 16-byte aligned");
+  if (a.out_dtype != SCONV_F32 && a.out_dtype != SCONV_F16 && a.out_dtype != SCONV_BF16)
+    fail(SCONV_ERR_ARG, "unsupported output dtype");
+  const int kc = w.k_pad % 64 == 0 ? 64 : (w.k_pad % 32 == 0 ? 32 : 16);
+  const int64_t row_blocks = ceil_div<int64_t>(a.n_out, 128);
+  if (row_blocks > INT32_MAX / 16) fail(SCONV_ERR_ARG, "layer too large");
+  // block_n: widest multiple of 16 (<= 256) that still gives ~2 tiles per SM; narrower
+  // blocks re-gather A from L2 once per extra n block.
+  int bn = a.block_n;
+  if (bn <= 0) {
+    bn = std::min(w.n_pad, 256);
+    while (bn > 32 && row_blocks * ceil_div(w.n_pad, bn) < 2 * ctx.num_sms && (bn / 2) % 16 == 0) bn /= 2;
+  }
+  bn = std::min(bn, w.n_pad);
+  if (bn % 16 != 0 || bn > 256) fail(SCONV_ERR_ARG, "block_n must be a multiple of 16 <= 256");
+  FusedParams prm{};
+  prm.f_in = static_cast<const unsigned char*>(a.f_in);
+  prm.ld_in_bytes = a.ld_in * 2;
+  prm.nbr = a.nbr;
+  prm.n_out = a.n_out;
+  prm.K3 = w.K3;
+  prm.num_kb = w.k_pad / kc;
+  prm.block_n = bn;
+  prm.n_pad = w.n_pad;
+  prm.n_blocks = ceil_div(w.n_pad, bn);
+  prm.num_tiles = static_cast<int>(row_blocks * prm.n_blocks);
+  prm.c_out = w.c_out;
+  prm.out = a.out;
+  prm.ld_out = a.ld_out;
+  prm.res = a.res;
+  prm.ld_res = a.ld_res;
+  prm.relu = a.relu;
+  {
+    const int64_t align = a.out_dtype == SCONV_F32 ? 4 : 8;  // elements per 16 bytes
+    prm.vec = a.ld_out % align == 0 && (!a.res || a.ld_res % align == 0) &&
+              reinterpret_cast<uintptr_t>(a.out) % 16 == 0 && reinterpret_cast<uintptr_t>(a.res) % 16 == 0;
+  }
+  prm.bf16 = w.dtype == SCONV_BF16;
+  prm.a_bytes = 128u * kc * 2u;
+  prm.b_bytes = static_cast<uint32_t>(bn) * kc * 2u;
+  prm.stage_bytes = (prm.a_bytes + prm.b_bytes + 1023u) & ~1023u;
+  prm.idx_off = kStages * prm.stage_bytes;
+  prm.bar_off = prm.idx_off + 2u * w.K3 * 128u * 4u;
+  uint32_t cols = 32;
+  while (cols < 2u * static_cast<uint32_t>(bn)) cols <<= 1;
+  prm.tmem_cols = cols;
+  const size_t smem = 1024 + prm.bar_off + (2 * kStages + 8 + 2 + 8) * 8 + 16;
+  if (smem > 227 * 1024) fail(SCONV_ERR_ARG, "fused layer tile does not fit in shared memory");
+  const CUtensorMap tB = make_tensor_map_2d(w.buf.get(), w.dtype, w.k_pad, static_cast<uint64_t>(w.K3) * w.n_pad, kc,
+                                            static_cast<uint32_t>(bn), kc);
+  if (a.out_dtype == SCONV_F32)
+    launch_kc<float>(ctx, a, prm, smem, tB, kc);
+  else if (a.out_dtype == SCONV_F16)
+    launch_kc<__half>(ctx, a, prm, smem, tB, kc);
+  else
+    launch_kc<__nv_bfloat16>(ctx, a, prm, smem, tB, kc);
+}
+
+void convert_rows(Ctx& ctx, const void* src, int src_dtype, int64_t n, int c, int64_t ld_src, void* dst, int dst_dtype,
+                  int64_t ld_dst) {
+  if (n == 0) return;
+  const int64_t total = n * ld_dst;
+  const unsigned blocks = static_cast<unsigned>(ceil_div<int64_t>(total, 256));
+  auto go = [&](auto* s, auto* d) {
+    ctx.launch("k_convert_rows", [&] {
+      k_convert_rows<<<blocks, 256, 0, ctx.stream>>>(s, n, c, ld_src, d, ld_dst);
+    });
+  };
+  auto with_dst = [&](auto* s) {
+    if (dst_dtype == SCONV_F16)
+      go(s, static_cast<__half*>(dst));
+    else if (dst_dtype == SCONV_BF16)
+      go(s, static_cast<__nv_bfloat16*>(dst));
+    else
+      go(s, static_cast<float*>(dst));
+  };
+  if (src_dtype == SCONV_F32)
+    with_dst(static_cast<const float*>(src));
+  else if (src_dtype == SCONV_F16)
+    with_dst(static_cast<const __half*>(src));
+  else
+    with_dst(static_cast<const __nv_bfloat16*>(src));
+}
+
+}  // namespace sconvb

@@ -1,0 +1,33 @@
+// Fused output-stationary SC layer: gather -> tcgen05 GEMM -> ascending-k
+// reduction in TMEM -> epilogue, one kernel, no gather buffer and no per-offset partials.
+#pragma once
+
+#include "ctx.hpp"
+#include "gmas.hpp"
+
+namespace sconvb {
+
+struct FusedArgs {
+  const void* f_in = nullptr;  // 16-bit (the weight dtype) [n_in][ld_in]; columns [c_in, k_pad) zero
+  int64_t ld_in = 0;
+  const int32_t* nbr = nullptr;  // [K3][n_out]: input row of (k, i) or -1 (MapData::nbr_in)
+  int64_t n_out = 0;
+  const WeightData* w = nullptr;
+  void* out = nullptr;  // [n_out][ld_out] of out_dtype
+  int out_dtype = SCONV_F32;
+  int64_t ld_out = 0;
+  const void* res = nullptr;  // optional residual [n_out][ld_res] of out_dtype, added before ReLU
+  int64_t ld_res = 0;
+  int relu = 0;
+  int block_n = 0;  // 0 = choose (fill the SMs)
+};
+
+// true when the fused kernel supports this layer (K3 <= 64, 16-bit operands)
+bool fused_supported(int K3, int c_in, int c_out);
+void launch_conv_fused(Ctx& ctx, const FusedArgs& a);
+
+// f32/f16/bf16 [n][c] -> 16-bit [n][ld] (zero padded columns), dtype = operand type
+void convert_rows(Ctx& ctx, const void* src, int src_dtype, int64_t n, int c, int64_t ld_src, void* dst, int dst_dtype,
+                  int64_t ld_dst);
+
+}  // namespace sconvb

@@ -14,73 +14,17 @@
 //
 // Warp roles (192 threads): warp 0 = TMA producer, warp 1 = TMEM owner + single-thread
 // MMA issuer, warps 2-5 = epilogue (warp w reads TMEM lanes 32*(w%4) .. +31).
-#include <cuda.h>
-#include <cudaTypedefs.h>
-
 #include <algorithm>
 #include <string>
 
 #include "common.cuh"
 #include "gemm_sm100.hpp"
+#include "sm100.cuh"
 
 namespace sconvb {
 namespace {
 
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  const uint32_t addr = smem_u32(bar);
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n\t}" ::"r"(addr),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
-          smem_u32(dst)),
-      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
-      : "memory");
-}
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
-}
-__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                       uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-
-// UMMA shared-memory descriptor, K-major operand with hardware swizzle (one swizzle atom
-// spans the whole K chunk): SBO = 8 rows * swizzle bytes, LBO unused, version 1.
-template <int KC>
-__device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
-  constexpr uint64_t kSwizzleBytes = KC * 2;
-  constexpr uint64_t kLayout = KC == 64 ? 2 : (KC == 32 ? 4 : 6);  // SW128 / SW64 / SW32
-  uint64_t d = 0;
-  d |= static_cast<uint64_t>((addr >> 4) & 0x3FFF);
-  d |= static_cast<uint64_t>((8 * kSwizzleBytes) >> 4) << 32;
-  d |= uint64_t{1} << 46;
-  d |= kLayout << 61;
-  return d;
-}
+using namespace sm100;
 
 constexpr int kGemmThreads = 192;
 
@@ -272,7 +216,7 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-CUtensorMap make_map(const void* base, int dtype, uint64_t inner, uint64_t outer, uint32_t box_inner,
+CUtensorMap make_map_impl(const void* base, int dtype, uint64_t inner, uint64_t outer, uint32_t box_inner,
                      uint32_t box_outer, int kc) {
   CUtensorMap m;
   const cuuint64_t dims[2] = {inner, outer};
@@ -306,8 +250,8 @@ void launch_kc(Ctx& ctx, const GemmArgs& a) {
   SCONV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kGemmThreads, smem));
   occ = std::max(1, std::min<int>(occ, static_cast<int>(512u / cols)));  // never oversubscribe TMEM
   const int grid = std::max(1, std::min(a.num_tiles, ctx.num_sms * occ));
-  const CUtensorMap tA = make_map(a.a, a.dtype, a.k_pad, a.rows, KC, 128, KC);
-  const CUtensorMap tB = make_map(a.b, a.dtype, a.k_pad, static_cast<uint64_t>(a.num_offsets) * a.n_pad, KC,
+  const CUtensorMap tA = make_tensor_map_2d(a.a, a.dtype, a.k_pad, a.rows, KC, 128, KC);
+  const CUtensorMap tB = make_tensor_map_2d(a.b, a.dtype, a.k_pad, static_cast<uint64_t>(a.num_offsets) * a.n_pad, KC,
                                   static_cast<uint32_t>(block_n), KC);
   const uint32_t fmt = a.dtype == SCONV_BF16 ? 1u : 0u;
   const uint32_t idesc_base = (1u << 4) | (fmt << 7) | (fmt << 10) | ((128u >> 4) << 24);
@@ -318,6 +262,11 @@ void launch_kc(Ctx& ctx, const GemmArgs& a) {
 }
 
 }  // namespace
+
+CUtensorMap make_tensor_map_2d(const void* base, int dtype, uint64_t inner, uint64_t outer, uint32_t box_inner,
+                               uint32_t box_outer, int kc) {
+  return make_map_impl(base, dtype, inner, outer, box_inner, box_outer, kc);
+}
 
 int gemm_chunk(int k_pad) { return k_pad % 64 == 0 ? 64 : (k_pad % 32 == 0 ? 32 : 16); }
 

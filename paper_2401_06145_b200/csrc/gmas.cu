@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "conv_fused.hpp"
 #include "gemm_sm100.hpp"
 #include "gmas.hpp"
 #include "map.hpp"
@@ -88,7 +89,7 @@ struct Cvt<float> {
 // k_gather: slot s -> member (binary search over row0 in shared memory) -> canonical
 // pair m = map_start[k] + r -> input row j = pair_in[m].
 template <int T, class TIn, class TOp>
-__global__ void __launch_bounds__(256) k_gather(const TIn* __restrict__ f_in, int c_in,
+__global__ void __launch_bounds__(256) k_gather(const TIn* __restrict__ f_in, int c_in, int64_t ld_in,
                                                 const __grid_constant__ LayerPlan plan,
                                                 const int32_t* __restrict__ map_start,
                                                 const int32_t* __restrict__ pair_in, int64_t rows, int k_pad,
@@ -116,7 +117,7 @@ __global__ void __launch_bounds__(256) k_gather(const TIn* __restrict__ f_in, in
   float v[T];
   if (r < mb.z) {
     const int32_t j = __ldg(pair_in + __ldg(map_start + mb.x) + r);
-    const TIn* src = f_in + static_cast<int64_t>(j) * c_in + t * T;
+    const TIn* src = f_in + static_cast<int64_t>(j) * ld_in + t * T;
     if constexpr (std::is_same<TIn, float>::value && T % 4 == 0) {
 #pragma unroll
       for (int e = 0; e < T; e += 4) {
@@ -168,6 +169,7 @@ template <int T, class TOut>
 __global__ void __launch_bounds__(256) k_scatter(const float* __restrict__ gemm_out, int c_out,
                                                  const int32_t* __restrict__ nbr_pos, int64_t n_out, int K3,
                                                  const __grid_constant__ LayerPlan plan, TOut* __restrict__ f_out,
+                                                 int64_t ld_out, const TOut* __restrict__ res, int64_t ld_res,
                                                  int relu) {
   __shared__ int32_t s_delta[kMaxOffsets];
   for (int t = threadIdx.x; t < K3; t += blockDim.x) s_delta[t] = plan.delta[t];
@@ -205,13 +207,17 @@ __global__ void __launch_bounds__(256) k_scatter(const float* __restrict__ gemm_
       }
     }
   }
+  if (res)
+#pragma unroll
+    for (int e = 0; e < T; ++e) acc[e] += Cvt<TOut>::to(res[i * ld_res + t * T + e]);  // residual epilogue
   if (relu)
 #pragma unroll
     for (int e = 0; e < T; ++e) acc[e] = fmaxf(acc[e], 0.f);  // fused ReLU epilogue (network driver)
-  TOut* dst = f_out + i * c_out + t * T;
-  if constexpr (std::is_same<TOut, float>::value && T % 4 == 0) {
+  TOut* dst = f_out + i * ld_out + t * T;
+  if (std::is_same<TOut, float>::value && T % 4 == 0 && ld_out % 4 == 0) {
 #pragma unroll
-    for (int e = 0; e < T; e += 4) *reinterpret_cast<float4*>(dst + e) = make_float4(acc[e], acc[e + 1], acc[e + 2], acc[e + 3]);
+    for (int e = 0; e < T; e += 4)
+      reinterpret_cast<float4*>(dst)[e / 4] = make_float4(acc[e], acc[e + 1], acc[e + 2], acc[e + 3]);
   } else {
 #pragma unroll
     for (int e = 0; e < T; ++e) dst[e] = Cvt<TOut>::from(acc[e]);
@@ -248,7 +254,9 @@ template <int T, class TP, class TOut>
 __global__ void __launch_bounds__(kScatThreads) k_scatter_seg(const TP* __restrict__ partials, int c_out,
                                                                const int32_t* __restrict__ nbr_pos, int64_t n_out,
                                                                int K3, const __grid_constant__ LayerPlan plan,
-                                                               TOut* __restrict__ f_out, int relu, int TI) {
+                                                               TOut* __restrict__ f_out, int64_t ld_out,
+                                                               const TOut* __restrict__ res, int64_t ld_res, int relu,
+                                                               int TI) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int row_bytes = c_out * static_cast<int>(sizeof(TP));
   TP* s_rows = reinterpret_cast<TP*>(smem);                                      // stages x TI rows
@@ -362,11 +370,16 @@ __global__ void __launch_bounds__(kScatThreads) k_scatter_seg(const TP* __restri
     if (p >= pairs) break;
     const int r = p / G, g = p - r * G;
     if (r >= n) continue;
-    TOut* dst = f_out + (i0 + r) * c_out + g * T;
+    TOut* dst = f_out + (i0 + r) * ld_out + g * T;
+    if (res) {
+      const TOut* rr = res + (i0 + r) * ld_res + g * T;
+#pragma unroll
+      for (int e = 0; e < T; ++e) acc[j][e] += Cvt<TOut>::to(rr[e]);
+    }
     if (relu)
 #pragma unroll
       for (int e = 0; e < T; ++e) acc[j][e] = fmaxf(acc[j][e], 0.f);
-    if constexpr (std::is_same<TOut, float>::value && T % 4 == 0) {
+    if (std::is_same<TOut, float>::value && T % 4 == 0 && ld_out % 4 == 0) {
 #pragma unroll
       for (int e = 0; e < T; e += 4)
         *reinterpret_cast<float4*>(dst + e) = make_float4(acc[j][e], acc[j][e + 1], acc[j][e + 2], acc[j][e + 3]);
@@ -381,13 +394,13 @@ constexpr int kBlock = 256;
 inline unsigned blocks_for(int64_t n) { return static_cast<unsigned>(std::max<int64_t>(1, ceil_div<int64_t>(n, kBlock))); }
 
 template <class TIn, class TOp>
-void gather_dispatch(Ctx& ctx, int T, const void* f_in, int c_in, const LayerPlan& plan, const int32_t* starts,
-                     const int32_t* pair_in, int64_t rows, int k_pad, void* buf) {
+void gather_dispatch(Ctx& ctx, int T, const void* f_in, int c_in, int64_t ld_in, const LayerPlan& plan,
+                     const int32_t* starts, const int32_t* pair_in, int64_t rows, int k_pad, void* buf) {
   const int64_t work = rows * (c_in / T);
   auto go = [&](auto kern) {
     ctx.launch("k_gather", [&] {
-      kern<<<blocks_for(work), kBlock, 0, ctx.stream>>>(static_cast<const TIn*>(f_in), c_in, plan, starts, pair_in,
-                                                        rows, k_pad, static_cast<TOp*>(buf));
+      kern<<<blocks_for(work), kBlock, 0, ctx.stream>>>(static_cast<const TIn*>(f_in), c_in, ld_in, plan, starts,
+                                                        pair_in, rows, k_pad, static_cast<TOp*>(buf));
     });
   };
   switch (T) {
@@ -409,12 +422,13 @@ void gather_dispatch(Ctx& ctx, int T, const void* f_in, int c_in, const LayerPla
 
 template <class TOut>
 void scatter_dispatch(Ctx& ctx, int T, const float* gemm_out, int c_out, const int32_t* nbr, int64_t n_out, int K3,
-                      const LayerPlan& plan, void* f_out, int relu) {
+                      const LayerPlan& plan, const LayerIO& io) {
   const int64_t work = n_out * (c_out / T);
   auto go = [&](auto kern) {
     ctx.launch("k_scatter", [&] {
       kern<<<blocks_for(work), kBlock, 0, ctx.stream>>>(gemm_out, c_out, nbr, n_out, K3, plan,
-                                                        static_cast<TOut*>(f_out), relu);
+                                                        static_cast<TOut*>(io.f_out), io.ld_out,
+                                                        static_cast<const TOut*>(io.res), io.ld_res, io.relu);
     });
   };
   switch (T) {
@@ -448,14 +462,15 @@ bool seg_scatter_ok(int c_out, int T, int part_bytes) {
 
 template <class TP, class TOut>
 void scatter_seg_dispatch(Ctx& ctx, int T, const TP* partials, int c_out, const int32_t* nbr, int64_t n_out, int K3,
-                          const LayerPlan& plan, void* f_out, int relu) {
+                          const LayerPlan& plan, const LayerIO& io) {
   const int TI = scatter_rows(c_out, T, sizeof(TP));
   const size_t smem = static_cast<size_t>(kScatStages) * TI * c_out * sizeof(TP) + sizeof(int32_t) * (K3 * TI + 3 * K3) + 16;
   auto go = [&](auto kern) {
     SCONV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     ctx.launch("k_scatter", [&] {
       kern<<<static_cast<unsigned>(ceil_div<int64_t>(n_out, TI)), kScatThreads, smem, ctx.stream>>>(
-          partials, c_out, nbr, n_out, K3, plan, static_cast<TOut*>(f_out), relu, TI);
+          partials, c_out, nbr, n_out, K3, plan, static_cast<TOut*>(io.f_out), io.ld_out,
+          static_cast<const TOut*>(io.res), io.ld_res, io.relu, TI);
     });
   };
   switch (T) {
@@ -539,14 +554,10 @@ std::unique_ptr<WeightData> create_weights(Ctx& ctx, const float* w, int mem, in
 }
 
 // ---------------------------------------------------------------- layer forward
-void layer_forward(Ctx& ctx, MapData& m, const WeightData& w, const void* f_in, int f_in_dtype, int f_in_mem,
-                   const sconv_exec_cfg& cfg, void* f_out, int f_out_dtype, int f_out_mem, int relu) {
-  if (w.K3 != m.K3) fail(SCONV_ERR_ARG, "weight count does not match the kernel volume");
-  if (f_in_dtype != SCONV_F32 && f_in_dtype != SCONV_F16 && f_in_dtype != SCONV_BF16)
-    fail(SCONV_ERR_ARG, "unsupported input dtype");
-  if (f_out_dtype != SCONV_F32 && f_out_dtype != SCONV_F16 && f_out_dtype != SCONV_BF16)
-    fail(SCONV_ERR_ARG, "unsupported output dtype");
-  if (f_in_dtype != SCONV_F32 && f_in_dtype != w.dtype) fail(SCONV_ERR_ARG, "16-bit input must match the weight dtype");
+namespace {
+
+// Minuet GMaS on device buffers: plan -> gather -> grouped GEMM -> scatter.
+void gmas_forward(Ctx& ctx, MapData& m, const WeightData& w, const sconv_exec_cfg& cfg, const LayerIO& io) {
   const cudaStream_t st = ctx.stream;
   const int c_in = w.c_in, c_out = w.c_out, K3 = m.K3;
   int Tg = cfg.gather_tile, Ts = cfg.scatter_tile;
@@ -565,72 +576,61 @@ void layer_forward(Ctx& ctx, MapData& m, const WeightData& w, const void* f_in, 
   m.gather_tile = Tg;
   m.scatter_tile = Ts;
   const int64_t R = plan.buffer_length;
-
-  // input features to device if needed
-  DevBuf fin_dev, fout_dev;
-  const void* fin = f_in;
-  if (f_in_mem == SCONV_MEM_HOST && m.n_in > 0) {
-    const size_t bytes = dtype_size(f_in_dtype) * m.n_in * c_in;
-    fin_dev.alloc(bytes, st);
-    SCONV_CUDA(cudaMemcpyAsync(fin_dev.get(), f_in, bytes, cudaMemcpyHostToDevice, st));
-    fin = fin_dev.get();
+  const size_t out_elem = dtype_size(io.out_dtype);
+  if (R == 0 || m.n_in == 0) {
+    if (io.res == nullptr && io.ld_out == c_out) {
+      SCONV_CUDA(cudaMemsetAsync(io.f_out, 0, out_elem * m.n_out * c_out, st));
+      return;
+    }
   }
-  void* fout = f_out;
-  const size_t out_bytes = dtype_size(f_out_dtype) * m.n_out * c_out;
-  if (f_out_mem == SCONV_MEM_HOST && m.n_out > 0) {
-    fout_dev.alloc(out_bytes, st);
-    fout = fout_dev.get();
-  }
-  if (m.n_out > 0 && (R == 0 || m.n_in == 0)) {
-    SCONV_CUDA(cudaMemsetAsync(fout, 0, out_bytes, st));
-  } else if (m.n_out > 0) {
-    // ---- plan (members in buffer order, GEMM tile prefix, scatter deltas): a kernel
-    // parameter, so consecutive layers never race on a staging buffer.
-    if (plan.order.size() > static_cast<size_t>(kMaxOffsets)) fail(SCONV_ERR_ARG, "too many offsets");
-    auto lp = std::make_unique<LayerPlan>();
-    const int block_n = std::min(w.n_pad, 256);
-    lp->block_n = block_n;
-    lp->n_blocks = ceil_div(w.n_pad, block_n);
-    lp->nm = 0;
-    lp->tile_start[0] = 0;
-    for (const auto& g : plan.groups)
-      for (int q = g.begin; q < g.end; ++q) {
-        const int k = plan.order[q];
-        lp->members[lp->nm] = make_int4(k, static_cast<int>(plan.buffer_offsets[k]), static_cast<int>(m.sizes[k]),
-                                        static_cast<int>(g.height));
-        lp->tile_start[lp->nm + 1] = lp->tile_start[lp->nm] + ceil_div(static_cast<int>(g.height), 128) * lp->n_blocks;
-        ++lp->nm;
-      }
-    lp->num_tiles = lp->tile_start[lp->nm];
-    for (int k = 0; k < K3; ++k)
-      lp->delta[k] = plan.buffer_offsets[k] >= 0 ? static_cast<int32_t>(plan.buffer_offsets[k] - m.starts[k]) : 0;
+  // ---- plan (members in buffer order, GEMM tile prefix, scatter deltas): a kernel
+  // parameter, so consecutive layers never race on a staging buffer.
+  if (plan.order.size() > static_cast<size_t>(kMaxOffsets)) fail(SCONV_ERR_ARG, "too many offsets");
+  auto lp = std::make_unique<LayerPlan>();
+  const int block_n = std::min(w.n_pad, 256);
+  lp->block_n = block_n;
+  lp->n_blocks = ceil_div(w.n_pad, block_n);
+  lp->nm = 0;
+  lp->tile_start[0] = 0;
+  for (const auto& g : plan.groups)
+    for (int q = g.begin; q < g.end; ++q) {
+      const int k = plan.order[q];
+      lp->members[lp->nm] = make_int4(k, static_cast<int>(plan.buffer_offsets[k]), static_cast<int>(m.sizes[k]),
+                                      static_cast<int>(g.height));
+      lp->tile_start[lp->nm + 1] = lp->tile_start[lp->nm] + ceil_div(static_cast<int>(g.height), 128) * lp->n_blocks;
+      ++lp->nm;
+    }
+  lp->num_tiles = lp->tile_start[lp->nm];
+  for (int k = 0; k < K3; ++k)
+    lp->delta[k] = plan.buffer_offsets[k] >= 0 ? static_cast<int32_t>(plan.buffer_offsets[k] - m.starts[k]) : 0;
 
+  const int k_pad = w.k_pad;
+  const bool part_f16 = cfg.partial_f16 && w.dtype == SCONV_F16 && seg_scatter_ok(c_out, Ts, 2);
+  const int part_bytes = part_f16 ? 2 : 4;
+  if (R > 0 && m.n_in > 0) {
     // ---- gather
-    const int k_pad = w.k_pad;
     ctx.gather_buf.reserve(static_cast<size_t>(R) * k_pad * 2, st);
     if (k_pad != c_in) SCONV_CUDA(cudaMemsetAsync(ctx.gather_buf.get(), 0, static_cast<size_t>(R) * k_pad * 2, st));
     const int32_t* starts = m.map_start.get<int32_t>();
     const int32_t* pin_idx = m.pair_in.get<int32_t>();
+    void* gb = ctx.gather_buf.get();
     if (w.dtype == SCONV_F16) {
-      if (f_in_dtype == SCONV_F32)
-        gather_dispatch<float, __half>(ctx, Tg, fin, c_in, *lp, starts, pin_idx, R, k_pad, ctx.gather_buf.get());
+      if (io.in_dtype == SCONV_F32)
+        gather_dispatch<float, __half>(ctx, Tg, io.f_in, c_in, io.ld_in, *lp, starts, pin_idx, R, k_pad, gb);
       else
-        gather_dispatch<__half, __half>(ctx, Tg, fin, c_in, *lp, starts, pin_idx, R, k_pad, ctx.gather_buf.get());
+        gather_dispatch<__half, __half>(ctx, Tg, io.f_in, c_in, io.ld_in, *lp, starts, pin_idx, R, k_pad, gb);
     } else {
-      if (f_in_dtype == SCONV_F32)
-        gather_dispatch<float, __nv_bfloat16>(ctx, Tg, fin, c_in, *lp, starts, pin_idx, R, k_pad,
-                                              ctx.gather_buf.get());
+      if (io.in_dtype == SCONV_F32)
+        gather_dispatch<float, __nv_bfloat16>(ctx, Tg, io.f_in, c_in, io.ld_in, *lp, starts, pin_idx, R, k_pad, gb);
       else
-        gather_dispatch<__nv_bfloat16, __nv_bfloat16>(ctx, Tg, fin, c_in, *lp, starts, pin_idx, R, k_pad,
-                                                      ctx.gather_buf.get());
+        gather_dispatch<__nv_bfloat16, __nv_bfloat16>(ctx, Tg, io.f_in, c_in, io.ld_in, *lp, starts, pin_idx, R, k_pad,
+                                                      gb);
     }
-    // ---- grouped GEMM
-    // per-offset partials: f16 when computing in f16 (halves the largest stream), else fp32
-    const bool part_f16 = cfg.partial_f16 && w.dtype == SCONV_F16 && seg_scatter_ok(c_out, Ts, 2);
-    const int part_bytes = part_f16 ? 2 : 4;
+    // ---- grouped GEMM: per-offset partials, f16 when computing in f16 (halves the largest
+    // stream), else fp32
     ctx.gemm_out.reserve(static_cast<size_t>(R) * c_out * part_bytes, st);
     GemmArgs ga;
-    ga.a = ctx.gather_buf.get();
+    ga.a = gb;
     ga.b = w.buf.get();
     ga.plan = lp.get();
     ga.num_tiles = lp->num_tiles;
@@ -645,34 +645,111 @@ void layer_forward(Ctx& ctx, MapData& m, const WeightData& w, const void* f_in, 
     ga.out = ctx.gemm_out.get();
     ga.out_f16 = part_f16;
     launch_grouped_gemm(ctx, ga);
-    // ---- scatter
-    const int32_t* nbr = m.nbr_pos.get<int32_t>();
-    if (part_f16) {
-      if (f_out_dtype == SCONV_F32)
-        scatter_seg_dispatch<__half, float>(ctx, Ts, ctx.gemm_out.get<__half>(), c_out, nbr, m.n_out, K3, *lp, fout, relu);
-      else if (f_out_dtype == SCONV_F16)
-        scatter_seg_dispatch<__half, __half>(ctx, Ts, ctx.gemm_out.get<__half>(), c_out, nbr, m.n_out, K3, *lp, fout,
-                                             relu);
-      else
-        scatter_seg_dispatch<__half, __nv_bfloat16>(ctx, Ts, ctx.gemm_out.get<__half>(), c_out, nbr, m.n_out, K3, *lp,
-                                                    fout, relu);
-    } else if (seg_scatter_ok(c_out, Ts, 4)) {
-      if (f_out_dtype == SCONV_F32)
-        scatter_seg_dispatch<float, float>(ctx, Ts, ctx.gemm_out.get<float>(), c_out, nbr, m.n_out, K3, *lp, fout, relu);
-      else if (f_out_dtype == SCONV_F16)
-        scatter_seg_dispatch<float, __half>(ctx, Ts, ctx.gemm_out.get<float>(), c_out, nbr, m.n_out, K3, *lp, fout, relu);
-      else
-        scatter_seg_dispatch<float, __nv_bfloat16>(ctx, Ts, ctx.gemm_out.get<float>(), c_out, nbr, m.n_out, K3, *lp,
-                                                   fout, relu);
-    } else {
-      if (f_out_dtype == SCONV_F32)
-        scatter_dispatch<float>(ctx, Ts, ctx.gemm_out.get<float>(), c_out, nbr, m.n_out, K3, *lp, fout, relu);
-      else if (f_out_dtype == SCONV_F16)
-        scatter_dispatch<__half>(ctx, Ts, ctx.gemm_out.get<float>(), c_out, nbr, m.n_out, K3, *lp, fout, relu);
-      else
-        scatter_dispatch<__nv_bfloat16>(ctx, Ts, ctx.gemm_out.get<float>(), c_out, nbr, m.n_out, K3, *lp, fout, relu);
-    }
   }
+  // ---- scatter (rows without matches: zero [+ residual])
+  const int32_t* nbr = m.nbr_pos.get<int32_t>();
+  if (part_f16) {
+    if (io.out_dtype == SCONV_F32)
+      scatter_seg_dispatch<__half, float>(ctx, Ts, ctx.gemm_out.get<__half>(), c_out, nbr, m.n_out, K3, *lp, io);
+    else if (io.out_dtype == SCONV_F16)
+      scatter_seg_dispatch<__half, __half>(ctx, Ts, ctx.gemm_out.get<__half>(), c_out, nbr, m.n_out, K3, *lp, io);
+    else
+      scatter_seg_dispatch<__half, __nv_bfloat16>(ctx, Ts, ctx.gemm_out.get<__half>(), c_out, nbr, m.n_out, K3, *lp,
+                                                  io);
+  } else if (seg_scatter_ok(c_out, Ts, 4)) {
+    if (io.out_dtype == SCONV_F32)
+      scatter_seg_dispatch<float, float>(ctx, Ts, ctx.gemm_out.get<float>(), c_out, nbr, m.n_out, K3, *lp, io);
+    else if (io.out_dtype == SCONV_F16)
+      scatter_seg_dispatch<float, __half>(ctx, Ts, ctx.gemm_out.get<float>(), c_out, nbr, m.n_out, K3, *lp, io);
+    else
+      scatter_seg_dispatch<float, __nv_bfloat16>(ctx, Ts, ctx.gemm_out.get<float>(), c_out, nbr, m.n_out, K3, *lp, io);
+  } else {
+    if (io.out_dtype == SCONV_F32)
+      scatter_dispatch<float>(ctx, Ts, ctx.gemm_out.get<float>(), c_out, nbr, m.n_out, K3, *lp, io);
+    else if (io.out_dtype == SCONV_F16)
+      scatter_dispatch<__half>(ctx, Ts, ctx.gemm_out.get<float>(), c_out, nbr, m.n_out, K3, *lp, io);
+    else
+      scatter_dispatch<__nv_bfloat16>(ctx, Ts, ctx.gemm_out.get<float>(), c_out, nbr, m.n_out, K3, *lp, io);
+  }
+}
+
+// Fused output-stationary dataflow (conv_fused.cu): operands must be 16-bit rows of at least
+// k_pad zero-padded columns; anything else is converted once into the gather scratch.
+void fused_forward(Ctx& ctx, MapData& m, const WeightData& w, const LayerIO& io) {
+  m.buffer_length = 0;
+  m.groups = 0;
+  m.padding_overhead = 0.0;
+  m.gather_tile = m.scatter_tile = 0;
+  const void* fin = io.f_in;
+  int64_t ld = io.ld_in;
+  const bool direct = io.in_dtype == w.dtype && ld % 8 == 0 && ld >= w.k_pad && (w.k_pad == w.c_in || io.in_zero_padded);
+  if (!direct && m.n_in > 0) {
+    ctx.gather_buf.reserve(static_cast<size_t>(m.n_in) * w.k_pad * 2, ctx.stream);
+    convert_rows(ctx, io.f_in, io.in_dtype, m.n_in, w.c_in, io.ld_in, ctx.gather_buf.get(), w.dtype, w.k_pad);
+    fin = ctx.gather_buf.get();
+    ld = w.k_pad;
+  }
+  FusedArgs a;
+  a.f_in = fin;
+  a.ld_in = ld;
+  a.nbr = m.nbr_in.get<int32_t>();
+  a.n_out = m.n_out;
+  a.w = &w;
+  a.out = io.f_out;
+  a.out_dtype = io.out_dtype;
+  a.ld_out = io.ld_out;
+  a.res = io.res;
+  a.ld_res = io.ld_res;
+  a.relu = io.relu;
+  launch_conv_fused(ctx, a);
+}
+
+}  // namespace
+
+void layer_forward_dev(Ctx& ctx, MapData& m, const WeightData& w, const sconv_exec_cfg& cfg, int dataflow,
+                       const LayerIO& io) {
+  if (w.K3 != m.K3) fail(SCONV_ERR_ARG, "weight count does not match the kernel volume");
+  if (io.in_dtype != SCONV_F32 && io.in_dtype != SCONV_F16 && io.in_dtype != SCONV_BF16)
+    fail(SCONV_ERR_ARG, "unsupported input dtype");
+  if (io.out_dtype != SCONV_F32 && io.out_dtype != SCONV_F16 && io.out_dtype != SCONV_BF16)
+    fail(SCONV_ERR_ARG, "unsupported output dtype");
+  if (io.in_dtype != SCONV_F32 && io.in_dtype != w.dtype) fail(SCONV_ERR_ARG, "16-bit input must match the weight dtype");
+  if (io.ld_in < w.c_in || io.ld_out < w.c_out || (io.res && io.ld_res < w.c_out))
+    fail(SCONV_ERR_ARG, "row stride smaller than the channel count");
+  if (m.n_out == 0) return;
+  if (dataflow == SCONV_DATAFLOW_FUSED && fused_supported(m.K3, w.c_in, w.c_out))
+    fused_forward(ctx, m, w, io);
+  else
+    gmas_forward(ctx, m, w, cfg, io);
+}
+
+void layer_forward(Ctx& ctx, MapData& m, const WeightData& w, const void* f_in, int f_in_dtype, int f_in_mem,
+                   const sconv_exec_cfg& cfg, void* f_out, int f_out_dtype, int f_out_mem, int relu) {
+  const cudaStream_t st = ctx.stream;
+  DevBuf fin_dev, fout_dev;
+  const void* fin = f_in;
+  if (f_in_mem == SCONV_MEM_HOST && m.n_in > 0) {
+    const size_t bytes = dtype_size(f_in_dtype) * m.n_in * w.c_in;
+    fin_dev.alloc(bytes, st);
+    SCONV_CUDA(cudaMemcpyAsync(fin_dev.get(), f_in, bytes, cudaMemcpyHostToDevice, st));
+    fin = fin_dev.get();
+  }
+  void* fout = f_out;
+  const size_t out_bytes = dtype_size(f_out_dtype) * m.n_out * w.c_out;
+  if (f_out_mem == SCONV_MEM_HOST && m.n_out > 0) {
+    fout_dev.alloc(out_bytes, st);
+    fout = fout_dev.get();
+  }
+  LayerIO io;
+  io.f_in = fin;
+  io.in_dtype = f_in_dtype;
+  io.ld_in = w.c_in;
+  io.f_out = fout;
+  io.out_dtype = f_out_dtype;
+  io.ld_out = w.c_out;
+  io.relu = relu;
+  layer_forward_dev(ctx, m, w, cfg, cfg.dataflow == SCONV_DATAFLOW_FUSED ? SCONV_DATAFLOW_FUSED : SCONV_DATAFLOW_GMAS,
+                    io);
   if (f_out_mem == SCONV_MEM_HOST && m.n_out > 0) {
     SCONV_CUDA(cudaMemcpyAsync(f_out, fout, out_bytes, cudaMemcpyDeviceToHost, st));
     ctx.sync();

@@ -54,6 +54,23 @@ int padded_k(int c_in);
 void layer_forward(Ctx& ctx, MapData& m, const WeightData& w, const void* f_in, int f_in_dtype, int f_in_mem,
                    const sconv_exec_cfg& cfg, void* f_out, int f_out_dtype, int f_out_mem, int relu = 0);
 
+// Device-resident layer I/O (network driver): strided rows, optional residual + ReLU epilogue.
+struct LayerIO {
+  const void* f_in = nullptr;
+  int in_dtype = SCONV_F32;
+  int64_t ld_in = 0;           // row stride (elements)
+  bool in_zero_padded = false;  // columns [c_in, ld_in) are zero (fused dataflow may read them)
+  void* f_out = nullptr;
+  int out_dtype = SCONV_F32;
+  int64_t ld_out = 0;
+  const void* res = nullptr;  // residual rows (out_dtype, Q order) added before the ReLU
+  int64_t ld_res = 0;
+  int relu = 0;
+};
+// dataflow: SCONV_DATAFLOW_GMAS or SCONV_DATAFLOW_FUSED (cfg.dataflow AUTO is resolved by callers)
+void layer_forward_dev(Ctx& ctx, MapData& m, const WeightData& w, const sconv_exec_cfg& cfg, int dataflow,
+                       const LayerIO& io);
+
 }  // namespace sconvb
 
 struct sconv_weights : sconvb::WeightData {};

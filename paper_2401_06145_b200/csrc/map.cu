@@ -578,10 +578,11 @@ __global__ void __launch_bounds__(kSearchThreads) k_scan_counts(const int32_t* _
 }
 
 // Canonical positions: m = chunk_off[k, c] + rank of the hit inside the chunk (query
-// order). One CTA per query chunk; warp w emits offsets k = w, w+8, ... with ballot ranks,
+// order), written to a second table (the input-row table stays for the fused dataflow). One CTA per query chunk; warp w emits offsets k = w, w+8, ... with ballot ranks,
 // so no CTA-level barrier is needed.
 template <int QPL>
-__global__ void __launch_bounds__(kSearchThreads) k_emit(int32_t* __restrict__ nbr, int64_t n_q, int K3,
+__global__ void __launch_bounds__(kSearchThreads) k_emit(const int32_t* __restrict__ nbr, int32_t* __restrict__ pos,
+                                                          int64_t n_q, int K3,
                                                           int64_t nchunk, int ngroups, const int32_t* __restrict__ chunk_off,
                                                           const int32_t* __restrict__ tile_base,
                                                           int32_t* __restrict__ pair_in, int32_t* __restrict__ pair_out) {
@@ -592,7 +593,8 @@ __global__ void __launch_bounds__(kSearchThreads) k_emit(int32_t* __restrict__ n
   const int64_t lo = c * CQ;
   const unsigned lt = (1u << lane) - 1u;
   for (int k = grp + warp * ngroups; k < K3; k += K3) {
-    int32_t* row = nbr + int64_t{k} * n_q + lo;
+    const int32_t* row = nbr + int64_t{k} * n_q + lo;
+    int32_t* prow = pos + int64_t{k} * n_q + lo;
     const int64_t ci = int64_t{k} * nchunk + c;
     int base = __ldg(chunk_off + ci) + __ldg(tile_base + ci / kScanTile);
     int32_t j[QPL];
@@ -608,7 +610,7 @@ __global__ void __launch_bounds__(kSearchThreads) k_emit(int32_t* __restrict__ n
           pair_in[m] = j[u];
           pair_out[m] = static_cast<int32_t>(lo + u * 32 + lane);
         }
-        row[u * 32 + lane] = m;
+        prow[u * 32 + lane] = m;
       }
       base += __popc(bal);
     }
@@ -870,11 +872,13 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
   SCONV_CUDA(cudaMemcpyAsync(m->offsets.get(), pin_off, sizeof(int3) * K3, cudaMemcpyHostToDevice, st));
   m->map_start.alloc(sizeof(int32_t) * (K3 + 1), st);
   m->nbr_pos.alloc(sizeof(int32_t) * std::max<int64_t>(1, int64_t{K3} * n_out), st);
+  m->nbr_in.alloc(sizeof(int32_t) * std::max<int64_t>(1, int64_t{K3} * n_out), st);
   const int B = cfg.block_B, C = cfg.block_C;
   // upper bound on the match count: every query hits at most once
   const int64_t max_pairs = std::min<int64_t>(int64_t{K3} * n_out, int64_t{K3} * n);
   if (n == 0 || n_out == 0) {
     SCONV_CUDA(cudaMemsetAsync(m->map_start.get(), 0, sizeof(int32_t) * (K3 + 1), st));
+    if (n_out > 0) SCONV_CUDA(cudaMemsetAsync(m->nbr_in.get(), 0xFF, sizeof(int32_t) * int64_t{K3} * n_out, st));
     if (n_out > 0)
       SCONV_CUDA(cudaMemsetAsync(m->nbr_pos.get(), 0xFF, sizeof(int32_t) * int64_t{K3} * n_out, st));
   } else {
@@ -907,7 +911,7 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
       ctx.launch("k_search", [&] {
         kern<<<static_cast<unsigned>(nchunk2 * ngroups), kSearchThreads, smem, st>>>(
             src, src_idx, n, B, q, n_out, m->offsets.get<int3>(), K3, kmin_off, kmax_off, nchunk2, ngroups, cap_blocks,
-            m->nbr_pos.get<int32_t>(), counts.get<int32_t>(), offs.get<int32_t>(), ctx.done_counter(),
+            m->nbr_in.get<int32_t>(), counts.get<int32_t>(), offs.get<int32_t>(), ctx.done_counter(),
             m->map_start.get<int32_t>());
       });
     };
@@ -925,7 +929,8 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
     auto emit = [&](auto kern) {
       ctx.launch("k_emit", [&] {
         kern<<<static_cast<unsigned>(nchunk2 * ngroups), kSearchThreads, 0, st>>>(
-            m->nbr_pos.get<int32_t>(), n_out, K3, nchunk2, ngroups, offs.get<int32_t>(), tiles.get<int32_t>(),
+            m->nbr_in.get<int32_t>(), m->nbr_pos.get<int32_t>(), n_out, K3, nchunk2, ngroups, offs.get<int32_t>(),
+            tiles.get<int32_t>(),
             m->pair_in.get<int32_t>(),
                                                                         m->pair_out.get<int32_t>());
       });

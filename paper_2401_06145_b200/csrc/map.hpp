@@ -22,6 +22,7 @@ struct MapData {
   DevBuf map_start;  // int32 x (K3 + 1): canonical list starts
   DevBuf pair_in, pair_out;  // int32 x |M|, canonical order (k, then i)
   DevBuf nbr_pos;            // int32 x K3 x n_out: canonical position m of (k, i) or -1
+  DevBuf nbr_in;             // int32 x K3 x n_out: input row j of (k, i) or -1 (fused dataflow)
   std::vector<int64_t> sizes;      // n_k (host)
   std::vector<int32_t> starts;     // map_start (host copy)
   int64_t total = 0;

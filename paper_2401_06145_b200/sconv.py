@@ -26,6 +26,7 @@ OK, ERR_ARG, ERR_RANGE, ERR_CUDA, ERR_OOM, ERR_STATE = range(6)
 MEM_HOST, MEM_DEVICE = 0, 1
 F32, F16, BF16 = 0, 1, 2
 GROUP_MAP_ORDER, GROUP_SORTED = 0, 1
+DATAFLOW_GMAS, DATAFLOW_FUSED, DATAFLOW_AUTO = 0, 1, 2
 
 
 class SconvError(RuntimeError):
@@ -56,7 +57,7 @@ class MapCfg(C.Structure):
 class ExecCfg(C.Structure):
     _fields_ = [("policy", C.c_int), ("epsilon", C.c_double), ("max_batch", C.c_int),
                 ("gather_tile", C.c_int), ("scatter_tile", C.c_int), ("compute_dtype", C.c_int),
-                ("partial_f16", C.c_int)]
+                ("partial_f16", C.c_int), ("dataflow", C.c_int), ("fuse_residual", C.c_int)]
 
 
 class MapInfo(C.Structure):
@@ -205,8 +206,11 @@ def map_cfg(K=3, offset_scale=1, out_stride=1, transposed=False, B=256, Cq=512) 
 
 
 def exec_cfg(policy=GROUP_SORTED, epsilon=0.25, max_batch=16, gather_tile=0, scatter_tile=0,
-             compute_dtype=F16, partial_f16=1) -> ExecCfg:
-    return ExecCfg(policy, epsilon, max_batch, gather_tile, scatter_tile, compute_dtype, partial_f16)
+             compute_dtype=F16, partial_f16=1, dataflow=None, fuse_residual=1) -> ExecCfg:
+    """dataflow: GMAS (Minuet gather/GEMM/scatter), FUSED (one output-stationary kernel) or
+    AUTO (networks: per-conv choice by timing); None = GMAS for layers, AUTO for networks."""
+    return ExecCfg(policy, epsilon, max_batch, gather_tile, scatter_tile, compute_dtype, partial_f16,
+                   -1 if dataflow is None else dataflow, fuse_residual)
 
 
 class KernelMap:
