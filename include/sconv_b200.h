@@ -199,13 +199,20 @@ sconv_status sconv_net_forward(sconv_ctx* ctx, sconv_net* net, const int32_t* xy
                                const float* feats, int f_mem, int c_in);
 sconv_status sconv_net_tensor_info(sconv_ctx* ctx, const sconv_net* net, int tensor, int64_t* n, int* channels,
                                    int* coordset);
-/* Host readback: coordinates (n x 3, sorted unless the tensor is the unsorted raw input) and fp32 features. */
+/* Host readback: coordinates (n x 3, sorted unless the tensor is the unsorted raw input) and fp32
+ * features (activations are stored in the compute dtype and widened on device). A tensor whose
+ * producing conv was folded into a residual epilogue (cfg.fuse_residual) returns SCONV_ERR_STATE. */
 sconv_status sconv_net_read_tensor(sconv_ctx* ctx, const sconv_net* net, int tensor, int32_t* xyz, float* feats);
-/* Device view of a tensor's fp32 features (valid until the next forward). */
-sconv_status sconv_net_tensor_device(const sconv_net* net, int tensor, const float** feats);
+/* Device view of a tensor's features: pointer, dtype (sconv_dtype) and row stride in elements
+ * (valid until the next forward). */
+sconv_status sconv_net_tensor_device(const sconv_net* net, int tensor, const void** feats, int* dtype, int64_t* ld);
 sconv_status sconv_net_stats(const sconv_net* net, int* maps_built, int* convs);
-/* Per CONV op (execution order) of the last forward: {n_in, n_out, |M|, R_pad, c_in, c_out, k_pad, K3}. */
-sconv_status sconv_net_conv_stats(const sconv_net* net, int conv, int64_t* out8);
+/* Per CONV op (execution order) of the last forward: {n_in, n_out, |M|, R_pad (0 if fused), c_in, c_out,
+ * k_pad, K3, dataflow, residual_folded}. */
+sconv_status sconv_net_conv_stats(const sconv_net* net, int conv, int64_t* out10);
+/* AUTO dataflow measurements of the tuning forward for op index `op` (ms; -1 when the op was
+ * not tuned): Minuet GMaS vs the fused kernel. */
+sconv_status sconv_net_conv_timings(const sconv_net* net, int op, double* gmas_ms, double* fused_ms);
 void sconv_net_free(sconv_ctx* ctx, sconv_net* net);
 
 /* ---------------- utilities (cli gen) ----------------

@@ -11,6 +11,7 @@
 
 #include "common.cuh"
 #include "ctx.hpp"
+#include "conv_fused.hpp"
 #include "gmas.hpp"
 #include "map.hpp"
 #include "net.hpp"
@@ -578,10 +579,15 @@ sconv_status sconv_net_read_tensor(sconv_ctx* ctx, const sconv_net* net, int ten
   return guarded(ctx, [&] {
     if (!net || tensor < 0 || tensor >= static_cast<int>(net->tensors.size())) fail(SCONV_ERR_ARG, "bad tensor");
     const NetTensor& t = net->tensors[tensor];
+    if (t.fused_away) fail(SCONV_ERR_STATE, "tensor was folded into a fused residual epilogue");
     if (t.coordset < 0) fail(SCONV_ERR_STATE, "tensor not produced");
-    if (feats && t.n > 0)
-      SCONV_CUDA(cudaMemcpyAsync(feats, t.feats.get(), sizeof(float) * t.n * t.channels, cudaMemcpyDeviceToHost,
+    if (feats && t.n > 0) {
+      auto* n = const_cast<sconv_net*>(net);
+      n->readback.reserve(sizeof(float) * t.n * t.channels, ctx->stream);
+      convert_rows(*ctx, t.feats.get(), t.dtype, t.n, t.channels, t.ld, n->readback.get(), SCONV_F32, t.channels);
+      SCONV_CUDA(cudaMemcpyAsync(feats, n->readback.get(), sizeof(float) * t.n * t.channels, cudaMemcpyDeviceToHost,
                                  ctx->stream));
+    }
     if (xyz && t.n > 0) {
       const CoordSet& cs = net->coordsets[t.coordset];
       if (cs.keys) {
@@ -597,9 +603,13 @@ sconv_status sconv_net_read_tensor(sconv_ctx* ctx, const sconv_net* net, int ten
   });
 }
 
-sconv_status sconv_net_tensor_device(const sconv_net* net, int tensor, const float** feats) {
+sconv_status sconv_net_tensor_device(const sconv_net* net, int tensor, const void** feats, int* dtype, int64_t* ld) {
   if (!net || tensor < 0 || tensor >= static_cast<int>(net->tensors.size()) || !feats) return SCONV_ERR_ARG;
-  *feats = net->tensors[tensor].feats.get<float>();
+  const NetTensor& t = net->tensors[tensor];
+  if (t.fused_away || t.coordset < 0) return SCONV_ERR_STATE;
+  *feats = t.feats.get();
+  if (dtype) *dtype = t.dtype;
+  if (ld) *ld = t.ld;
   return SCONV_OK;
 }
 
@@ -614,9 +624,16 @@ sconv_status sconv_net_stats(const sconv_net* net, int* maps_built, int* convs) 
   return SCONV_OK;
 }
 
-sconv_status sconv_net_conv_stats(const sconv_net* net, int conv, int64_t* out8) {
-  if (!net || !out8 || conv < 0 || conv >= static_cast<int>(net->conv_stats.size())) return SCONV_ERR_ARG;
-  for (int i = 0; i < 8; ++i) out8[i] = net->conv_stats[conv][i];
+sconv_status sconv_net_conv_stats(const sconv_net* net, int conv, int64_t* out10) {
+  if (!net || !out10 || conv < 0 || conv >= static_cast<int>(net->conv_stats.size())) return SCONV_ERR_ARG;
+  for (int i = 0; i < 10; ++i) out10[i] = net->conv_stats[conv][i];
+  return SCONV_OK;
+}
+
+sconv_status sconv_net_conv_timings(const sconv_net* net, int op, double* gmas_ms, double* fused_ms) {
+  if (!net || op < 0 || op >= static_cast<int>(net->auto_ms.size())) return SCONV_ERR_ARG;
+  if (gmas_ms) *gmas_ms = net->auto_ms[op][0];
+  if (fused_ms) *fused_ms = net->auto_ms[op][1];
   return SCONV_OK;
 }
 

@@ -15,8 +15,11 @@
 //   warps 0-3  gather producers: index rows of the tile (prefetched one tile ahead into
 //              registers, published in shared memory), cp.async 16-byte chunks with the
 //              UMMA 128/64/32-byte XOR swizzle, zero-fill for missing neighbours; thread 0
-//              also TMA-loads the weight tile W_k^T. Completion: cp.async.wait_group ->
-//              fence.proxy.async -> mbarrier arrive (129 arrivals incl. the TMA expect_tx).
+//              also TMA-loads the weight tile W_k^T. Completion is tracked by the hardware:
+//              cp.async.mbarrier.arrive.noinc (no wait in the producer; 129 arrivals incl.
+//              the TMA expect_tx), so a producer runs up to a whole ring ahead of the MMA.
+//              The MMA thread executes fence.proxy.async after the barrier wait, making the
+//              generic-proxy cp.async writes visible to the tensor core's async-proxy reads.
 //   warps 4-7  epilogue: tcgen05.ld (32 lanes x 16 columns) -> + residual -> ReLU -> store
 //   warp 8     TMEM owner; lane 0 issues tcgen05.mma (M=128, N=block_n, K=16) and commits
 // Two TMEM accumulators let the epilogue of tile t overlap the MMAs of tile t+1.
@@ -34,7 +37,12 @@ using namespace sm100;
 
 constexpr int kProducers = 128, kEpiWarps = 4;
 constexpr int kThreads = kProducers + 32 * kEpiWarps + 32;  // 288
-constexpr int kStages = 4, kLook = kStages - 1;             // cp.async stages in flight per thread
+constexpr int kMaxStages = 12;
+// Tile-info ring (active-offset masks, producers -> MMA). Producers run at most one ring
+// (<= kMaxStages stages, >= 1 per tile) ahead of the MMA, so kInfo > kMaxStages slots never
+// block on a tile the MMA has not reached.
+constexpr int kInfo = 16;
+static_assert(kInfo > kMaxStages, "tile-info ring must cover the stage ring");
 
 template <class T>
 struct OutCvt;
@@ -123,37 +131,41 @@ struct FusedParams {
   int relu;
   int vec;  // 16-byte aligned output / residual rows
   uint32_t stage_bytes, a_bytes, b_bytes, idx_off, bar_off;
+  int stages;  // smem ring depth
   uint32_t tmem_cols;
   int bf16;
 };
 
 // NK = compile-time offset count (registers prefetch the next tile's index rows), 0 = runtime
 template <int NK, int KC, class TOut>
-__global__ void __launch_bounds__(kThreads, 1) k_conv_fused(const __grid_constant__ CUtensorMap tmB,
+__global__ void __launch_bounds__(kThreads, 2) k_conv_fused(const __grid_constant__ CUtensorMap tmB,
                                                            const __grid_constant__ FusedParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t{1023});
-  int32_t* s_idx = reinterpret_cast<int32_t*>(smem + p.idx_off);  // [2][K3][128]
+  int32_t* s_idx = reinterpret_cast<int32_t*>(smem + p.idx_off);  // [K3][128] rows of the current tile
+  const int S = p.stages;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.bar_off);
-  uint64_t* empty = full + kStages;
-  uint64_t* tfull = empty + kStages;
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
   uint64_t* ifull = tempty + 2;
-  uint64_t* iempty = ifull + 2;
-  uint64_t* s_mask = iempty + 2;       // [2] active-offset mask per tile slot
-  uint64_t* s_part = s_mask + 2;       // [2][4] per-producer-warp partial masks
+  uint64_t* iempty = ifull + kInfo;
+  uint64_t* s_mask = iempty + kInfo;   // [kInfo] active-offset mask per tile slot
+  uint64_t* s_part = s_mask + kInfo;   // [2][4] per-producer-warp partial masks
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_part + 8);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int K3 = p.K3;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], kProducers + 1);
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], kEpiWarps);
+    }
+    for (int a = 0; a < kInfo; ++a) {
       mbar_init(&ifull[a], 1);
       mbar_init(&iempty[a], 1);
     }
@@ -186,12 +198,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_fused(const __grid_constan
       for (int k = 0; k < NR; ++k) jn[k] = ok ? __ldg(p.nbr + int64_t{k} * p.n_out + i) : -1;
     };
     if (NK > 0) load_rows(blockIdx.x);
-    uint32_t issued = 0, arrived = 0;  // sequential stage counters
+    uint32_t issued = 0;  // sequential stage counter
     int it = 0;
     for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
       const int buf = it & 1;
       const int nb = t % p.n_blocks;
-      int32_t* srow = s_idx + buf * K3 * 128;
+      int32_t* srow = s_idx;
+      if (it > 0) named_bar(1, kProducers);  // every producer finished reading the previous tile's rows
       uint64_t mine = 0;
       if constexpr (NK > 0) {
 #pragma unroll
@@ -215,9 +228,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_fused(const __grid_constan
       uint64_t mask = s_part[buf * 4] | s_part[buf * 4 + 1] | s_part[buf * 4 + 2] | s_part[buf * 4 + 3];
       if (mask == 0) mask = 1;  // no neighbour at all: one all-zero stage keeps the accumulator defined
       if (tid == 0) {
-        mbar_wait(&iempty[buf], ((it >> 1) & 1) ^ 1);
-        s_mask[buf] = mask;
-        mbar_arrive(&ifull[buf]);
+        const int slot = it % kInfo;
+        mbar_wait(&iempty[slot], ((it / kInfo) & 1) ^ 1);
+        s_mask[slot] = mask;
+        mbar_arrive(&ifull[slot]);
       }
       for (uint64_t m = mask; m; m &= m - 1) {
         const int k = __ffsll(static_cast<long long>(m)) - 1;
@@ -226,8 +240,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_fused(const __grid_constan
 #pragma unroll
         for (int q = 0; q < CPR; ++q) j[q] = sk[rbase + q * RPP];
         for (int kb = 0; kb < p.num_kb; ++kb) {
-          const int stage = static_cast<int>(issued % kStages);
-          mbar_wait(&empty[stage], ((issued / kStages) & 1) ^ 1);
+          const int stage = static_cast<int>(issued % S);
+          mbar_wait(&empty[stage], ((issued / S) & 1) ^ 1);
           uint8_t* sa = smem + stage * p.stage_bytes;
           if (tid == 0) {
             mbar_expect_tx(&full[stage], p.b_bytes);
@@ -240,20 +254,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_fused(const __grid_constan
             const unsigned char* src = col + static_cast<int64_t>(j[q] >= 0 ? j[q] : 0) * p.ld_in_bytes;
             cp_async16(sa32 + a_off[q], src, j[q] >= 0 ? 16u : 0u);
           }
-          cp_async_commit();
+          cp_async_arrive_noinc(&full[stage]);
           ++issued;
-          if (issued - arrived > static_cast<uint32_t>(kLook)) {
-            cp_async_wait<kLook>();
-            fence_proxy_async_smem();
-            mbar_arrive(&full[arrived % kStages]);
-            ++arrived;
-          }
         }
       }
     }
-    cp_async_wait<0>();
-    fence_proxy_async_smem();
-    for (; arrived < issued; ++arrived) mbar_arrive(&full[arrived % kStages]);
   } else if (warp == 8) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
@@ -262,21 +267,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_fused(const __grid_constan
       uint32_t acc_phase = 0;
       int it = 0;
       for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
-        const int buf = it & 1;
         const int nb = t % p.n_blocks;
         const int n_tile = min(p.block_n, p.n_pad - nb * p.block_n);
         const uint32_t idesc = idesc_f16(p.bf16, n_tile);
-        mbar_wait(&ifull[buf], (it >> 1) & 1);
-        const uint64_t mask = s_mask[buf];
-        mbar_arrive(&iempty[buf]);
+        const int slot = it % kInfo;
+        mbar_wait(&ifull[slot], (it / kInfo) & 1);
+        const uint64_t mask = s_mask[slot];
+        mbar_arrive(&iempty[slot]);
         mbar_wait(&tempty[acc], acc_phase ^ 1u);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * p.block_n);
         uint32_t accumulate = 0;
         for (uint64_t m = mask; m; m &= m - 1) {
           for (int kb = 0; kb < p.num_kb; ++kb) {
-            const int stage = static_cast<int>(consumed % kStages);
-            mbar_wait(&full[stage], (consumed / kStages) & 1);
+            const int stage = static_cast<int>(consumed % S);
+            mbar_wait(&full[stage], (consumed / S) & 1);
+            fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tensor core reads
             tc_fence_after();
             const uint32_t sa = smem_u32(smem + stage * p.stage_bytes);
             const uint32_t sb = sa + p.a_bytes;
@@ -376,6 +382,7 @@ template <int NK, int KC, class TOut>
 void launch_t(Ctx& ctx, const FusedArgs& a, const FusedParams& prm, size_t smem, const CUtensorMap& tB) {
   auto kern = k_conv_fused<NK, KC, TOut>;
   SCONV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  SCONV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   int occ = 0;
   SCONV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem));
   occ = std::max(1, std::min<int>(occ, static_cast<int>(512u / prm.tmem_cols)));  // never oversubscribe TMEM
@@ -452,12 +459,22 @@ void launch_conv_fused(Ctx& ctx, const FusedArgs& a) {
   prm.a_bytes = 128u * kc * 2u;
   prm.b_bytes = static_cast<uint32_t>(bn) * kc * 2u;
   prm.stage_bytes = (prm.a_bytes + prm.b_bytes + 1023u) & ~1023u;
-  prm.idx_off = kStages * prm.stage_bytes;
-  prm.bar_off = prm.idx_off + 2u * w.K3 * 128u * 4u;
+  // Ring depth: two CTAs per SM (independent pipelines) when >= 6 stages fit in half the
+  // shared memory, else one CTA with up to kMaxStages stages.
+  const uint32_t idx_bytes = static_cast<uint32_t>(w.K3) * 128u * 4u;
+  const uint32_t fixed = 1024u + idx_bytes + (2 * kMaxStages + 3 * kInfo + 16) * 8u + 64u;
+  const uint32_t half = 113u * 1024u, whole = 227u * 1024u;
+  int stages = fixed < half ? static_cast<int>((half - fixed) / prm.stage_bytes) : 0;
+  if (stages < 6) stages = static_cast<int>((whole - fixed) / prm.stage_bytes);
+  stages = std::min(stages, kMaxStages);
+  if (stages < 2) fail(SCONV_ERR_ARG, "fused layer tile does not fit in shared memory");
+  prm.stages = stages;
+  prm.idx_off = static_cast<uint32_t>(stages) * prm.stage_bytes;
+  prm.bar_off = prm.idx_off + idx_bytes;
   uint32_t cols = 32;
   while (cols < 2u * static_cast<uint32_t>(bn)) cols <<= 1;
   prm.tmem_cols = cols;
-  const size_t smem = 1024 + prm.bar_off + (2 * kStages + 8 + 2 + 8) * 8 + 16;
+  const size_t smem = 1024 + prm.bar_off + (2 * stages + 4 + 3 * kInfo + 8 + 1) * 8 + 16;
   if (smem > 227 * 1024) fail(SCONV_ERR_ARG, "fused layer tile does not fit in shared memory");
   const CUtensorMap tB = make_tensor_map_2d(w.buf.get(), w.dtype, w.k_pad, static_cast<uint64_t>(w.K3) * w.n_pad, kc,
                                             static_cast<uint32_t>(bn), kc);

@@ -2,9 +2,19 @@
 // BASELINE configs 2-5): an op list over tensors, executed asynchronously on the context
 // stream with a cross-layer kernel-map cache.
 //
-//   CONV    out = [relu](SC layer(in; K, offset_scale, out_stride, transposed/target))
+//   CONV    out = [relu](SC layer(in; K, offset_scale, out_stride, transposed/target) [+ res])
 //   ADD     out = [relu](a + b)           (residual; same coordinates)
 //   CONCAT  out = [a | b]                 (U-Net skip; same coordinates)
+//
+// Activations live on device in the compute dtype (f16 / bf16): the GEMM operands are
+// 16-bit anyway, so storing fp32 between layers only doubled the traffic. Accumulation
+// stays fp32 (TMEM / scatter registers); ADD sums in fp32 and rounds once.
+//
+// Plan (once per network): an ADD whose operand is produced by a CONV that nothing else
+// reads is folded into that conv's epilogue (out = [relu](conv + other)); the conv's own
+// output is never materialised. Per conv the dataflow is GMaS (Minuet gather/GEMM/scatter)
+// or the fused output-stationary kernel; AUTO times both on the first forward and keeps
+// the faster one (the Alg. 2 tuning idea applied to the dataflow).
 //
 // Coordinates live in "coordinate sets" (sorted packed keys on device). A map is keyed by
 // (input coordinate set, K, offset scale, out stride, transposed, target set) and built
@@ -12,6 +22,8 @@
 // (SPEC.md:528 sort reuse), so only the raw input and strided layers ever sort. Map builds
 // sync once each (sizes + error flags); GMaS launches never sync.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -20,6 +32,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "conv_fused.hpp"
 #include "gmas.hpp"
 #include "map.hpp"
 #include "net.hpp"
@@ -27,35 +40,87 @@
 namespace sconvb {
 namespace {
 
-__global__ void k_add(const float* __restrict__ a, const float* __restrict__ b, float* __restrict__ out, int64_t n4,
-                      int relu) {
+template <class T>
+struct H16;
+template <>
+struct H16<__half> {
+  static __device__ __forceinline__ float2 to2(__half2 v) { return __half22float2(v); }
+  static __device__ __forceinline__ __half2 from2(float a, float b) { return __floats2half2_rn(a, b); }
+  using T2 = __half2;
+};
+template <>
+struct H16<__nv_bfloat16> {
+  static __device__ __forceinline__ float2 to2(__nv_bfloat162 v) { return __bfloat1622float2(v); }
+  static __device__ __forceinline__ __nv_bfloat162 from2(float a, float b) { return __floats2bfloat162_rn(a, b); }
+  using T2 = __nv_bfloat162;
+};
+
+// out = [relu](a + b), 16-bit operands, fp32 sum, 8 elements per thread (16-byte vectors)
+template <class T>
+__global__ void k_add(const T* __restrict__ a, const T* __restrict__ b, T* __restrict__ out, int64_t n8, int relu) {
   const int64_t i = blockIdx.x * int64_t{blockDim.x} + threadIdx.x;
-  if (i >= n4) return;
-  const float4 x = reinterpret_cast<const float4*>(a)[i], y = reinterpret_cast<const float4*>(b)[i];
-  float4 r = make_float4(x.x + y.x, x.y + y.y, x.z + y.z, x.w + y.w);
-  if (relu) r = make_float4(fmaxf(r.x, 0.f), fmaxf(r.y, 0.f), fmaxf(r.z, 0.f), fmaxf(r.w, 0.f));
-  reinterpret_cast<float4*>(out)[i] = r;
+  if (i >= n8) return;
+  const uint4 x = reinterpret_cast<const uint4*>(a)[i], y = reinterpret_cast<const uint4*>(b)[i];
+  uint4 r;
+  const auto* xa = reinterpret_cast<const typename H16<T>::T2*>(&x);
+  const auto* ya = reinterpret_cast<const typename H16<T>::T2*>(&y);
+  auto* ra = reinterpret_cast<typename H16<T>::T2*>(&r);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float2 p = H16<T>::to2(xa[e]), q = H16<T>::to2(ya[e]);
+    float s0 = p.x + q.x, s1 = p.y + q.y;
+    if (relu) {
+      s0 = fmaxf(s0, 0.f);
+      s1 = fmaxf(s1, 0.f);
+    }
+    ra[e] = H16<T>::from2(s0, s1);
+  }
+  reinterpret_cast<uint4*>(out)[i] = r;
 }
 
-__global__ void k_add_scalar(const float* __restrict__ a, const float* __restrict__ b, float* __restrict__ out,
-                             int64_t n, int relu) {
+template <class T>
+__global__ void k_add_scalar(const T* __restrict__ a, const T* __restrict__ b, T* __restrict__ out, int64_t n,
+                             int relu) {
   const int64_t i = blockIdx.x * int64_t{blockDim.x} + threadIdx.x;
   if (i >= n) return;
-  const float r = a[i] + b[i];
-  out[i] = relu ? fmaxf(r, 0.f) : r;
+  const float r = static_cast<float>(a[i]) + static_cast<float>(b[i]);
+  out[i] = static_cast<T>(relu ? fmaxf(r, 0.f) : r);
 }
 
-__global__ void k_concat(const float* __restrict__ a, int ca, const float* __restrict__ b, int cb,
-                         float* __restrict__ out, int64_t n) {
+// [a | b] along channels; 16-bit elements moved as raw 2-byte words (exact)
+__global__ void k_concat(const uint16_t* __restrict__ a, int64_t lda, int ca, const uint16_t* __restrict__ b,
+                         int64_t ldb, int cb, uint16_t* __restrict__ out, int64_t n) {
   const int c = ca + cb;
   const int64_t i = blockIdx.x * int64_t{blockDim.x} + threadIdx.x;
   if (i >= n * c) return;
   const int64_t r = i / c;
   const int ch = static_cast<int>(i - r * c);
-  out[i] = ch < ca ? a[r * ca + ch] : b[r * cb + ch - ca];
+  out[i] = ch < ca ? a[r * lda + ch] : b[r * ldb + ch - ca];
+}
+
+// vectorised: 8 channels (16 bytes) per thread when every row segment is 16-byte aligned
+__global__ void k_concat8(const uint4* __restrict__ a, int64_t lda8, int ca8, const uint4* __restrict__ b,
+                          int64_t ldb8, int cb8, uint4* __restrict__ out, int64_t n) {
+  const int c8 = ca8 + cb8;
+  const int64_t i = blockIdx.x * int64_t{blockDim.x} + threadIdx.x;
+  if (i >= n * c8) return;
+  const int64_t r = i / c8;
+  const int ch = static_cast<int>(i - r * c8);
+  out[i] = ch < ca8 ? a[r * lda8 + ch] : b[r * ldb8 + ch - ca8];
+}
+
+// SCONV_DEBUG_SYNC=1: synchronise and log after every conv (locates a faulting launch)
+bool debug_sync() {
+  static const bool on = [] {
+    const char* e = std::getenv("SCONV_DEBUG_SYNC");
+    return e && e[0] == '1';
+  }();
+  return on;
 }
 
 inline unsigned blocks(int64_t n) { return static_cast<unsigned>(std::max<int64_t>(1, (n + 255) / 256)); }
+
+int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 
 }  // namespace
 
@@ -78,11 +143,59 @@ void NetData::check_ops() const {
   }
 }
 
+void NetData::make_plan() {
+  const int n_ops = static_cast<int>(ops.size());
+  plan.assign(n_ops, OpPlan{});
+  auto_ms.assign(n_ops, {-1.0, -1.0});
+  std::vector<int> producer(num_tensors, -1), readers(num_tensors, 0);
+  for (int i = 0; i < n_ops; ++i) {
+    const NetOp& o = ops[i];
+    producer[o.out] = i;
+    ++readers[o.in];
+    if (o.kind != kOpConv) ++readers[o.b];
+    if (o.kind == kOpConv && o.transposed) ++readers[o.target];  // coordinates only, but keep it materialised
+    plan[i].out = o.out;
+    plan[i].relu = o.relu;
+    if (o.kind == kOpConv) plan[i].dataflow = cfg.dataflow;
+  }
+  if (!cfg.fuse_residual) return;
+  for (int a = 0; a < n_ops; ++a) {
+    const NetOp& add = ops[a];
+    if (add.kind != kOpAdd) continue;
+    int best = -1, other = -1;
+    for (int side = 0; side < 2; ++side) {
+      const int t = side == 0 ? add.in : add.b, u = side == 0 ? add.b : add.in;
+      const int p = producer[t];
+      if (p < 0 || p > a || ops[p].kind != kOpConv || plan[p].skip || plan[p].res >= 0) continue;
+      if (ops[p].relu || readers[t] != 1 || t == output_tensor) continue;
+      const int pu = u == input_tensor ? -1 : producer[u];
+      if (pu >= p) continue;  // the other operand must exist when the conv runs
+      if (p > best) {
+        best = p;
+        other = u;
+      }
+    }
+    if (best < 0) continue;
+    plan[best].out = add.out;
+    plan[best].res = other;
+    plan[best].relu = add.relu;
+    plan[a].skip = true;
+  }
+}
+
 void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f_dtype, int f_mem, int c_in) {
   if (f_dtype != SCONV_F32) fail(SCONV_ERR_ARG, "network input features must be fp32");
   const cudaStream_t st = ctx.stream;
+  if (!planned) {
+    make_plan();
+    planned = true;
+  }
+  const int act = cfg.compute_dtype;
   tensors.resize(num_tensors);
-  for (auto& t : tensors) t.coordset = -1;
+  for (auto& t : tensors) {
+    t.coordset = -1;
+    t.fused_away = false;
+  }
   coordsets.clear();
   maps.clear();
   maps_built = 0;
@@ -94,15 +207,26 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
   tin.coordset = 0;
   tin.n = input.n;
   tin.channels = c_in;
-  const size_t in_bytes = sizeof(float) * input.n * c_in;
-  tin.feats.reserve(std::max<size_t>(in_bytes, 16), st);
-  if (input.n > 0)
-    SCONV_CUDA(cudaMemcpyAsync(tin.feats.get(), feats, in_bytes,
-                               f_mem == SCONV_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st));
-  for (const NetOp& o : ops) {
+  tin.dtype = act;
+  tin.ld = round_up(c_in, 16);  // zero padded: the fused gather reads whole 16-channel chunks
+  tin.feats.reserve(std::max<size_t>(2 * input.n * tin.ld, 16), st);
+  if (input.n > 0) {
+    const float* src = static_cast<const float*>(feats);
+    DevBuf staged;
+    if (f_mem == SCONV_MEM_HOST) {
+      staged.alloc(sizeof(float) * input.n * c_in, st);
+      SCONV_CUDA(cudaMemcpyAsync(staged.get(), feats, sizeof(float) * input.n * c_in, cudaMemcpyHostToDevice, st));
+      src = staged.get<float>();
+    }
+    convert_rows(ctx, src, SCONV_F32, input.n, c_in, c_in, tin.feats.get(), act, tin.ld);
+  }
+  for (int oi = 0; oi < static_cast<int>(ops.size()); ++oi) {
+    const NetOp& o = ops[oi];
+    OpPlan& pl = plan[oi];
+    if (pl.skip) continue;
     NetTensor& a = tensors.at(o.in);
     if (a.coordset < 0) fail(SCONV_ERR_STATE, "op reads a tensor that was not produced yet");
-    NetTensor& out = tensors.at(o.out);
+    NetTensor& out = tensors.at(pl.out);
     if (o.kind == kOpConv) {
       if (a.channels != o.c_in) fail(SCONV_ERR_ARG, "conv input channels mismatch");
       int tgt = -1;
@@ -113,7 +237,7 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
       const MapKey key{a.coordset, o.K, o.offset_scale, o.transposed ? 1 : o.out_stride, o.transposed, tgt};
       auto it = maps.find(key);
       if (it == maps.end()) {
-        sconv_map_cfg cfg{o.K, o.offset_scale, o.out_stride, o.transposed, block_B, block_C};
+        sconv_map_cfg mcfg{o.K, o.offset_scale, o.out_stride, o.transposed, block_B, block_C};
         const CoordSet& cs = coordsets[a.coordset];
         MapSource P;
         if (cs.raw && !cs.keys) {
@@ -131,7 +255,7 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
           T.n = ct.n;
           T.sorted = true;
         }
-        auto m = build_map(ctx, P, cfg, o.transposed ? &T : nullptr);
+        auto m = build_map(ctx, P, mcfg, o.transposed ? &T : nullptr);
         ++maps_built;
         if (!coordsets[a.coordset].keys && coordsets[a.coordset].sorted)
           coordsets[a.coordset].keys = m->src_keys;  // sorted raw input: its packed keys, same row order
@@ -151,52 +275,122 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
       if (wt == weights.end()) fail(SCONV_ERR_STATE, "conv weights not set");
       const WeightData& w = *wt->second;
       if (w.c_in != o.c_in || w.c_out != o.c_out || w.K3 != m.K3) fail(SCONV_ERR_ARG, "weight shape mismatch");
+      if (w.dtype != act) fail(SCONV_ERR_ARG, "weight dtype must match the network compute dtype");
+      const NetTensor* res = nullptr;
+      if (pl.res >= 0) {
+        res = &tensors.at(pl.res);
+        if (res->coordset < 0) fail(SCONV_ERR_STATE, "residual operand not produced yet");
+        if (res->channels != o.c_out || res->n != m.n_out) fail(SCONV_ERR_ARG, "add operands need the same shape");
+      }
+      // the output buffer may be read below (residual or input of a re-used tensor id): fresh allocation
+      DevBuf nb;
+      nb.alloc(std::max<size_t>(2 * static_cast<size_t>(m.n_out) * o.c_out, 16), st);
+      LayerIO io;
+      io.f_in = a.feats.get();
+      io.in_dtype = a.dtype;
+      io.ld_in = a.ld;
+      io.in_zero_padded = true;  // every tensor's padding columns are written as zeros
+      io.f_out = nb.get();
+      io.out_dtype = act;
+      io.ld_out = o.c_out;
+      io.res = res ? res->feats.get() : nullptr;
+      io.ld_res = res ? res->ld : 0;
+      io.relu = pl.relu;
+      int df = pl.dataflow;
+      if (df == SCONV_DATAFLOW_AUTO) {
+        // time both dataflows once on this input (1 warm-up + 2 timed runs each, min)
+        cudaEvent_t e0, e1;
+        SCONV_CUDA(cudaEventCreate(&e0));
+        SCONV_CUDA(cudaEventCreate(&e1));
+        double best[2] = {1e30, 1e30};
+        for (int rep = 0; rep < 3; ++rep)
+          for (int d = 0; d < 2; ++d) {
+            SCONV_CUDA(cudaEventRecord(e0, st));
+            layer_forward_dev(ctx, m, w, cfg, d == 0 ? SCONV_DATAFLOW_GMAS : SCONV_DATAFLOW_FUSED, io);
+            SCONV_CUDA(cudaEventRecord(e1, st));
+            SCONV_CUDA(cudaEventSynchronize(e1));
+            float ms = 0;
+            SCONV_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+            if (rep > 0) best[d] = std::min(best[d], static_cast<double>(ms));
+          }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        auto_ms[oi] = {best[0], best[1]};
+        pl.dataflow = best[1] <= best[0] ? SCONV_DATAFLOW_FUSED : SCONV_DATAFLOW_GMAS;
+        df = pl.dataflow;
+      }
+      layer_forward_dev(ctx, m, w, cfg, df, io);
+      if (debug_sync()) {
+        std::fprintf(stderr, "[sconv] op %d conv K3=%d n_in=%lld n_out=%lld c_in=%d c_out=%d dataflow=%d ...", oi, m.K3,
+                     static_cast<long long>(m.n_in), static_cast<long long>(m.n_out), w.c_in, w.c_out, df);
+        ctx.sync();
+        std::fprintf(stderr, " ok\n");
+      }
       out.coordset = it->second.out_cs;
       out.n = m.n_out;
       out.channels = o.c_out;
-      out.feats.reserve(std::max<size_t>(sizeof(float) * out.n * out.channels, 16), st);
-      sconv_exec_cfg c = cfg;
-      c.compute_dtype = w.dtype;
-      layer_forward(ctx, m, w, a.feats.get(), SCONV_F32, SCONV_MEM_DEVICE, c, out.feats.get(), SCONV_F32,
-                    SCONV_MEM_DEVICE, o.relu);
-      conv_stats.push_back({m.n_in, m.n_out, m.total, m.buffer_length, w.c_in, w.c_out, w.k_pad, m.K3});
+      out.dtype = act;
+      out.ld = o.c_out;
+      out.feats = std::move(nb);
+      if (pl.out != o.out) tensors.at(o.out).fused_away = true;
+      conv_stats.push_back({m.n_in, m.n_out, m.total, df == SCONV_DATAFLOW_FUSED ? 0 : m.buffer_length, w.c_in, w.c_out,
+                            w.k_pad, m.K3, df, pl.res >= 0 ? 1 : 0});
     } else {
       NetTensor& b = tensors.at(o.b);
       if (b.coordset < 0) fail(SCONV_ERR_STATE, "op reads a tensor that was not produced yet");
       if (a.coordset != b.coordset || a.n != b.n) fail(SCONV_ERR_ARG, "add/concat operands need the same coordinates");
       const int64_t n = a.n;
+      DevBuf nb;
       if (o.kind == kOpAdd) {
         if (a.channels != b.channels) fail(SCONV_ERR_ARG, "add operands need the same channels");
-        // operands may alias the output (in-place residual): allocate the output separately
-        DevBuf nb;
-        nb.alloc(std::max<size_t>(sizeof(float) * n * a.channels, 16), st);
+        if (a.ld != a.channels || b.ld != b.channels) fail(SCONV_ERR_ARG, "add operands must be dense rows");
+        // operands may alias the output tensor id (in-place residual): separate allocation
+        nb.alloc(std::max<size_t>(2 * static_cast<size_t>(n) * a.channels, 16), st);
         const int64_t total = n * a.channels;
-        if (total % 4 == 0)
+        if (total % 8 == 0) {
+          if (act == SCONV_F16)
+            ctx.launch("k_add", [&] {
+              k_add<__half><<<blocks(total / 8), 256, 0, st>>>(a.feats.get<__half>(), b.feats.get<__half>(),
+                                                               nb.get<__half>(), total / 8, o.relu);
+            });
+          else
+            ctx.launch("k_add", [&] {
+              k_add<__nv_bfloat16><<<blocks(total / 8), 256, 0, st>>>(
+                  a.feats.get<__nv_bfloat16>(), b.feats.get<__nv_bfloat16>(), nb.get<__nv_bfloat16>(), total / 8, o.relu);
+            });
+        } else if (act == SCONV_F16) {
           ctx.launch("k_add", [&] {
-            k_add<<<blocks(total / 4), 256, 0, st>>>(a.feats.get<float>(), b.feats.get<float>(), nb.get<float>(),
-                                                     total / 4, o.relu);
+            k_add_scalar<__half><<<blocks(total), 256, 0, st>>>(a.feats.get<__half>(), b.feats.get<__half>(),
+                                                                nb.get<__half>(), total, o.relu);
+          });
+        } else {
+          ctx.launch("k_add", [&] {
+            k_add_scalar<__nv_bfloat16><<<blocks(total), 256, 0, st>>>(
+                a.feats.get<__nv_bfloat16>(), b.feats.get<__nv_bfloat16>(), nb.get<__nv_bfloat16>(), total, o.relu);
+          });
+        }
+        out.channels = a.channels;
+      } else {
+        const int c = a.channels + b.channels;
+        nb.alloc(std::max<size_t>(2 * static_cast<size_t>(n) * c, 16), st);
+        if (a.channels % 8 == 0 && b.channels % 8 == 0 && a.ld % 8 == 0 && b.ld % 8 == 0)
+          ctx.launch("k_concat", [&] {
+            k_concat8<<<blocks(n * c / 8), 256, 0, st>>>(a.feats.get<uint4>(), a.ld / 8, a.channels / 8,
+                                                         b.feats.get<uint4>(), b.ld / 8, b.channels / 8, nb.get<uint4>(),
+                                                         n);
           });
         else
-          ctx.launch("k_add", [&] {
-            k_add_scalar<<<blocks(total), 256, 0, st>>>(a.feats.get<float>(), b.feats.get<float>(), nb.get<float>(),
-                                                        total, o.relu);
+          ctx.launch("k_concat", [&] {
+            k_concat<<<blocks(n * c), 256, 0, st>>>(a.feats.get<uint16_t>(), a.ld, a.channels, b.feats.get<uint16_t>(),
+                                                    b.ld, b.channels, nb.get<uint16_t>(), n);
           });
-        out.channels = a.channels;
-        out.coordset = a.coordset;
-        out.n = n;
-        out.feats = std::move(nb);
-      } else {
-        DevBuf nb;
-        nb.alloc(std::max<size_t>(sizeof(float) * n * (a.channels + b.channels), 16), st);
-        ctx.launch("k_concat", [&] {
-          k_concat<<<blocks(n * (a.channels + b.channels)), 256, 0, st>>>(
-              a.feats.get<float>(), a.channels, b.feats.get<float>(), b.channels, nb.get<float>(), n);
-        });
-        out.channels = a.channels + b.channels;
-        out.coordset = a.coordset;
-        out.n = n;
-        out.feats = std::move(nb);
+        out.channels = c;
       }
+      out.coordset = a.coordset;
+      out.n = n;
+      out.dtype = act;
+      out.ld = out.channels;
+      out.feats = std::move(nb);
     }
   }
 }

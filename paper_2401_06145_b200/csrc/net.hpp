@@ -26,7 +26,19 @@ struct NetTensor {
   int coordset = -1;
   int64_t n = 0;
   int channels = 0;
-  DevBuf feats;  // fp32 [n][channels], rows in the coordinate set's order
+  int dtype = SCONV_F16;  // activations are stored in the compute dtype (f16 / bf16)
+  int64_t ld = 0;         // row stride (elements); the network input is zero padded to 16
+  bool fused_away = false;  // folded into a later op's epilogue (never materialised)
+  DevBuf feats;  // [n][ld], rows in the coordinate set's order
+};
+
+// Per-op execution plan derived from the op list (residual folding, dataflow choice).
+struct OpPlan {
+  bool skip = false;  // ADD folded into a conv epilogue
+  int out = -1;       // tensor written (the ADD's output when folded)
+  int res = -1;       // residual tensor added in the epilogue (-1: none)
+  int relu = 0;
+  int dataflow = -1;  // resolved per conv (AUTO: timed on the first forward)
 };
 
 struct CoordSet {
@@ -54,10 +66,16 @@ struct NetData {
   MapSource raw_input;
   DevBuf input_xyz;  // device copy of host input coordinates
   int maps_built = 0;
-  // per CONV op of the last forward: n_in, n_out, |M|, R_pad, c_in, c_out, k_pad, K3
-  std::vector<std::array<int64_t, 8>> conv_stats;
+  std::vector<OpPlan> plan;
+  bool planned = false;
+  std::vector<std::array<double, 2>> auto_ms;  // per op: GMaS / fused ms of the tuning forward
+  DevBuf readback;  // f32 staging for host reads
+  // per CONV op of the last forward: n_in, n_out, |M|, R_pad (0 when fused), c_in, c_out, k_pad, K3,
+  // dataflow, residual folded (0/1)
+  std::vector<std::array<int64_t, 10>> conv_stats;
 
   void check_ops() const;
+  void make_plan();
   void forward(Ctx& ctx, const MapSource& input, const void* feats, int f_dtype, int f_mem, int c_in);
 };
 

@@ -208,35 +208,55 @@ class Network:
         return xyz, f
 
     def device_output(self):
-        p = C.c_void_p()
-        self.ctx.check(self.ctx.lib.sconv_net_tensor_device(self.h, self.g.output, C.byref(p)))
-        return p.value
+        """(pointer, dtype, row stride) of the output tensor on device."""
+        p, dt, ld = C.c_void_p(), C.c_int(), C.c_int64()
+        self.ctx.check(self.ctx.lib.sconv_net_tensor_device(self.h, self.g.output, C.byref(p), C.byref(dt),
+                                                            C.byref(ld)))
+        return p.value, dt.value, ld.value
 
     def stats(self):
         mb, nc = C.c_int(), C.c_int()
         self.ctx.check(self.ctx.lib.sconv_net_stats(self.h, C.byref(mb), C.byref(nc)))
         return dict(maps_built=mb.value, convs=nc.value)
 
+    STAT_KEYS = ["n_in", "n_out", "M", "R", "c_in", "c_out", "k_pad", "K3", "dataflow", "residual"]
+
     def conv_stats(self):
-        """Per conv (execution order): n_in, n_out, M, R_pad, c_in, c_out, k_pad, K3."""
+        """Per conv (execution order): n_in, n_out, M, R_pad (0 when fused), c_in, c_out, k_pad, K3,
+        dataflow (0 GMaS / 1 fused), residual (ADD folded into the epilogue)."""
         out = []
         for i in range(len(self.g.convs())):
-            v = np.zeros(8, np.int64)
+            v = np.zeros(10, np.int64)
             if self.ctx.lib.sconv_net_conv_stats(self.h, i, S._ptr(v)) != S.OK:
                 break
-            out.append(dict(zip(["n_in", "n_out", "M", "R", "c_in", "c_out", "k_pad", "K3"], v.tolist())))
+            out.append(dict(zip(self.STAT_KEYS, v.tolist())))
         return out
 
-    def algo_bytes(self):
-        """Algorithmic bytes per kernel type summed over the convs (this path's dtypes:
-        fp32 features, 16-bit gather buffer, fp32 GEMM partials)."""
-        g = e = s = sc = 0
+    def auto_timings(self):
+        """Per op index: (GMaS ms, fused ms) measured by the AUTO tuning forward (-1: not tuned)."""
+        out = {}
+        for i, o in enumerate(self.g.ops):
+            if o.kind != CONV:
+                continue
+            a, b = C.c_double(), C.c_double()
+            self.ctx.check(self.ctx.lib.sconv_net_conv_timings(self.h, i, C.byref(a), C.byref(b)))
+            out[i] = (a.value, b.value)
+        return out
+
+    def algo_bytes(self, part_bytes=2):
+        """Algorithmic bytes per kernel type summed over the convs (SURVEY §8d with this path's dtypes:
+        16-bit activations, 16-bit gather buffer, `part_bytes` GEMM partials, 16-bit outputs).
+        Fused convs: input rows read once (2*ci*n), the nbr table (4*K3*q), output (+residual) once."""
+        g = e = s = f = 0
         for st in self.conv_stats():
-            n, q, M, R, ci, co, kp, K3 = (st[k] for k in ["n_in", "n_out", "M", "R", "c_in", "c_out", "k_pad", "K3"])
-            g += 4 * ci * n + 2 * kp * R + 4 * M
-            e += 2 * kp * R + 4 * co * R + 2 * K3 * ci * co
-            s += 4 * co * M + 4 * K3 * q + 4 * co * q
-        return {"k_gather": g, "k_gemm_grouped": e, "k_scatter": s}
+            n, q, M, R, ci, co, kp, K3, df, res = (st[k] for k in self.STAT_KEYS)
+            if df == 1:
+                f += 2 * ci * n + 4 * K3 * q + 2 * co * q * (2 if res else 1)
+                continue
+            g += 2 * ci * n + 2 * kp * R + 4 * M
+            e += 2 * kp * R + part_bytes * co * R + 2 * K3 * ci * co
+            s += part_bytes * co * M + 4 * K3 * q + 2 * co * q * (2 if res else 1)
+        return {"k_gather": g, "k_gemm_grouped": e, "k_scatter": s, "k_conv_fused": f}
 
     def free(self):
         if self.h:

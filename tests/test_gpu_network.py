@@ -1,11 +1,14 @@
 """Network driver parity on the GPU (BASELINE configs 2-4 graphs on small synthetic scenes).
 
-Layer-wise with teacher forcing: every CONV op's GPU input tensor is fed to
-the CPU oracle (same coordinates; features and weights rounded to the GPU operand type);
-output coordinates must be bit-exact and features within 2e-6 of max|out| (only the
-accumulation order differs); against the unrounded fp32 oracle the north_star tolerance
-(max <= 1e-2, mean <= 1e-3) must hold per layer. ADD / CONCAT are checked exactly. The
-end-to-end error through the whole graph is reported and bounded loosely.
+Layer-wise with teacher forcing: every CONV op's GPU input tensor (16-bit
+activations, read back exactly) is fed to the CPU oracle with the same coordinates and the
+weights rounded to the GPU operand type; output coordinates must be bit-exact and the
+features must equal the oracle's output rounded to f16 up to one f16 ulp (only the fp32
+accumulation order differs before the final rounding). Against the unrounded fp32 oracle
+the north_star tolerance (max <= 1e-2, mean <= 1e-3) must hold per layer. ADD / CONCAT are
+checked exactly (fp32 sum of the 16-bit operands, rounded once). Both dataflows (Minuet
+GMaS and the fused output-stationary kernel) are teacher-forced; the default network
+(AUTO dataflow, residual ADDs folded into conv epilogues) is checked end to end.
 """
 import numpy as np
 import pytest
@@ -28,11 +31,19 @@ def rel(g, r):
     return d.max() / s, d.mean() / max(np.abs(r).mean(), 1e-30)
 
 
-def teacher_forced(ctx, g, weights, coords, feats, max_convs=None):
-    """fp32 partials (strict same-operand parity); the default f16-partial network is checked
-    end to end in test_minkunet42_small_scan."""
+def assert_f16_rounded(g, r):
+    """g = r rounded to f16, allowing one f16 ulp (2^-10 relative) for accumulation-order ties."""
+    r64, g64 = r.astype(np.float64), g.astype(np.float64)
+    tol = np.abs(r64) * 2.0 ** -10 + 4e-6 * max(np.abs(r64).max(), 1e-30)
+    bad = np.abs(g64 - r64) > tol
+    assert not bad.any(), (int(bad.sum()), float(np.abs(g64 - r64).max()))
+
+
+def teacher_forced(ctx, g, weights, coords, feats, dataflow=sc.DATAFLOW_GMAS, max_convs=None):
+    """fp32 partials for GMaS (strict same-operand parity); residual folding off so every
+    tensor is materialised. The default network is checked end to end in the tests below."""
     ora = load_oracle()
-    net = N.Network(ctx, g, weights, sc.exec_cfg(partial_f16=0))
+    net = N.Network(ctx, g, weights, sc.exec_cfg(partial_f16=0, dataflow=dataflow, fuse_residual=0))
     net.forward(coords, feats, True)
     checked = 0
     worst = (0.0, 0.0)
@@ -42,15 +53,15 @@ def teacher_forced(ctx, g, weights, coords, feats, max_convs=None):
         if o.kind == N.CONV:
             if max_convs is not None and checked >= max_convs:
                 continue
+            np.testing.assert_array_equal(fin, f16(fin))  # activations are 16-bit
             W = weights[o.weight]
             tgt = net.read(o.b)[0] if o.transposed else None
-            oq, of, _ = ora.layer_forward(xin, True, f16(fin), f16(W), o.K, o.offset_scale, o.out_stride,
+            oq, of, _ = ora.layer_forward(xin, True, fin, f16(W), o.K, o.offset_scale, o.out_stride,
                                           bool(o.transposed), tgt, workers=8)
             if o.relu:
                 of = np.maximum(of, 0)
             np.testing.assert_array_equal(xout, oq)
-            mx, _ = rel(fout, of)
-            assert mx <= 2e-6, (o, mx)
+            assert_f16_rounded(fout, of)
             _, of32, _ = ora.layer_forward(xin, True, fin, W, o.K, o.offset_scale, o.out_stride, bool(o.transposed),
                                            tgt, workers=8)
             if o.relu:
@@ -62,7 +73,7 @@ def teacher_forced(ctx, g, weights, coords, feats, max_convs=None):
         elif o.kind == N.ADD:
             xb, fb = net.read(o.b)
             ref = fin + fb
-            np.testing.assert_array_equal(fout, np.maximum(ref, 0) if o.relu else ref)
+            np.testing.assert_array_equal(fout, f16(np.maximum(ref, 0) if o.relu else ref))
         else:
             xb, fb = net.read(o.b)
             np.testing.assert_array_equal(fout, np.concatenate([fin, fb], 1))
@@ -88,40 +99,65 @@ def oracle_graph(g, weights, coords, feats):
     return T[g.output]
 
 
-def test_minkunet42_small_scan(ctx):
+@pytest.mark.parametrize("dataflow", [sc.DATAFLOW_GMAS, sc.DATAFLOW_FUSED])
+def test_minkunet42_small_scan(ctx, dataflow):
     coords, feats = D.kitti_scan(3, n_azimuth=400)
     g = N.minkunet42()
     w = N.init_weights(g, 7)
-    net, checked, worst = teacher_forced(ctx, g, w, coords, feats)
+    net, checked, worst = teacher_forced(ctx, g, w, coords, feats, dataflow)
     assert checked == 49
     st = net.stats()
     # 5 submanifold (ts 1..16) + 4 down + 4 transposed + 4 1x1 identity maps (ts 2..16 ... ts 1)
     assert st["convs"] == 49 and st["maps_built"] <= 18
+    assert all(s["dataflow"] == dataflow for s in net.conv_stats())
+    print(f"MinkUNet42 teacher-forced (dataflow={dataflow}): per-layer worst {worst}")
+
+
+def test_minkunet42_end_to_end(ctx):
+    """Default network (AUTO dataflow per conv, residual ADDs folded into conv epilogues) and
+    the unfolded GMaS-only network against the fp32 oracle graph."""
+    coords, feats = D.kitti_scan(3, n_azimuth=400)
+    g = N.minkunet42()
+    w = N.init_weights(g, 7)
     q, ref = oracle_graph(g, w, coords, feats)
-    for pf in (0, 1):
-        net = N.Network(ctx, g, w, sc.exec_cfg(partial_f16=pf))
+    outs = {}
+    for name, cfg in [("default", sc.exec_cfg(dataflow=sc.DATAFLOW_AUTO)),
+                      ("fused", sc.exec_cfg(dataflow=sc.DATAFLOW_FUSED)),
+                      ("gmas-unfolded", sc.exec_cfg(dataflow=sc.DATAFLOW_GMAS, fuse_residual=0))]:
+        net = N.Network(ctx, g, w, cfg)
         net.forward(coords, feats)
         xo, fo = net.read(g.output)
         np.testing.assert_array_equal(xo, q)
         mx, mean = rel(fo, ref)
-        print(f"MinkUNet42 end-to-end (partial_f16={pf}): |P|={len(coords)} max_rel={mx:.2e} mean_rel={mean:.2e};"
-              f" per-layer worst {worst}")
-        assert mx <= 1e-2 and mean <= 1e-3
+        st = net.conv_stats()
+        print(f"MinkUNet42 end-to-end ({name}): |P|={len(coords)} max_rel={mx:.2e} mean_rel={mean:.2e} "
+              f"fused={sum(s['dataflow'] for s in st)}/{len(st)} folded={sum(s['residual'] for s in st)}")
+        # 16-bit activations through 49 layers: end to end bounded loosely (per layer is the gate)
+        assert mx <= 3e-2 and mean <= 3e-3, (name, mx, mean)
+        outs[name] = fo
+        if name != "gmas-unfolded":
+            assert sum(s["residual"] for s in st) == 16  # every residual ADD folded
+            with pytest.raises(sc.LogicError):
+                net.read(g.ops[-2].out)  # the folded conv's own output is never materialised
+    # folding the ADD changes only where one rounding happens
+    assert rel(outs["fused"], outs["gmas-unfolded"])[0] <= 3e-2
 
 
-def test_sparse_resnet21d_small_room(ctx):
+@pytest.mark.parametrize("dataflow", [sc.DATAFLOW_GMAS, sc.DATAFLOW_FUSED])
+def test_sparse_resnet21d_small_room(ctx, dataflow):
     coords, feats = D.s3dis_room(2, n_points=60000, resolution=0.05)
     g = N.sparse_resnet21d()
     w = N.init_weights(g, 3)
-    net, checked, _ = teacher_forced(ctx, g, w, coords, feats)
+    net, checked, _ = teacher_forced(ctx, g, w, coords, feats, dataflow)
     assert checked == 21
 
 
-def test_unet_pair_object(ctx):
+@pytest.mark.parametrize("dataflow", [sc.DATAFLOW_GMAS, sc.DATAFLOW_FUSED])
+def test_unet_pair_object(ctx, dataflow):
     coords, feats = D.shapenet_object(5, n_points=40000)
     g = N.unet_pair()
     w = N.init_weights(g, 5)
-    net, checked, _ = teacher_forced(ctx, g, w, coords, feats)
+    net, checked, _ = teacher_forced(ctx, g, w, coords, feats, dataflow)
     assert checked == 2
     xo, fo = net.read(g.output)
     np.testing.assert_array_equal(xo, coords)  # transposed conv lands on the input coordinates

@@ -178,6 +178,7 @@ def test_layer_parity(ctx, oracle, K, s, n, extent, cin, cout):
     (3, 1, 3000, 25, 128, 256),  # N = 256 accumulator
     (3, 1, 3000, 25, 48, 40),    # C_out not a multiple of 16 (padded N, scalar epilogue)
     (1, 1, 1000, 20, 32, 48),
+    (1, 1, 8000, 25, 128, 256),  # 2 stages per tile << cp.async look-ahead (tile-info ring depth)
     (3, 1, 300, 10, 32, 32),     # fewer rows than one 128-row tile
 ])
 def test_fused_layer_parity(ctx, oracle, K, s, n, extent, cin, cout):
