@@ -325,7 +325,11 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     ctx = sc.Context(local)
-    stream = torch.cuda.current_stream()
+    # One real (non-default) stream shared by torch and the library: events, the L2 flush and
+    # every kernel are ordered on it (the legacy default stream, handle 0, is not ordered with
+    # the context's own non-blocking stream).
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
     wl = make_workload(args, ctx, torch, rank)
     for _ in range(args.warmup):

@@ -24,7 +24,11 @@
 //   warp 8     TMEM owner; lane 0 issues tcgen05.mma (M=128, N=block_n, K=16) and commits
 // Two TMEM accumulators let the epilogue of tile t overlap the MMAs of tile t+1.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <map>
 #include <string>
+#include <vector>
 
 #include "common.cuh"
 #include "conv_fused.hpp"
@@ -132,16 +136,34 @@ struct FusedParams {
   int vec;  // 16-byte aligned output / residual rows
   uint32_t stage_bytes, a_bytes, b_bytes, idx_off, bar_off;
   int stages;  // smem ring depth
+  unsigned long long* trace;  // debug 5: CTA 0 event timeline {kind<<56 | seq<<32 | t_lo}
+  int debug;   // profiling experiments only (SCONV_FUSED_DEBUG bits): 1 no gather copies, 2 no MMAs,
+               // 4 no weight TMA (plain arrive), 8 CTA-0 timeline trace
   uint32_t tmem_cols;
   int bf16;
 };
+
+// debug 5 timeline: each event kind owns a 1024-slot region, written with plain stores by a
+// single thread (no atomics: the trace must not perturb the pipeline)
+__device__ __forceinline__ void trace_ev(const FusedParams& p, int kind, int seq, unsigned& n) {
+  if (p.trace && blockIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (n < 1024)
+      p.trace[kind * 1024 + n] = (static_cast<unsigned long long>(kind) << 56) |
+                                 (static_cast<unsigned long long>(seq & 0xFFFFFF) << 32) | (t & 0xFFFFFFFFull);
+    ++n;
+  }
+}
 
 // NK = compile-time offset count (registers prefetch the next tile's index rows), 0 = runtime
 template <int NK, int KC, class TOut>
 __global__ void __launch_bounds__(kThreads, 2) k_conv_fused(const __grid_constant__ CUtensorMap tmB,
                                                            const __grid_constant__ FusedParams p) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t{1023});
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-byte aligned base (SW128 atoms) derived by OFFSET from the __shared__ array, so the
+  // compiler keeps the shared address space (LDS/STS, not generic LD/ST) for every access
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   int32_t* s_idx = reinterpret_cast<int32_t*>(smem + p.idx_off);  // [K3][128] rows of the current tile
   const int S = p.stages;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.bar_off);
@@ -158,7 +180,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_conv_fused(const __grid_constan
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], kProducers + 1);
+      mbar_init(&full[s], (p.debug & 16) ? 4 + 1 : kProducers + 1);
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -176,6 +198,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_conv_fused(const __grid_constan
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  unsigned tr1 = 0, tr2 = 0, tr3 = 0, tr4 = 0, tr5 = 0, tr6 = 0;  // debug-5 trace cursors
 
   if (warp < 4) {
     // ------------------------------------------------------------ gather producers
@@ -198,11 +221,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_conv_fused(const __grid_constan
       for (int k = 0; k < NR; ++k) jn[k] = ok ? __ldg(p.nbr + int64_t{k} * p.n_out + i) : -1;
     };
     if (NK > 0) load_rows(blockIdx.x);
-    uint32_t issued = 0;  // sequential stage counter
+    int stage = 0;
+    uint32_t phase = 0;
+    const uint32_t smem_base = smem_u32(smem);
     int it = 0;
     for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
       const int buf = it & 1;
-      const int nb = t % p.n_blocks;
+      if (tid == 0) trace_ev(p, 1, it, tr1);
+      const int nb = t % p.n_blocks;  // one division per tile
       int32_t* srow = s_idx;
       if (it > 0) named_bar(1, kProducers);  // every producer finished reading the previous tile's rows
       uint64_t mine = 0;
@@ -233,36 +259,65 @@ __global__ void __launch_bounds__(kThreads, 2) k_conv_fused(const __grid_constan
         s_mask[slot] = mask;
         mbar_arrive(&ifull[slot]);
       }
+      const int b_row0 = nb * p.block_n;
+      if (p.debug & 32) {  // experiment: bare ring skeleton (same stage count, no work, no trace)
+        const int n_st = __popcll(mask) * p.num_kb;
+        for (int u = 0; u < n_st; ++u) {
+          mbar_wait(&empty[stage], phase ^ 1u);
+          if (lane == 0) mbar_arrive(&full[stage]);
+          if (tid == 0) mbar_arrive(&full[stage]);
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+        mask = 0;
+      }
       for (uint64_t m = mask; m; m &= m - 1) {
         const int k = __ffsll(static_cast<long long>(m)) - 1;
         const int32_t* sk = srow + k * 128;
-        int32_t j[CPR];
+        const unsigned char* src[CPR];  // this thread's source chunks for offset k (kb = 0)
+        uint32_t nbytes[CPR];
 #pragma unroll
-        for (int q = 0; q < CPR; ++q) j[q] = sk[rbase + q * RPP];
+        for (int q = 0; q < CPR; ++q) {
+          const int32_t j = sk[rbase + q * RPP];
+          src[q] = src_col + static_cast<int64_t>(j >= 0 ? j : 0) * p.ld_in_bytes;
+          nbytes[q] = j >= 0 ? 16u : 0u;
+        }
+        const int b_row = k * p.n_pad + b_row0;
         for (int kb = 0; kb < p.num_kb; ++kb) {
-          const int stage = static_cast<int>(issued % S);
-          mbar_wait(&empty[stage], ((issued / S) & 1) ^ 1);
-          uint8_t* sa = smem + stage * p.stage_bytes;
+          mbar_wait(&empty[stage], phase ^ 1u);
+          const uint32_t sa32 = smem_base + static_cast<uint32_t>(stage) * p.stage_bytes;
           if (tid == 0) {
-            mbar_expect_tx(&full[stage], p.b_bytes);
-            tma_load_2d(sa + p.a_bytes, &tmB, kb * KC, k * p.n_pad + nb * p.block_n, &full[stage]);
+            if (p.debug & 4) {
+              mbar_arrive(&full[stage]);
+            } else {
+              mbar_expect_tx(&full[stage], p.b_bytes);
+              tma_load_2d(smem + stage * p.stage_bytes + p.a_bytes, &tmB, kb * KC, b_row, &full[stage]);
+            }
           }
-          const uint32_t sa32 = smem_u32(sa);
-          const unsigned char* col = src_col + kb * (KC * 2);
+          if (!(p.debug & 1)) {
 #pragma unroll
-          for (int q = 0; q < CPR; ++q) {
-            const unsigned char* src = col + static_cast<int64_t>(j[q] >= 0 ? j[q] : 0) * p.ld_in_bytes;
-            cp_async16(sa32 + a_off[q], src, j[q] >= 0 ? 16u : 0u);
+            for (int q = 0; q < CPR; ++q) cp_async16(sa32 + a_off[q], src[q] + kb * (KC * 2), nbytes[q]);
           }
-          cp_async_arrive_noinc(&full[stage]);
-          ++issued;
+          if (p.debug & 16) {  // experiment: one (plain) arrival per warp instead of one per thread
+            if (lane == 0) mbar_arrive(&full[stage]);
+          } else {
+            cp_async_arrive_noinc(&full[stage]);
+          }
+          if (tid == 0) trace_ev(p, 2, stage, tr2);
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1u;
+          }
         }
       }
     }
   } else if (warp == 8) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
-      uint32_t consumed = 0;
+      int stage = 0;
+      uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
       int it = 0;
@@ -280,22 +335,31 @@ __global__ void __launch_bounds__(kThreads, 2) k_conv_fused(const __grid_constan
         uint32_t accumulate = 0;
         for (uint64_t m = mask; m; m &= m - 1) {
           for (int kb = 0; kb < p.num_kb; ++kb) {
-            const int stage = static_cast<int>(consumed % S);
-            mbar_wait(&full[stage], (consumed / S) & 1);
-            fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tensor core reads
-            tc_fence_after();
+            mbar_wait(&full[stage], phase);
+            trace_ev(p, 3, stage, tr3);
+            if (!(p.debug & 1)) fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tensor core reads
+            if (!(p.debug & 128)) tc_fence_after();
             const uint32_t sa = smem_u32(smem + stage * p.stage_bytes);
             const uint32_t sb = sa + p.a_bytes;
+            if (!(p.debug & 2)) {
 #pragma unroll
-            for (int kk = 0; kk < KC / 16; ++kk) {
-              tc_mma(d_tmem, smem_desc<KC>(sa + kk * 32), smem_desc<KC>(sb + kk * 32), idesc, accumulate);
-              accumulate = 1;
+              for (int kk = 0; kk < KC / 16; ++kk) {
+                tc_mma(d_tmem, smem_desc<KC>(sa + kk * 32), smem_desc<KC>(sb + kk * 32), idesc, accumulate);
+                accumulate = 1;
+              }
             }
-            tc_commit(&empty[stage]);  // frees the stage once these MMAs retire
-            ++consumed;
+            if (p.debug & 64)
+              mbar_arrive(&empty[stage]);  // experiment: plain arrive instead of tcgen05.commit
+            else
+              tc_commit(&empty[stage]);  // frees the stage once these MMAs retire
+            if (++stage == S) {
+              stage = 0;
+              phase ^= 1u;
+            }
           }
         }
         tc_commit(&tfull[acc]);
+        trace_ev(p, 4, it, tr4);
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1u;
@@ -316,7 +380,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_conv_fused(const __grid_constan
       const int64_t i = static_cast<int64_t>(t / p.n_blocks) * 128 + q * 32 + lane;
       const bool valid = i < p.n_out;
       const int ncols = min(n_tile, p.c_out - n0);
-      mbar_wait(&tfull[acc], acc_phase);
+      mbar_wait_backoff(&tfull[acc], acc_phase);  // idle warps yield issue slots to the producers
+      if (warp == 4 && lane == 0) trace_ev(p, 5, t, tr5);
       tc_fence_after();
       TOut* orow = out + i * p.ld_out + n0;
       const TOut* rrow = res ? res + i * p.ld_res + n0 : nullptr;
@@ -353,6 +418,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_conv_fused(const __grid_constan
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (warp == 4 && lane == 0) trace_ev(p, 6, t, tr6);
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1u;
@@ -381,12 +447,29 @@ __global__ void k_convert_rows(const TS* __restrict__ src, int64_t n, int c, int
 template <int NK, int KC, class TOut>
 void launch_t(Ctx& ctx, const FusedArgs& a, const FusedParams& prm, size_t smem, const CUtensorMap& tB) {
   auto kern = k_conv_fused<NK, KC, TOut>;
-  SCONV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  SCONV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-  int occ = 0;
-  SCONV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem));
-  occ = std::max(1, std::min<int>(occ, static_cast<int>(512u / prm.tmem_cols)));  // never oversubscribe TMEM
+  // Resident CTAs per SM from the kernel's own budget (the runtime occupancy query reported 1
+  // where ncu's launch statistics show 2): 228 KB shared memory (1 KB reserved per CTA), the
+  // register file, and TMEM (512 columns). Attributes are set once per instantiation/device.
+  static thread_local std::map<int, int> regs_cache;
+  int regs;
+  const auto hit = regs_cache.find(ctx.device);
+  if (hit != regs_cache.end()) {
+    regs = hit->second;
+  } else {
+    SCONV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    SCONV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    cudaFuncAttributes fa{};
+    SCONV_CUDA(cudaFuncGetAttributes(&fa, kern));
+    regs = fa.numRegs;
+    regs_cache[ctx.device] = regs;
+  }
+  const int by_smem = static_cast<int>((228u * 1024u) / (smem + 1024u));
+  const int by_regs = 65536 / std::max(1, ((regs * 32 + 255) / 256 * 256) * (kThreads / 32));
+  int occ = std::max(1, std::min({by_smem, by_regs, static_cast<int>(512u / prm.tmem_cols), 2}));
   const int grid = std::max(1, std::min(prm.num_tiles, ctx.num_sms * occ));
+  if (std::getenv("SCONV_DEBUG_SYNC"))
+    std::fprintf(stderr, "[sconv] k_conv_fused<%d,%d> tiles=%d grid=%d occ=%d smem=%zu stages=%d bn=%d cols=%u\n", NK, KC,
+                 prm.num_tiles, grid, occ, smem, prm.stages, prm.block_n, prm.tmem_cols);
   ctx.launch("k_conv_fused", [&] { kern<<<grid, kThreads, smem, ctx.stream>>>(tB, prm); });
 }
 
@@ -450,6 +533,13 @@ void launch_conv_fused(Ctx& ctx, const FusedArgs& a) {
   prm.res = a.res;
   prm.ld_res = a.ld_res;
   prm.relu = a.relu;
+  if (const char* e = std::getenv("SCONV_FUSED_DEBUG")) prm.debug = std::atoi(e);
+  DevBuf trace;
+  if (prm.debug & 8) {
+    trace.alloc(8192 * 8, ctx.stream);
+    SCONV_CUDA(cudaMemsetAsync(trace.get(), 0, 8192 * 8, ctx.stream));
+    prm.trace = trace.get<unsigned long long>();
+  }
   {
     const int64_t align = a.out_dtype == SCONV_F32 ? 4 : 8;  // elements per 16 bytes
     prm.vec = a.ld_out % align == 0 && (!a.res || a.ld_res % align == 0) &&
@@ -478,6 +568,25 @@ void launch_conv_fused(Ctx& ctx, const FusedArgs& a) {
   if (smem > 227 * 1024) fail(SCONV_ERR_ARG, "fused layer tile does not fit in shared memory");
   const CUtensorMap tB = make_tensor_map_2d(w.buf.get(), w.dtype, w.k_pad, static_cast<uint64_t>(w.K3) * w.n_pad, kc,
                                             static_cast<uint32_t>(bn), kc);
+  struct TraceDump {  // debug 5: print CTA 0's timeline after the launch
+    Ctx& ctx;
+    DevBuf& buf;
+    ~TraceDump() {
+      if (!buf.get()) return;
+      std::vector<unsigned long long> h(8192);
+      cudaMemcpyAsync(h.data(), buf.get(), 8192 * 8, cudaMemcpyDeviceToHost, ctx.stream);
+      cudaStreamSynchronize(ctx.stream);
+      std::vector<unsigned long long> ev;
+      for (auto e : h)
+        if (e) ev.push_back(e);
+      const size_t n = ev.size();
+      std::sort(ev.begin(), ev.end(), [](auto a, auto b) { return (a & 0xFFFFFFFFull) < (b & 0xFFFFFFFFull); });
+      const unsigned long long t0 = n ? (ev[0] & 0xFFFFFFFFull) : 0;
+      for (auto e : ev)
+        std::fprintf(stderr, "[trace] %8.3f us kind=%llu seq=%llu\n", ((e & 0xFFFFFFFFull) - t0) * 1e-3, e >> 56,
+                     (e >> 32) & 0xFFFFFF);
+    }
+  } dump{ctx, trace};
   if (a.out_dtype == SCONV_F32)
     launch_kc<float>(ctx, a, prm, smem, tB, kc);
   else if (a.out_dtype == SCONV_F16)

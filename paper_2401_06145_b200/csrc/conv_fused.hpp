@@ -10,6 +10,7 @@ namespace sconvb {
 struct FusedArgs {
   const void* f_in = nullptr;  // 16-bit (the weight dtype) [n_in][ld_in]; columns [c_in, k_pad) zero
   int64_t ld_in = 0;
+  int64_t n_in = 0;
   const int32_t* nbr = nullptr;  // [K3][n_out]: input row of (k, i) or -1 (MapData::nbr_in)
   int64_t n_out = 0;
   const WeightData* w = nullptr;

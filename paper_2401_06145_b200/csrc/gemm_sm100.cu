@@ -15,6 +15,7 @@
 // Warp roles (192 threads): warp 0 = TMA producer, warp 1 = TMEM owner + single-thread
 // MMA issuer, warps 2-5 = epilogue (warp w reads TMEM lanes 32*(w%4) .. +31).
 #include <algorithm>
+#include <map>
 #include <string>
 
 #include "common.cuh"
@@ -216,11 +217,11 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-CUtensorMap make_map_impl(const void* base, int dtype, uint64_t inner, uint64_t outer, uint32_t box_inner,
-                     uint32_t box_outer, int kc) {
+CUtensorMap make_map_impl(const void* base, int dtype, uint64_t inner, uint64_t outer, uint64_t stride_bytes,
+                          uint32_t box_inner, uint32_t box_outer, int kc) {
   CUtensorMap m;
   const cuuint64_t dims[2] = {inner, outer};
-  const cuuint64_t strides[1] = {inner * 2};
+  const cuuint64_t strides[1] = {stride_bytes};
   const cuuint32_t box[2] = {box_inner, box_outer};
   const cuuint32_t estr[2] = {1, 1};
   const CUtensorMapSwizzle sw = kc == 64 ? CU_TENSOR_MAP_SWIZZLE_128B
@@ -245,9 +246,17 @@ void launch_kc(Ctx& ctx, const GemmArgs& a) {
   uint32_t cols = 32;
   while (cols < 2u * static_cast<uint32_t>(block_n)) cols <<= 1;
   auto kern = k_gemm_grouped<KC, TOut>;
-  SCONV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  static thread_local std::map<size_t, int> occ_cache;  // per (instantiation, smem): host overhead
   int occ = 0;
-  SCONV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kGemmThreads, smem));
+  const size_t key = smem * 64 + static_cast<size_t>(ctx.device);  // attributes are per device
+  const auto hit = occ_cache.find(key);
+  if (hit != occ_cache.end()) {
+    occ = hit->second;
+  } else {
+    SCONV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    SCONV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kGemmThreads, smem));
+    occ_cache[key] = occ;
+  }
   occ = std::max(1, std::min<int>(occ, static_cast<int>(512u / cols)));  // never oversubscribe TMEM
   const int grid = std::max(1, std::min(a.num_tiles, ctx.num_sms * occ));
   const CUtensorMap tA = make_tensor_map_2d(a.a, a.dtype, a.k_pad, a.rows, KC, 128, KC);
@@ -265,7 +274,12 @@ void launch_kc(Ctx& ctx, const GemmArgs& a) {
 
 CUtensorMap make_tensor_map_2d(const void* base, int dtype, uint64_t inner, uint64_t outer, uint32_t box_inner,
                                uint32_t box_outer, int kc) {
-  return make_map_impl(base, dtype, inner, outer, box_inner, box_outer, kc);
+  return make_map_impl(base, dtype, inner, outer, inner * 2, box_inner, box_outer, kc);
+}
+
+CUtensorMap make_tensor_map_2d_strided(const void* base, int dtype, uint64_t inner, uint64_t outer,
+                                       uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer, int kc) {
+  return make_map_impl(base, dtype, inner, outer, row_stride_bytes, box_inner, box_outer, kc);
 }
 
 int gemm_chunk(int k_pad) { return k_pad % 64 == 0 ? 64 : (k_pad % 32 == 0 ? 32 : 16); }

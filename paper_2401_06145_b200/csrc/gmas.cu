@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cstring>
 #include <numeric>
+#include <set>
 #include <vector>
 
 #include "common.cuh"
@@ -466,7 +467,10 @@ void scatter_seg_dispatch(Ctx& ctx, int T, const TP* partials, int c_out, const 
   const int TI = scatter_rows(c_out, T, sizeof(TP));
   const size_t smem = static_cast<size_t>(kScatStages) * TI * c_out * sizeof(TP) + sizeof(int32_t) * (K3 * TI + 3 * K3) + 16;
   auto go = [&](auto kern) {
-    SCONV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    // once per kernel (keyed by address: tile variants share one function-pointer type)
+    static thread_local std::set<std::pair<const void*, int>> attr_set;
+    if (attr_set.insert({reinterpret_cast<const void*>(kern), ctx.device}).second)
+      SCONV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     ctx.launch("k_scatter", [&] {
       kern<<<static_cast<unsigned>(ceil_div<int64_t>(n_out, TI)), kScatThreads, smem, ctx.stream>>>(
           partials, c_out, nbr, n_out, K3, plan, static_cast<TOut*>(io.f_out), io.ld_out,
@@ -692,6 +696,7 @@ void fused_forward(Ctx& ctx, MapData& m, const WeightData& w, const LayerIO& io)
   FusedArgs a;
   a.f_in = fin;
   a.ld_in = ld;
+  a.n_in = m.n_in;
   a.nbr = m.nbr_in.get<int32_t>();
   a.n_out = m.n_out;
   a.w = &w;

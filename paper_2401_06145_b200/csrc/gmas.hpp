@@ -8,7 +8,7 @@
 
 namespace sconvb {
 
-constexpr int kMaxOffsets = 512;  // K <= 8
+constexpr int kMaxOffsets = 343;  // K <= 7 (the LayerPlan kernel parameter stays ~8 KB)
 
 // Per-layer GMaS plan, passed BY VALUE as a kernel parameter (CUDA >= 12.1 allows 32 KB of
 // parameters), so no host->device copy (and no pinned staging) is needed between layers.

@@ -24,6 +24,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// same, for warps off the critical path: back off between polls so spinning does not steal
+// issue slots from the producer warps on the same scheduler
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  for (;;) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (done) return;
+    __nanosleep(256);
+  }
+}
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -35,6 +51,15 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
           smem_u32(dst)),
       "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+// TMA gather4: rows r.x..r.w (outer coordinate; out-of-range = zero-filled row) of a 2D
+// tensor map with box {inner, 1}, columns from c0, to 4 consecutive swizzled smem rows.
+__device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* map, int c0, int4 r, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(r.x), "r"(r.y), "r"(r.z), "r"(r.w)
       : "memory");
 }
 // 16-byte global -> shared copy (L2 only); src_bytes = 0 writes 16 zero bytes (zfill).
@@ -123,5 +148,8 @@ __host__ __device__ __forceinline__ uint32_t idesc_f16(int dtype_is_bf16, int n)
 // Host: 2D K-major tensor map over a [outer][inner] 16-bit array, swizzle matching KC.
 CUtensorMap make_tensor_map_2d(const void* base, int dtype, uint64_t inner, uint64_t outer, uint32_t box_inner,
                                uint32_t box_outer, int kc);
+// Same with an explicit row stride (bytes, multiple of 16).
+CUtensorMap make_tensor_map_2d_strided(const void* base, int dtype, uint64_t inner, uint64_t outer,
+                                       uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer, int kc);
 
 }  // namespace sconvb

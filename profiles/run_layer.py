@@ -48,7 +48,9 @@ if a.time:
     ctx.set_profiling(True)
     ctx.profile_reset()
 ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+_stream = torch.cuda.Stream()  # a real stream: the legacy default (handle 0) would not order with the library's
+torch.cuda.set_stream(_stream)
+ctx.set_stream(_stream.cuda_stream)
 ev0.record()
 for _ in range(a.steps):
     step()

@@ -28,7 +28,9 @@ g = bench.graph(a.workload)
 net = N.Network(ctx, g, N.init_weights(g, 1), sc.exec_cfg(dataflow=df))
 coords, feats = bench.scene(a.workload, 0)
 xyz_d, f_d = torch.from_numpy(coords).cuda(), torch.from_numpy(feats).cuda()
-ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+_stream = torch.cuda.Stream()  # a real stream: the legacy default (handle 0) would not order with the library's
+torch.cuda.set_stream(_stream)
+ctx.set_stream(_stream.cuda_stream)
 if a.time:
     ctx.set_profiling(True)
 for _ in range(a.steps):
