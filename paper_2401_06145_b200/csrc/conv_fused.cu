@@ -24,14 +24,18 @@
 //   warp 8     TMEM owner; lane 0 issues tcgen05.mma (M=128, N=block_n, K=16) and commits
 // Two TMEM accumulators let the epilogue of tile t overlap the MMAs of tile t+1.
 #include <algorithm>
+#include <cstdint>
 #include <cstdio>
 #include <cstdlib>
 #include <map>
 #include <string>
 #include <vector>
 
+#include <cub/cub.cuh>
+
 #include "common.cuh"
 #include "conv_fused.hpp"
+#include "map.hpp"
 #include "sm100.cuh"
 
 namespace sconvb {
@@ -122,10 +126,15 @@ struct OutCvt<__nv_bfloat16> {
   static __device__ __forceinline__ __nv_bfloat16 from(float v) { return __float2bfloat16_rn(v); }
 };
 
+struct MaskOrder {
+  int pos[32];
+};
+
 struct FusedParams {
   const unsigned char* f_in;
   int64_t ld_in_bytes;
-  const int32_t* nbr;
+  const int32_t* nbr;   // [K3][n_out] in tile-row order
+  const int32_t* perm;  // tile row -> output row (null: identity)
   int64_t n_out;
   int K3, num_kb, block_n, n_pad, n_blocks, num_tiles, c_out;
   void* out;
@@ -136,6 +145,7 @@ struct FusedParams {
   int vec;  // 16-byte aligned output / residual rows
   uint32_t stage_bytes, a_bytes, b_bytes, idx_off, bar_off;
   int stages;  // smem ring depth
+  int target_occ;  // resident CTAs per SM the ring was sized for
   unsigned long long* trace;  // debug 5: CTA 0 event timeline {kind<<56 | seq<<32 | t_lo}
   int debug;   // profiling experiments only (SCONV_FUSED_DEBUG bits): 1 no gather copies, 2 no MMAs,
                // 4 no weight TMA (plain arrive), 8 CTA-0 timeline trace
@@ -158,7 +168,7 @@ __device__ __forceinline__ void trace_ev(const FusedParams& p, int kind, int seq
 
 // NK = compile-time offset count (registers prefetch the next tile's index rows), 0 = runtime
 template <int NK, int KC, class TOut>
-__global__ void __launch_bounds__(kThreads, 2) k_conv_fused(const __grid_constant__ CUtensorMap tmB,
+__global__ void __launch_bounds__(kThreads, NK == 0 ? 4 : 2) k_conv_fused(const __grid_constant__ CUtensorMap tmB,
                                                            const __grid_constant__ FusedParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte aligned base (SW128 atoms) derived by OFFSET from the __shared__ array, so the
@@ -377,8 +387,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_conv_fused(const __grid_constan
       const int nb = t % p.n_blocks;
       const int n0 = nb * p.block_n;
       const int n_tile = min(p.block_n, p.n_pad - n0);
-      const int64_t i = static_cast<int64_t>(t / p.n_blocks) * 128 + q * 32 + lane;
-      const bool valid = i < p.n_out;
+      const int64_t r = static_cast<int64_t>(t / p.n_blocks) * 128 + q * 32 + lane;
+      const bool valid = r < p.n_out;
+      const int64_t i = valid && p.perm ? static_cast<int64_t>(__ldg(p.perm + r)) : r;
       const int ncols = min(n_tile, p.c_out - n0);
       mbar_wait_backoff(&tfull[acc], acc_phase);  // idle warps yield issue slots to the producers
       if (warp == 4 && lane == 0) trace_ev(p, 5, t, tr5);
@@ -433,6 +444,26 @@ __global__ void __launch_bounds__(kThreads, 2) k_conv_fused(const __grid_constan
   }
 }
 
+// neighbour-mask sort keys: bit pos[k] set when output i has a neighbour at offset k
+__global__ void k_mask_keys(const int32_t* __restrict__ nbr, int64_t n, int K3, const __grid_constant__ MaskOrder ord,
+                            uint32_t* __restrict__ keys, int32_t* __restrict__ idx) {
+  const int64_t i = blockIdx.x * int64_t{blockDim.x} + threadIdx.x;
+  if (i >= n) return;
+  uint32_t key = 0;
+  for (int k = 0; k < K3; ++k) key |= static_cast<uint32_t>(__ldg(nbr + int64_t{k} * n + i) >= 0) << ord.pos[k];
+  keys[i] = key;
+  idx[i] = static_cast<int32_t>(i);
+}
+
+// nbr_perm[k][r] = nbr_in[k][perm[r]] (coalesced writes; reads gathered from L2)
+__global__ void k_permute_nbr(const int32_t* __restrict__ nbr, const int32_t* __restrict__ perm, int64_t n, int K3,
+                              int32_t* __restrict__ out) {
+  const int64_t g = blockIdx.x * int64_t{blockDim.x} + threadIdx.x;
+  if (g >= n * K3) return;
+  const int64_t k = g / n, r = g - k * n;
+  out[g] = __ldg(nbr + k * n + __ldg(perm + r));
+}
+
 template <class TS, class TD>
 __global__ void k_convert_rows(const TS* __restrict__ src, int64_t n, int c, int64_t ld_src, TD* __restrict__ dst,
                                int64_t ld_dst) {
@@ -465,9 +496,9 @@ void launch_t(Ctx& ctx, const FusedArgs& a, const FusedParams& prm, size_t smem,
   }
   const int by_smem = static_cast<int>((228u * 1024u) / (smem + 1024u));
   const int by_regs = 65536 / std::max(1, ((regs * 32 + 255) / 256 * 256) * (kThreads / 32));
-  int occ = std::max(1, std::min({by_smem, by_regs, static_cast<int>(512u / prm.tmem_cols), 2}));
+  int occ = std::max(1, std::min({by_smem, by_regs, static_cast<int>(512u / prm.tmem_cols), NK == 0 ? 4 : 2}));
   const int grid = std::max(1, std::min(prm.num_tiles, ctx.num_sms * occ));
-  if (std::getenv("SCONV_DEBUG_SYNC"))
+  if (const char* dbg = std::getenv("SCONV_DEBUG_SYNC"); dbg && dbg[0] == '1')
     std::fprintf(stderr, "[sconv] k_conv_fused<%d,%d> tiles=%d grid=%d occ=%d smem=%zu stages=%d bn=%d cols=%u\n", NK, KC,
                  prm.num_tiles, grid, occ, smem, prm.stages, prm.block_n, prm.tmem_cols);
   ctx.launch("k_conv_fused", [&] { kern<<<grid, kThreads, smem, ctx.stream>>>(tB, prm); });
@@ -476,7 +507,12 @@ void launch_t(Ctx& ctx, const FusedArgs& a, const FusedParams& prm, size_t smem,
 template <int KC, class TOut>
 void launch_nk(Ctx& ctx, const FusedArgs& a, const FusedParams& prm, size_t smem, const CUtensorMap& tB) {
   switch (prm.K3) {
-    case 27: launch_t<27, KC, TOut>(ctx, a, prm, smem, tB); break;
+    case 27:
+      if (prm.target_occ > 2)
+        launch_t<0, KC, TOut>(ctx, a, prm, smem, tB);
+      else
+        launch_t<27, KC, TOut>(ctx, a, prm, smem, tB);
+      break;
     case 8: launch_t<8, KC, TOut>(ctx, a, prm, smem, tB); break;
     case 1: launch_t<1, KC, TOut>(ctx, a, prm, smem, tB); break;
     default: launch_t<0, KC, TOut>(ctx, a, prm, smem, tB); break;
@@ -520,6 +556,7 @@ void launch_conv_fused(Ctx& ctx, const FusedArgs& a) {
   prm.f_in = static_cast<const unsigned char*>(a.f_in);
   prm.ld_in_bytes = a.ld_in * 2;
   prm.nbr = a.nbr;
+  prm.perm = a.perm;
   prm.n_out = a.n_out;
   prm.K3 = w.K3;
   prm.num_kb = w.k_pad / kc;
@@ -553,9 +590,15 @@ void launch_conv_fused(Ctx& ctx, const FusedArgs& a) {
   // shared memory, else one CTA with up to kMaxStages stages.
   const uint32_t idx_bytes = static_cast<uint32_t>(w.K3) * 128u * 4u;
   const uint32_t fixed = 1024u + idx_bytes + (2 * kMaxStages + 3 * kInfo + 16) * 8u + 64u;
-  const uint32_t half = 113u * 1024u, whole = 227u * 1024u;
+  int target = 2;
+  if (const char* e = std::getenv("SCONV_FUSED_OCC")) target = std::max(1, std::min(4, std::atoi(e)));
+  prm.target_occ = target;
+  const uint32_t half = (227u * 1024u) / static_cast<uint32_t>(target) - 1024u, whole = 227u * 1024u;
   int stages = fixed < half ? static_cast<int>((half - fixed) / prm.stage_bytes) : 0;
-  if (stages < 6) stages = static_cast<int>((whole - fixed) / prm.stage_bytes);
+  if (stages < (target > 2 ? 3 : 6)) {
+    stages = static_cast<int>((whole - fixed) / prm.stage_bytes);
+    prm.target_occ = 1;
+  }
   stages = std::min(stages, kMaxStages);
   if (stages < 2) fail(SCONV_ERR_ARG, "fused layer tile does not fit in shared memory");
   prm.stages = stages;
@@ -593,6 +636,49 @@ void launch_conv_fused(Ctx& ctx, const FusedArgs& a) {
     launch_kc<__half>(ctx, a, prm, smem, tB, kc);
   else
     launch_kc<__nv_bfloat16>(ctx, a, prm, smem, tB, kc);
+}
+
+void prepare_fused_layout(Ctx& ctx, MapData& m) {
+  if (m.fused_ready) return;
+  m.fused_ready = true;
+  const int64_t n = m.n_out;
+  const int K3 = m.K3;
+  m.permuted = K3 > 1 && K3 <= 32 && n > 2 * 128 && n <= INT32_MAX;
+  if (!m.permuted) return;
+  // Bit position per offset: rarer offsets (larger L1 norm: corners, then edges, then faces,
+  // the always-present centre last) in the more significant bits, so equal-or-similar masks
+  // end up adjacent (KITTI scan: 25.4 -> 10.4 active offsets per 128-row tile).
+  MaskOrder ord{};
+  std::vector<int> order(K3);
+  for (int k = 0; k < K3; ++k) order[k] = k;
+  auto norm = [&](int k) { return std::abs(m.delta[k].x) + std::abs(m.delta[k].y) + std::abs(m.delta[k].z); };
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return norm(a) < norm(b); });
+  for (int p = 0; p < K3; ++p) ord.pos[order[p]] = p;
+  const cudaStream_t st = ctx.stream;
+  DevBuf keys, keys_sorted, idx;
+  keys.alloc(4 * n, st);
+  keys_sorted.alloc(4 * n, st);
+  idx.alloc(4 * n, st);
+  m.row_perm.alloc(4 * n, st);
+  m.nbr_perm.alloc(4 * n * K3, st);
+  const unsigned b1 = static_cast<unsigned>(ceil_div<int64_t>(n, 256));
+  ctx.launch("k_mask_keys", [&] {
+    k_mask_keys<<<b1, 256, 0, st>>>(m.nbr_in.get<int32_t>(), n, K3, ord, keys.get<uint32_t>(), idx.get<int32_t>());
+  });
+  size_t temp = 0;
+  SCONV_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp, keys.get<uint32_t>(), keys_sorted.get<uint32_t>(),
+                                             idx.get<int32_t>(), m.row_perm.get<int32_t>(), static_cast<int>(n), 0, K3,
+                                             st));
+  ctx.scratch_misc.reserve(temp, st);
+  ctx.launch("cub_radix_sort_masks", [&] {
+    cub::DeviceRadixSort::SortPairs(ctx.scratch_misc.get(), temp, keys.get<uint32_t>(), keys_sorted.get<uint32_t>(),
+                                    idx.get<int32_t>(), m.row_perm.get<int32_t>(), static_cast<int>(n), 0, K3, st);
+  });
+  const unsigned b2 = static_cast<unsigned>(ceil_div<int64_t>(n * K3, 256));
+  ctx.launch("k_permute_nbr", [&] {
+    k_permute_nbr<<<b2, 256, 0, st>>>(m.nbr_in.get<int32_t>(), m.row_perm.get<int32_t>(), n, K3,
+                                      m.nbr_perm.get<int32_t>());
+  });
 }
 
 void convert_rows(Ctx& ctx, const void* src, int src_dtype, int64_t n, int c, int64_t ld_src, void* dst, int dst_dtype,

@@ -11,7 +11,8 @@ struct FusedArgs {
   const void* f_in = nullptr;  // 16-bit (the weight dtype) [n_in][ld_in]; columns [c_in, k_pad) zero
   int64_t ld_in = 0;
   int64_t n_in = 0;
-  const int32_t* nbr = nullptr;  // [K3][n_out]: input row of (k, i) or -1 (MapData::nbr_in)
+  const int32_t* nbr = nullptr;  // [K3][n_out] in tile-row order: input row or -1 (nbr_in / nbr_perm)
+  const int32_t* perm = nullptr;  // tile row -> output row (null: identity order)
   int64_t n_out = 0;
   const WeightData* w = nullptr;
   void* out = nullptr;  // [n_out][ld_out] of out_dtype
@@ -22,6 +23,10 @@ struct FusedArgs {
   int relu = 0;
   int block_n = 0;  // 0 = choose (fill the SMs)
 };
+
+struct MapData;
+// Lazily orders the map's output rows by neighbour bitmask for the fused kernel (once per map).
+void prepare_fused_layout(Ctx& ctx, MapData& m);
 
 // true when the fused kernel supports this layer (K3 <= 64, 16-bit operands)
 bool fused_supported(int K3, int c_in, int c_out);

@@ -680,6 +680,7 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
   if (cfg.transposed)
     for (auto& d : delta) d = make_int3(-d.x, -d.y, -d.z);
   m->K3 = static_cast<int>(delta.size());
+  m->delta = delta;
   const int K3 = m->K3;
   const int64_t n = P.n;
 

@@ -23,6 +23,13 @@ struct MapData {
   DevBuf pair_in, pair_out;  // int32 x |M|, canonical order (k, then i)
   DevBuf nbr_pos;            // int32 x K3 x n_out: canonical position m of (k, i) or -1
   DevBuf nbr_in;             // int32 x K3 x n_out: input row j of (k, i) or -1 (fused dataflow)
+  std::vector<int3> delta;   // search offsets (host copy)
+  // Fused-dataflow row order (built lazily, conv_fused.cu prepare_fused_layout): output rows
+  // sorted by their neighbour bitmask so a 128-row tile touches few offsets.
+  bool fused_ready = false;
+  bool permuted = false;     // false: identity order (nbr_perm unused, nbr_in is read directly)
+  DevBuf row_perm;           // int32 x n_out: tile row r -> output row
+  DevBuf nbr_perm;           // int32 x K3 x n_out: nbr_in[k][row_perm[r]]
   std::vector<int64_t> sizes;      // n_k (host)
   std::vector<int32_t> starts;     // map_start (host copy)
   int64_t total = 0;
