@@ -323,6 +323,7 @@ sconv_status sconv_map_build_chained(sconv_ctx* ctx, const sconv_map* prev, cons
 sconv_status sconv_map_get_info(sconv_ctx* ctx, const sconv_map* m, sconv_map_info* info) {
   return guarded(ctx, [&] {
     if (!m || !info) fail(SCONV_ERR_ARG, "null argument");
+    ensure_canonical(*ctx, const_cast<MapData&>(static_cast<const MapData&>(*m)));
     info->num_inputs = m->n_in;
     info->num_outputs = m->n_out;
     info->num_offsets = m->K3;
@@ -339,6 +340,7 @@ sconv_status sconv_map_read(sconv_ctx* ctx, const sconv_map* m, int32_t* out_xyz
                             int32_t* out_idx) {
   return guarded(ctx, [&] {
     if (!m) fail(SCONV_ERR_ARG, "null map");
+    ensure_canonical(*ctx, const_cast<MapData&>(static_cast<const MapData&>(*m)));
     if (out_xyz && m->n_out > 0) {
       std::vector<uint64_t> keys(m->n_out);
       SCONV_CUDA(cudaMemcpyAsync(keys.data(), m->q_keys_ptr(), keys.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));

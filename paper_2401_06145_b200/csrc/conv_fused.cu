@@ -644,6 +644,7 @@ void prepare_fused_layout(Ctx& ctx, MapData& m) {
   const int64_t n = m.n_out;
   const int K3 = m.K3;
   m.permuted = K3 > 1 && K3 <= 32 && n > 2 * 128 && n <= INT32_MAX;
+  if (const char* e = std::getenv("SCONV_NO_PERMUTE"); e && e[0] == '1') m.permuted = false;  // experiments
   if (!m.permuted) return;
   // Bit position per offset: rarer offsets (larger L1 norm: corners, then edges, then faces,
   // the always-present centre last) in the more significant bits, so equal-or-similar masks

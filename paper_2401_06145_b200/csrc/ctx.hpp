@@ -116,9 +116,10 @@ struct Ctx {
   // scratch (grow-only, stream ordered)
   DevBuf scratch_sort, scratch_misc, flush_buf;
   DevBuf gather_buf, gemm_out, plan_dev;
-  // Pinned host staging, carved into fixed regions so an in-flight async copy from one
-  // region is never overwritten by another purpose. Every map build ends with a stream
-  // sync, so a region's next reuse always follows completion of its previous copy.
+  // Pinned host staging, carved into fixed regions, used ONLY for device->host readbacks that
+  // are followed by a stream sync (map sizes / flags). Host->device inputs of a map build are
+  // generated on the device instead: lazy (network) map builds end without a sync, so a
+  // staging region reused by the next build could be overwritten before its copy ran.
   static constexpr size_t kPinFlagsBytes = 8192, kPinReadbackBytes = 16384, kPinPlanBytes = 1 << 20;
   unsigned char* pinned = nullptr;
   void* pin_flags() { return pinned; }

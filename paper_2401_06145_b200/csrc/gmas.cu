@@ -562,6 +562,7 @@ namespace {
 
 // Minuet GMaS on device buffers: plan -> gather -> grouped GEMM -> scatter.
 void gmas_forward(Ctx& ctx, MapData& m, const WeightData& w, const sconv_exec_cfg& cfg, const LayerIO& io) {
+  ensure_canonical(ctx, m);  // GMaS needs the per-offset sizes and canonical pair lists
   const cudaStream_t st = ctx.stream;
   const int c_in = w.c_in, c_out = w.c_out, K3 = m.K3;
   int Tg = cfg.gather_tile, Ts = cfg.scatter_tile;

@@ -60,6 +60,25 @@ __global__ void k_pack_keys(const int32_t* __restrict__ xyz, int64_t n, uint64_t
   }
 }
 
+__global__ void k_init_flags(MapFlags* f) {
+  f->bad_coord = f->bad_target = f->bad_floor = ULLONG_MAX;
+  f->unsorted = f->target_unsorted = 0;
+  f->bbox[0] = f->bbox[1] = f->bbox[2] = INT_MAX;
+  f->bbox[3] = f->bbox[4] = f->bbox[5] = INT_MIN;
+  f->wide = f->big_bucket = 0;
+}
+
+// weight offsets (weight_offsets_ext order: a outer, b, c inner; odd K centred, even K in
+// [0, K-1]) times the offset scale, negated for transposed maps
+__global__ void k_make_offsets(int3* __restrict__ d, int K, int scale, int transposed, int K3) {
+  for (int k = threadIdx.x; k < K3; k += blockDim.x) {
+    const int lo = (K % 2 == 1) ? -(K / 2) : 0;
+    const int a = k / (K * K) + lo, b = (k / K) % K + lo, c = k % K + lo;
+    const int sg = transposed ? -scale : scale;
+    d[k] = make_int3(a * sg, b * sg, c * sg);
+  }
+}
+
 __global__ void k_iota(int32_t* __restrict__ v, int64_t n) {
   const int64_t i = blockIdx.x * int64_t{blockDim.x} + threadIdx.x;
   if (i < n) v[i] = static_cast<int32_t>(i);
@@ -665,13 +684,65 @@ std::vector<int3> weight_offsets_ext(int K, int scale) {
   return d;
 }
 
+namespace {
+void launch_canonical(Ctx& ctx, MapData& m) {
+  auto& pd = m.pending;
+  const cudaStream_t st = ctx.stream;
+  ctx.launch("k_scan_counts", [&] {
+    k_scan_counts<<<static_cast<unsigned>(pd.ntiles), kSearchThreads, 0, st>>>(
+        pd.counts.get<int32_t>(), pd.grid, pd.offs.get<int32_t>(), pd.tiles.get<int32_t>(), pd.nchunk, m.K3,
+        m.map_start.get<int32_t>(), ctx.done_counter());
+  });
+  auto emit = [&](auto kern) {
+    ctx.launch("k_emit", [&] {
+      kern<<<static_cast<unsigned>(pd.nchunk * pd.ngroups), kSearchThreads, 0, st>>>(
+          m.nbr_in.get<int32_t>(), m.nbr_pos.get<int32_t>(), m.n_out, m.K3, pd.nchunk, pd.ngroups,
+          pd.offs.get<int32_t>(), pd.tiles.get<int32_t>(), m.pair_in.get<int32_t>(), m.pair_out.get<int32_t>());
+    });
+  };
+  switch (pd.qpl) {
+    case 1: emit(k_emit<1>); break;
+    case 2: emit(k_emit<2>); break;
+    case 4: emit(k_emit<4>); break;
+    default: emit(k_emit<8>); break;
+  }
+}
+
+// flags + list starts -> host (one sync); sizes / total
+void read_starts(Ctx& ctx, MapData& m, const void* flags, MapFlags* f) {
+  const int K3 = m.K3;
+  if (sizeof(MapFlags) + sizeof(int32_t) * (K3 + 1) > Ctx::kPinReadbackBytes) fail(SCONV_ERR_ARG, "kernel too large");
+  auto* pin2 = static_cast<unsigned char*>(ctx.pin_readback());
+  SCONV_CUDA(cudaMemcpyAsync(pin2, flags, sizeof(MapFlags), cudaMemcpyDeviceToHost, ctx.stream));
+  SCONV_CUDA(cudaMemcpyAsync(pin2 + sizeof(MapFlags), m.map_start.get(), sizeof(int32_t) * (K3 + 1),
+                             cudaMemcpyDeviceToHost, ctx.stream));
+  ctx.sync();
+  std::memcpy(f, pin2, sizeof(MapFlags));
+  m.starts.resize(K3 + 1);
+  std::memcpy(m.starts.data(), pin2 + sizeof(MapFlags), sizeof(int32_t) * (K3 + 1));
+  m.sizes.resize(K3);
+  for (int k = 0; k < K3; ++k) m.sizes[k] = m.starts[k + 1] - m.starts[k];
+  m.total = m.starts[K3];
+}
+}  // namespace
+
+void ensure_canonical(Ctx& ctx, MapData& m) {
+  if (m.canonical) return;
+  if (m.pending.grid > 0) launch_canonical(ctx, m);
+  MapFlags f;
+  read_starts(ctx, m, m.pending.flags.get(), &f);  // lazy maps carry no coordinate checks
+  m.pending = MapData::Pending{};
+  m.canonical = true;
+}
+
 std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map_cfg& cfg, const MapSource* target,
-                                   bool force_wide) {
+                                   bool force_wide, bool lazy) {
   if (cfg.block_B < 4 || cfg.block_B > 1024 || cfg.block_B % 4 != 0)
     fail(SCONV_ERR_ARG, "block size B must be a multiple of 4 in [4, 1024]");
   if (cfg.block_C < 1 || cfg.block_C > 4096) fail(SCONV_ERR_ARG, "query block size C must be in [1, 4096]");
   if (!cfg.transposed && cfg.out_stride < 1) fail(SCONV_ERR_ARG, "stride must be positive");
   if (P.n < 0 || P.n > INT32_MAX / 2) fail(SCONV_ERR_ARG, "point count out of supported range");
+  if (lazy && (!P.keys || (cfg.transposed && (!target || !target->keys)))) lazy = false;
   auto m = std::make_unique<MapData>();
   m->cfg = cfg;
   m->n_in = P.n;
@@ -687,10 +758,10 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
   DevBuf flags_buf;
   flags_buf.alloc(sizeof(MapFlags), st);
   MapFlags* flags = flags_buf.get<MapFlags>();
-  MapFlags init{ULLONG_MAX, ULLONG_MAX, ULLONG_MAX, 0, 0, {INT_MAX, INT_MAX, INT_MAX, INT_MIN, INT_MIN, INT_MIN}, 0, 0};
+  // initialised on the device: lazy builds end without a sync, so no host staging buffer may be
+  // reused by the next build while this build's copies are still queued
+  ctx.launch("k_init_flags", [&] { k_init_flags<<<1, 1, 0, st>>>(flags); });
   auto* pin = reinterpret_cast<MapFlags*>(ctx.pin_flags());
-  pin[0] = init;
-  SCONV_CUDA(cudaMemcpyAsync(flags, pin, sizeof(MapFlags), cudaMemcpyHostToDevice, st));
 
   // ---- source array
   DevBuf xyz_dev;
@@ -867,10 +938,9 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
 
   // ---- search
   m->offsets.alloc(sizeof(int3) * K3, st);
-  static_assert(sizeof(MapFlags) + 512 * sizeof(int3) <= Ctx::kPinFlagsBytes, "pinned flags region");
-  int3* pin_off = reinterpret_cast<int3*>(reinterpret_cast<unsigned char*>(ctx.pin_flags()) + 2 * sizeof(MapFlags));
-  std::memcpy(pin_off, delta.data(), sizeof(int3) * K3);
-  SCONV_CUDA(cudaMemcpyAsync(m->offsets.get(), pin_off, sizeof(int3) * K3, cudaMemcpyHostToDevice, st));
+  ctx.launch("k_make_offsets", [&] {  // same enumeration as weight_offsets_ext, generated on device
+    k_make_offsets<<<1, 512, 0, st>>>(m->offsets.get<int3>(), cfg.kernel_size, cfg.offset_scale, cfg.transposed, K3);
+  });
   m->map_start.alloc(sizeof(int32_t) * (K3 + 1), st);
   m->nbr_pos.alloc(sizeof(int32_t) * std::max<int64_t>(1, int64_t{K3} * n_out), st);
   m->nbr_in.alloc(sizeof(int32_t) * std::max<int64_t>(1, int64_t{K3} * n_out), st);
@@ -922,43 +992,29 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
       case 4: go(k_search<4>); break;
       default: go(k_search<8>); break;
     }
-    ctx.launch("k_scan_counts", [&] {
-      k_scan_counts<<<static_cast<unsigned>(ntiles), kSearchThreads, 0, st>>>(
-          counts.get<int32_t>(), grid2, offs.get<int32_t>(), tiles.get<int32_t>(), nchunk2, K3,
-          m->map_start.get<int32_t>(), ctx.done_counter());
-    });
-    auto emit = [&](auto kern) {
-      ctx.launch("k_emit", [&] {
-        kern<<<static_cast<unsigned>(nchunk2 * ngroups), kSearchThreads, 0, st>>>(
-            m->nbr_in.get<int32_t>(), m->nbr_pos.get<int32_t>(), n_out, K3, nchunk2, ngroups, offs.get<int32_t>(),
-            tiles.get<int32_t>(),
-            m->pair_in.get<int32_t>(),
-                                                                        m->pair_out.get<int32_t>());
-      });
-    };
-    switch (qpl) {
-      case 1: emit(k_emit<1>); break;
-      case 2: emit(k_emit<2>); break;
-      case 4: emit(k_emit<4>); break;
-      default: emit(k_emit<8>); break;
-    }
+    auto& pd = m->pending;
+    pd.counts = std::move(counts);
+    pd.offs = std::move(offs);
+    pd.tiles = std::move(tiles);
+    pd.nchunk = nchunk2;
+    pd.grid = grid2;
+    pd.ntiles = ntiles;
+    pd.ngroups = ngroups;
+    pd.qpl = qpl;
+    if (!lazy) launch_canonical(ctx, *m);
+  }
+  if (lazy) {  // canonical lists + readback deferred to ensure_canonical()
+    m->canonical = false;
+    m->total = -1;
+    m->pending.flags = std::move(flags_buf);
+    return m;
   }
   // ---- readback: flags + canonical list starts (one sync per map)
-  if (sizeof(MapFlags) + sizeof(int32_t) * (K3 + 1) > Ctx::kPinReadbackBytes) fail(SCONV_ERR_ARG, "kernel too large");
-  auto* pin2 = static_cast<unsigned char*>(ctx.pin_readback());
-  SCONV_CUDA(cudaMemcpyAsync(pin2, flags, sizeof(MapFlags), cudaMemcpyDeviceToHost, st));
-  SCONV_CUDA(cudaMemcpyAsync(pin2 + sizeof(MapFlags), m->map_start.get(), sizeof(int32_t) * (K3 + 1),
-                             cudaMemcpyDeviceToHost, st));
-  ctx.sync();
   MapFlags f;
-  std::memcpy(&f, pin2, sizeof(f));
+  read_starts(ctx, *m, flags, &f);
+  m->pending = MapData::Pending{};
   check_flags(f);
   if (f.wide || f.big_bucket) return build_map(ctx, P, cfg, target, true);  // exact fallback: CUB 64-bit sort
-  m->starts.resize(K3 + 1);
-  std::memcpy(m->starts.data(), pin2 + sizeof(MapFlags), sizeof(int32_t) * (K3 + 1));
-  m->sizes.resize(K3);
-  for (int k = 0; k < K3; ++k) m->sizes[k] = m->starts[k + 1] - m->starts[k];
-  m->total = m->starts[K3];
   return m;
 }
 

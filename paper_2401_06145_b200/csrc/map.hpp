@@ -33,6 +33,14 @@ struct MapData {
   std::vector<int64_t> sizes;      // n_k (host)
   std::vector<int32_t> starts;     // map_start (host copy)
   int64_t total = 0;
+  // Canonical pair lists (scan + emit + one readback sync) are built lazily for network maps:
+  // the fused dataflow needs only nbr_in (ensure_canonical() before using sizes/pairs/nbr_pos).
+  bool canonical = true;
+  struct Pending {
+    DevBuf counts, offs, tiles, flags;
+    int64_t nchunk = 0, grid = 0, ntiles = 0;
+    int ngroups = 0, qpl = 0;
+  } pending;
   // last GMaS stats
   int64_t buffer_length = 0;
   int groups = 0;
@@ -52,8 +60,12 @@ struct MapSource {
   int64_t n = 0;
 };
 
+// lazy: skip the canonical lists and the end-of-build sync (only for maps over existing sorted
+// device keys, whose coordinates were validated when they were first built).
 std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map_cfg& cfg, const MapSource* target,
-                                   bool force_wide = false);
+                                   bool force_wide = false, bool lazy = false);
+// Builds the canonical pair lists of a lazily built map (no-op otherwise): scan + emit + sync.
+void ensure_canonical(Ctx& ctx, MapData& m);
 
 // Weight offsets (reference weight_offsets + SURVEY §2.2 even-K extension), lexicographic.
 std::vector<int3> weight_offsets_ext(int K, int scale);

@@ -255,7 +255,9 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
           T.n = ct.n;
           T.sorted = true;
         }
-        auto m = build_map(ctx, P, mcfg, o.transposed ? &T : nullptr);
+        // maps over the network's own (already validated) coordinate sets skip the canonical
+        // lists and the end-of-build sync unless a GMaS conv asks for them
+        auto m = build_map(ctx, P, mcfg, o.transposed ? &T : nullptr, false, /*lazy=*/true);
         ++maps_built;
         if (!coordsets[a.coordset].keys && coordsets[a.coordset].sorted)
           coordsets[a.coordset].keys = m->src_keys;  // sorted raw input: its packed keys, same row order

@@ -201,6 +201,32 @@ def test_fused_layer_parity(ctx, oracle, K, s, n, extent, cin, cout):
     assert mx <= 1e-2 and mean <= 1e-3, (mx, mean)
 
 
+@pytest.mark.parametrize("transposed", [False, True])
+def test_fused_even_kernel_and_transposed(ctx, oracle, transposed):
+    """K=2 s=2 down-sampling and its transposed map (U-Net up-conv) through the fused kernel
+    (rows ordered by neighbour mask) against the oracle on the same 16-bit operands."""
+    rng = np.random.default_rng(12)
+    fine = sort_rows(random_cloud(rng, 9000, 40))
+    down = sc.KernelMap.build(ctx, fine, True, 2, 1, 2)
+    coarse = down.read()[0]
+    if transposed:
+        m = sc.KernelMap.build(ctx, coarse, True, 2, 1, 1, transposed=True, target=fine)
+        xin, cin, cout, ref_args = coarse, 64, 32, dict(transposed=True, target=fine)
+    else:
+        m, xin, cin, cout, ref_args = down, fine, 32, 64, {}
+    F = rng.random((len(xin), cin), dtype=np.float32)
+    W = ((rng.random((8, cin, cout)) * 0.2 - 0.1)).astype(np.float32)
+    w = sc.Weights(ctx, W)
+    got = sc.layer_forward(ctx, m, w, F, sc.exec_cfg(dataflow=sc.DATAFLOW_FUSED))
+    if transposed:
+        _, of, _ = oracle.layer_forward(xin, True, f16(F), f16(W), 2, 1, 1, True, fine)
+    else:
+        _, of, _ = oracle.layer_forward(xin, True, f16(F), f16(W), 2, 1, 2)
+    assert rel_errors(got, of)[0] <= 5e-6
+    gm = sc.layer_forward(ctx, m, w, F, sc.exec_cfg(partial_f16=0))
+    assert rel_errors(got, gm)[0] <= 5e-6
+
+
 def test_fused_matches_gmas(ctx):
     """Both dataflows on one map: fp32-partial GMaS and the fused kernel agree to fp32 rounding."""
     rng = np.random.default_rng(21)
