@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <climits>
 #include <cstring>
+#include <functional>
 #include <string>
 
 #include "common.cuh"
@@ -32,6 +33,8 @@ struct MapFlags {
   int bbox[6];                   // min x,y,z / max x,y,z of P (unsorted path)
   int wide;                      // compact key needs > 32 bits: rebuild with the 64-bit CUB sort
   int big_bucket;                // a sort bucket exceeds kMaxBucket: rebuild with the 64-bit CUB sort
+  int fbox[6];                   // bbox of the Eq. 1 floored coordinates (strided maps)
+  int fwide;                     // floored compact key needs > 32 bits: redo with 64-bit keys
 };
 
 // ---------------------------------------------------------------- key packing
@@ -60,17 +63,19 @@ __global__ void k_pack_keys(const int32_t* __restrict__ xyz, int64_t n, uint64_t
   }
 }
 
-__global__ void k_init_flags(MapFlags* f) {
-  f->bad_coord = f->bad_target = f->bad_floor = ULLONG_MAX;
-  f->unsorted = f->target_unsorted = 0;
-  f->bbox[0] = f->bbox[1] = f->bbox[2] = INT_MAX;
-  f->bbox[3] = f->bbox[4] = f->bbox[5] = INT_MIN;
-  f->wide = f->big_bucket = 0;
-}
-
-// weight offsets (weight_offsets_ext order: a outer, b, c inner; odd K centred, even K in
-// [0, K-1]) times the offset scale, negated for transposed maps
-__global__ void k_make_offsets(int3* __restrict__ d, int K, int scale, int transposed, int K3) {
+// One launch per map build: flag init + weight offsets (weight_offsets_ext order: a outer,
+// b, c inner; odd K centred, even K in [0, K-1]) times the offset scale, negated when transposed
+__global__ void k_init_map(MapFlags* f, int3* __restrict__ d, int K, int scale, int transposed, int K3) {
+  if (threadIdx.x == 0) {
+    f->bad_coord = f->bad_target = f->bad_floor = ULLONG_MAX;
+    f->unsorted = f->target_unsorted = 0;
+    f->bbox[0] = f->bbox[1] = f->bbox[2] = INT_MAX;
+    f->bbox[3] = f->bbox[4] = f->bbox[5] = INT_MIN;
+    f->wide = f->big_bucket = 0;
+    f->fbox[0] = f->fbox[1] = f->fbox[2] = INT_MAX;
+    f->fbox[3] = f->fbox[4] = f->fbox[5] = INT_MIN;
+    f->fwide = 0;
+  }
   for (int k = threadIdx.x; k < K3; k += blockDim.x) {
     const int lo = (K % 2 == 1) ? -(K / 2) : 0;
     const int a = k / (K * K) + lo, b = (k / K) % K + lo, c = k % K + lo;
@@ -263,6 +268,79 @@ __global__ void k_floor_keys(const uint64_t* __restrict__ src, const int32_t* __
     return;
   }
   out[i] = pack_key_unchecked(static_cast<int32_t>(fx), static_cast<int32_t>(fy), static_cast<int32_t>(fz));
+}
+
+// Eq. 1 floor + bbox of the floored coordinates (warp-reduced atomics), for 32-bit compact keys
+__global__ void k_floor_bbox(const uint64_t* __restrict__ src, const int32_t* __restrict__ src_idx, int64_t n, int s,
+                             uint64_t* __restrict__ out, MapFlags* flags) {
+  const int64_t i = blockIdx.x * int64_t{blockDim.x} + threadIdx.x;
+  int mn[3] = {INT_MAX, INT_MAX, INT_MAX}, mx[3] = {INT_MIN, INT_MIN, INT_MIN};
+  if (i < n) {
+    int32_t x, y, z;
+    unpack_key(src[i], x, y, z);
+    const int64_t f[3] = {floor_div(x, s) * s, floor_div(y, s) * s, floor_div(z, s) * s};
+    if (!in_range(f[0]) || !in_range(f[1]) || !in_range(f[2])) {
+      const int axis = !in_range(f[0]) ? 0 : (!in_range(f[1]) ? 1 : 2);
+      const int64_t j = src_idx ? src_idx[i] : i;
+      atomicMin(&flags->bad_floor, static_cast<unsigned long long>(j * 3 + axis));
+      out[i] = 0;
+    } else {
+      out[i] = pack_key_unchecked(static_cast<int32_t>(f[0]), static_cast<int32_t>(f[1]), static_cast<int32_t>(f[2]));
+#pragma unroll
+      for (int a = 0; a < 3; ++a) mn[a] = mx[a] = static_cast<int>(f[a]);
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      mn[a] = min(mn[a], __shfl_xor_sync(0xFFFFFFFFu, mn[a], o));
+      mx[a] = max(mx[a], __shfl_xor_sync(0xFFFFFFFFu, mx[a], o));
+    }
+  if ((threadIdx.x & 31) == 0 && mn[0] != INT_MAX)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      atomicMin(&flags->fbox[a], mn[a]);
+      atomicMax(&flags->fbox[3 + a], mx[a]);
+    }
+}
+
+// floored packed key -> left-aligned... (right-aligned) compact u32 key (x, y, z offsets in units of
+// the stride, minimal bit widths; order preserving)
+__device__ __forceinline__ bool floor_compact_widths(const MapFlags* f, int s, int& bx, int& by, int& bz) {
+  bx = bits_for((int64_t{f->fbox[3]} - f->fbox[0]) / s);
+  by = bits_for((int64_t{f->fbox[4]} - f->fbox[1]) / s);
+  bz = bits_for((int64_t{f->fbox[5]} - f->fbox[2]) / s);
+  return bx + by + bz <= 32;
+}
+
+__global__ void k_floor_compact(const uint64_t* __restrict__ fl, int64_t n, int s, MapFlags* flags,
+                                uint32_t* __restrict__ out) {
+  const int64_t i = blockIdx.x * int64_t{blockDim.x} + threadIdx.x;
+  if (i >= n) return;
+  int bx, by, bz;
+  if (!floor_compact_widths(flags, s, bx, by, bz)) {
+    if (i == 0) flags->fwide = 1;
+    out[i] = 0;
+    return;
+  }
+  int32_t x, y, z;
+  unpack_key(fl[i], x, y, z);
+  out[i] = (static_cast<uint32_t>((x - flags->fbox[0]) / s) << (by + bz)) |
+           (static_cast<uint32_t>((y - flags->fbox[1]) / s) << bz) | static_cast<uint32_t>((z - flags->fbox[2]) / s);
+}
+
+__global__ void k_floor_expand(const uint32_t* __restrict__ ck, const int64_t* __restrict__ count, int s,
+                               const MapFlags* flags, uint64_t* __restrict__ out) {
+  const int64_t i = blockIdx.x * int64_t{blockDim.x} + threadIdx.x;
+  if (i >= *count || flags->fwide) return;
+  int bx, by, bz;
+  floor_compact_widths(flags, s, bx, by, bz);
+  const uint32_t c = ck[i];
+  const int32_t x = flags->fbox[0] + static_cast<int32_t>(c >> (by + bz)) * s;
+  const int32_t y = flags->fbox[1] + static_cast<int32_t>((c >> bz) & ((1u << by) - 1u)) * s;
+  const int32_t z = flags->fbox[2] + static_cast<int32_t>(c & ((1u << bz) - 1u)) * s;
+  out[i] = pack_key_unchecked(x, y, z);
 }
 
 // ---------------------------------------------------------------- double-traversed search
@@ -760,7 +838,10 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
   MapFlags* flags = flags_buf.get<MapFlags>();
   // initialised on the device: lazy builds end without a sync, so no host staging buffer may be
   // reused by the next build while this build's copies are still queued
-  ctx.launch("k_init_flags", [&] { k_init_flags<<<1, 1, 0, st>>>(flags); });
+  m->offsets.alloc(sizeof(int3) * K3, st);
+  ctx.launch("k_init_map", [&] {
+    k_init_map<<<1, 512, 0, st>>>(flags, m->offsets.get<int3>(), cfg.kernel_size, cfg.offset_scale, cfg.transposed, K3);
+  });
   auto* pin = reinterpret_cast<MapFlags*>(ctx.pin_flags());
 
   // ---- source array
@@ -839,6 +920,8 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
 
   // ---- output coordinates Q
   bool need_nout_sync = false;
+  DevBuf fl, fs;  // strided: floored keys / sort scratch (function scope: the wide fallback reuses them)
+  std::function<void()> strided_wide;
   DevBuf nsel;
   DevBuf target_xyz_dev;
   if (cfg.transposed) {
@@ -866,26 +949,56 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
     m->q_keys = m->src_keys;  // stride-1 alias: one array serves as source and query
     m->n_out = n;
   } else {
-    DevBuf fl, fs;
     fl.alloc(sizeof(uint64_t) * std::max<int64_t>(n, 1), st);
     fs.alloc(sizeof(uint64_t) * std::max<int64_t>(n, 1), st);
     m->q_keys = std::make_shared<DevBuf>();
     m->q_keys->alloc(sizeof(uint64_t) * slack(n), st);
     nsel.alloc(sizeof(int64_t), st);
     if (n > 0) {
+      // Eq. 1 on device: floor -> 32-bit bbox-relative compact keys (4 radix passes instead of 8)
+      // -> sort -> unique -> expand; the 64-bit path below runs only if the compact key is wide.
       ctx.launch("k_floor_keys", [&] {
-        k_floor_keys<<<grid_for(n), kThreads, 0, st>>>(src, src_idx, n, cfg.out_stride, fl.get<uint64_t>(), flags);
+        k_floor_bbox<<<grid_for(n), kThreads, 0, st>>>(src, src_idx, n, cfg.out_stride, fl.get<uint64_t>(), flags);
       });
-      sort_keys(ctx, fl.get<uint64_t>(), fs.get<uint64_t>(), n);
+      uint32_t* c32 = reinterpret_cast<uint32_t*>(fs.get<uint64_t>());  // fs is 8n bytes: two u32 arrays
+      uint32_t* s32 = c32 + n;
+      ctx.launch("k_floor_compact", [&] {
+        k_floor_compact<<<grid_for(n), kThreads, 0, st>>>(fl.get<uint64_t>(), n, cfg.out_stride, flags, c32);
+      });
+      {
+        size_t temp = 0;
+        SCONV_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, temp, c32, s32, static_cast<int>(n), 0, 32, st));
+        ctx.scratch_sort.reserve(temp, st);
+        ctx.launch("cub_radix_sort_keys", [&] {
+          cub::DeviceRadixSort::SortKeys(ctx.scratch_sort.get(), temp, c32, s32, static_cast<int>(n), 0, 32, st);
+        });
+      }
+      uint32_t* u32 = reinterpret_cast<uint32_t*>(fl.get<uint64_t>());  // floored keys no longer needed
       size_t temp = 0;
-      SCONV_CUDA(cub::DeviceSelect::Unique(nullptr, temp, fs.get<uint64_t>(), m->q_keys->get<uint64_t>(),
-                                           nsel.get<int64_t>(), n, st));
+      SCONV_CUDA(cub::DeviceSelect::Unique(nullptr, temp, s32, u32, nsel.get<int64_t>(), n, st));
       ctx.scratch_misc.reserve(temp, st);
       ctx.launch("cub_select_unique", [&] {
-        cub::DeviceSelect::Unique(ctx.scratch_misc.get(), temp, fs.get<uint64_t>(), m->q_keys->get<uint64_t>(),
-                                  nsel.get<int64_t>(), n, st);
+        cub::DeviceSelect::Unique(ctx.scratch_misc.get(), temp, s32, u32, nsel.get<int64_t>(), n, st);
+      });
+      ctx.launch("k_floor_expand", [&] {
+        k_floor_expand<<<grid_for(n), kThreads, 0, st>>>(u32, nsel.get<int64_t>(), cfg.out_stride, flags,
+                                                          m->q_keys->get<uint64_t>());
       });
       need_nout_sync = true;
+      strided_wide = [&, n] {  // exact 64-bit fallback (coordinate span beyond 32 compact bits)
+        ctx.launch("k_floor_keys", [&] {
+          k_floor_keys<<<grid_for(n), kThreads, 0, st>>>(src, src_idx, n, cfg.out_stride, fl.get<uint64_t>(), flags);
+        });
+        sort_keys(ctx, fl.get<uint64_t>(), fs.get<uint64_t>(), n);
+        size_t t2 = 0;
+        SCONV_CUDA(cub::DeviceSelect::Unique(nullptr, t2, fs.get<uint64_t>(), m->q_keys->get<uint64_t>(),
+                                             nsel.get<int64_t>(), n, st));
+        ctx.scratch_misc.reserve(t2, st);
+        ctx.launch("cub_select_unique", [&] {
+          cub::DeviceSelect::Unique(ctx.scratch_misc.get(), t2, fs.get<uint64_t>(), m->q_keys->get<uint64_t>(),
+                                    nsel.get<int64_t>(), n, st);
+        });
+      };
     } else {
       m->n_out = 0;
     }
@@ -929,6 +1042,11 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
     static_assert(2 * sizeof(MapFlags) <= Ctx::kPinFlagsBytes, "pinned flags region");
     ctx.sync();
     check_flags(pin[0]);
+    if (pin[0].fwide && strided_wide) {  // rare: redo the output coordinates with 64-bit keys
+      strided_wide();
+      SCONV_CUDA(cudaMemcpyAsync(&pin[1], nsel.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+      ctx.sync();
+    }
     int64_t nout;
     std::memcpy(&nout, &pin[1], sizeof(int64_t));
     m->n_out = nout;
@@ -937,10 +1055,6 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
   const uint64_t* q = m->q_keys_ptr();
 
   // ---- search
-  m->offsets.alloc(sizeof(int3) * K3, st);
-  ctx.launch("k_make_offsets", [&] {  // same enumeration as weight_offsets_ext, generated on device
-    k_make_offsets<<<1, 512, 0, st>>>(m->offsets.get<int3>(), cfg.kernel_size, cfg.offset_scale, cfg.transposed, K3);
-  });
   m->map_start.alloc(sizeof(int32_t) * (K3 + 1), st);
   m->nbr_pos.alloc(sizeof(int32_t) * std::max<int64_t>(1, int64_t{K3} * n_out), st);
   m->nbr_in.alloc(sizeof(int32_t) * std::max<int64_t>(1, int64_t{K3} * n_out), st);
