@@ -14,7 +14,8 @@ ms_per_step = latency of one step. Workloads (BASELINE.json configs):
 
 Multi-GPU (configs[4] shape): one process per GPU, each rank runs its OWN scene
 (scene seed = base + rank): scene sharding with no data-path collective -> weak scaling;
-NCCL is used for the barrier and the max-over-ranks timing only.
+NCCL carries the one-time weight broadcast from rank 0 (shard.broadcast_weights), the
+barrier and the max-over-ranks timing.
 
 Inputs are device resident before the timed region; L2 (126 MB) is flushed by a 256 MB
 memset between timed steps, outside the events. Timing: CUDA events per step on the
@@ -145,12 +146,18 @@ def oracle_crop(c, f, n):
 class NetWorkload:
     """A whole network forward per step; C4 runs a batch of objects (one after another)."""
 
-    def __init__(self, name, ctx, torch, seed, dtype, B, C):
+    def __init__(self, name, ctx, torch, seed, dtype, B, C, dist=None):
         import paper_2401_06145_b200 as sc
         from paper_2401_06145_b200 import network as N
         self.name, self.sc = name, sc
         self.g = graph(name)
-        self.w = N.init_weights(self.g, 1)
+        if dist is not None:  # scene sharding: weights made on rank 0, one NCCL broadcast (SURVEY §8e)
+            from paper_2401_06145_b200.shard import broadcast_weights
+            shapes = {o.weight: (o.K ** 3, o.c_in, o.c_out) for o in self.g.convs()}
+            w0 = N.init_weights(self.g, 1) if dist.get_rank() == 0 else None
+            self.w = broadcast_weights(w0, shapes, src=0, device=torch.device("cuda", torch.cuda.current_device()))
+        else:
+            self.w = N.init_weights(self.g, 1)
         self.net = N.Network(ctx, self.g, self.w, sc.exec_cfg(compute_dtype=dtype), B, C)
         n_obj = 8 if name == "c4_unet_pair_shapenet" else 1
         self.scenes = [scene(name, seed * 100 + i) for i in range(n_obj)]
@@ -259,11 +266,11 @@ class LayerWorkload:
         return self.N / statistics.median(times), f"{len(times)} full C1 layers on the oracle, median"
 
 
-def make_workload(args, ctx, torch, rank):
+def make_workload(args, ctx, torch, rank, dist=None):
     dtype = 1 if args.dtype == "f16" else 2
     if args.workload == "c1_layer_100k":
         return LayerWorkload(args.workload, ctx, torch, 1 + rank, dtype, args.B, args.C)
-    return NetWorkload(args.workload, ctx, torch, rank, dtype, args.B, args.C)
+    return NetWorkload(args.workload, ctx, torch, rank, dtype, args.B, args.C, dist)
 
 
 # ---------------------------------------------------------------- reference arm (CPU oracle)
@@ -331,7 +338,7 @@ def main():
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
-    wl = make_workload(args, ctx, torch, rank)
+    wl = make_workload(args, ctx, torch, rank, dist)
     for _ in range(args.warmup):
         wl.step()
     torch.cuda.synchronize()
