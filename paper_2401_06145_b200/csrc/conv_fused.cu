@@ -145,10 +145,13 @@ struct FusedParams {
   int vec;  // 16-byte aligned output / residual rows
   uint32_t stage_bytes, a_bytes, b_bytes, idx_off, bar_off;
   int stages;  // smem ring depth
+  int G;       // (offset, K-chunk) units per stage
+  int* tile_counter;  // dynamic tile queue (zeroed before the launch)
+  uint32_t unit_bytes;  // one unit's A + B slot (1024-aligned)
   int target_occ;  // resident CTAs per SM the ring was sized for
   unsigned long long* trace;  // debug 5: CTA 0 event timeline {kind<<56 | seq<<32 | t_lo}
   int debug;   // profiling experiments only (SCONV_FUSED_DEBUG bits): 1 no gather copies, 2 no MMAs,
-               // 4 no weight TMA (plain arrive), 8 CTA-0 timeline trace
+               // 4 no weight TMA (plain arrive), 8 CTA-0 timeline trace, 256 no epilogue
   uint32_t tmem_cols;
   int bf16;
 };
@@ -184,7 +187,9 @@ __global__ void __launch_bounds__(kThreads, NK == 0 ? 4 : 2) k_conv_fused(const 
   uint64_t* iempty = ifull + kInfo;
   uint64_t* s_mask = iempty + kInfo;   // [kInfo] active-offset mask per tile slot
   uint64_t* s_part = s_mask + kInfo;   // [2][4] per-producer-warp partial masks
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_part + 8);
+  int32_t* s_tile = reinterpret_cast<int32_t*>(s_part + 8);  // [kInfo] tile id per slot (-1: done)
+  int32_t* s_tq = s_tile + kInfo;                             // [4] producers' tile look-ahead
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_tq + 4);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int K3 = p.K3;
 
@@ -199,7 +204,7 @@ __global__ void __launch_bounds__(kThreads, NK == 0 ? 4 : 2) k_conv_fused(const 
     }
     for (int a = 0; a < kInfo; ++a) {
       mbar_init(&ifull[a], 1);
-      mbar_init(&iempty[a], 1);
+      mbar_init(&iempty[a], 1 + kEpiWarps);  // MMA thread + each epilogue warp
     }
     mbar_fence_init();
   }
@@ -208,7 +213,7 @@ __global__ void __launch_bounds__(kThreads, NK == 0 ? 4 : 2) k_conv_fused(const 
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  unsigned tr1 = 0, tr2 = 0, tr3 = 0, tr4 = 0, tr5 = 0, tr6 = 0;  // debug-5 trace cursors
+  unsigned tr1 = 0, tr2 = 0, tr3 = 0, tr4 = 0, tr5 = 0, tr6 = 0, tr7 = 0;  // debug-8 trace cursors
 
   if (warp < 4) {
     // ------------------------------------------------------------ gather producers
@@ -230,17 +235,31 @@ __global__ void __launch_bounds__(kThreads, NK == 0 ? 4 : 2) k_conv_fused(const 
 #pragma unroll
       for (int k = 0; k < NR; ++k) jn[k] = ok ? __ldg(p.nbr + int64_t{k} * p.n_out + i) : -1;
     };
-    if (NK > 0) load_rows(blockIdx.x);
+    // Dynamic tile queue (global atomic counter), dispensed densest-first: row blocks are in
+    // neighbour-mask order, so the last blocks carry the most active offsets; handing them out
+    // first balances the CTAs (longest-processing-time-first).
+    auto grab = [&]() -> int {
+      const int q = atomicAdd(p.tile_counter, 1);
+      return q < p.num_tiles ? p.num_tiles - 1 - q : -1;
+    };
+    if (tid == 0) {
+      s_tq[0] = grab();
+      s_tq[1] = grab();
+    }
+    named_bar(1, kProducers);
+    int t = s_tq[0], t_next = s_tq[1];
+    if (NK > 0 && t >= 0) load_rows(t);
     int stage = 0;
     uint32_t phase = 0;
     const uint32_t smem_base = smem_u32(smem);
     int it = 0;
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
+    for (; t >= 0; ++it) {
       const int buf = it & 1;
       if (tid == 0) trace_ev(p, 1, it, tr1);
       const int nb = t % p.n_blocks;  // one division per tile
       int32_t* srow = s_idx;
       if (it > 0) named_bar(1, kProducers);  // every producer finished reading the previous tile's rows
+      if (tid == 0) s_tq[(it + 2) & 3] = t_next >= 0 ? grab() : -1;  // the tile after next
       uint64_t mine = 0;
       if constexpr (NK > 0) {
 #pragma unroll
@@ -248,7 +267,7 @@ __global__ void __launch_bounds__(kThreads, NK == 0 ? 4 : 2) k_conv_fused(const 
           srow[k * 128 + tid] = jn[k];
           mine |= static_cast<uint64_t>(jn[k] >= 0) << k;
         }
-        if (t + static_cast<int>(gridDim.x) < p.num_tiles) load_rows(t + gridDim.x);  // next tile, in flight
+        if (t_next >= 0) load_rows(t_next);  // next tile's index rows, in flight during this tile
       } else {
         const int64_t i = static_cast<int64_t>(t / p.n_blocks) * 128 + tid;
         for (int k = 0; k < K3; ++k) {
@@ -267,22 +286,14 @@ __global__ void __launch_bounds__(kThreads, NK == 0 ? 4 : 2) k_conv_fused(const 
         const int slot = it % kInfo;
         mbar_wait(&iempty[slot], ((it / kInfo) & 1) ^ 1);
         s_mask[slot] = mask;
+        s_tile[slot] = t;
         mbar_arrive(&ifull[slot]);
       }
       const int b_row0 = nb * p.block_n;
-      if (p.debug & 32) {  // experiment: bare ring skeleton (same stage count, no work, no trace)
-        const int n_st = __popcll(mask) * p.num_kb;
-        for (int u = 0; u < n_st; ++u) {
-          mbar_wait(&empty[stage], phase ^ 1u);
-          if (lane == 0) mbar_arrive(&full[stage]);
-          if (tid == 0) mbar_arrive(&full[stage]);
-          if (++stage == S) {
-            stage = 0;
-            phase ^= 1u;
-          }
-        }
-        mask = 0;
-      }
+      // Units (k, kb) in ascending k, G units per stage: one barrier round trip per G units
+      // (the handshake, not the bytes, bounds narrow layers). Slot u of a stage holds A_u then B_u.
+      int units_left = __popcll(mask) * p.num_kb, in_stage = 0, stage_units = 0;
+      uint32_t slot32 = 0;
       for (uint64_t m = mask; m; m &= m - 1) {
         const int k = __ffsll(static_cast<long long>(m)) - 1;
         const int32_t* sk = srow + k * 128;
@@ -296,32 +307,45 @@ __global__ void __launch_bounds__(kThreads, NK == 0 ? 4 : 2) k_conv_fused(const 
         }
         const int b_row = k * p.n_pad + b_row0;
         for (int kb = 0; kb < p.num_kb; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1u);
-          const uint32_t sa32 = smem_base + static_cast<uint32_t>(stage) * p.stage_bytes;
-          if (tid == 0) {
-            if (p.debug & 4) {
-              mbar_arrive(&full[stage]);
-            } else {
-              mbar_expect_tx(&full[stage], p.b_bytes);
-              tma_load_2d(smem + stage * p.stage_bytes + p.a_bytes, &tmB, kb * KC, b_row, &full[stage]);
+          if (in_stage == 0) {
+            if (tid == 0) trace_ev(p, 7, stage, tr7);  // about to wait for a free stage
+            mbar_wait(&empty[stage], phase ^ 1u);
+            stage_units = min(p.G, units_left);
+            slot32 = smem_base + static_cast<uint32_t>(stage) * p.stage_bytes;
+            if (tid == 0) {
+              if (p.debug & 4)
+                mbar_arrive(&full[stage]);
+              else
+                mbar_expect_tx(&full[stage], static_cast<uint32_t>(stage_units) * p.b_bytes);
             }
           }
+          if (tid == 0 && !(p.debug & 4))
+            tma_load_2d(smem + (slot32 - smem_base) + p.a_bytes, &tmB, kb * KC, b_row, &full[stage]);
           if (!(p.debug & 1)) {
 #pragma unroll
-            for (int q = 0; q < CPR; ++q) cp_async16(sa32 + a_off[q], src[q] + kb * (KC * 2), nbytes[q]);
+            for (int q = 0; q < CPR; ++q) cp_async16(slot32 + a_off[q], src[q] + kb * (KC * 2), nbytes[q]);
           }
-          if (p.debug & 16) {  // experiment: one (plain) arrival per warp instead of one per thread
-            if (lane == 0) mbar_arrive(&full[stage]);
-          } else {
+          --units_left;
+          slot32 += p.unit_bytes;
+          if (++in_stage == stage_units) {
             cp_async_arrive_noinc(&full[stage]);
-          }
-          if (tid == 0) trace_ev(p, 2, stage, tr2);
-          if (++stage == S) {
-            stage = 0;
-            phase ^= 1u;
+            if (tid == 0) trace_ev(p, 2, stage, tr2);
+            in_stage = 0;
+            if (++stage == S) {
+              stage = 0;
+              phase ^= 1u;
+            }
           }
         }
       }
+      t = t_next;
+      t_next = s_tq[(it + 2) & 3];
+    }
+    if (tid == 0) {  // end-of-work marker for the MMA and the epilogue
+      const int slot = it % kInfo;
+      mbar_wait(&iempty[slot], ((it / kInfo) & 1) ^ 1);
+      s_tile[slot] = -1;
+      mbar_arrive(&ifull[slot]);
     }
   } else if (warp == 8) {
     // ------------------------------------------------------------ MMA issuer
@@ -330,26 +354,28 @@ __global__ void __launch_bounds__(kThreads, NK == 0 ? 4 : 2) k_conv_fused(const 
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      int it = 0;
-      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
-        const int nb = t % p.n_blocks;
-        const int n_tile = min(p.block_n, p.n_pad - nb * p.block_n);
-        const uint32_t idesc = idesc_f16(p.bf16, n_tile);
+      for (int it = 0;; ++it) {
         const int slot = it % kInfo;
         mbar_wait(&ifull[slot], (it / kInfo) & 1);
         const uint64_t mask = s_mask[slot];
+        const int t = s_tile[slot];
         mbar_arrive(&iempty[slot]);
-        mbar_wait(&tempty[acc], acc_phase ^ 1u);
+        if (t < 0) break;
+        const int nb = t % p.n_blocks;
+        const int n_tile = min(p.block_n, p.n_pad - nb * p.block_n);
+        const uint32_t idesc = idesc_f16(p.bf16, n_tile);
+        if (!(p.debug & 256)) mbar_wait(&tempty[acc], acc_phase ^ 1u);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * p.block_n);
         uint32_t accumulate = 0;
-        for (uint64_t m = mask; m; m &= m - 1) {
-          for (int kb = 0; kb < p.num_kb; ++kb) {
-            mbar_wait(&full[stage], phase);
-            trace_ev(p, 3, stage, tr3);
-            if (!(p.debug & 1)) fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tensor core reads
-            if (!(p.debug & 128)) tc_fence_after();
-            const uint32_t sa = smem_u32(smem + stage * p.stage_bytes);
+        for (int units_left = __popcll(mask) * p.num_kb; units_left > 0;) {
+          const int su = min(p.G, units_left);
+          mbar_wait(&full[stage], phase);
+          trace_ev(p, 3, stage, tr3);
+          if (!(p.debug & 1)) fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tensor core reads
+          tc_fence_after();
+          uint32_t sa = smem_u32(smem + stage * p.stage_bytes);
+          for (int u = 0; u < su; ++u, sa += p.unit_bytes) {
             const uint32_t sb = sa + p.a_bytes;
             if (!(p.debug & 2)) {
 #pragma unroll
@@ -358,14 +384,12 @@ __global__ void __launch_bounds__(kThreads, NK == 0 ? 4 : 2) k_conv_fused(const 
                 accumulate = 1;
               }
             }
-            if (p.debug & 64)
-              mbar_arrive(&empty[stage]);  // experiment: plain arrive instead of tcgen05.commit
-            else
-              tc_commit(&empty[stage]);  // frees the stage once these MMAs retire
-            if (++stage == S) {
-              stage = 0;
-              phase ^= 1u;
-            }
+          }
+          tc_commit(&empty[stage]);  // frees the stage once these MMAs retire
+          units_left -= su;
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1u;
           }
         }
         tc_commit(&tfull[acc]);
@@ -383,7 +407,13 @@ __global__ void __launch_bounds__(kThreads, NK == 0 ? 4 : 2) k_conv_fused(const 
     uint32_t acc_phase = 0;
     TOut* out = static_cast<TOut*>(p.out);
     const TOut* res = static_cast<const TOut*>(p.res);
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+    for (int it = 0; !(p.debug & 256); ++it) {
+      const int slot = it % kInfo;
+      mbar_wait_backoff(&ifull[slot], (it / kInfo) & 1);
+      const int t = s_tile[slot];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&iempty[slot]);
+      if (t < 0) break;
       const int nb = t % p.n_blocks;
       const int n0 = nb * p.block_n;
       const int n_tile = min(p.block_n, p.n_pad - n0);
@@ -585,8 +615,12 @@ void launch_conv_fused(Ctx& ctx, const FusedArgs& a) {
   prm.bf16 = w.dtype == SCONV_BF16;
   prm.a_bytes = 128u * kc * 2u;
   prm.b_bytes = static_cast<uint32_t>(bn) * kc * 2u;
-  prm.stage_bytes = (prm.a_bytes + prm.b_bytes + 1023u) & ~1023u;
-  // Ring depth: two CTAs per SM (independent pipelines) when >= 6 stages fit in half the
+  prm.unit_bytes = (prm.a_bytes + prm.b_bytes + 1023u) & ~1023u;
+  // G units per stage: ~32 KB stages (one barrier round trip per G units of work)
+  prm.G = std::max(1, static_cast<int>((32u * 1024u) / prm.unit_bytes));
+  if (const char* e = std::getenv("SCONV_FUSED_G")) prm.G = std::max(1, std::atoi(e));
+  prm.stage_bytes = static_cast<uint32_t>(prm.G) * prm.unit_bytes;
+  // Ring depth: two CTAs per SM (independent pipelines) when >= 3 stages fit in half the
   // shared memory, else one CTA with up to kMaxStages stages.
   const uint32_t idx_bytes = static_cast<uint32_t>(w.K3) * 128u * 4u;
   const uint32_t fixed = 1024u + idx_bytes + (2 * kMaxStages + 3 * kInfo + 16) * 8u + 64u;
@@ -595,7 +629,7 @@ void launch_conv_fused(Ctx& ctx, const FusedArgs& a) {
   prm.target_occ = target;
   const uint32_t half = (227u * 1024u) / static_cast<uint32_t>(target) - 1024u, whole = 227u * 1024u;
   int stages = fixed < half ? static_cast<int>((half - fixed) / prm.stage_bytes) : 0;
-  if (stages < (target > 2 ? 3 : 6)) {
+  if (stages < 3) {
     stages = static_cast<int>((whole - fixed) / prm.stage_bytes);
     prm.target_occ = 1;
   }
@@ -607,10 +641,13 @@ void launch_conv_fused(Ctx& ctx, const FusedArgs& a) {
   uint32_t cols = 32;
   while (cols < 2u * static_cast<uint32_t>(bn)) cols <<= 1;
   prm.tmem_cols = cols;
-  const size_t smem = 1024 + prm.bar_off + (2 * stages + 4 + 3 * kInfo + 8 + 1) * 8 + 16;
+  const size_t smem = 1024 + prm.bar_off + (2 * stages + 4 + 3 * kInfo + 8) * 8 + (kInfo + 4 + 1) * 4 + 16;
   if (smem > 227 * 1024) fail(SCONV_ERR_ARG, "fused layer tile does not fit in shared memory");
   const CUtensorMap tB = make_tensor_map_2d(w.buf.get(), w.dtype, w.k_pad, static_cast<uint64_t>(w.K3) * w.n_pad, kc,
                                             static_cast<uint32_t>(bn), kc);
+  ctx.fused_counter.reserve(16, ctx.stream);
+  SCONV_CUDA(cudaMemsetAsync(ctx.fused_counter.get(), 0, sizeof(int), ctx.stream));
+  prm.tile_counter = ctx.fused_counter.get<int>();
   struct TraceDump {  // debug 5: print CTA 0's timeline after the launch
     Ctx& ctx;
     DevBuf& buf;
