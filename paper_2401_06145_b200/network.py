@@ -200,11 +200,19 @@ class Network:
                                                           C.byref(cs)))
         return n.value, ch.value, cs.value
 
-    def read(self, t):
+    def read(self, t, feats_out: Optional[np.ndarray] = None, coords: bool = True):
+        """Host copy of tensor t: (coords or None, fp32 features). feats_out (e.g. a pinned
+        array) receives the features in place when given."""
         n, ch, _ = self.info(t)
-        xyz = np.empty((n, 3), np.int32)
-        f = np.empty((n, ch), np.float32)
-        self.ctx.check(self.ctx.lib.sconv_net_read_tensor(self.ctx.h, self.h, t, S._ptr(xyz), S._ptr(f)))
+        xyz = np.empty((n, 3), np.int32) if coords else None
+        if feats_out is not None:
+            if feats_out.shape != (n, ch) or feats_out.dtype != np.float32 or not feats_out.flags.c_contiguous:
+                raise ValueError("feats_out must be a contiguous float32 array of shape (n, channels)")
+            f = feats_out
+        else:
+            f = np.empty((n, ch), np.float32)
+        self.ctx.check(self.ctx.lib.sconv_net_read_tensor(self.ctx.h, self.h, t, S._ptr(xyz) if coords else None,
+                                                          S._ptr(f)))
         return xyz, f
 
     def device_output(self):

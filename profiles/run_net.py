@@ -21,6 +21,8 @@ p.add_argument("--workload", default="c2_minkunet42_kitti")
 p.add_argument("--dataflow", default="fused", choices=["fused", "gmas", "auto"])
 p.add_argument("--steps", type=int, default=1)
 p.add_argument("--time", action="store_true", help="print per-kernel event times")
+p.add_argument("--profile-last", action="store_true",
+               help="cudaProfilerStart/Stop around the last forward (ncu --profile-from-start off)")
 a = p.parse_args()
 df = {"fused": sc.DATAFLOW_FUSED, "gmas": sc.DATAFLOW_GMAS, "auto": sc.DATAFLOW_AUTO}[a.dataflow]
 ctx = sc.Context(0)
@@ -33,8 +35,15 @@ torch.cuda.set_stream(_stream)
 ctx.set_stream(_stream.cuda_stream)
 if a.time:
     ctx.set_profiling(True)
-for _ in range(a.steps):
+for step in range(a.steps):
+    last = step == a.steps - 1
+    if a.profile_last and last:
+        torch.cuda.synchronize()
+        torch.cuda.cudart().cudaProfilerStart()
     net.forward(device_xyz=xyz_d.data_ptr(), device_feats=f_d.data_ptr(), n=len(coords), sorted_=True)
+    if a.profile_last and last:
+        torch.cuda.synchronize()
+        torch.cuda.cudart().cudaProfilerStop()
 torch.cuda.synchronize()
 if a.time:
     for k, (n, ms) in sorted(ctx.profile().items(), key=lambda kv: -kv[1][1]):

@@ -3,6 +3,7 @@
 
   python profiles/summarize.py launches <launches.csv> <out.md>     # per-kernel launch list shares
   python profiles/summarize.py full <prof.ncu-rep> <out.md> [traffic.json]  # --set full metrics
+  python profiles/summarize.py steady <launches.csv> <out.md> <traffic.json>  # time + DRAM per launch
 """
 import collections
 import csv
@@ -14,7 +15,7 @@ import sys
 
 def short(name):
     """Bare kernel name with template args: 'k_gather<8, float, __half>' / 'cub::DeviceRadixSort...'."""
-    n = name.split("(")[0].replace("void ", "").strip()
+    n = name.replace("(anonymous namespace)::", "").replace("<unnamed>::", "").split("(")[0].replace("void ", "").strip()
     head = n.split("<")[0]
     base = head.split("::")[-1]
     if head.startswith("cub::"):
@@ -100,5 +101,51 @@ def full(rep, out, traffic_json=None):
 if __name__ == "__main__":
     if sys.argv[1] == "launches":
         launches(sys.argv[2], sys.argv[3])
-    else:
+    elif sys.argv[1] == "full":
         full(sys.argv[2], sys.argv[3], sys.argv[4] if len(sys.argv) > 4 else None)
+
+
+def steady(csv_path, out, traffic_json):
+    """Launch list of one steady-state forward with gpu__time_duration + dram bytes per launch
+    (--cache-control none): per-kernel share of device time and mean DRAM traffic per launch
+    (the bench's roofline.traffic)."""
+    rows = list(csv.reader(open(csv_path)))
+    h = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+    hdr, data = rows[h], rows[h + 1:]
+    ki, mi, vi, ui, ii = (hdr.index(x) for x in ("Kernel Name", "Metric Name", "Metric Value", "Metric Unit", "ID"))
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "ns": 1e-3, "usecond": 1,
+             "us": 1, "msecond": 1e3, "ms": 1e3}
+    per = collections.OrderedDict()
+    for r in data:
+        if len(r) <= vi:
+            continue
+        d = per.setdefault(r[ii], {"name": short(r[ki])})
+        d[r[mi]] = float(r[vi].replace(",", "")) * scale.get(r[ui], 1)
+    agg = collections.defaultdict(lambda: [0, 0.0, 0.0])
+    for d in per.values():
+        a = agg[d["name"].split("<")[0]]
+        a[0] += 1
+        a[1] += d.get("gpu__time_duration.sum", 0.0)
+        a[2] += d.get("dram__bytes_read.sum", 0.0) + d.get("dram__bytes_write.sum", 0.0)
+    total = sum(a[1] for a in agg.values())
+    lines = [f"# steady-state launch list ({csv_path})", "",
+             "One network forward after warm-up (AUTO dataflow decided), ncu --clock-control none",
+             "--cache-control none (L2 warm across launches, as in the bench); times are serialised.", "",
+             "| kernel | launches | total us | share | mean us | mean DRAM MB/launch |", "|---|---:|---:|---:|---:|---:|"]
+    for k, (n, t, b) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+        lines.append(f"| {k} | {n} | {t:.1f} | {t / total:.1%} | {t / n:.2f} | {b / n / 1e6:.2f} |")
+    lines.append(f"| total | {sum(a[0] for a in agg.values())} | {total:.1f} | 100% | | |")
+    open(out, "w").write("\n".join(lines) + "\n")
+    tr = {}
+    try:
+        tr = json.load(open(traffic_json))
+    except Exception:
+        pass
+    for k, (n, t, b) in agg.items():
+        tr[k] = b / n
+    json.dump(tr, open(traffic_json, "w"), indent=1)
+    print("\n".join(lines))
+
+
+if __name__ == "__main__" and sys.argv[1] == "steady":
+    steady(sys.argv[2], sys.argv[3], sys.argv[4])
