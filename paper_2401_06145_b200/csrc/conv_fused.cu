@@ -170,7 +170,7 @@ __device__ __forceinline__ void trace_ev(const FusedParams& p, int kind, int seq
 }
 
 // NK = compile-time offset count (registers prefetch the next tile's index rows), 0 = runtime
-template <int NK, int KC, class TOut>
+template <int NK, int KC, class TOut, bool REG = false>
 __global__ void __launch_bounds__(kThreads, NK == 0 ? 4 : 2) k_conv_fused(const __grid_constant__ CUtensorMap tmB,
                                                            const __grid_constant__ FusedParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -215,7 +215,109 @@ __global__ void __launch_bounds__(kThreads, NK == 0 ? 4 : 2) k_conv_fused(const 
   const uint32_t tmem_base = *tmem_slot;
   unsigned tr1 = 0, tr2 = 0, tr3 = 0, tr4 = 0, tr5 = 0, tr6 = 0, tr7 = 0;  // debug-8 trace cursors
 
-  if (warp < 4) {
+  if (REG && warp < 4) {
+    // ------------------------------------------------------------ gather producers, register indices
+    // Thread tid owns tile row tid: its K3 input-row indices are loaded into registers at the
+    // tile start (independent LDGs) and never go through shared memory. Copy instruction q of
+    // warp w covers rows 32w + lane/CPR + q*(32/CPR) (whole rows, coalesced); lanes get the
+    // row indices from the owner lane by shuffle.
+    constexpr int CPR = KC / 8, RPI = 32 / CPR;
+    constexpr int NR = NK > 0 ? NK : 1;
+    const int tid = threadIdx.x;
+    const int chunk = lane % CPR, rsub = lane / CPR;
+    uint32_t a_off[CPR];
+#pragma unroll
+    for (int q = 0; q < CPR; ++q) a_off[q] = swizzled_offset<KC>(32 * warp + rsub + q * RPI, chunk);
+    const unsigned char* src_col = p.f_in + chunk * 16;
+    auto grab = [&]() -> int {
+      const int q = atomicAdd(p.tile_counter, 1);
+      return q < p.num_tiles ? p.num_tiles - 1 - q : -1;
+    };
+    if (tid == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+      s_tq[0] = grab();
+    }
+    named_bar(1, kProducers);
+    int t = s_tq[0];
+    int stage = 0;
+    uint32_t phase = 0;
+    const uint32_t smem_base = smem_u32(smem);
+    int it = 0;
+    for (; t >= 0; ++it) {
+      const int buf = it & 1;
+      if (it > 0) named_bar(1, kProducers);
+      if (tid == 0) s_tq[(it + 1) & 3] = grab();
+      const int nb = t % p.n_blocks;
+      int jc[NR];
+      {
+        const int64_t i = static_cast<int64_t>(t / p.n_blocks) * 128 + tid;
+        const bool ok = i < p.n_out;
+#pragma unroll
+        for (int k = 0; k < NR; ++k) jc[k] = ok ? __ldg(p.nbr + int64_t{k} * p.n_out + i) : -1;
+      }
+      uint64_t mine = 0;
+#pragma unroll
+      for (int k = 0; k < NR; ++k) mine |= static_cast<uint64_t>(jc[k] >= 0) << k;
+      const uint32_t lo = __reduce_or_sync(0xFFFFFFFFu, static_cast<uint32_t>(mine));
+      const uint32_t hi = __reduce_or_sync(0xFFFFFFFFu, static_cast<uint32_t>(mine >> 32));
+      if (lane == 0) s_part[buf * 4 + warp] = (static_cast<uint64_t>(hi) << 32) | lo;
+      named_bar(1, kProducers);
+      uint64_t mask = s_part[buf * 4] | s_part[buf * 4 + 1] | s_part[buf * 4 + 2] | s_part[buf * 4 + 3];
+      if (mask == 0) mask = 1;
+      if (tid == 0) {
+        const int slot = it % kInfo;
+        mbar_wait(&iempty[slot], ((it / kInfo) & 1) ^ 1);
+        s_mask[slot] = mask;
+        s_tile[slot] = t;
+        mbar_arrive(&ifull[slot]);
+      }
+      const int b_row0 = nb * p.block_n;
+      int units_left = __popcll(mask) * p.num_kb, in_stage = 0, stage_units = 0;
+      uint32_t slot32 = 0;
+#pragma unroll 1
+      for (int k = 0; k < NR; ++k) {
+        const int32_t jk = jc[0];
+#pragma unroll
+        for (int r = 0; r + 1 < NR; ++r) jc[r] = jc[r + 1];
+        if (!((mask >> k) & 1)) continue;
+        int32_t j[CPR];
+#pragma unroll
+        for (int q = 0; q < CPR; ++q) j[q] = __shfl_sync(0xFFFFFFFFu, jk, rsub + q * RPI);
+        const int b_row = k * p.n_pad + b_row0;
+        for (int kb = 0; kb < p.num_kb; ++kb) {
+          if (in_stage == 0) {
+            mbar_wait(&empty[stage], phase ^ 1u);
+            stage_units = min(p.G, units_left);
+            slot32 = smem_base + static_cast<uint32_t>(stage) * p.stage_bytes;
+            if (tid == 0) mbar_expect_tx(&full[stage], static_cast<uint32_t>(stage_units) * p.b_bytes);
+          }
+          if (tid == 0) tma_load_2d(smem + (slot32 - smem_base) + p.a_bytes, &tmB, kb * KC, b_row, &full[stage]);
+          const unsigned char* col = src_col + kb * (KC * 2);
+#pragma unroll
+          for (int q = 0; q < CPR; ++q)
+            cp_async16(slot32 + a_off[q], col + static_cast<int64_t>(j[q] >= 0 ? j[q] : 0) * p.ld_in_bytes,
+                       j[q] >= 0 ? 16u : 0u);
+          --units_left;
+          slot32 += p.unit_bytes;
+          if (++in_stage == stage_units) {
+            cp_async_arrive_noinc(&full[stage]);
+            in_stage = 0;
+            if (++stage == S) {
+              stage = 0;
+              phase ^= 1u;
+            }
+          }
+        }
+      }
+      t = s_tq[(it + 1) & 3];
+    }
+    if (tid == 0) {
+      const int slot = it % kInfo;
+      mbar_wait(&iempty[slot], ((it / kInfo) & 1) ^ 1);
+      s_tile[slot] = -1;
+      mbar_arrive(&ifull[slot]);
+    }
+  } else if (warp < 4) {
     // ------------------------------------------------------------ gather producers
     const int tid = threadIdx.x;
     constexpr int CPR = KC / 8;      // 16-byte chunks per row
@@ -508,12 +610,24 @@ __global__ void k_convert_rows(const TS* __restrict__ src, int64_t n, int c, int
 template <int NK, int KC, class TOut>
 void launch_t(Ctx& ctx, const FusedArgs& a, const FusedParams& prm, size_t smem, const CUtensorMap& tB) {
   auto kern = k_conv_fused<NK, KC, TOut>;
+  int variant = 0;
+  if constexpr (NK > 0) {  // register-resident row indices (SCONV_FUSED_REG=0: shared-memory variant)
+    static const bool reg = [] {
+      const char* e = std::getenv("SCONV_FUSED_REG");
+      return !(e && e[0] == '0');
+    }();
+    if (reg) {
+      kern = k_conv_fused<NK, KC, TOut, true>;
+      variant = 1;
+    }
+  }
   // Resident CTAs per SM from the kernel's own budget (the runtime occupancy query reported 1
   // where ncu's launch statistics show 2): 228 KB shared memory (1 KB reserved per CTA), the
   // register file, and TMEM (512 columns). Attributes are set once per instantiation/device.
   static thread_local std::map<int, int> regs_cache;
   int regs;
-  const auto hit = regs_cache.find(ctx.device);
+  const int cache_key = ctx.device * 2 + variant;
+  const auto hit = regs_cache.find(cache_key);
   if (hit != regs_cache.end()) {
     regs = hit->second;
   } else {
@@ -522,7 +636,7 @@ void launch_t(Ctx& ctx, const FusedArgs& a, const FusedParams& prm, size_t smem,
     cudaFuncAttributes fa{};
     SCONV_CUDA(cudaFuncGetAttributes(&fa, kern));
     regs = fa.numRegs;
-    regs_cache[ctx.device] = regs;
+    regs_cache[cache_key] = regs;
   }
   const int by_smem = static_cast<int>((228u * 1024u) / (smem + 1024u));
   const int by_regs = 65536 / std::max(1, ((regs * 32 + 255) / 256 * 256) * (kThreads / 32));
