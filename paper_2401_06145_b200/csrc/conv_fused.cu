@@ -692,7 +692,11 @@ void launch_conv_fused(Ctx& ctx, const FusedArgs& a) {
   int bn = a.block_n;
   if (bn <= 0) {
     bn = std::min(w.n_pad, 256);
-    while (bn > 32 && row_blocks * ceil_div(w.n_pad, bn) < 2 * ctx.num_sms && (bn / 2) % 16 == 0) bn /= 2;
+    // ~one tile per SM: each extra n block re-gathers the tile's A rows from L2 (measured: fewer,
+    // wider tiles win on the wide deep layers, e.g. 7780 rows 256->256: 100 -> 61 us)
+    int want = ctx.num_sms;
+    if (const char* e = std::getenv("SCONV_FUSED_TILES")) want = std::max(1, std::atoi(e));
+    while (bn > 32 && row_blocks * ceil_div(w.n_pad, bn) < want && (bn / 2) % 16 == 0) bn /= 2;
   }
   bn = std::min(bn, w.n_pad);
   if (bn % 16 != 0 || bn > 256) fail(SCONV_ERR_ARG, "block_n must be a multiple of 16 <= 256");
