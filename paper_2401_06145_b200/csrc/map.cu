@@ -65,8 +65,8 @@ __global__ void k_pack_keys(const int32_t* __restrict__ xyz, int64_t n, uint64_t
 
 // One launch per map build: flag init + weight offsets (weight_offsets_ext order: a outer,
 // b, c inner; odd K centred, even K in [0, K-1]) times the offset scale, negated when transposed
-__global__ void k_init_map(MapFlags* f, int3* __restrict__ d, int K, int scale, int transposed, int K3) {
-  if (threadIdx.x == 0) {
+__global__ void k_init_flags(MapFlags* f) {
+  {
     f->bad_coord = f->bad_target = f->bad_floor = ULLONG_MAX;
     f->unsorted = f->target_unsorted = 0;
     f->bbox[0] = f->bbox[1] = f->bbox[2] = INT_MAX;
@@ -75,12 +75,6 @@ __global__ void k_init_map(MapFlags* f, int3* __restrict__ d, int K, int scale, 
     f->fbox[0] = f->fbox[1] = f->fbox[2] = INT_MAX;
     f->fbox[3] = f->fbox[4] = f->fbox[5] = INT_MIN;
     f->fwide = 0;
-  }
-  for (int k = threadIdx.x; k < K3; k += blockDim.x) {
-    const int lo = (K % 2 == 1) ? -(K / 2) : 0;
-    const int a = k / (K * K) + lo, b = (k / K) % K + lo, c = k % K + lo;
-    const int sg = transposed ? -scale : scale;
-    d[k] = make_int3(a * sg, b * sg, c * sg);
   }
 }
 
@@ -346,6 +340,16 @@ __global__ void k_floor_expand(const uint32_t* __restrict__ ck, const int64_t* _
 // ---------------------------------------------------------------- double-traversed search
 constexpr int kSearchThreads = 256;
 
+// Weight offset k generated in registers (weight_offsets_ext order: a outer, b, c inner; odd K
+// centred, even K in [0, K-1]; times the signed scale: negative for transposed maps).
+struct OffsetGen {
+  int K, scale;
+  __device__ __forceinline__ int3 at(int k) const {
+    const int lo = (K % 2 == 1) ? -(K / 2) : 0;
+    return make_int3((k / (K * K) + lo) * scale, ((k / K) % K + lo) * scale, (k % K + lo) * scale);
+  }
+};
+
 __device__ __forceinline__ uint64_t pivot_of(const uint64_t* src, int64_t n_src, int B, int64_t b) {
   return __ldg(src + min((b + 1) * B, n_src) - 1);
 }
@@ -468,7 +472,7 @@ __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity)
 template <int QPL>
 __global__ void __launch_bounds__(kSearchThreads) k_search(
     const uint64_t* __restrict__ src, const int32_t* __restrict__ src_idx, int64_t n_src, int B,
-    const uint64_t* __restrict__ q, int64_t n_q, const int3* __restrict__ offsets, int K3, int kmin_off,
+    const uint64_t* __restrict__ q, int64_t n_q, OffsetGen og, int K3, int kmin_off,
     int kmax_off, int64_t nchunk, int ngroups, int cap_blocks, int32_t* __restrict__ nbr,
     int32_t* __restrict__ chunk_count, int32_t* __restrict__ chunk_off, unsigned* __restrict__ done,
     int32_t* __restrict__ map_start) {
@@ -498,7 +502,7 @@ __global__ void __launch_bounds__(kSearchThreads) k_search(
   __syncthreads();
   const int64_t nb = (n_src + B - 1) / B;
   if (warp < 2) {  // window: blocks holding [q_first + delta_lexmin, q_last + delta_lexmax]
-    const uint64_t key = warp == 0 ? segment_key(s_q[0], offsets[kmin_off]) : segment_key(s_q[len - 1], offsets[kmax_off]);
+    const uint64_t key = warp == 0 ? segment_key(s_q[0], og.at(kmin_off)) : segment_key(s_q[len - 1], og.at(kmax_off));
     const int64_t hint = (((warp == 0 ? lo : lo + len - 1) * n_src) / max(n_q, int64_t{1})) / B;
     const int64_t b = warp_first_pivot_ge(src, n_src, B, 0, nb, key, lane, hint);
     if (lane == 0) {
@@ -532,7 +536,7 @@ __global__ void __launch_bounds__(kSearchThreads) k_search(
     // key just below this slice: queries <= it belong to earlier slices (or to nothing)
     const uint64_t floor_key = (empty || sb == 0) ? 0 : __ldg(src + g0 - 1);
     for (int k = my_k; k < K3; k += K3) {  // at most one iteration
-      const int3 d = offsets[k];
+      const int3 d = og.at(k);
       // lane-contiguous queries: lane L owns chunk positions [L*QPL, (L+1)*QPL), so a lane's
       // consecutive sorted queries can be merged against the sorted block (galloping)
       const int qb = lane * QPL;
@@ -838,10 +842,11 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
   MapFlags* flags = flags_buf.get<MapFlags>();
   // initialised on the device: lazy builds end without a sync, so no host staging buffer may be
   // reused by the next build while this build's copies are still queued
-  m->offsets.alloc(sizeof(int3) * K3, st);
-  ctx.launch("k_init_map", [&] {
-    k_init_map<<<1, 512, 0, st>>>(flags, m->offsets.get<int3>(), cfg.kernel_size, cfg.offset_scale, cfg.transposed, K3);
-  });
+  // flags are written only by coordinate packing / Eq. 1 floor (raw coordinates, strided
+  // layers); chained stride-1 / transposed maps over existing keys skip the init launch
+  const bool flags_used = !lazy || !P.keys || (!cfg.transposed && cfg.out_stride != 1) ||
+                          (cfg.transposed && target && !target->keys);
+  if (flags_used) ctx.launch("k_init_flags", [&] { k_init_flags<<<1, 1, 0, st>>>(flags); });
   auto* pin = reinterpret_cast<MapFlags*>(ctx.pin_flags());
 
   // ---- source array
@@ -1095,7 +1100,8 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
       SCONV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
       ctx.launch("k_search", [&] {
         kern<<<static_cast<unsigned>(nchunk2 * ngroups), kSearchThreads, smem, st>>>(
-            src, src_idx, n, B, q, n_out, m->offsets.get<int3>(), K3, kmin_off, kmax_off, nchunk2, ngroups, cap_blocks,
+            src, src_idx, n, B, q, n_out, OffsetGen{cfg.kernel_size, cfg.transposed ? -cfg.offset_scale : cfg.offset_scale},
+            K3, kmin_off, kmax_off, nchunk2, ngroups, cap_blocks,
             m->nbr_in.get<int32_t>(), counts.get<int32_t>(), offs.get<int32_t>(), ctx.done_counter(),
             m->map_start.get<int32_t>());
       });

@@ -18,7 +18,6 @@ struct MapData {
   bool src_identity = true;
   // sorted output (Q) keys; aliases src_keys for stride 1 (geometry.hpp:163)
   std::shared_ptr<DevBuf> q_keys;
-  DevBuf offsets;    // int3 x K3 (search offsets: negated when transposed)
   DevBuf map_start;  // int32 x (K3 + 1): canonical list starts
   DevBuf pair_in, pair_out;  // int32 x |M|, canonical order (k, then i)
   DevBuf nbr_pos;            // int32 x K3 x n_out: canonical position m of (k, i) or -1
