@@ -228,14 +228,33 @@ class LayerWorkload:
         self.points = self.N
         m = self._map()
         self.tg, self.ts, _ = sc.tune_layer(ctx, m, self.w, self.F_d.data_ptr(), sc.F32, rounds=5)
-        self.cfg = sc.exec_cfg(compute_dtype=dtype, gather_tile=self.tg, scatter_tile=self.ts)
-        sc.layer_forward_device(ctx, m, self.w, self.F_d.data_ptr(), sc.F32, self.out_d.data_ptr(), sc.F32, self.cfg)
+        sc.layer_forward_device(ctx, m, self.w, self.F_d.data_ptr(), sc.F32, self.out_d.data_ptr(), sc.F32,
+                                sc.exec_cfg(compute_dtype=dtype, gather_tile=self.tg, scatter_tile=self.ts))
         self.info = m.info()
         m.free()
+        # dataflow choice (Alg. 2 style, setup only): time whole steps (Map + layer) with each
+        # and keep the faster -- Minuet's GMaS with tuned tiles, or the fused kernel
+        best = None
+        for df in (sc.DATAFLOW_GMAS, sc.DATAFLOW_FUSED):
+            self.cfg = sc.exec_cfg(compute_dtype=dtype, gather_tile=self.tg, scatter_tile=self.ts, dataflow=df)
+            for _ in range(3):
+                self.step()
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(5)]
+            for a, e in ev:
+                a.record()
+                self.step()
+                e.record()
+            torch.cuda.synchronize()
+            ms = statistics.median(a.elapsed_time(e) for a, e in ev)
+            if best is None or ms < best[0]:
+                best = (ms, df)
+        self.dataflow = best[1]
+        self.cfg = sc.exec_cfg(compute_dtype=dtype, gather_tile=self.tg, scatter_tile=self.ts, dataflow=self.dataflow)
         self.config = {"model": "single SC layer K=3 s=1", "N": self.N, "E": self.E, "C_in": self.c,
                        "C_out": self.c, "gather_tile": self.tg, "scatter_tile": self.ts,
                        "matches": self.info.total_matches, "buffer_length": self.info.buffer_length,
-                       "groups": self.info.groups, "padding_overhead": self.info.padding_overhead}
+                       "groups": self.info.groups, "padding_overhead": self.info.padding_overhead,
+                       "dataflow": "fused" if self.dataflow == sc.DATAFLOW_FUSED else "gmas"}
 
     def _map(self):
         return self.sc.KernelMap.build(self.ctx, None, False, 3, 1, 1, device_ptr=self.xyz_d.data_ptr(), n=self.N,
@@ -260,6 +279,7 @@ class LayerWorkload:
         return {"k_search": 8 * N + 8 * nq + 12 * K3, "k_emit": 8 * M + 4 * K3 * nq,
                 "k_gather": 4 * c * N + 2 * c * R + 4 * M, "k_gemm_grouped": 2 * c * R + 4 * c * R + 2 * K3 * c * c,
                 "k_scatter": 4 * c * M + 4 * K3 * nq + 4 * c * nq, "k_bucket_rank": 8 * N + 12 * N,
+                "k_conv_fused": 2 * c * N + 4 * K3 * nq + 4 * c * nq,
                 "k_bucket_scatter": 16 * N, "k_pack_compact": 20 * N, "k_bbox": 12 * N}
 
     def cpu_sample(self, workers, budget_s=20.0):

@@ -78,6 +78,20 @@ __global__ void k_init_flags(MapFlags* f) {
   }
 }
 
+// 1x1 (K=1) stride-1 map over a sorted set: Q = P, every output is its own single neighbour.
+__global__ void k_identity_map(int64_t n, int32_t* __restrict__ nbr_in, int32_t* __restrict__ nbr_pos,
+                               int32_t* __restrict__ pair_in, int32_t* __restrict__ pair_out,
+                               int32_t* __restrict__ map_start) {
+  const int64_t i = blockIdx.x * int64_t{blockDim.x} + threadIdx.x;
+  if (i == 0) {
+    map_start[0] = 0;
+    map_start[1] = static_cast<int32_t>(n);
+  }
+  if (i >= n) return;
+  const int32_t v = static_cast<int32_t>(i);
+  nbr_in[i] = nbr_pos[i] = pair_in[i] = pair_out[i] = v;
+}
+
 __global__ void k_iota(int32_t* __restrict__ v, int64_t n) {
   const int64_t i = blockIdx.x * int64_t{blockDim.x} + threadIdx.x;
   if (i < n) v[i] = static_cast<int32_t>(i);
@@ -1071,6 +1085,20 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
     if (n_out > 0) SCONV_CUDA(cudaMemsetAsync(m->nbr_in.get(), 0xFF, sizeof(int32_t) * int64_t{K3} * n_out, st));
     if (n_out > 0)
       SCONV_CUDA(cudaMemsetAsync(m->nbr_pos.get(), 0xFF, sizeof(int32_t) * int64_t{K3} * n_out, st));
+  } else if (K3 == 1 && cfg.kernel_size == 1 && !cfg.transposed && cfg.out_stride == 1 && m->src_identity &&
+             m->q_keys == m->src_keys) {
+    // identity map (1x1 conv on the same sorted coordinates): no search, sizes known on the host
+    m->pair_in.alloc(sizeof(int32_t) * n, st);
+    m->pair_out.alloc(sizeof(int32_t) * n, st);
+    ctx.launch("k_identity_map", [&] {
+      k_identity_map<<<grid_for(n), kThreads, 0, st>>>(n, m->nbr_in.get<int32_t>(), m->nbr_pos.get<int32_t>(),
+                                                       m->pair_in.get<int32_t>(), m->pair_out.get<int32_t>(),
+                                                       m->map_start.get<int32_t>());
+    });
+    m->starts = {0, static_cast<int32_t>(n)};
+    m->sizes = {n};
+    m->total = n;
+    if (lazy) return m;  // nothing pending; flags were not touched
   } else {
     // Work item = one CTA per chunk of CQ = 32*QPL sorted queries (CQ <= C), all offsets.
     const int qpl = C >= 256 ? 8 : (C >= 128 ? 4 : (C >= 64 ? 2 : 1));

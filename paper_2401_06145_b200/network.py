@@ -179,6 +179,7 @@ class Network:
         ctx.check(ctx.lib.sconv_net_create(ctx.h, S._ptr(rows), len(g.ops), g.n_tensors, g.input, g.output,
                                            C.byref(cfg), B, Cq, C.byref(h)))
         self.h = h
+        ctx.adopt(self)
         for wid, w in weights.items():
             w = np.ascontiguousarray(w, np.float32)
             ctx.check(ctx.lib.sconv_net_set_weights(ctx.h, h, wid, S._ptr(w), S.MEM_HOST, *w.shape))

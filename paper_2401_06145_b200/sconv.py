@@ -13,6 +13,7 @@ of the library (``load()``), and every compute call goes through the sm_100a ker
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 import os
 from dataclasses import dataclass, field
 from typing import Optional
@@ -154,6 +155,11 @@ class Context:
         if st != OK:
             _raise(st, self.lib.sconv_global_last_error().decode())
         self.h = h
+        self._children = weakref.WeakSet()  # maps / weights / networks: freed before the context
+
+    def adopt(self, obj):
+        self._children.add(obj)
+        return obj
 
     def check(self, st: int):
         if st != OK:
@@ -161,6 +167,11 @@ class Context:
 
     def close(self):
         if getattr(self, "h", None):
+            for c in list(getattr(self, "_children", ())):  # device objects die before their context
+                try:
+                    c.free()
+                except Exception:
+                    pass
             self.lib.sconv_ctx_destroy(self.h)
             self.h = None
 
@@ -219,6 +230,7 @@ class KernelMap:
 
     def __init__(self, ctx: Context, handle):
         self.ctx, self.h = ctx, handle
+        ctx.adopt(self)
 
     @classmethod
     def build(cls, ctx: Context, coords, sorted_: bool = False, K=3, offset_scale=1, out_stride=1,
@@ -283,6 +295,7 @@ class Weights:
         ctx.check(ctx.lib.sconv_weights_create(ctx.h, _ptr(w), MEM_HOST, w.shape[0], w.shape[1], w.shape[2],
                                                dtype, C.byref(h)))
         self.h = h
+        ctx.adopt(self)
 
     def free(self):
         if self.h:
