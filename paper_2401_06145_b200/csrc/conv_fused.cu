@@ -798,9 +798,11 @@ void prepare_fused_layout(Ctx& ctx, MapData& m) {
   m.fused_ready = true;
   const int64_t n = m.n_out;
   const int K3 = m.K3;
-  // Only submanifold-style maps (K3 >= 27) are reordered: in U-Nets they serve 4-8 convs each,
-  // so the sort (~40 us at 1.2e5 rows) amortises; the K=2 down / up maps serve one conv.
-  m.permuted = K3 >= 27 && K3 <= 32 && n > 2 * 128 && n <= INT32_MAX;
+  // Only submanifold maps (stride 1, not transposed, K3 >= 27) are reordered: networks reuse
+  // them for 4-8 convs, so the sort (~40 us at 1.2e5 rows) amortises; strided / transposed
+  // maps serve a single conv.
+  m.permuted = K3 >= 27 && K3 <= 32 && m.cfg.out_stride == 1 && !m.cfg.transposed && n > 2 * 128 &&
+               n <= INT32_MAX;
   if (const char* e = std::getenv("SCONV_NO_PERMUTE"); e && e[0] == '1') m.permuted = false;  // experiments
   if (!m.permuted) return;
   // Bit position per offset: rarer offsets (larger L1 norm: corners, then edges, then faces,
