@@ -90,6 +90,7 @@ typedef struct {
 
 /* ---------------- context ---------------- */
 sconv_status sconv_ctx_create(int device, sconv_ctx** out);
+/* Free every map / weight set / network of the context before destroying it. */
 void sconv_ctx_destroy(sconv_ctx* ctx);
 const char* sconv_last_error(const sconv_ctx* ctx);
 /* Use an existing cudaStream_t (NULL = the context's own stream). */

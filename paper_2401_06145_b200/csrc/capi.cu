@@ -195,6 +195,7 @@ void sconv_ctx_destroy(sconv_ctx* ctx) {
     ctx->gather_buf.release();
     ctx->gemm_out.release();
     ctx->plan_dev.release();
+    ctx->fused_counter.release();  // every Ctx-owned DevBuf: freed on the stream before it dies
   }
   cudaStreamSynchronize(ctx->stream);
   for (auto& p : ctx->pending) {

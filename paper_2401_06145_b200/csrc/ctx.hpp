@@ -117,6 +117,7 @@ struct Ctx {
   DevBuf scratch_sort, scratch_misc, flush_buf;
   DevBuf gather_buf, gemm_out, plan_dev;
   DevBuf fused_counter;  // dynamic tile queue of the fused kernel
+  // (sconv_ctx_destroy releases every DevBuf above before destroying the stream)
   // Pinned host staging, carved into fixed regions, used ONLY for device->host readbacks that
   // are followed by a stream sync (map sizes / flags). Host->device inputs of a map build are
   // generated on the device instead: lazy (network) map builds end without a sync, so a

@@ -141,3 +141,31 @@ def shapenet_object(seed: int = 0, n_points: int = 120_000, grid: int = 128, cha
     p = np.clip(np.concatenate(pts), 0, 1 - 1e-9) * grid
     feats = rng.random((len(p), channels))
     return voxelize(p, feats, 1.0)
+
+
+def batch_clouds(clouds, spacing=256):
+    """Several clouds as ONE sparse tensor (the usual batch-in-coordinates encoding): cloud b is
+    shifted by b * spacing along x, so no kernel offset or stride floor can reach across clouds
+    when spacing exceeds every cloud's x extent plus the network's reach and is a multiple of its
+    largest tensor stride. Returns (coords sorted, feats, row ranges per cloud); sorting keeps the
+    clouds contiguous and in order because x is the most significant key field.
+
+    clouds: list of (coords int32 [n, 3], feats float32 [n, c])."""
+    xs, fs, ranges, start = [], [], [], 0
+    for b, (c, f) in enumerate(clouds):
+        cc = c.astype(np.int64).copy()
+        if len(c):
+            # shift by a multiple of `spacing`: residues modulo every power-of-two stride <= spacing
+            # are kept, so Eq. 1 floors group voxels exactly as in the unbatched cloud
+            base = (int(c[:, 0].min()) // spacing) * spacing
+            if int(c[:, 0].max()) - base >= spacing // 2:
+                raise ValueError("cloud x extent too large for the batch spacing")
+            cc[:, 0] += b * spacing - base
+        order = np.lexsort((cc[:, 2], cc[:, 1], cc[:, 0]))
+        xs.append(cc[order])
+        fs.append(f[order])
+        ranges.append((start, start + len(c)))
+        start += len(c)
+    coords = np.concatenate(xs).astype(np.int32) if xs else np.zeros((0, 3), np.int32)
+    return coords, np.concatenate(fs).astype(np.float32), ranges
+
