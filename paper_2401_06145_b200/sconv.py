@@ -22,6 +22,8 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libsconv_b200.so")
+# SCONV_LIB overrides the library path (A/B measurements of two builds on the same box)
+LIB_PATH = os.environ.get("SCONV_LIB", LIB_PATH)
 
 OK, ERR_ARG, ERR_RANGE, ERR_CUDA, ERR_OOM, ERR_STATE = range(6)
 MEM_HOST, MEM_DEVICE = 0, 1
