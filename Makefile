@@ -4,7 +4,7 @@ ARCH     := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3 --expt-relaxed-constexpr -Xptxas -v
 PKG      := paper_2401_06145_b200
 SRC      := $(PKG)/csrc
-CU       := $(SRC)/map.cu $(SRC)/gmas.cu $(SRC)/gemm_sm100.cu $(SRC)/conv_fused.cu $(SRC)/net.cu $(SRC)/capi.cu
+CU       := $(SRC)/map.cu $(SRC)/gmas.cu $(SRC)/gemm_sm100.cu $(SRC)/conv_fused.cu $(SRC)/voxelize.cu $(SRC)/net.cu $(SRC)/capi.cu
 HDR      := $(wildcard $(SRC)/*.hpp $(SRC)/*.cuh) include/sconv_b200.h
 OBJ      := $(patsubst $(SRC)/%.cu,build/%.o,$(CU))
 LIB      := $(PKG)/libsconv_b200.so

@@ -216,6 +216,18 @@ sconv_status sconv_net_conv_stats(const sconv_net* net, int conv, int64_t* out10
 sconv_status sconv_net_conv_timings(const sconv_net* net, int op, double* gmas_ms, double* fused_ms);
 void sconv_net_free(sconv_ctx* ctx, sconv_net* net);
 
+/* ---------------- voxelization (the step before the path) ----------------
+ * Replaces voxelize(points, features, resolution) (proj/include/sconv/geometry.hpp:180-255), bit
+ * for bit: voxel = floor(p / resolution) in double; duplicates merged by the mean of their
+ * feature rows accumulated in double in the reference's canonical order (point coordinates,
+ * then feature values); output sorted by packed key. points: n x 3 double; feats: n x channels
+ * float (channels may be 0, feats NULL); out_xyz (n x 3) / out_feats (n x channels) sized for
+ * n voxels, in out_mem. Errors: "resolution must be positive" (ARG), "voxel index <a> out of
+ * range" (RANGE) for the first offending point in input order. */
+sconv_status sconv_voxelize(sconv_ctx* ctx, const double* points, int64_t n, int points_mem, const float* feats,
+                            int64_t channels, int feats_mem, double resolution, int32_t* out_xyz, float* out_feats,
+                            int out_mem, int64_t* n_voxels);
+
 /* ---------------- utilities (cli gen) ----------------
  * N unique coordinates uniform in [0,E)^3 from Rng(stream_seed(seed,0)) (x,y,z order,
  * duplicates rejected), then N x C features U[0,1) from the same stream. Host buffers. */

@@ -115,6 +115,30 @@ inline std::pair<CoordsPtr, KernelMap> build_kernel_map_sorted(Context& ctx, con
   return {Q, std::move(km)};
 }
 
+// voxelize (geometry.hpp:180-255) on the GPU: same voxels, same mean-merged features, bit for bit.
+inline PointCloud voxelize(Context& ctx, const std::vector<std::array<double, 3>>& points, const Matrix& features,
+                           double resolution) {
+  const auto n = static_cast<std::int64_t>(points.size());
+  const std::int64_t channels = features.empty() ? 0 : features.cols();
+  if (channels > 0 && features.rows() != n) throw std::invalid_argument("feature row count does not match point count");
+  std::vector<std::int32_t> xyz(static_cast<std::size_t>(3 * n));
+  std::vector<float> f(static_cast<std::size_t>(std::max<std::int64_t>(1, n * channels)));
+  std::int64_t nv = 0;
+  ctx.check_status(sconv_voxelize(ctx.get(), n ? points[0].data() : nullptr, n, SCONV_MEM_HOST,
+                                  channels ? features.row(0) : nullptr, channels, SCONV_MEM_HOST, resolution,
+                                  xyz.data(), f.data(), SCONV_MEM_HOST, &nv));
+  xyz.resize(static_cast<std::size_t>(3 * nv));
+  PointCloud out;
+  out.coords = make_coords(detail::unflatten(xyz, nv));
+  if (channels > 0) {
+    out.features = Matrix(nv, channels);
+    for (std::int64_t r = 0; r < nv; ++r)
+      for (std::int64_t c = 0; c < channels; ++c) out.features(r, c) = f[static_cast<std::size_t>(r * channels + c)];
+  }
+  out.sorted = true;
+  return out;
+}
+
 // sc_layer_forward. W: K^3 matrices C_in x C_out, flattened [k][cin][cout].
 inline PointCloud sc_layer_forward(Context& ctx, const PointCloud& cloud, const std::vector<float>& W, int c_out,
                                    int K, int s, const LayerConfig& cfg = {}) {

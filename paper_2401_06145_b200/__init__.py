@@ -7,7 +7,7 @@ from .sconv import (  # noqa: F401
     BF16, DATAFLOW_AUTO, DATAFLOW_FUSED, DATAFLOW_GMAS, F16, F32, GROUP_MAP_ORDER, GROUP_SORTED, MEM_DEVICE, MEM_HOST, Context, CudaError, ExecCfg,
     InvalidArgument, KernelMap, LogicError, MapCfg, OutOfRange, PointCloud, SconvError, Weights,
     build_kernel_map_sorted, exec_cfg, generate_synthetic, generate_weights, layer_forward, layer_forward_device,
-    load, map_cfg, plan_groups, sc_layer_forward, tune_layer, weight_offsets,
+    load, map_cfg, plan_groups, sc_layer_forward, tune_layer, voxelize, weight_offsets,
 )
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -13,6 +13,7 @@
 #include "ctx.hpp"
 #include "conv_fused.hpp"
 #include "gmas.hpp"
+#include "voxelize.hpp"
 #include "map.hpp"
 #include "net.hpp"
 
@@ -643,6 +644,17 @@ sconv_status sconv_net_conv_timings(const sconv_net* net, int op, double* gmas_m
 void sconv_net_free(sconv_ctx* ctx, sconv_net* net) {
   if (ctx) cudaStreamSynchronize(ctx->stream);
   delete net;
+}
+
+sconv_status sconv_voxelize(sconv_ctx* ctx, const double* points, int64_t n, int points_mem, const float* feats,
+                            int64_t channels, int feats_mem, double resolution, int32_t* out_xyz, float* out_feats,
+                            int out_mem, int64_t* n_voxels) {
+  return guarded(ctx, [&] {
+    if (!n_voxels || (n > 0 && (!points || !out_xyz || (channels > 0 && !out_feats))))
+      fail(SCONV_ERR_ARG, "null argument");
+    *n_voxels = voxelize(*ctx, points, n, points_mem, feats, channels, feats_mem, resolution, out_xyz, out_feats,
+                         out_mem);
+  });
 }
 
 sconv_status sconv_generate_synthetic(int64_t N, int64_t E, int64_t C, uint64_t seed, int32_t* xyz, float* feats) {

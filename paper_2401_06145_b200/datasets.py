@@ -62,7 +62,9 @@ def _ray_cylinder(o, d, cx, cy, r, h):
 
 
 def kitti_scan(seed: int = 0, n_azimuth: int = 2900, beams: int = 64, max_range: float = 80.0,
-               resolution: float = 0.05):
+               resolution: float = 0.05, raw: bool = False):
+    """Simulated 64-beam LiDAR scan; raw=True returns the points (float64) + features before
+    voxelization (the input of voxelize)."""
     rng = np.random.default_rng(np.random.SeedSequence([seed, 0x4B495454]))
     o = np.array([0.0, 0.0, 1.73])
     el = np.deg2rad(np.linspace(-24.8, 2.0, beams))
@@ -87,6 +89,8 @@ def kitti_scan(seed: int = 0, n_azimuth: int = 2900, beams: int = 64, max_range:
     p += rng.normal(0, 0.01, p.shape)
     inten = rng.random((len(p), 1))
     feats = np.concatenate([p, inten], 1)
+    if raw:
+        return p, feats.astype(np.float32)
     return voxelize(p, feats, resolution)
 
 

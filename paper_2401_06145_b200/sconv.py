@@ -111,6 +111,7 @@ SIGNATURES = [
     ("sconv_net_read_tensor", _I, [_P, _P, _I, _P, _P]),
     ("sconv_net_tensor_device", _I, [_P, _I, C.POINTER(_P), C.POINTER(_I), C.POINTER(_I64)]),
     ("sconv_net_conv_timings", _I, [_P, _I, C.POINTER(_D), C.POINTER(_D)]),
+    ("sconv_voxelize", _I, [_P, _P, _I64, _I, _P, _I64, _I, _D, _P, _P, _I, C.POINTER(_I64)]),
     ("sconv_net_stats", _I, [_P, C.POINTER(_I), C.POINTER(_I)]),
     ("sconv_net_conv_stats", _I, [_P, _I, _P]),
     ("sconv_net_free", None, [_P, _P]),
@@ -309,6 +310,23 @@ class Weights:
             self.free()
         except Exception:
             pass
+
+
+def voxelize(ctx: Context, points: np.ndarray, features: Optional[np.ndarray], resolution: float) -> "PointCloud":
+    """GPU voxelize (reference geometry.hpp:180-255): points [n, 3] float64, features [n, C] float32
+    or None -> PointCloud of sorted voxel coordinates and mean-merged features (sorted=True)."""
+    pts = np.ascontiguousarray(points, np.float64).reshape(-1, 3)
+    n = len(pts)
+    f = None if features is None else np.ascontiguousarray(features, np.float32).reshape(n, -1)
+    ch = 0 if f is None else f.shape[1]
+    oxyz = np.empty((max(n, 1), 3), np.int32)
+    of = np.empty((max(n, 1), max(ch, 1)), np.float32)
+    nv = C.c_int64()
+    ctx.check(ctx.lib.sconv_voxelize(ctx.h, _ptr(pts), n, MEM_HOST, _ptr(f) if f is not None else None, ch, MEM_HOST,
+                                     float(resolution), _ptr(oxyz), _ptr(of), MEM_HOST, C.byref(nv)))
+    k = nv.value
+    feats_out = of[:k, :ch].copy() if ch else np.zeros((k, 0), np.float32)
+    return PointCloud(oxyz[:k].copy(), feats_out, True)
 
 
 def layer_forward(ctx: Context, kmap: KernelMap, w: Weights, features: np.ndarray, cfg: Optional[ExecCfg] = None,

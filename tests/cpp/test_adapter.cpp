@@ -60,7 +60,23 @@ int main() {
   } catch (const std::out_of_range& e) {
     threw = std::string(e.what()) == "coordinate x out of range: 1048576";
   }
-  std::printf("adapter: |Q|=%zu |M|=%lld max_rel=%.3g threw=%d\n", out.coords->size(),
-              static_cast<long long>(km.total()), maxerr / scale, threw ? 1 : 0);
-  return (maxerr / scale <= 1e-2 && threw) ? 0 : 1;
+  // GPU voxelize vs the reference's own voxelize (geometry.hpp:180-255): identical, bit for bit
+  std::vector<std::array<double, 3>> pts;
+  Matrix vf(3000, 5);
+  for (int i = 0; i < 3000; ++i) {
+    pts.push_back({std::sin(i * 0.37) * 7.0, std::cos(i * 0.11) * 3.0, (i % 97) * 0.031});
+    for (int c = 0; c < 5; ++c) vf(i, c) = static_cast<float>(std::sin(i * 1.7 + c));
+  }
+  const PointCloud vr = voxelize(pts, vf, 0.25);
+  const PointCloud vg = gpu::voxelize(ctx, pts, vf, 0.25);
+  bool vox_ok = vr.coords->size() == vg.coords->size() && vg.sorted;
+  for (std::size_t i = 0; vox_ok && i < vr.coords->size(); ++i) {
+    vox_ok = (*vr.coords)[i] == (*vg.coords)[i];
+    for (int c = 0; vox_ok && c < 5; ++c)
+      vox_ok = vr.features(static_cast<std::int64_t>(i), c) == vg.features(static_cast<std::int64_t>(i), c);
+  }
+  std::printf("adapter: |Q|=%zu |M|=%lld max_rel=%.3g threw=%d voxelize_exact=%d (%zu voxels)\n",
+              out.coords->size(), static_cast<long long>(km.total()), maxerr / scale, threw ? 1 : 0, vox_ok ? 1 : 0,
+              vr.coords->size());
+  return (maxerr / scale <= 1e-2 && threw && vox_ok) ? 0 : 1;
 }
