@@ -61,7 +61,14 @@ typedef struct {
   int transposed;   /* 1: output coordinates = target, offsets negated */
   int block_B;      /* source block size B (SPEC.md:247 default 256) */
   int block_C;      /* balanced query-block cap C (default 512) */
+  int backend;      /* sconv_map_backend: SORTED (Minuet, default) or HASH (SPEC.md:114-160 baseline) */
 } sconv_map_cfg;
+
+/* Map backend. SORTED: segmented query sorting + double-traversed binary search (Minuet).
+ * HASH: the SPEC's hash-table baseline (capacity = smallest power of two >= 2N, 64-bit
+ * Fibonacci multiplicative hash, linear probing) on the GPU. Both produce the
+ * identical canonical KernelMap (SPEC.md:367 backend equivalence). */
+typedef enum { SCONV_MAP_SORTED = 0, SCONV_MAP_HASH = 1 } sconv_map_backend;
 
 /* GMaS configuration (SPEC.md:359 config{grouping policy, eps, max_batch, tiles}). */
 typedef struct {

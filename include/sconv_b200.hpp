@@ -93,7 +93,7 @@ inline CoordList unflatten(const std::vector<std::int32_t>& v, std::int64_t n) {
 inline std::pair<CoordsPtr, KernelMap> build_kernel_map_sorted(Context& ctx, const PointCloud& P, int K, int s,
                                                                int B = 256, int C = 512) {
   const auto xyz = detail::flatten(*P.coords);
-  sconv_map_cfg cfg{K, s, s, 0, B, C};
+  sconv_map_cfg cfg{K, s, s, 0, B, C, SCONV_MAP_SORTED};
   sconv_map* m = nullptr;
   ctx.check_status(sconv_map_build(ctx.get(), xyz.data(), P.size(), SCONV_MEM_HOST, P.sorted ? 1 : 0, &cfg, nullptr,
                                    0, SCONV_MEM_HOST, &m));

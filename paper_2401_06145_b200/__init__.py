@@ -4,7 +4,7 @@ The compute path is libsconv_b200.so (hand-written sm_100a CUDA behind a C ABI,
 include/sconv_b200.h); this package is its Python binding. No CPU fallback exists.
 """
 from .sconv import (  # noqa: F401
-    BF16, DATAFLOW_AUTO, DATAFLOW_FUSED, DATAFLOW_GMAS, F16, F32, GROUP_MAP_ORDER, GROUP_SORTED, MEM_DEVICE, MEM_HOST, Context, CudaError, ExecCfg,
+    BF16, DATAFLOW_AUTO, DATAFLOW_FUSED, DATAFLOW_GMAS, F16, F32, GROUP_MAP_ORDER, GROUP_SORTED, MAP_HASH, MAP_SORTED, MEM_DEVICE, MEM_HOST, Context, CudaError, ExecCfg,
     InvalidArgument, KernelMap, LogicError, MapCfg, OutOfRange, PointCloud, SconvError, Weights,
     build_kernel_map_sorted, exec_cfg, generate_synthetic, generate_weights, layer_forward, layer_forward_device,
     load, map_cfg, plan_groups, sc_layer_forward, tune_layer, voxelize, weight_offsets,

@@ -84,6 +84,7 @@ sconv_map_cfg default_map_cfg(int K, int s) {
   c.transposed = 0;
   c.block_B = 256;
   c.block_C = 512;
+  c.backend = SCONV_MAP_SORTED;
   return c;
 }
 

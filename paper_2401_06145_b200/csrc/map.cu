@@ -732,6 +732,58 @@ __global__ void __launch_bounds__(kSearchThreads) k_emit(const int32_t* __restri
   }
 }
 
+// ---------------------------------------------------------------- hash-table baseline
+// SPEC.md:114-160 (the §3 Shortcoming #1 baseline): open addressing, capacity = smallest power
+// of two >= 2N, 64-bit Fibonacci multiplicative hash, linear probing; every (i, k) probes
+// pack(q_i + delta_k). Writes the same nbr table and per-(k, chunk) hit counts as k_search, so
+// the canonical lists come from the same scan / emit kernels (backend equivalence).
+constexpr uint64_t kFib = 0x9E3779B97F4A7C15ull, kEmptySlot = ~uint64_t{0};
+
+__global__ void k_hash_insert(const uint64_t* __restrict__ keys, const int32_t* __restrict__ idx, int64_t n,
+                              uint64_t* __restrict__ slot_keys, int32_t* __restrict__ slot_vals, int shift,
+                              uint64_t mask) {
+  const int64_t i = blockIdx.x * int64_t{blockDim.x} + threadIdx.x;
+  if (i >= n) return;
+  const uint64_t key = keys[i];
+  uint64_t h = (key * kFib) >> shift;
+  for (;;) {  // keys are unique: a slot is either empty or another key
+    const unsigned long long prev = atomicCAS(reinterpret_cast<unsigned long long*>(slot_keys + h),
+                                              static_cast<unsigned long long>(kEmptySlot),
+                                              static_cast<unsigned long long>(key));
+    if (prev == kEmptySlot) {
+      slot_vals[h] = idx ? idx[i] : static_cast<int32_t>(i);
+      return;
+    }
+    h = (h + 1) & mask;
+  }
+}
+
+// grid (query chunks of blockDim.x, K3): one query per thread
+__global__ void k_hash_query(const uint64_t* __restrict__ q, int64_t n_q, OffsetGen og,
+                             const uint64_t* __restrict__ slot_keys, const int32_t* __restrict__ slot_vals, int shift,
+                             uint64_t mask, int64_t nchunk, int32_t* __restrict__ nbr, int32_t* __restrict__ counts) {
+  const int64_t c = blockIdx.x;
+  const int k = blockIdx.y;
+  const int64_t i = c * blockDim.x + threadIdx.x;
+  int32_t j = -1;
+  if (i < n_q) {
+    const uint64_t key = segment_key(q[i], og.at(k));  // out of range: saturated, never stored
+    uint64_t h = (key * kFib) >> shift;
+    for (;;) {
+      const uint64_t s = __ldg(slot_keys + h);
+      if (s == key) {
+        j = __ldg(slot_vals + h);
+        break;
+      }
+      if (s == kEmptySlot) break;
+      h = (h + 1) & mask;
+    }
+    nbr[int64_t{k} * n_q + i] = j;
+  }
+  const int hits = __syncthreads_count(j >= 0);
+  if (threadIdx.x == 0) counts[int64_t{k} * nchunk + c] = hits;
+}
+
 constexpr int kThreads = 256;
 // Key / index arrays carry slack so 16-byte bulk copies may run past the last element.
 inline int64_t slack(int64_t n) { return ((n + 3) & ~int64_t{3}) + 4; }
@@ -1121,24 +1173,43 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
       if (lex_less(delta[k], delta[kmin_off])) kmin_off = k;
       if (lex_less(delta[kmax_off], delta[k])) kmax_off = k;
     }
-    const int cap_blocks = std::max(1, static_cast<int>((24 * 1024) / (12 * B)));
-    const int ngroups = ceil_div(K3, kSearchThreads / 32);  // CTA = chunk x group of <= 8 offsets
-    const size_t smem = size_t{12} * cap_blocks * B;
-    auto go = [&](auto kern) {
-      SCONV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-      ctx.launch("k_search", [&] {
-        kern<<<static_cast<unsigned>(nchunk2 * ngroups), kSearchThreads, smem, st>>>(
-            src, src_idx, n, B, q, n_out, OffsetGen{cfg.kernel_size, cfg.transposed ? -cfg.offset_scale : cfg.offset_scale},
-            K3, kmin_off, kmax_off, nchunk2, ngroups, cap_blocks,
-            m->nbr_in.get<int32_t>(), counts.get<int32_t>(), offs.get<int32_t>(), ctx.done_counter(),
-            m->map_start.get<int32_t>());
+    const int ngroups = ceil_div(K3, kSearchThreads / 32);  // search / emit CTA = chunk x <= 8 offsets
+    if (cfg.backend == SCONV_MAP_HASH) {
+      int lg = 1;
+      while ((int64_t{1} << lg) < 2 * n) ++lg;  // capacity: smallest power of two >= 2N
+      const uint64_t cap = uint64_t{1} << lg;
+      m->hash_keys.alloc(8 * cap, st);
+      m->hash_vals.alloc(4 * cap, st);
+      SCONV_CUDA(cudaMemsetAsync(m->hash_keys.get(), 0xFF, 8 * cap, st));
+      ctx.launch("k_hash_insert", [&] {
+        k_hash_insert<<<grid_for(n), kThreads, 0, st>>>(src, src_idx, n, m->hash_keys.get<uint64_t>(),
+                                                        m->hash_vals.get<int32_t>(), 64 - lg, cap - 1);
       });
-    };
-    switch (qpl) {
-      case 1: go(k_search<1>); break;
-      case 2: go(k_search<2>); break;
-      case 4: go(k_search<4>); break;
-      default: go(k_search<8>); break;
+      ctx.launch("k_hash_query", [&] {
+        k_hash_query<<<dim3(static_cast<unsigned>(nchunk2), static_cast<unsigned>(K3)), CQ, 0, st>>>(
+            q, n_out, OffsetGen{cfg.kernel_size, cfg.transposed ? -cfg.offset_scale : cfg.offset_scale},
+            m->hash_keys.get<uint64_t>(), m->hash_vals.get<int32_t>(), 64 - lg, cap - 1, nchunk2,
+            m->nbr_in.get<int32_t>(), counts.get<int32_t>());
+      });
+    } else {
+      const int cap_blocks = std::max(1, static_cast<int>((24 * 1024) / (12 * B)));
+      const size_t smem = size_t{12} * cap_blocks * B;
+      auto go = [&](auto kern) {
+        SCONV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        ctx.launch("k_search", [&] {
+          kern<<<static_cast<unsigned>(nchunk2 * ngroups), kSearchThreads, smem, st>>>(
+              src, src_idx, n, B, q, n_out, OffsetGen{cfg.kernel_size, cfg.transposed ? -cfg.offset_scale : cfg.offset_scale},
+              K3, kmin_off, kmax_off, nchunk2, ngroups, cap_blocks,
+              m->nbr_in.get<int32_t>(), counts.get<int32_t>(), offs.get<int32_t>(), ctx.done_counter(),
+              m->map_start.get<int32_t>());
+        });
+      };
+      switch (qpl) {
+        case 1: go(k_search<1>); break;
+        case 2: go(k_search<2>); break;
+        case 4: go(k_search<4>); break;
+        default: go(k_search<8>); break;
+      }
     }
     auto& pd = m->pending;
     pd.counts = std::move(counts);

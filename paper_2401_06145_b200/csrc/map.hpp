@@ -23,6 +23,7 @@ struct MapData {
   DevBuf nbr_pos;            // int32 x K3 x n_out: canonical position m of (k, i) or -1
   DevBuf nbr_in;             // int32 x K3 x n_out: input row j of (k, i) or -1 (fused dataflow)
   std::vector<int3> delta;   // search offsets (host copy)
+  DevBuf hash_keys, hash_vals;  // hash backend index, kept for inspection
   // Fused-dataflow row order (built lazily, conv_fused.cu prepare_fused_layout): output rows
   // sorted by their neighbour bitmask so a 128-row tile touches few offsets.
   bool fused_ready = false;

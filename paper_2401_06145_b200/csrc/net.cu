@@ -237,7 +237,7 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
       const MapKey key{a.coordset, o.K, o.offset_scale, o.transposed ? 1 : o.out_stride, o.transposed, tgt};
       auto it = maps.find(key);
       if (it == maps.end()) {
-        sconv_map_cfg mcfg{o.K, o.offset_scale, o.out_stride, o.transposed, block_B, block_C};
+        sconv_map_cfg mcfg{o.K, o.offset_scale, o.out_stride, o.transposed, block_B, block_C, SCONV_MAP_SORTED};
         const CoordSet& cs = coordsets[a.coordset];
         MapSource P;
         if (cs.raw && !cs.keys) {

@@ -30,6 +30,7 @@ MEM_HOST, MEM_DEVICE = 0, 1
 F32, F16, BF16 = 0, 1, 2
 GROUP_MAP_ORDER, GROUP_SORTED = 0, 1
 DATAFLOW_GMAS, DATAFLOW_FUSED, DATAFLOW_AUTO = 0, 1, 2
+MAP_SORTED, MAP_HASH = 0, 1
 
 
 class SconvError(RuntimeError):
@@ -54,7 +55,7 @@ class LogicError(SconvError):
 
 class MapCfg(C.Structure):
     _fields_ = [("kernel_size", C.c_int), ("offset_scale", C.c_int), ("out_stride", C.c_int),
-                ("transposed", C.c_int), ("block_B", C.c_int), ("block_C", C.c_int)]
+                ("transposed", C.c_int), ("block_B", C.c_int), ("block_C", C.c_int), ("backend", C.c_int)]
 
 
 class ExecCfg(C.Structure):
@@ -216,8 +217,9 @@ class Context:
         self.check(self.lib.sconv_ctx_flush_l2(self.h, nbytes))
 
 
-def map_cfg(K=3, offset_scale=1, out_stride=1, transposed=False, B=256, Cq=512) -> MapCfg:
-    return MapCfg(K, offset_scale, out_stride, 1 if transposed else 0, B, Cq)
+def map_cfg(K=3, offset_scale=1, out_stride=1, transposed=False, B=256, Cq=512, backend=0) -> MapCfg:
+    """backend: MAP_SORTED (Minuet double-traversed search) or MAP_HASH (SPEC hash baseline)."""
+    return MapCfg(K, offset_scale, out_stride, 1 if transposed else 0, B, Cq, backend)
 
 
 def exec_cfg(policy=GROUP_SORTED, epsilon=0.25, max_batch=16, gather_tile=0, scatter_tile=0,
@@ -237,9 +239,9 @@ class KernelMap:
 
     @classmethod
     def build(cls, ctx: Context, coords, sorted_: bool = False, K=3, offset_scale=1, out_stride=1,
-              transposed=False, target=None, B=256, Cq=512, device_ptr: Optional[int] = None,
+              transposed=False, target=None, B=256, Cq=512, device_ptr: Optional[int] = None, backend=0,
               n: Optional[int] = None) -> "KernelMap":
-        cfg = map_cfg(K, offset_scale, out_stride, transposed, B, Cq)
+        cfg = map_cfg(K, offset_scale, out_stride, transposed, B, Cq, backend)
         h = C.c_void_p()
         tgt = None
         if target is not None:

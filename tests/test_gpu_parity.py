@@ -63,6 +63,23 @@ def test_map_parity(ctx, oracle, K, s, n, extent, presorted, B, Cq):
     assert_map_equal(gpu, ora)
 
 
+@pytest.mark.parametrize("K,s,n,extent,presorted", [
+    (3, 1, 20000, 40, False), (3, 1, 20000, 400, False), (5, 2, 4000, 25, True), (1, 1, 1000, 30, True),
+    (3, 2, 20000, 50, False), (3, 1, 7, 5, False),
+])
+def test_hash_backend_equivalence(ctx, oracle, K, s, n, extent, presorted):
+    """The SPEC's hash-table baseline on the GPU builds the identical canonical map."""
+    rng = np.random.default_rng(K * 7 + n)
+    xyz = random_cloud(rng, n, extent, origin=-extent // 3)
+    if presorted:
+        xyz = sort_rows(xyz)
+    got = sc.KernelMap.build(ctx, xyz, presorted, K, s, s, backend=sc.MAP_HASH).read()
+    assert_map_equal(got, oracle.layer_map(xyz, presorted, K, s, s, backend=1))
+    ref = sc.KernelMap.build(ctx, xyz, presorted, K, s, s).read()
+    for a, b in zip(got, ref):
+        np.testing.assert_array_equal(a, b)
+
+
 def test_map_range_edges(ctx, oracle):
     """Clouds touching COORD_MIN / COORD_MAX (the SPEC sentinel edge case)."""
     rng = np.random.default_rng(5)
