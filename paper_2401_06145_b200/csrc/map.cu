@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <string>
@@ -469,152 +470,130 @@ __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity)
 }
 
 // Output-chunk double-traversed search. A CTA owns CQ = 32*QPL consecutive sorted queries
-// q_i and ALL K^3 offsets. Their segment keys {q_i + delta_k} lie between
-// q_first + delta_lexmin and q_last + delta_lexmax (translation preserves lexicographic
-// order), so ONE window of whole source blocks covers every segment of the chunk: it is
-// found with two warp-cooperative pivot searches and staged in shared memory by a single
-// bulk (TMA) copy, then reused by all K^3 offsets (windows larger than the shared-memory
-// capacity are processed in block-aligned slices). Warp w handles offsets k = w, w+8, ...:
+// q_i and up to 8 offsets, one per warp; warps run independently (no CTA barrier). For its
+// offset delta_k a warp's segment keys {q_i + delta_k} lie in [q_first + delta_k,
+// q_last + delta_k] (translation preserves lexicographic order), so only the source blocks
+// holding that range can match: the warp finds them with two warp-cooperative pivot
+// searches and stages them in ITS OWN shared-memory window with one bulk (TMA) copy per
+// array (windows above the per-warp capacity are processed in block-aligned slices).
+// Per-offset windows are ~CQ keys whatever the cloud density; a window shared by all
+// offsets would span every x-slice the offsets reach (~3 slices of a dense cloud).
 //   * segment keys of the CQ queries live in registers (lane-major => sorted across lanes);
 //   * BACKWARD search: every staged block pivot is compared with the whole sorted segment
-//     (one ballot per register row) -> its upper bound, i.e. the block's query sub-range
-//     (SPEC.md:208-216);
+//     -> its upper bound, i.e. the block's query sub-range;
 //   * FORWARD search: each query is binary-searched only inside its own staged block,
-//     <= ceil(log2(B+1)) steps.
-// Results go to the dense k-major table (coalesced rows) and per-(k, chunk) hit counts,
-// scanned by the last CTA to finish (canonical order: k, then chunk).
+//     <= ceil(log2(B+1)) steps, galloping between a lane's consecutive queries
+//     (SPEC.md:226-234).
+// Results go to the dense k-major table (coalesced rows) and per-(k, chunk) hit counts.
 template <int QPL>
 __global__ void __launch_bounds__(kSearchThreads) k_search(
     const uint64_t* __restrict__ src, const int32_t* __restrict__ src_idx, int64_t n_src, int B,
-    const uint64_t* __restrict__ q, int64_t n_q, OffsetGen og, int K3, int kmin_off,
-    int kmax_off, int64_t nchunk, int ngroups, int cap_blocks, int32_t* __restrict__ nbr,
-    int32_t* __restrict__ chunk_count, int32_t* __restrict__ chunk_off, unsigned* __restrict__ done,
-    int32_t* __restrict__ map_start) {
+    const uint64_t* __restrict__ q, int64_t n_q, OffsetGen og, int K3, int64_t nchunk, int ngroups,
+    int cap_blocks, int32_t* __restrict__ nbr, int32_t* __restrict__ chunk_count) {
   constexpr int CQ = 32 * QPL;
   constexpr int kWarps = kSearchThreads / 32;
   extern __shared__ __align__(16) unsigned char smem[];
-  const int cap = cap_blocks * B;
-  uint64_t* s_win = reinterpret_cast<uint64_t*>(smem);           // cap staged keys
-  int32_t* s_widx = reinterpret_cast<int32_t*>(s_win + cap);     // cap staged indices
-  __shared__ uint64_t s_q[CQ];
-  __shared__ __align__(8) uint64_t s_bar;
-  __shared__ int64_t s_blo, s_bhi;
-  __shared__ int s_warp[kWarps];
-  __shared__ bool s_last;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  __shared__ __align__(8) uint64_t s_bar[kWarps];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int cap = cap_blocks * B;  // keys per warp window
+  uint64_t* s_win = reinterpret_cast<uint64_t*>(smem) + int64_t{warp} * cap;
+  int32_t* s_widx = reinterpret_cast<int32_t*>(reinterpret_cast<uint64_t*>(smem) + int64_t{kWarps} * cap) +
+                    int64_t{warp} * cap;
   const int64_t c = blockIdx.x / ngroups;
   const int grp = static_cast<int>(blockIdx.x - c * ngroups);
-  const int my_k = grp + warp * ngroups;  // one offset per warp (CTA = chunk x offset group)
-  int my_cnt = 0;
-  const int64_t lo = c * CQ;
-  const int len = static_cast<int>(min(static_cast<int64_t>(CQ), n_q - lo));
-  if (tid == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_bar)) : "memory");
+  const int k = grp + warp * ngroups;  // this warp's offset
+  if (k >= K3) return;
+  uint64_t* bar = &s_bar[warp];
+  if (lane == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (int t = tid; t < CQ; t += kSearchThreads) s_q[t] = t < len ? __ldg(q + lo + t) : ~uint64_t{0};
-  __syncthreads();
-  const int64_t nb = (n_src + B - 1) / B;
-  if (warp < 2) {  // window: blocks holding [q_first + delta_lexmin, q_last + delta_lexmax]
-    const uint64_t key = warp == 0 ? segment_key(s_q[0], og.at(kmin_off)) : segment_key(s_q[len - 1], og.at(kmax_off));
-    const int64_t hint = (((warp == 0 ? lo : lo + len - 1) * n_src) / max(n_q, int64_t{1})) / B;
-    const int64_t b = warp_first_pivot_ge(src, n_src, B, 0, nb, key, lane, hint);
-    if (lane == 0) {
-      if (warp == 0)
-        s_blo = b;
-      else
-        s_bhi = min(b, nb - 1);
-    }
+  __syncwarp();
+  const int64_t lo = c * CQ;
+  const int len = static_cast<int>(min(static_cast<int64_t>(CQ), n_q - lo));
+  const int3 d = og.at(k);
+  // lane-contiguous queries: lane L owns chunk positions [L*QPL, (L+1)*QPL), so a lane's
+  // consecutive sorted queries can be merged against the sorted block (galloping)
+  const int qb = lane * QPL;
+  uint64_t key[QPL];
+  int res[QPL];
+#pragma unroll
+  for (int u = 0; u < QPL; ++u) {
+    key[u] = qb + u < len ? segment_key(__ldg(q + lo + qb + u), d) : ~uint64_t{0};
+    res[u] = -1;
   }
-  __syncthreads();
-  const int64_t blo = s_blo, bhi = s_bhi;
+  const uint64_t key_lo = segment_key(__ldg(q + lo), d), key_hi = segment_key(__ldg(q + lo + len - 1), d);
+  const int64_t nb = (n_src + B - 1) / B;
+  const int64_t blo =
+      warp_first_pivot_ge(src, n_src, B, 0, nb, key_lo, lane, ((lo * n_src) / max(n_q, int64_t{1})) / B);
+  const int64_t bhi =
+      blo >= nb ? blo : min(warp_first_pivot_ge(src, n_src, B, blo, nb, key_hi, lane, blo + (len + B - 1) / B), nb - 1);
   uint32_t phase = 0;
-  bool first_slice = true;
-  for (int64_t sb = blo; first_slice || sb <= bhi; sb += cap_blocks) {
-    const bool empty = blo >= nb || sb > bhi;  // no source block can match: write misses only
-    const int nblk = empty ? 0 : static_cast<int>(min(static_cast<int64_t>(cap_blocks), bhi - sb + 1));
+  for (int64_t sb = blo; sb < nb && sb <= bhi; sb += cap_blocks) {
+    const int nblk = static_cast<int>(min(static_cast<int64_t>(cap_blocks), bhi - sb + 1));
     const int64_t g0 = sb * B;
-    const int wlen = empty ? 0 : static_cast<int>(min(static_cast<int64_t>(nblk) * B, n_src - g0));
-    if (tid == 0 && wlen > 0) {  // one bulk copy per array (16-byte granules; arrays carry slack)
+    const int wlen = static_cast<int>(min(static_cast<int64_t>(nblk) * B, n_src - g0));
+    if (lane == 0) {  // one bulk copy per array (16-byte granules; arrays carry slack)
       const uint32_t kb = static_cast<uint32_t>((wlen + 3) & ~3);
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&s_bar)),
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                    "r"(kb * 8u + (src_idx ? kb * 4u : 0u))
                    : "memory");
-      bulk_g2s(s_win, src + g0, kb * 8u, &s_bar);
-      if (src_idx) bulk_g2s(s_widx, src_idx + g0, kb * 4u, &s_bar);
+      bulk_g2s(s_win, src + g0, kb * 8u, bar);
+      if (src_idx) bulk_g2s(s_widx, src_idx + g0, kb * 4u, bar);
     }
-    if (wlen > 0) {
-      mbar_wait_parity(&s_bar, phase);
-      phase ^= 1u;
+    mbar_wait_parity(bar, phase);
+    phase ^= 1u;
+    // key just below this slice: queries <= it belong to earlier slices
+    const uint64_t floor_key = sb == blo ? 0 : __ldg(src + g0 - 1);
+    int blk[QPL];  // block of each query inside the slice, -1 = not in this slice
+#pragma unroll
+    for (int u = 0; u < QPL; ++u) blk[u] = key[u] != ~uint64_t{0} && (sb == blo || key[u] > floor_key) ? 0 : -1;
+    // BACKWARD search: each staged pivot splits the sorted segment; queries above pivot_b
+    // move to block b+1, above the last pivot they are outside the slice.
+    for (int bb = 0; bb < nblk; ++bb) {
+      const uint64_t piv = s_win[min((bb + 1) * B, wlen) - 1];
+#pragma unroll
+      for (int u = 0; u < QPL; ++u)
+        if (blk[u] == bb && key[u] > piv) blk[u] = bb + 1 < nblk ? bb + 1 : -1;
     }
-    // key just below this slice: queries <= it belong to earlier slices (or to nothing)
-    const uint64_t floor_key = (empty || sb == 0) ? 0 : __ldg(src + g0 - 1);
-    for (int k = my_k; k < K3; k += K3) {  // at most one iteration
-      const int3 d = og.at(k);
-      // lane-contiguous queries: lane L owns chunk positions [L*QPL, (L+1)*QPL), so a lane's
-      // consecutive sorted queries can be merged against the sorted block (galloping)
-      const int qb = lane * QPL;
-      uint64_t key[QPL];
+    // FORWARD search inside the block: branchless lower bound for the first query of a
+    // block, then galloping from the previous position for the following (sorted) ones.
+    int p = 0, pblk = -1;
 #pragma unroll
-      for (int u = 0; u < QPL; ++u) key[u] = qb + u < len ? segment_key(__ldg(q + lo + qb + u), d) : ~uint64_t{0};
-      int blk[QPL];  // block of each query inside the slice, -1 = not in this slice
-#pragma unroll
-      for (int u = 0; u < QPL; ++u) {
-        blk[u] = (sb == blo && !empty) || key[u] > floor_key ? 0 : -1;
-        if (empty || key[u] == ~uint64_t{0}) blk[u] = -1;
-      }
-      // BACKWARD search: each staged pivot splits the sorted segment; queries above pivot_b
-      // move to block b+1, above the last pivot they are outside the slice.
-      for (int bb = 0; bb < nblk; ++bb) {
-        const uint64_t piv = s_win[min((bb + 1) * B, wlen) - 1];
-#pragma unroll
-        for (int u = 0; u < QPL; ++u)
-          if (blk[u] == bb && key[u] > piv) blk[u] = bb + 1 < nblk ? bb + 1 : -1;
-      }
-      // FORWARD search inside the block: branchless lower bound for the first query of a
-      // block, then galloping from the previous position for the following (sorted) ones.
-      int res[QPL];
-      int p = 0, pblk = -1;
-#pragma unroll
-      for (int u = 0; u < QPL; ++u) {
-        res[u] = -1;
-        if (blk[u] < 0) continue;
-        const int w0 = blk[u] * B, end = w0 + min(B, wlen - w0);
-        bool bsearch = blk[u] != pblk;
-        if (!bsearch) {
-          int steps = 0;
-          while (p < end - 1 && s_win[p] < key[u] && steps < 6) {
-            ++p;
-            ++steps;
-          }
-          bsearch = p < end - 1 && s_win[p] < key[u];
+    for (int u = 0; u < QPL; ++u) {
+      if (blk[u] < 0) continue;
+      const int w0 = blk[u] * B, end = w0 + min(B, wlen - w0);
+      bool bsearch = blk[u] != pblk;
+      if (!bsearch) {
+        int steps = 0;
+        while (p < end - 1 && s_win[p] < key[u] && steps < 6) {
+          ++p;
+          ++steps;
         }
-        if (bsearch) {
-          int base = blk[u] != pblk ? w0 : p, n = end - base;
-          while (n > 1) {
-            const int h = n >> 1;
-            base += s_win[base + h - 1] < key[u] ? h : 0;
-            n -= h;
-          }
-          p = base;
+        bsearch = p < end - 1 && s_win[p] < key[u];
+      }
+      if (bsearch) {
+        int base = blk[u] != pblk ? w0 : p, n = end - base;
+        while (n > 1) {
+          const int h = n >> 1;
+          base += s_win[base + h - 1] < key[u] ? h : 0;
+          n -= h;
         }
-        pblk = blk[u];
-        if (s_win[p] == key[u]) res[u] = src_idx ? s_widx[p] : static_cast<int32_t>(g0 + p);
+        p = base;
       }
-      int32_t* row = nbr + int64_t{k} * n_q + lo + qb;
-      int cnt = 0;
-#pragma unroll
-      for (int u = 0; u < QPL; ++u) {
-        if (qb + u < len && (first_slice || res[u] >= 0)) row[u] = res[u];
-        cnt += __popc(__ballot_sync(0xFFFFFFFFu, res[u] >= 0));
-      }
-      my_cnt += cnt;
+      pblk = blk[u];
+      if (s_win[p] == key[u]) res[u] = src_idx ? s_widx[p] : static_cast<int32_t>(g0 + p);
     }
-    first_slice = false;
-    __syncthreads();  // the next slice overwrites the window
-    if (empty) break;
+    __syncwarp();  // the next slice overwrites the window
   }
-  if (lane == 0 && my_k < K3) chunk_count[int64_t{my_k} * nchunk + c] = my_cnt;
+  int32_t* row = nbr + int64_t{k} * n_q + lo + qb;
+  int cnt = 0;
+#pragma unroll
+  for (int u = 0; u < QPL; ++u) {
+    if (qb + u < len) row[u] = res[u];
+    cnt += __popc(__ballot_sync(0xFFFFFFFFu, res[u] >= 0));
+  }
+  if (lane == 0) chunk_count[int64_t{k} * nchunk + c] = cnt;
 }
 
 // Exclusive scan of the (k, chunk) hit counts in canonical order: each CTA scans a tile of
@@ -1165,14 +1144,6 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
     tiles.alloc(sizeof(int32_t) * ntiles, st);
     m->pair_in.alloc(sizeof(int32_t) * std::max<int64_t>(1, max_pairs), st);
     m->pair_out.alloc(sizeof(int32_t) * std::max<int64_t>(1, max_pairs), st);
-    int kmin_off = 0, kmax_off = 0;  // lexicographically smallest / largest search offset
-    auto lex_less = [](const int3& a, const int3& b) {
-      return a.x != b.x ? a.x < b.x : (a.y != b.y ? a.y < b.y : a.z < b.z);
-    };
-    for (int k = 1; k < K3; ++k) {
-      if (lex_less(delta[k], delta[kmin_off])) kmin_off = k;
-      if (lex_less(delta[kmax_off], delta[k])) kmax_off = k;
-    }
     const int ngroups = ceil_div(K3, kSearchThreads / 32);  // search / emit CTA = chunk x <= 8 offsets
     if (cfg.backend == SCONV_MAP_HASH) {
       int lg = 1;
@@ -1192,16 +1163,19 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
             m->nbr_in.get<int32_t>(), counts.get<int32_t>());
       });
     } else {
-      const int cap_blocks = std::max(1, static_cast<int>((24 * 1024) / (12 * B)));
-      const size_t smem = size_t{12} * cap_blocks * B;
+      // per-warp window: ~768 keys (a 256-query chunk's segment spans ~2-3 blocks of 256)
+      static const int cap_keys = [] {
+        const char* e = std::getenv("SCONV_SEARCH_CAP");  // experiments
+        return e ? std::max(4, std::atoi(e)) : 768;
+      }();
+      const int cap_blocks = std::max(1, cap_keys / B);
+      const size_t smem = size_t{12} * (kSearchThreads / 32) * cap_blocks * B;
       auto go = [&](auto kern) {
         SCONV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         ctx.launch("k_search", [&] {
           kern<<<static_cast<unsigned>(nchunk2 * ngroups), kSearchThreads, smem, st>>>(
               src, src_idx, n, B, q, n_out, OffsetGen{cfg.kernel_size, cfg.transposed ? -cfg.offset_scale : cfg.offset_scale},
-              K3, kmin_off, kmax_off, nchunk2, ngroups, cap_blocks,
-              m->nbr_in.get<int32_t>(), counts.get<int32_t>(), offs.get<int32_t>(), ctx.done_counter(),
-              m->map_start.get<int32_t>());
+              K3, nchunk2, ngroups, cap_blocks, m->nbr_in.get<int32_t>(), counts.get<int32_t>());
         });
       };
       switch (qpl) {
