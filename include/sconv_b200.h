@@ -235,6 +235,21 @@ sconv_status sconv_voxelize(sconv_ctx* ctx, const double* points, int64_t n, int
                             int64_t channels, int feats_mem, double resolution, int32_t* out_xyz, float* out_feats,
                             int out_mem, int64_t* n_voxels);
 
+/* ---------------- point-cloud files (SURVEY §8f rank 3 "ingestion") ----------------
+ * ".mpc" binary: magic "MPC1", little-endian u32 N, u32 C, N x 3 int32 voxel coordinates, N x C
+ * float32 features. ".xyz" text: one point per line "x y z f1 ... fC" (whitespace-separated
+ * decimals; blank lines and '#' comments skipped; every line the same column count).
+ * sconv_cloud_file_info detects the format (a ".mpc" name or the MPC1 magic) and returns N and C (parses a whole
+ * .xyz file); the read calls take buffers of exactly that shape (host memory). Errors are ARG
+ * with "mpc parse error at offset <o>: ..." / "xyz parse error at line <l>: ...". An .xyz
+ * cloud is float points (voxelize it with sconv_voxelize); an .mpc cloud is already voxels. */
+enum sconv_file_format { SCONV_FILE_MPC = 0, SCONV_FILE_XYZ = 1 };
+sconv_status sconv_cloud_file_info(const char* path, int* format, int64_t* n, int64_t* channels);
+sconv_status sconv_mpc_read(const char* path, int32_t* xyz, float* feats, int64_t n, int64_t channels);
+sconv_status sconv_mpc_write(const char* path, const int32_t* xyz, const float* feats, int64_t n, int64_t channels);
+sconv_status sconv_xyz_read(const char* path, double* points, float* feats, int64_t n, int64_t channels);
+sconv_status sconv_xyz_write(const char* path, const double* points, const float* feats, int64_t n, int64_t channels);
+
 /* ---------------- utilities (cli gen) ----------------
  * N unique coordinates uniform in [0,E)^3 from Rng(stream_seed(seed,0)) (x,y,z order,
  * duplicates rejected), then N x C features U[0,1) from the same stream. Host buffers. */

@@ -139,6 +139,48 @@ inline PointCloud voxelize(Context& ctx, const std::vector<std::array<double, 3>
   return out;
 }
 
+// Point-cloud files. .mpc -> PointCloud of voxel coordinates (sorted = false);
+// .xyz -> float points + features (the input of voxelize). Parse errors: std::invalid_argument.
+inline PointCloud read_mpc(const std::string& path) {
+  int fmt = 0;
+  std::int64_t n = 0, c = 0;
+  check(sconv_cloud_file_info(path.c_str(), &fmt, &n, &c), sconv_global_last_error());
+  if (fmt != SCONV_FILE_MPC) throw std::invalid_argument("mpc parse error at offset 0: bad magic");
+  std::vector<std::int32_t> xyz(static_cast<std::size_t>(3 * n));
+  std::vector<float> f(static_cast<std::size_t>(std::max<std::int64_t>(1, n * c)));
+  check(sconv_mpc_read(path.c_str(), xyz.data(), f.data(), n, c), sconv_global_last_error());
+  PointCloud out;
+  out.coords = make_coords(detail::unflatten(xyz, n));
+  if (c > 0) {
+    out.features = Matrix(n, c);
+    for (std::int64_t r = 0; r < n; ++r)
+      for (std::int64_t k = 0; k < c; ++k) out.features(r, k) = f[static_cast<std::size_t>(r * c + k)];
+  }
+  out.sorted = false;
+  return out;
+}
+
+inline void write_mpc(const std::string& path, const PointCloud& cloud) {
+  const auto xyz = detail::flatten(*cloud.coords);
+  const std::int64_t c = cloud.channels();
+  check(sconv_mpc_write(path.c_str(), xyz.data(), c ? cloud.features.row(0) : nullptr, cloud.size(), c),
+        sconv_global_last_error());
+}
+
+inline std::pair<std::vector<std::array<double, 3>>, Matrix> read_xyz(const std::string& path) {
+  int fmt = 0;
+  std::int64_t n = 0, c = 0;
+  check(sconv_cloud_file_info(path.c_str(), &fmt, &n, &c), sconv_global_last_error());
+  if (fmt != SCONV_FILE_XYZ) throw std::invalid_argument("xyz parse error at line 1: binary .mpc file");
+  std::vector<std::array<double, 3>> pts(static_cast<std::size_t>(n));
+  std::vector<float> f(static_cast<std::size_t>(std::max<std::int64_t>(1, n * c)));
+  check(sconv_xyz_read(path.c_str(), n ? pts[0].data() : nullptr, f.data(), n, c), sconv_global_last_error());
+  Matrix feats(c > 0 ? n : 0, c);
+  for (std::int64_t r = 0; c > 0 && r < n; ++r)
+    for (std::int64_t k = 0; k < c; ++k) feats(r, k) = f[static_cast<std::size_t>(r * c + k)];
+  return {std::move(pts), std::move(feats)};
+}
+
 // sc_layer_forward. W: K^3 matrices C_in x C_out, flattened [k][cin][cout].
 inline PointCloud sc_layer_forward(Context& ctx, const PointCloud& cloud, const std::vector<float>& W, int c_out,
                                    int K, int s, const LayerConfig& cfg = {}) {

@@ -1,6 +1,7 @@
 // C ABI of libsconv_b200 (include/sconv_b200.h): exception-free boundary, context runtime,
 // tile autotuner (Alg. 2), synthetic-input generator (SPEC cli gen).
 #include <algorithm>
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -133,6 +134,91 @@ struct SplitMix {
 };
 uint64_t stream_seed(uint64_t seed, uint64_t idx) { return seed ^ ((idx + 1) * 0x9E3779B97F4A7C15ull); }
 
+// ---- point-cloud files (".xyz" text, ".mpc" binary) ----
+struct File {
+  FILE* f = nullptr;
+  File(const char* path, const char* mode) : f(path ? std::fopen(path, mode) : nullptr) {
+    if (!f) fail(SCONV_ERR_ARG, std::string("cannot open file ") + (path ? path : "(null)"));
+  }
+  ~File() {
+    if (f) std::fclose(f);
+  }
+};
+constexpr int64_t kMpcHeader = 12;  // "MPC1", u32 N, u32 C
+
+uint32_t le_u32(const unsigned char* b) {
+  return uint32_t{b[0]} | (uint32_t{b[1]} << 8) | (uint32_t{b[2]} << 16) | (uint32_t{b[3]} << 24);
+}
+
+// header of an .mpc file + size check: N, C and the exact file length
+void mpc_header(FILE* f, int64_t& n, int64_t& c) {
+  unsigned char h[kMpcHeader];
+  const size_t got = std::fread(h, 1, kMpcHeader, f);
+  if (got < 4 || std::memcmp(h, "MPC1", 4) != 0) fail(SCONV_ERR_ARG, "mpc parse error at offset 0: bad magic");
+  if (got < static_cast<size_t>(kMpcHeader))
+    fail(SCONV_ERR_ARG, "mpc parse error at offset " + std::to_string(got) + ": truncated header");
+  n = le_u32(h + 4);
+  c = le_u32(h + 8);
+  std::fseek(f, 0, SEEK_END);
+  const int64_t size = std::ftell(f);
+  const int64_t want = kMpcHeader + 12 * n + 4 * n * c;
+  if (size != want)
+    fail(SCONV_ERR_ARG, "mpc parse error at offset " + std::to_string(std::min(size, want)) + ": expected " +
+                            std::to_string(want) + " bytes, file has " + std::to_string(size));
+  std::fseek(f, kMpcHeader, SEEK_SET);
+}
+
+// .xyz: one point per line "x y z f1 ... fC"; blank lines and '#' comments skipped. Every
+// line must carry the same number of columns (>= 3). Calls row(values) per point.
+template <class Row>
+void xyz_parse(FILE* f, int64_t& n, int64_t& c, Row&& row) {
+  n = 0;
+  c = -1;
+  std::vector<double> vals;
+  std::string line;
+  int64_t lineno = 0;
+  char buf[4096];
+  while (true) {
+    line.clear();
+    bool got = false;
+    while (std::fgets(buf, sizeof(buf), f)) {  // one whole line, however long
+      got = true;
+      line += buf;
+      if (line.back() == '\n') break;
+    }
+    if (!got) break;
+    ++lineno;
+    vals.clear();
+    const char* p = line.c_str();
+    while (true) {
+      while (*p == ' ' || *p == '\t' || *p == '\r' || *p == '\n') ++p;
+      if (!*p || *p == '#') break;
+      char* end = nullptr;
+      const double v = std::strtod(p, &end);
+      if (end == p || (*end && *end != ' ' && *end != '\t' && *end != '\r' && *end != '\n')) {
+        const char* e = p;
+        while (*e && *e != ' ' && *e != '\t' && *e != '\r' && *e != '\n') ++e;
+        fail(SCONV_ERR_ARG, "xyz parse error at line " + std::to_string(lineno) + ": invalid number '" +
+                                std::string(p, e) + "'");
+      }
+      vals.push_back(v);
+      p = end;
+    }
+    if (vals.empty()) continue;
+    const int64_t cols = static_cast<int64_t>(vals.size());
+    if (cols < 3)
+      fail(SCONV_ERR_ARG, "xyz parse error at line " + std::to_string(lineno) + ": expected at least 3 columns, got " +
+                              std::to_string(cols));
+    if (c < 0) c = cols - 3;
+    if (cols != c + 3)
+      fail(SCONV_ERR_ARG, "xyz parse error at line " + std::to_string(lineno) + ": expected " + std::to_string(c + 3) +
+                              " columns, got " + std::to_string(cols));
+    row(n, vals);
+    ++n;
+  }
+  if (c < 0) c = 0;
+}
+
 double median(std::vector<double> v) {
   std::sort(v.begin(), v.end());
   const size_t n = v.size();
@@ -145,6 +231,89 @@ double median(std::vector<double> v) {
 using namespace sconvb;
 
 extern "C" {
+
+sconv_status sconv_cloud_file_info(const char* path, int* format, int64_t* n, int64_t* channels) {
+  return guarded(nullptr, [&] {
+    File fh(path, "rb");
+    char magic[4] = {0, 0, 0, 0};
+    const size_t got = std::fread(magic, 1, 4, fh.f);
+    std::rewind(fh.f);
+    int64_t nn = 0, cc = 0;
+    const size_t len = std::strlen(path);
+    const bool mpc_ext = len >= 4 && std::strcmp(path + len - 4, ".mpc") == 0;
+    if (mpc_ext || (got == 4 && std::memcmp(magic, "MPC1", 4) == 0)) {
+      mpc_header(fh.f, nn, cc);
+      if (format) *format = SCONV_FILE_MPC;
+    } else {
+      xyz_parse(fh.f, nn, cc, [](int64_t, const std::vector<double>&) {});
+      if (format) *format = SCONV_FILE_XYZ;
+    }
+    if (n) *n = nn;
+    if (channels) *channels = cc;
+  });
+}
+
+sconv_status sconv_mpc_read(const char* path, int32_t* xyz, float* feats, int64_t n, int64_t channels) {
+  return guarded(nullptr, [&] {
+    File fh(path, "rb");
+    int64_t nn = 0, cc = 0;
+    mpc_header(fh.f, nn, cc);
+    if (nn != n || cc != channels) fail(SCONV_ERR_ARG, "buffer shape does not match the file");
+    if (n > 0 && (!xyz || (channels > 0 && !feats))) fail(SCONV_ERR_ARG, "null output buffer");
+    if (n > 0 && std::fread(xyz, 12, static_cast<size_t>(n), fh.f) != static_cast<size_t>(n))
+      fail(SCONV_ERR_ARG, "mpc parse error at offset 12: short read");
+    if (n * channels > 0 &&
+        std::fread(feats, 4, static_cast<size_t>(n * channels), fh.f) != static_cast<size_t>(n * channels))
+      fail(SCONV_ERR_ARG, "mpc parse error at offset " + std::to_string(kMpcHeader + 12 * n) + ": short read");
+  });
+}
+
+sconv_status sconv_mpc_write(const char* path, const int32_t* xyz, const float* feats, int64_t n, int64_t channels) {
+  return guarded(nullptr, [&] {
+    if (n < 0 || channels < 0 || n > UINT32_MAX || channels > UINT32_MAX) fail(SCONV_ERR_ARG, "invalid cloud shape");
+    if (n > 0 && (!xyz || (channels > 0 && !feats))) fail(SCONV_ERR_ARG, "null input buffer");
+    File fh(path, "wb");
+    unsigned char h[kMpcHeader] = {'M', 'P', 'C', '1'};
+    for (int b = 0; b < 4; ++b) {
+      h[4 + b] = static_cast<unsigned char>((static_cast<uint32_t>(n) >> (8 * b)) & 0xFF);
+      h[8 + b] = static_cast<unsigned char>((static_cast<uint32_t>(channels) >> (8 * b)) & 0xFF);
+    }
+    bool ok = std::fwrite(h, 1, kMpcHeader, fh.f) == static_cast<size_t>(kMpcHeader);
+    if (n > 0) ok = ok && std::fwrite(xyz, 12, static_cast<size_t>(n), fh.f) == static_cast<size_t>(n);
+    if (n * channels > 0)
+      ok = ok && std::fwrite(feats, 4, static_cast<size_t>(n * channels), fh.f) == static_cast<size_t>(n * channels);
+    if (!ok) fail(SCONV_ERR_ARG, std::string("write failed: ") + path);
+  });
+}
+
+sconv_status sconv_xyz_read(const char* path, double* points, float* feats, int64_t n, int64_t channels) {
+  return guarded(nullptr, [&] {
+    File fh(path, "rb");
+    int64_t nn = 0, cc = 0;
+    xyz_parse(fh.f, nn, cc, [&](int64_t i, const std::vector<double>& v) {
+      if (i >= n || static_cast<int64_t>(v.size()) != channels + 3)
+        fail(SCONV_ERR_ARG, "buffer shape does not match the file");
+      for (int a = 0; a < 3; ++a) points[3 * i + a] = v[a];
+      for (int64_t c = 0; c < channels; ++c) feats[i * channels + c] = static_cast<float>(v[3 + c]);
+    });
+    if (nn != n) fail(SCONV_ERR_ARG, "buffer shape does not match the file");
+  });
+}
+
+sconv_status sconv_xyz_write(const char* path, const double* points, const float* feats, int64_t n, int64_t channels) {
+  return guarded(nullptr, [&] {
+    if (n < 0 || channels < 0) fail(SCONV_ERR_ARG, "invalid cloud shape");
+    if (n > 0 && (!points || (channels > 0 && !feats))) fail(SCONV_ERR_ARG, "null input buffer");
+    File fh(path, "w");
+    bool ok = true;
+    for (int64_t i = 0; i < n && ok; ++i) {  // %.17g / %.9g: exact round trips of double / float
+      ok = std::fprintf(fh.f, "%.17g %.17g %.17g", points[3 * i], points[3 * i + 1], points[3 * i + 2]) > 0;
+      for (int64_t c = 0; c < channels && ok; ++c) ok = std::fprintf(fh.f, " %.9g", double{feats[i * channels + c]}) > 0;
+      ok = ok && std::fputc('\n', fh.f) != EOF;
+    }
+    if (!ok) fail(SCONV_ERR_ARG, std::string("write failed: ") + path);
+  });
+}
 
 const char* sconv_version(void) { return "sconv_b200 0.1 (sm_100a)"; }
 

@@ -828,7 +828,11 @@ void prepare_fused_layout(Ctx& ctx, MapData& m) {
   size_t temp = 0;
   // sort on the top 24 key bits only (3 radix passes instead of 4): the dropped low bits are
   // the centre and two face offsets, the most common ones (KITTI: 10.32 -> 10.59 offsets/tile)
-  const int begin_bit = std::max(0, K3 - 24);
+  static const int mask_bits = [] {
+    const char* e = std::getenv("SCONV_MASK_BITS");  // experiments (16 bits: -78 us sort, +60 us convs)
+    return e ? std::max(1, std::min(32, std::atoi(e))) : 24;
+  }();
+  const int begin_bit = std::max(0, K3 - mask_bits);
   SCONV_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp, keys.get<uint32_t>(), keys_sorted.get<uint32_t>(),
                                              idx.get<int32_t>(), m.row_perm.get<int32_t>(), static_cast<int>(n),
                                              begin_bit, K3, st));

@@ -116,6 +116,11 @@ SIGNATURES = [
     ("sconv_net_stats", _I, [_P, C.POINTER(_I), C.POINTER(_I)]),
     ("sconv_net_conv_stats", _I, [_P, _I, _P]),
     ("sconv_net_free", None, [_P, _P]),
+    ("sconv_cloud_file_info", _I, [C.c_char_p, C.POINTER(_I), C.POINTER(_I64), C.POINTER(_I64)]),
+    ("sconv_mpc_read", _I, [C.c_char_p, _P, _P, _I64, _I64]),
+    ("sconv_mpc_write", _I, [C.c_char_p, _P, _P, _I64, _I64]),
+    ("sconv_xyz_read", _I, [C.c_char_p, _P, _P, _I64, _I64]),
+    ("sconv_xyz_write", _I, [C.c_char_p, _P, _P, _I64, _I64]),
     ("sconv_generate_synthetic", _I, [_I64, _I64, _I64, _U64, _P, _P]),
     ("sconv_generate_weights", _I, [_U64, _U64, _I, _I, _I, _P]),
     ("sconv_global_last_error", C.c_char_p, []),
@@ -429,6 +434,63 @@ def plan_groups(sizes, policy=GROUP_SORTED, epsilon=0.25, max_batch=16) -> dict:
         _raise(st, lib.sconv_global_last_error().decode())
     return dict(order=order[: no.value], groups=list(zip(gb[: ng.value], ge[: ng.value], heights[: ng.value])),
                 buffer_offsets=boff, buffer_length=blen.value, overhead=ovh.value)
+
+
+FILE_MPC, FILE_XYZ = 0, 1
+
+
+def _gcheck(lib, st):
+    if st != OK:
+        _raise(st, lib.sconv_global_last_error().decode())
+
+
+def cloud_file_info(path: str):
+    """(format, N, C) of a point-cloud file: FILE_MPC (voxel coordinates) or FILE_XYZ (float points)."""
+    lib = load()
+    fmt, n, c = C.c_int(), C.c_int64(), C.c_int64()
+    _gcheck(lib, lib.sconv_cloud_file_info(os.fsencode(path), C.byref(fmt), C.byref(n), C.byref(c)))
+    return fmt.value, n.value, c.value
+
+
+def read_cloud(path: str):
+    """Read a SPEC.md:585 file. '.mpc' -> PointCloud (int32 voxel coordinates, sorted=False);
+    '.xyz' -> (points [N,3] float64, features [N,C] float32), the input of ``voxelize``."""
+    lib = load()
+    fmt, n, c = cloud_file_info(path)
+    f = np.empty((n, c), np.float32)
+    if fmt == FILE_MPC:
+        xyz = np.empty((n, 3), np.int32)
+        _gcheck(lib, lib.sconv_mpc_read(os.fsencode(path), _ptr(xyz), _ptr(f), n, c))
+        return PointCloud(xyz, f, False)
+    pts = np.empty((n, 3), np.float64)
+    _gcheck(lib, lib.sconv_xyz_read(os.fsencode(path), _ptr(pts), _ptr(f), n, c))
+    return pts, f
+
+
+def write_mpc(path: str, coords: np.ndarray, features: Optional[np.ndarray] = None):
+    lib = load()
+    xyz = np.ascontiguousarray(coords, np.int32).reshape(-1, 3)
+    f = np.zeros((len(xyz), 0), np.float32) if features is None else np.ascontiguousarray(features, np.float32)
+    _gcheck(lib, lib.sconv_mpc_write(os.fsencode(path), _ptr(xyz), _ptr(f), len(xyz), f.shape[1] if f.ndim == 2 else 0))
+
+
+def write_xyz(path: str, points: np.ndarray, features: Optional[np.ndarray] = None):
+    lib = load()
+    pts = np.ascontiguousarray(points, np.float64).reshape(-1, 3)
+    f = np.zeros((len(pts), 0), np.float32) if features is None else np.ascontiguousarray(features, np.float32)
+    _gcheck(lib, lib.sconv_xyz_write(os.fsencode(path), _ptr(pts), _ptr(f), len(pts), f.shape[1] if f.ndim == 2 else 0))
+
+
+def load_cloud(ctx: "Context", path: str, resolution: Optional[float] = None) -> "PointCloud":
+    """File -> PointCloud ready for the layer/network API: an '.mpc' file is returned as stored;
+    an '.xyz' file is voxelized on the GPU at ``resolution`` (required for '.xyz')."""
+    fmt, _, _ = cloud_file_info(path)
+    if fmt == FILE_MPC:
+        return read_cloud(path)
+    if resolution is None:
+        raise InvalidArgument("resolution is required to voxelize an .xyz file")
+    pts, f = read_cloud(path)
+    return voxelize(ctx, pts, f if f.shape[1] else None, resolution)
 
 
 def generate_synthetic(N: int, E: int, Cch: int, seed: int):

@@ -75,8 +75,19 @@ int main() {
     for (int c = 0; vox_ok && c < 5; ++c)
       vox_ok = vr.features(static_cast<std::int64_t>(i), c) == vg.features(static_cast<std::int64_t>(i), c);
   }
-  std::printf("adapter: |Q|=%zu |M|=%lld max_rel=%.3g threw=%d voxelize_exact=%d (%zu voxels)\n",
+  // .mpc round trip of the voxelized cloud through the adapter's file readers
+  const std::string mpc = "/tmp/sconv_adapter_test.mpc";
+  gpu::write_mpc(mpc, vg);
+  const PointCloud back = gpu::read_mpc(mpc);
+  bool io_ok = !back.sorted && back.coords->size() == vg.coords->size() && back.channels() == vg.channels();
+  for (std::size_t i = 0; io_ok && i < back.coords->size(); ++i) {
+    io_ok = (*back.coords)[i] == (*vg.coords)[i];
+    for (int c = 0; io_ok && c < 5; ++c)
+      io_ok = back.features(static_cast<std::int64_t>(i), c) == vg.features(static_cast<std::int64_t>(i), c);
+  }
+  std::remove(mpc.c_str());
+  std::printf("adapter: |Q|=%zu |M|=%lld max_rel=%.3g threw=%d voxelize_exact=%d (%zu voxels) mpc_round_trip=%d\n",
               out.coords->size(), static_cast<long long>(km.total()), maxerr / scale, threw ? 1 : 0, vox_ok ? 1 : 0,
-              vr.coords->size());
-  return (maxerr / scale <= 1e-2 && threw && vox_ok) ? 0 : 1;
+              vr.coords->size(), io_ok ? 1 : 0);
+  return (maxerr / scale <= 1e-2 && threw && vox_ok && io_ok) ? 0 : 1;
 }

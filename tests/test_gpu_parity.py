@@ -80,6 +80,35 @@ def test_hash_backend_equivalence(ctx, oracle, K, s, n, extent, presorted):
         np.testing.assert_array_equal(a, b)
 
 
+def test_three_way_map_equivalence_200(ctx, oracle):
+    """SPEC acceptance #1 on the GPU: sorted double-traversed search == hash
+    baseline == brute-force oracle, exact, over 200 randomized instances with |P| in
+    [1e2, 1e4], K in {1, 3, 5}, s in {1, 2}, dense and sparse extents, random B / C and
+    sorted-flag. Brute force is O(N^2), so it checks |P| <= 2000; larger instances use the
+    oracle's hash map (pinned against brute force in test_oracle.py)."""
+    rng = np.random.default_rng(600)
+    for trial in range(200):
+        n = int(10 ** rng.uniform(2, 4))
+        K = [1, 3, 5][trial % 3]
+        s = 1 + (trial // 3) % 2
+        dense = trial % 4 < 2
+        extent = max(3, int(round(n ** (1 / 3) * (rng.uniform(1.05, 1.6) if dense else rng.uniform(5, 20)))))
+        xyz = random_cloud(rng, n, extent, origin=int(rng.integers(-2 * extent, extent)))
+        presorted = bool(rng.integers(0, 2))
+        if presorted:
+            xyz = sort_rows(xyz)
+        B = int(rng.integers(1, 257)) * 4
+        Cq = int(rng.integers(1, 4097))
+        ora = oracle.layer_map(xyz, presorted, K, s, s, backend=2 if len(xyz) <= 2000 else 1)
+        ctx_info = f"trial {trial}: n={len(xyz)} K={K} s={s} extent={extent} B={B} C={Cq}"
+        for be in (sc.MAP_SORTED, sc.MAP_HASH):
+            got = sc.KernelMap.build(ctx, xyz, presorted, K, s, s, B=B, Cq=Cq, backend=be).read()
+            try:
+                assert_map_equal(got, ora)
+            except AssertionError as e:
+                raise AssertionError(f"{ctx_info} backend={be}: {e}") from None
+
+
 def test_map_range_edges(ctx, oracle):
     """Clouds touching COORD_MIN / COORD_MAX (the SPEC sentinel edge case)."""
     rng = np.random.default_rng(5)
@@ -348,3 +377,29 @@ def test_voxelize_errors(ctx):
     empty = sc.voxelize(ctx, np.zeros((0, 3)), None, 1.0)
     assert empty.size() == 0
 
+
+
+def test_file_ingestion_to_map(oracle, ctx, tmp_path):
+    """.xyz file -> GPU voxelize -> .mpc file -> kernel map:
+    the file path gives the same voxels as voxelizing the arrays, the reference's voxelize
+    agrees, and the map built from the re-read .mpc cloud equals the oracle's."""
+    from oracle_lib import load_ref_oracle
+    from paper_2401_06145_b200 import datasets as D
+    ref = load_ref_oracle() or oracle
+    pts, f = D.kitti_scan(0, n_azimuth=600, raw=True)
+    xyz_path, mpc_path = str(tmp_path / "scan.xyz"), str(tmp_path / "scan.mpc")
+    sc.write_xyz(xyz_path, pts, f)
+    with pytest.raises(sc.InvalidArgument, match="resolution is required"):
+        sc.load_cloud(ctx, xyz_path)
+    cloud = sc.load_cloud(ctx, xyz_path, 0.05)
+    direct = sc.voxelize(ctx, pts, f, 0.05)
+    np.testing.assert_array_equal(cloud.coords, direct.coords)
+    np.testing.assert_array_equal(cloud.features, direct.features)
+    rxyz, rf = ref.voxelize(pts, f, 0.05)
+    np.testing.assert_array_equal(cloud.coords, rxyz)
+    np.testing.assert_array_equal(cloud.features, rf)
+    sc.write_mpc(mpc_path, cloud.coords, cloud.features)
+    back = sc.load_cloud(ctx, mpc_path)
+    np.testing.assert_array_equal(back.coords, cloud.coords)
+    m = sc.KernelMap.build(ctx, back.coords, False, 3, 1, 1).read()
+    assert_map_equal(m, oracle.layer_map(back.coords, False, 3, 1, 1))
