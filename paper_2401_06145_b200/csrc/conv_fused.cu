@@ -217,11 +217,16 @@ __global__ void __launch_bounds__(kThreads, NK == 0 ? 4 : 2) k_conv_fused(const 
 
   if (REG && warp < 4) {
     // ------------------------------------------------------------ gather producers, register indices
-    // Thread tid owns tile row tid: its K3 input-row indices are loaded into registers at the
-    // tile start (independent LDGs) and never go through shared memory. Copy instruction q of
-    // warp w covers rows 32w + lane/CPR + q*(32/CPR) (whole rows, coalesced); lanes get the
-    // row indices from the owner lane by shuffle.
+    // Thread tid owns tile row tid: its K3 input-row indices are loaded at the tile start
+    // (independent LDGs, all in flight together) and published to the warp's own columns of
+    // the index table (no CTA barrier: only the same warp reads them). Copy instruction q of
+    // warp w covers rows 32w + lane/CPR + q*(32/CPR) (whole rows, coalesced); the offset loop
+    // visits only the tile's active offsets (set bits of the mask).
     constexpr int CPR = KC / 8, RPI = 32 / CPR;
+    // KC <= 32 (narrow chunks, 1-2 rows per copy instruction): row indices through the warp's
+    // columns of the shared index table, offset loop over set mask bits only. KC = 64: register
+    // rotation (the table variant measured slower there, though within run-to-run noise).
+    constexpr bool kTable = KC <= 32;
     constexpr int NR = NK > 0 ? NK : 1;
     const int tid = threadIdx.x;
     const int chunk = lane % CPR, rsub = lane / CPR;
@@ -238,7 +243,18 @@ __global__ void __launch_bounds__(kThreads, NK == 0 ? 4 : 2) k_conv_fused(const 
       s_tq[0] = grab();
     }
     named_bar(1, kProducers);
-    int t = s_tq[0];
+    int t = s_tq[0], t_next = -1;
+    // table variant: row indices one tile ahead, the next tile's LDGs in flight during this
+    // tile's gathers (the queue look-ahead stays one tile deep: deeper reservations unbalance the densest-first
+    // queue when a layer has only 1-3 tiles per CTA)
+    int jn[NR];
+    auto load_rows = [&](int tt) {
+      const int64_t i = static_cast<int64_t>(tt / p.n_blocks) * 128 + tid;
+      const bool ok = i < p.n_out;
+#pragma unroll
+      for (int k = 0; k < NR; ++k) jn[k] = ok ? __ldg(p.nbr + int64_t{k} * p.n_out + i) : -1;
+    };
+    if (kTable && t >= 0) load_rows(t);
     int stage = 0;
     uint32_t phase = 0;
     const uint32_t smem_base = smem_u32(smem);
@@ -248,22 +264,24 @@ __global__ void __launch_bounds__(kThreads, NK == 0 ? 4 : 2) k_conv_fused(const 
       if (it > 0) named_bar(1, kProducers);
       if (tid == 0) s_tq[(it + 1) & 3] = grab();
       const int nb = t % p.n_blocks;
+      if (!kTable) load_rows(t);  // rotation variant: no look-ahead (measured slower at 96 regs)
       int jc[NR];
-      {
-        const int64_t i = static_cast<int64_t>(t / p.n_blocks) * 128 + tid;
-        const bool ok = i < p.n_out;
 #pragma unroll
-        for (int k = 0; k < NR; ++k) jc[k] = ok ? __ldg(p.nbr + int64_t{k} * p.n_out + i) : -1;
-      }
+      for (int k = 0; k < NR; ++k) jc[k] = jn[k];
       uint64_t mine = 0;
 #pragma unroll
-      for (int k = 0; k < NR; ++k) mine |= static_cast<uint64_t>(jc[k] >= 0) << k;
+      for (int k = 0; k < NR; ++k) {
+        mine |= static_cast<uint64_t>(jc[k] >= 0) << k;
+        if constexpr (kTable) s_idx[k * 128 + tid] = jc[k];  // this warp's rows only: read back by the same warp
+      }
       const uint32_t lo = __reduce_or_sync(0xFFFFFFFFu, static_cast<uint32_t>(mine));
       const uint32_t hi = __reduce_or_sync(0xFFFFFFFFu, static_cast<uint32_t>(mine >> 32));
       if (lane == 0) s_part[buf * 4 + warp] = (static_cast<uint64_t>(hi) << 32) | lo;
       named_bar(1, kProducers);
       uint64_t mask = s_part[buf * 4] | s_part[buf * 4 + 1] | s_part[buf * 4 + 2] | s_part[buf * 4 + 3];
       if (mask == 0) mask = 1;
+      t_next = s_tq[(it + 1) & 3];  // published by the barrier above
+      if (kTable && t_next >= 0) load_rows(t_next);
       if (tid == 0) {
         const int slot = it % kInfo;
         mbar_wait(&iempty[slot], ((it / kInfo) & 1) ^ 1);
@@ -274,15 +292,26 @@ __global__ void __launch_bounds__(kThreads, NK == 0 ? 4 : 2) k_conv_fused(const 
       const int b_row0 = nb * p.block_n;
       int units_left = __popcll(mask) * p.num_kb, in_stage = 0, stage_units = 0;
       uint32_t slot32 = 0;
+      const int32_t* wrow = s_idx + 32 * warp + rsub;  // published before the named barrier above
+      uint64_t mm = mask;
 #pragma unroll 1
-      for (int k = 0; k < NR; ++k) {
-        const int32_t jk = jc[0];
-#pragma unroll
-        for (int r = 0; r + 1 < NR; ++r) jc[r] = jc[r + 1];
-        if (!((mask >> k) & 1)) continue;
+      for (int kk = 0; kTable ? mm != 0 : kk < NR; ++kk) {
+        int k;
         int32_t j[CPR];
+        if constexpr (kTable) {  // visit only the active offsets; indices from the warp's table
+          k = __ffsll(static_cast<long long>(mm)) - 1;
+          mm &= mm - 1;
 #pragma unroll
-        for (int q = 0; q < CPR; ++q) j[q] = __shfl_sync(0xFFFFFFFFu, jk, rsub + q * RPI);
+          for (int q = 0; q < CPR; ++q) j[q] = wrow[k * 128 + q * RPI];
+        } else {  // rotate the register array (no dynamic indexing), skip inactive offsets
+          k = kk;
+          const int32_t jk = jc[0];
+#pragma unroll
+          for (int r = 0; r + 1 < NR; ++r) jc[r] = jc[r + 1];
+          if (!((mask >> k) & 1)) continue;
+#pragma unroll
+          for (int q = 0; q < CPR; ++q) j[q] = __shfl_sync(0xFFFFFFFFu, jk, rsub + q * RPI);
+        }
         const int b_row = k * p.n_pad + b_row0;
         for (int kb = 0; kb < p.num_kb; ++kb) {
           if (in_stage == 0) {
@@ -309,7 +338,7 @@ __global__ void __launch_bounds__(kThreads, NK == 0 ? 4 : 2) k_conv_fused(const 
           }
         }
       }
-      t = s_tq[(it + 1) & 3];
+      t = t_next;
     }
     if (tid == 0) {
       const int slot = it % kInfo;
@@ -441,7 +470,6 @@ __global__ void __launch_bounds__(kThreads, NK == 0 ? 4 : 2) k_conv_fused(const 
         }
       }
       t = t_next;
-      t_next = s_tq[(it + 2) & 3];
     }
     if (tid == 0) {  // end-of-work marker for the MMA and the epilogue
       const int slot = it % kInfo;
