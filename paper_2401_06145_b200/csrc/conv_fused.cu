@@ -133,7 +133,7 @@ struct MaskOrder {
 struct FusedParams {
   const unsigned char* f_in;
   int64_t ld_in_bytes;
-  const int32_t* nbr;   // [K3][n_out] in tile-row order
+  const int32_t* nbr;   // [K3][n_out] in tile-row order (null: the 1x1 identity map, nbr[0][i] = i)
   const int32_t* perm;  // tile row -> output row (null: identity)
   int64_t n_out;
   int K3, num_kb, block_n, n_pad, n_blocks, num_tiles, c_out;
@@ -167,6 +167,15 @@ __device__ __forceinline__ void trace_ev(const FusedParams& p, int kind, int seq
                                  (static_cast<unsigned long long>(seq & 0xFFFFFF) << 32) | (t & 0xFFFFFFFFull);
     ++n;
   }
+}
+
+// input row of output i at offset k; a null table (only with K3 = 1: the 1x1 identity map) is
+// nbr[0][i] = i. The check is compiled into the NK = 1 (and runtime-K3) kernels only.
+template <int NK>
+__device__ __forceinline__ int32_t nbr_at(const FusedParams& p, int k, int64_t i) {
+  if constexpr (NK == 1 || NK == 0)
+    if (!p.nbr) return static_cast<int32_t>(i);
+  return __ldg(p.nbr + int64_t{k} * p.n_out + i);
 }
 
 // NK = compile-time offset count (registers prefetch the next tile's index rows), 0 = runtime
@@ -252,7 +261,7 @@ __global__ void __launch_bounds__(kThreads, NK == 0 ? 4 : 2) k_conv_fused(const 
       const int64_t i = static_cast<int64_t>(tt / p.n_blocks) * 128 + tid;
       const bool ok = i < p.n_out;
 #pragma unroll
-      for (int k = 0; k < NR; ++k) jn[k] = ok ? __ldg(p.nbr + int64_t{k} * p.n_out + i) : -1;
+      for (int k = 0; k < NR; ++k) jn[k] = ok ? nbr_at<NK>(p, k, i) : -1;
     };
     if (kTable && t >= 0) load_rows(t);
     int stage = 0;
@@ -364,7 +373,7 @@ __global__ void __launch_bounds__(kThreads, NK == 0 ? 4 : 2) k_conv_fused(const 
       const int64_t i = static_cast<int64_t>(t / p.n_blocks) * 128 + tid;
       const bool ok = i < p.n_out;
 #pragma unroll
-      for (int k = 0; k < NR; ++k) jn[k] = ok ? __ldg(p.nbr + int64_t{k} * p.n_out + i) : -1;
+      for (int k = 0; k < NR; ++k) jn[k] = ok ? nbr_at<NK>(p, k, i) : -1;
     };
     // Dynamic tile queue (global atomic counter), dispensed densest-first: row blocks are in
     // neighbour-mask order, so the last blocks carry the most active offsets; handing them out
@@ -402,7 +411,7 @@ __global__ void __launch_bounds__(kThreads, NK == 0 ? 4 : 2) k_conv_fused(const 
       } else {
         const int64_t i = static_cast<int64_t>(t / p.n_blocks) * 128 + tid;
         for (int k = 0; k < K3; ++k) {
-          const int32_t j = i < p.n_out ? __ldg(p.nbr + int64_t{k} * p.n_out + i) : -1;
+          const int32_t j = i < p.n_out ? nbr_at<NK>(p, k, i) : -1;
           srow[k * 128 + tid] = j;
           mine |= static_cast<uint64_t>(j >= 0) << k;
         }

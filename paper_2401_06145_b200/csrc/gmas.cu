@@ -699,7 +699,7 @@ void fused_forward(Ctx& ctx, MapData& m, const WeightData& w, const LayerIO& io)
   a.ld_in = ld;
   a.n_in = m.n_in;
   prepare_fused_layout(ctx, m);
-  a.nbr = m.permuted ? m.nbr_perm.get<int32_t>() : m.nbr_in.get<int32_t>();
+  a.nbr = m.identity_pending ? nullptr : (m.permuted ? m.nbr_perm.get<int32_t>() : m.nbr_in.get<int32_t>());
   a.perm = m.permuted ? m.row_perm.get<int32_t>() : nullptr;
   a.n_out = m.n_out;
   a.w = &w;

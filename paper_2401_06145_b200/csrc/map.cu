@@ -306,12 +306,28 @@ __global__ void k_floor_bbox(const uint64_t* __restrict__ src, const int32_t* __
       mn[a] = min(mn[a], __shfl_xor_sync(0xFFFFFFFFu, mn[a], o));
       mx[a] = max(mx[a], __shfl_xor_sync(0xFFFFFFFFu, mx[a], o));
     }
-  if ((threadIdx.x & 31) == 0 && mn[0] != INT_MAX)
+  // block reduction first: one atomic per bound per CTA, not per warp (same-address atomics
+  // serialise in L2: ~22k of them per 1.2e5-point layer took 11.7 us)
+  __shared__ int s_box[32][6];
+  const int warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  if ((threadIdx.x & 31) == 0)
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-      atomicMin(&flags->fbox[a], mn[a]);
-      atomicMax(&flags->fbox[3 + a], mx[a]);
+      s_box[warp][a] = mn[a];
+      s_box[warp][3 + a] = mx[a];
     }
+  __syncthreads();
+  if (threadIdx.x < 6) {
+    const int a = threadIdx.x;
+    int v = s_box[0][a];
+    for (int w = 1; w < nw; ++w) v = a < 3 ? min(v, s_box[w][a]) : max(v, s_box[w][a]);
+    if (a < 3 ? v != INT_MAX : v != INT_MIN) {
+      if (a < 3)
+        atomicMin(&flags->fbox[a], v);
+      else
+        atomicMax(&flags->fbox[a], v);
+    }
+  }
 }
 
 // floored packed key -> left-aligned... (right-aligned) compact u32 key (x, y, z offsets in units of
@@ -853,7 +869,19 @@ void read_starts(Ctx& ctx, MapData& m, const void* flags, MapFlags* f) {
 }
 }  // namespace
 
+void launch_identity(Ctx& ctx, MapData& m) {
+  if (!m.identity_pending) return;
+  m.identity_pending = false;
+  const int64_t n = m.n_out;
+  ctx.launch("k_identity_map", [&] {
+    k_identity_map<<<grid_for(n), kThreads, 0, ctx.stream>>>(n, m.nbr_in.get<int32_t>(), m.nbr_pos.get<int32_t>(),
+                                                             m.pair_in.get<int32_t>(), m.pair_out.get<int32_t>(),
+                                                             m.map_start.get<int32_t>());
+  });
+}
+
 void ensure_canonical(Ctx& ctx, MapData& m) {
+  launch_identity(ctx, m);
   if (m.canonical) return;
   if (m.pending.grid > 0) launch_canonical(ctx, m);
   MapFlags f;
@@ -1121,11 +1149,8 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
     // identity map (1x1 conv on the same sorted coordinates): no search, sizes known on the host
     m->pair_in.alloc(sizeof(int32_t) * n, st);
     m->pair_out.alloc(sizeof(int32_t) * n, st);
-    ctx.launch("k_identity_map", [&] {
-      k_identity_map<<<grid_for(n), kThreads, 0, st>>>(n, m->nbr_in.get<int32_t>(), m->nbr_pos.get<int32_t>(),
-                                                       m->pair_in.get<int32_t>(), m->pair_out.get<int32_t>(),
-                                                       m->map_start.get<int32_t>());
-    });
+    m->identity_pending = true;  // the fused kernel reads a null table as identity
+    if (!lazy) launch_identity(ctx, *m);
     m->starts = {0, static_cast<int32_t>(n)};
     m->sizes = {n};
     m->total = n;
