@@ -624,6 +624,167 @@ __global__ void k_mask_keys(const int32_t* __restrict__ nbr, int64_t n, int K3, 
   idx[i] = static_cast<int32_t>(i);
 }
 
+// ---------------------------------------------------------------- one-launch mask sort
+// The neighbour-mask permutation of a submanifold map in ONE cooperative launch instead of
+// mask kernel + CUB radix sort (histogram, scan, 3 onesweep passes) + permute kernel: every
+// one of those is latency bound at these sizes (~70 us per map whatever n). Stable LSD radix
+// sort of the 24 mask bits [begin_bit, begin_bit + 24) in three 8-bit passes, keys and values
+// in registers (tile of <= 256 * kSortMaxE rows per CTA), grid barriers between the phases:
+//   rank     stable rank of each row among its tile's rows with the same digit (warp match +
+//            per-warp digit counts, tile order = element e of thread t at e*256 + t)
+//   hist     tile digit counts -> cnt[digit][tile]          | grid barrier
+//   scan     per-digit exclusive scan across tiles + totals  | grid barrier
+//   scatter  pos = base[digit] + cnt[digit][tile] + rank; the last pass writes the row
+//            permutation and the permuted neighbour table (k_permute_nbr fused in; measured
+//            faster than a coalesced grid-stride copy after one more barrier)
+// Same bits, same stability as the CUB path => the identical permutation.
+constexpr int kSortThreads = 256, kSortMaxE = 4;
+
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks, unsigned& target) {
+  __syncthreads();
+  target += nblocks;  // barrier b of this launch completes at (b + 1) * nblocks arrivals
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1u);
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+    } while (v < target);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// exclusive scan of one int per thread over the CTA (kSortThreads threads); returns the total
+__device__ __forceinline__ int block_exclusive_scan(int v, int& excl, int* s_wsum) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int u = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if (lane >= o) incl += u;
+  }
+  if (lane == 31) s_wsum[warp] = incl;
+  __syncthreads();
+  int wp = 0, total = 0;
+#pragma unroll
+  for (int w = 0; w < kSortThreads / 32; ++w) {
+    wp += w < warp ? s_wsum[w] : 0;
+    total += s_wsum[w];
+  }
+  __syncthreads();
+  excl = wp + incl - v;
+  return total;
+}
+
+__global__ void __launch_bounds__(kSortThreads) k_mask_sort(
+    const int32_t* __restrict__ nbr, int64_t n, int K3, const __grid_constant__ MaskOrder ord, int begin_bit,
+    int tile, uint32_t* keys0, int32_t* vals0, uint32_t* keys1, int32_t* vals1, int* cnt, int* tot, unsigned* bar,
+    int32_t* __restrict__ perm, int32_t* __restrict__ nbr_perm) {
+  constexpr int W = kSortThreads / 32;
+  __shared__ int s_wc[W][257];  // per-warp digit counts -> exclusive offsets (257th: no element)
+  __shared__ int s_carry[256], s_off[256], s_wsum[W];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned G = gridDim.x;
+  const int64_t t0 = static_cast<int64_t>(blockIdx.x) * tile, t1 = min(n, t0 + tile);
+  unsigned target = 0;
+  uint32_t key[kSortMaxE];
+  int32_t val[kSortMaxE];
+#pragma unroll
+  for (int e = 0; e < kSortMaxE; ++e) {
+    const int64_t i = t0 + e * kSortThreads + tid;
+    key[e] = 0;
+    val[e] = static_cast<int32_t>(i);
+    if (i < t1)
+      for (int k = 0; k < K3; ++k) key[e] |= static_cast<uint32_t>(__ldg(nbr + int64_t{k} * n + i) >= 0) << ord.pos[k];
+  }
+  for (int pass = 0; pass < 3; ++pass) {
+    const int shift = begin_bit + 8 * pass;
+    if (pass > 0) {
+      const uint32_t* ki = pass == 1 ? keys1 : keys0;
+      const int32_t* vi = pass == 1 ? vals1 : vals0;
+#pragma unroll
+      for (int e = 0; e < kSortMaxE; ++e) {
+        const int64_t i = t0 + e * kSortThreads + tid;
+        if (i < t1) {
+          key[e] = __ldcg(ki + i);
+          val[e] = __ldcg(vi + i);
+        }
+      }
+    }
+    s_carry[tid] = 0;
+    int rank[kSortMaxE], dig[kSortMaxE];
+#pragma unroll
+    for (int e = 0; e < kSortMaxE; ++e) {
+      const bool ok = t0 + e * kSortThreads + tid < t1;
+      const int d = ok ? static_cast<int>((key[e] >> shift) & 255u) : 256;
+      dig[e] = d;
+      for (int q = tid; q < W * 257; q += kSortThreads) (&s_wc[0][0])[q] = 0;
+      __syncthreads();
+      const unsigned peers = __match_any_sync(0xFFFFFFFFu, d);
+      const int lrank = __popc(peers & ((1u << lane) - 1u));
+      if (lrank == 0) s_wc[warp][d] = __popc(peers);
+      __syncthreads();
+      {  // thread tid owns digit tid: exclusive prefix over warps, carried across rounds
+        int run = s_carry[tid];
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+          const int c = s_wc[w][tid];
+          s_wc[w][tid] = run;
+          run += c;
+        }
+        s_carry[tid] = run;
+      }
+      __syncthreads();
+      rank[e] = ok ? s_wc[warp][d] + lrank : 0;
+      __syncthreads();
+    }
+    cnt[static_cast<int64_t>(tid) * G + blockIdx.x] = s_carry[tid];  // tile histogram
+    grid_barrier(bar, G, target);
+    for (unsigned d = blockIdx.x; d < 256; d += G) {  // per-digit scan across the tiles
+      int* row = cnt + static_cast<int64_t>(d) * G;
+      int v[4], local = 0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const unsigned c = tid * 4u + u;
+        v[u] = c < G ? __ldcg(row + c) : 0;
+        local += v[u];
+      }
+      int excl;
+      const int total = block_exclusive_scan(local, excl, s_wsum);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const unsigned c = tid * 4u + u;
+        if (c < G) row[c] = excl;
+        excl += v[u];
+      }
+      if (tid == 0) tot[d] = total;
+    }
+    grid_barrier(bar, G, target);
+    {
+      int base;
+      block_exclusive_scan(__ldcg(tot + tid), base, s_wsum);
+      s_off[tid] = base + __ldcg(cnt + static_cast<int64_t>(tid) * G + blockIdx.x);
+    }
+    __syncthreads();
+    uint32_t* ko = pass == 0 ? keys1 : keys0;
+    int32_t* vo = pass == 0 ? vals1 : vals0;
+#pragma unroll
+    for (int e = 0; e < kSortMaxE; ++e) {
+      if (dig[e] > 255) continue;
+      const int64_t pos = s_off[dig[e]] + rank[e];
+      if (pass < 2) {
+        ko[pos] = key[e];
+        vo[pos] = val[e];
+      } else {
+        perm[pos] = val[e];
+        for (int k = 0; k < K3; ++k) nbr_perm[int64_t{k} * n + pos] = __ldg(nbr + int64_t{k} * n + val[e]);
+      }
+    }
+    if (pass < 2) grid_barrier(bar, G, target);
+  }
+}
+
 // nbr_perm[k][r] = nbr_in[k][perm[r]] (coalesced writes; reads gathered from L2)
 __global__ void k_permute_nbr(const int32_t* __restrict__ nbr, const int32_t* __restrict__ perm, int64_t n, int K3,
                               int32_t* __restrict__ out) {
@@ -841,6 +1002,7 @@ void prepare_fused_layout(Ctx& ctx, MapData& m) {
   m.permuted = K3 >= 27 && K3 <= 32 && m.cfg.out_stride == 1 && !m.cfg.transposed && n > 2 * 128 &&
                n <= INT32_MAX;
   if (const char* e = std::getenv("SCONV_NO_PERMUTE"); e && e[0] == '1') m.permuted = false;  // experiments
+  if (const char* e = std::getenv("SCONV_PERMUTE_MIN"); e && n < std::atoll(e)) m.permuted = false;
   if (!m.permuted) return;
   // Bit position per offset: rarer offsets (larger L1 norm: corners, then edges, then faces,
   // the always-present centre last) in the more significant bits, so equal-or-similar masks
@@ -858,6 +1020,52 @@ void prepare_fused_layout(Ctx& ctx, MapData& m) {
   idx.alloc(4 * n, st);
   m.row_perm.alloc(4 * n, st);
   m.nbr_perm.alloc(4 * n * K3, st);
+  static const int mask_bits = [] {
+    const char* e = std::getenv("SCONV_MASK_BITS");  // experiments (16 bits: -78 us sort, +60 us convs)
+    return e ? std::max(1, std::min(32, std::atoi(e))) : 24;
+  }();
+  // one cooperative launch when every row fits the co-resident CTAs' registers
+  static const int coop_cap = [] {
+    int per_sm = 0, dev = 0, sms = 0, coop = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mask_sort, kSortThreads, 0) != cudaSuccess) per_sm = 0;
+    return coop ? per_sm * sms : 0;
+  }();
+  const bool one_launch = mask_bits == 24 && K3 >= 24 && coop_cap > 0 &&
+                          n <= static_cast<int64_t>(coop_cap) * kSortThreads * kSortMaxE &&
+                          !(std::getenv("SCONV_MASK_SORT_CUB") && std::getenv("SCONV_MASK_SORT_CUB")[0] == '1');
+  if (one_launch) {
+    // smallest rows-per-CTA that fits the co-resident grid (1 element per thread when possible)
+    // one row per thread when the co-resident grid allows (measured: a grid capped near one CTA
+    // per SM, 4 rows per thread, is 1.6x slower: serial rank rounds, fewer loads in flight)
+    int e = 1;
+    while (ceil_div<int64_t>(n, int64_t{kSortThreads} * e) > coop_cap) ++e;
+    const int tile = kSortThreads * e;
+    const unsigned G = static_cast<unsigned>(ceil_div<int64_t>(n, tile));
+    DevBuf aux;
+    aux.alloc(sizeof(int) * (256 * static_cast<size_t>(G) + 256 + 4), st);
+    int* cnt = aux.get<int>();
+    int* tot = cnt + 256 * static_cast<size_t>(G);
+    unsigned* bar = reinterpret_cast<unsigned*>(tot + 256);
+    SCONV_CUDA(cudaMemsetAsync(bar, 0, 4 * sizeof(unsigned), st));
+    const int32_t* nbr = m.nbr_in.get<int32_t>();
+    int begin_bit = K3 - 24;
+    int64_t nn = n;
+    int K3v = K3, tilev = tile;
+    uint32_t *k0 = keys.get<uint32_t>(), *k1 = keys_sorted.get<uint32_t>();
+    DevBuf v1buf;
+    v1buf.alloc(4 * n, st);
+    int32_t *v0 = idx.get<int32_t>(), *v1 = v1buf.get<int32_t>();
+    int32_t *perm = m.row_perm.get<int32_t>(), *nperm = m.nbr_perm.get<int32_t>();
+    void* args[] = {&nbr, &nn, &K3v, &ord, &begin_bit, &tilev, &k0, &v0, &k1, &v1, &cnt, &tot, &bar, &perm, &nperm};
+    ctx.launch("k_mask_sort", [&] {
+      SCONV_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_mask_sort), dim3(G), dim3(kSortThreads),
+                                             args, 0, st));
+    });
+    return;
+  }
   const unsigned b1 = static_cast<unsigned>(ceil_div<int64_t>(n, 256));
   ctx.launch("k_mask_keys", [&] {
     k_mask_keys<<<b1, 256, 0, st>>>(m.nbr_in.get<int32_t>(), n, K3, ord, keys.get<uint32_t>(), idx.get<int32_t>());
@@ -865,10 +1073,6 @@ void prepare_fused_layout(Ctx& ctx, MapData& m) {
   size_t temp = 0;
   // sort on the top 24 key bits only (3 radix passes instead of 4): the dropped low bits are
   // the centre and two face offsets, the most common ones (KITTI: 10.32 -> 10.59 offsets/tile)
-  static const int mask_bits = [] {
-    const char* e = std::getenv("SCONV_MASK_BITS");  // experiments (16 bits: -78 us sort, +60 us convs)
-    return e ? std::max(1, std::min(32, std::atoi(e))) : 24;
-  }();
   const int begin_bit = std::max(0, K3 - mask_bits);
   SCONV_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp, keys.get<uint32_t>(), keys_sorted.get<uint32_t>(),
                                              idx.get<int32_t>(), m.row_perm.get<int32_t>(), static_cast<int>(n),
