@@ -36,6 +36,7 @@
 #include "common.cuh"
 #include "conv_fused.hpp"
 #include "map.hpp"
+#include "coop_sort.cuh"
 #include "sm100.cuh"
 
 namespace sconvb {
@@ -629,7 +630,7 @@ __global__ void k_mask_keys(const int32_t* __restrict__ nbr, int64_t n, int K3, 
 // mask kernel + CUB radix sort (histogram, scan, 3 onesweep passes) + permute kernel: every
 // one of those is latency bound at these sizes (~70 us per map whatever n). Stable LSD radix
 // sort of the 24 mask bits [begin_bit, begin_bit + 24) in three 8-bit passes, keys and values
-// in registers (tile of <= 256 * kSortMaxE rows per CTA), grid barriers between the phases:
+// in registers (tile of <= 256 * kCoopMaxE rows per CTA), grid barriers between the phases:
 //   rank     stable rank of each row among its tile's rows with the same digit (warp match +
 //            per-warp digit counts, tile order = element e of thread t at e*256 + t)
 //   hist     tile digit counts -> cnt[digit][tile]          | grid barrier
@@ -638,147 +639,52 @@ __global__ void k_mask_keys(const int32_t* __restrict__ nbr, int64_t n, int K3, 
 //            permutation and the permuted neighbour table (k_permute_nbr fused in; measured
 //            faster than a coalesced grid-stride copy after one more barrier)
 // Same bits, same stability as the CUB path => the identical permutation.
-constexpr int kSortThreads = 256, kSortMaxE = 4;
-
-__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks, unsigned& target) {
-  __syncthreads();
-  target += nblocks;  // barrier b of this launch completes at (b + 1) * nblocks arrivals
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(bar, 1u);
-    unsigned v;
-    do {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
-    } while (v < target);
-    __threadfence();
-  }
-  __syncthreads();
-}
-
-// exclusive scan of one int per thread over the CTA (kSortThreads threads); returns the total
-__device__ __forceinline__ int block_exclusive_scan(int v, int& excl, int* s_wsum) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int incl = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int u = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-    if (lane >= o) incl += u;
-  }
-  if (lane == 31) s_wsum[warp] = incl;
-  __syncthreads();
-  int wp = 0, total = 0;
-#pragma unroll
-  for (int w = 0; w < kSortThreads / 32; ++w) {
-    wp += w < warp ? s_wsum[w] : 0;
-    total += s_wsum[w];
-  }
-  __syncthreads();
-  excl = wp + incl - v;
-  return total;
-}
-
-__global__ void __launch_bounds__(kSortThreads) k_mask_sort(
+template <int E>
+__global__ void __launch_bounds__(kCoopThreads) k_mask_sort(
     const int32_t* __restrict__ nbr, int64_t n, int K3, const __grid_constant__ MaskOrder ord, int begin_bit,
     int tile, uint32_t* keys0, int32_t* vals0, uint32_t* keys1, int32_t* vals1, int* cnt, int* tot, unsigned* bar,
     int32_t* __restrict__ perm, int32_t* __restrict__ nbr_perm) {
-  constexpr int W = kSortThreads / 32;
-  __shared__ int s_wc[W][257];  // per-warp digit counts -> exclusive offsets (257th: no element)
-  __shared__ int s_carry[256], s_off[256], s_wsum[W];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x;
   const unsigned G = gridDim.x;
   const int64_t t0 = static_cast<int64_t>(blockIdx.x) * tile, t1 = min(n, t0 + tile);
   unsigned target = 0;
-  uint32_t key[kSortMaxE];
-  int32_t val[kSortMaxE];
+  uint32_t key[E];
+  int32_t val[E];
+  bool ok[E];
 #pragma unroll
-  for (int e = 0; e < kSortMaxE; ++e) {
-    const int64_t i = t0 + e * kSortThreads + tid;
+  for (int e = 0; e < E; ++e) {
+    const int64_t i = t0 + e * kCoopThreads + tid;
+    ok[e] = i < t1;
     key[e] = 0;
     val[e] = static_cast<int32_t>(i);
-    if (i < t1)
+    if (ok[e])
       for (int k = 0; k < K3; ++k) key[e] |= static_cast<uint32_t>(__ldg(nbr + int64_t{k} * n + i) >= 0) << ord.pos[k];
   }
   for (int pass = 0; pass < 3; ++pass) {
-    const int shift = begin_bit + 8 * pass;
     if (pass > 0) {
       const uint32_t* ki = pass == 1 ? keys1 : keys0;
       const int32_t* vi = pass == 1 ? vals1 : vals0;
 #pragma unroll
-      for (int e = 0; e < kSortMaxE; ++e) {
-        const int64_t i = t0 + e * kSortThreads + tid;
-        if (i < t1) {
+      for (int e = 0; e < E; ++e)
+        if (ok[e]) {
+          const int64_t i = t0 + e * kCoopThreads + tid;
           key[e] = __ldcg(ki + i);
           val[e] = __ldcg(vi + i);
         }
-      }
     }
-    s_carry[tid] = 0;
-    int rank[kSortMaxE], dig[kSortMaxE];
-#pragma unroll
-    for (int e = 0; e < kSortMaxE; ++e) {
-      const bool ok = t0 + e * kSortThreads + tid < t1;
-      const int d = ok ? static_cast<int>((key[e] >> shift) & 255u) : 256;
-      dig[e] = d;
-      for (int q = tid; q < W * 257; q += kSortThreads) (&s_wc[0][0])[q] = 0;
-      __syncthreads();
-      const unsigned peers = __match_any_sync(0xFFFFFFFFu, d);
-      const int lrank = __popc(peers & ((1u << lane) - 1u));
-      if (lrank == 0) s_wc[warp][d] = __popc(peers);
-      __syncthreads();
-      {  // thread tid owns digit tid: exclusive prefix over warps, carried across rounds
-        int run = s_carry[tid];
-#pragma unroll
-        for (int w = 0; w < W; ++w) {
-          const int c = s_wc[w][tid];
-          s_wc[w][tid] = run;
-          run += c;
-        }
-        s_carry[tid] = run;
-      }
-      __syncthreads();
-      rank[e] = ok ? s_wc[warp][d] + lrank : 0;
-      __syncthreads();
-    }
-    cnt[static_cast<int64_t>(tid) * G + blockIdx.x] = s_carry[tid];  // tile histogram
-    grid_barrier(bar, G, target);
-    for (unsigned d = blockIdx.x; d < 256; d += G) {  // per-digit scan across the tiles
-      int* row = cnt + static_cast<int64_t>(d) * G;
-      int v[4], local = 0;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const unsigned c = tid * 4u + u;
-        v[u] = c < G ? __ldcg(row + c) : 0;
-        local += v[u];
-      }
-      int excl;
-      const int total = block_exclusive_scan(local, excl, s_wsum);
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const unsigned c = tid * 4u + u;
-        if (c < G) row[c] = excl;
-        excl += v[u];
-      }
-      if (tid == 0) tot[d] = total;
-    }
-    grid_barrier(bar, G, target);
-    {
-      int base;
-      block_exclusive_scan(__ldcg(tot + tid), base, s_wsum);
-      s_off[tid] = base + __ldcg(cnt + static_cast<int64_t>(tid) * G + blockIdx.x);
-    }
-    __syncthreads();
+    int pos[E];
+    lsd_pass_positions<E>(key, ok, begin_bit + 8 * pass, pos, cnt, tot, bar, target);
     uint32_t* ko = pass == 0 ? keys1 : keys0;
     int32_t* vo = pass == 0 ? vals1 : vals0;
 #pragma unroll
-    for (int e = 0; e < kSortMaxE; ++e) {
-      if (dig[e] > 255) continue;
-      const int64_t pos = s_off[dig[e]] + rank[e];
+    for (int e = 0; e < E; ++e) {
+      if (!ok[e]) continue;
       if (pass < 2) {
-        ko[pos] = key[e];
-        vo[pos] = val[e];
+        ko[pos[e]] = key[e];
+        vo[pos[e]] = val[e];
       } else {
-        perm[pos] = val[e];
-        for (int k = 0; k < K3; ++k) nbr_perm[int64_t{k} * n + pos] = __ldg(nbr + int64_t{k} * n + val[e]);
+        perm[pos[e]] = val[e];
+        for (int k = 0; k < K3; ++k) nbr_perm[int64_t{k} * n + pos[e]] = __ldg(nbr + int64_t{k} * n + val[e]);
       }
     }
     if (pass < 2) grid_barrier(bar, G, target);
@@ -1030,39 +936,39 @@ void prepare_fused_layout(Ctx& ctx, MapData& m) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mask_sort, kSortThreads, 0) != cudaSuccess) per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mask_sort<kCoopMaxE>, kCoopThreads, 0) != cudaSuccess)
+      per_sm = 0;
     return coop ? per_sm * sms : 0;
   }();
   const bool one_launch = mask_bits == 24 && K3 >= 24 && coop_cap > 0 &&
-                          n <= static_cast<int64_t>(coop_cap) * kSortThreads * kSortMaxE &&
+                          n <= static_cast<int64_t>(coop_cap) * kCoopThreads * kCoopMaxE &&
                           !(std::getenv("SCONV_MASK_SORT_CUB") && std::getenv("SCONV_MASK_SORT_CUB")[0] == '1');
   if (one_launch) {
-    // smallest rows-per-CTA that fits the co-resident grid (1 element per thread when possible)
     // one row per thread when the co-resident grid allows (measured: a grid capped near one CTA
     // per SM, 4 rows per thread, is 1.6x slower: serial rank rounds, fewer loads in flight)
     int e = 1;
-    while (ceil_div<int64_t>(n, int64_t{kSortThreads} * e) > coop_cap) ++e;
-    const int tile = kSortThreads * e;
+    while (ceil_div<int64_t>(n, int64_t{kCoopThreads} * e) > coop_cap) e *= 2;
+    const int tile = kCoopThreads * e;
     const unsigned G = static_cast<unsigned>(ceil_div<int64_t>(n, tile));
-    DevBuf aux;
+    DevBuf aux, v1buf;
     aux.alloc(sizeof(int) * (256 * static_cast<size_t>(G) + 256 + 4), st);
+    v1buf.alloc(4 * n, st);
     int* cnt = aux.get<int>();
     int* tot = cnt + 256 * static_cast<size_t>(G);
     unsigned* bar = reinterpret_cast<unsigned*>(tot + 256);
     SCONV_CUDA(cudaMemsetAsync(bar, 0, 4 * sizeof(unsigned), st));
     const int32_t* nbr = m.nbr_in.get<int32_t>();
-    int begin_bit = K3 - 24;
+    int begin_bit = K3 - 24, K3v = K3, tilev = tile;
     int64_t nn = n;
-    int K3v = K3, tilev = tile;
     uint32_t *k0 = keys.get<uint32_t>(), *k1 = keys_sorted.get<uint32_t>();
-    DevBuf v1buf;
-    v1buf.alloc(4 * n, st);
     int32_t *v0 = idx.get<int32_t>(), *v1 = v1buf.get<int32_t>();
     int32_t *perm = m.row_perm.get<int32_t>(), *nperm = m.nbr_perm.get<int32_t>();
     void* args[] = {&nbr, &nn, &K3v, &ord, &begin_bit, &tilev, &k0, &v0, &k1, &v1, &cnt, &tot, &bar, &perm, &nperm};
+    const void* fn = e == 1   ? reinterpret_cast<const void*>(k_mask_sort<1>)
+                     : e == 2 ? reinterpret_cast<const void*>(k_mask_sort<2>)
+                              : reinterpret_cast<const void*>(k_mask_sort<4>);
     ctx.launch("k_mask_sort", [&] {
-      SCONV_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_mask_sort), dim3(G), dim3(kSortThreads),
-                                             args, 0, st));
+      SCONV_CUDA(cudaLaunchCooperativeKernel(fn, dim3(G), dim3(kCoopThreads), args, 0, st));
     });
     return;
   }

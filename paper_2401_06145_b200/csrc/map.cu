@@ -20,6 +20,7 @@
 #include <string>
 
 #include "common.cuh"
+#include "coop_sort.cuh"
 #include "map.hpp"
 
 namespace sconvb {
@@ -353,6 +354,144 @@ __global__ void k_floor_compact(const uint64_t* __restrict__ fl, int64_t n, int 
   unpack_key(fl[i], x, y, z);
   out[i] = (static_cast<uint32_t>((x - flags->fbox[0]) / s) << (by + bz)) |
            (static_cast<uint32_t>((y - flags->fbox[1]) / s) << bz) | static_cast<uint32_t>((z - flags->fbox[2]) / s);
+}
+
+// Eq. 1 output coordinates in ONE cooperative launch (replaces k_floor_bbox, k_floor_compact,
+// the CUB radix sort, CUB unique and k_floor_expand: ~10 latency-bound launches per strided
+// map). Phases, grid barriers between them (coop_sort.cuh):
+//   floor    floored coordinates in registers, range check, CTA-reduced bbox atomics
+//   compact  bbox-relative compact keys, (x, y, z) in the minimal bit widths (order preserving);
+//            wider than 32 bits: flag fwide and stop (the host redoes it with 64-bit keys)
+//   sort     stable LSD passes over only the ceil(bits / 8) digits the keys use
+//   unique   first-of-run flags, in-tile ranks + cross-tile prefix, expand to packed keys
+template <int E>
+__global__ void __launch_bounds__(kCoopThreads) k_floor_unique(const uint64_t* __restrict__ src,
+                                                              const int32_t* __restrict__ src_idx, int64_t n, int s,
+                                                              int tile, MapFlags* flags, uint32_t* buf0, uint32_t* buf1,
+                                                              int* cnt, int* tot, unsigned* bar,
+                                                              uint64_t* __restrict__ q_out, int64_t* __restrict__ nsel) {
+  const int tid = threadIdx.x;
+  const unsigned G = gridDim.x;
+  const int64_t t0 = static_cast<int64_t>(blockIdx.x) * tile, t1 = min(n, t0 + tile);
+  unsigned target = 0;
+  int32_t fc[E][3];
+  bool ok[E];
+  int mn[3] = {INT_MAX, INT_MAX, INT_MAX}, mx[3] = {INT_MIN, INT_MIN, INT_MIN};
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int64_t i = t0 + e * kCoopThreads + tid;
+    ok[e] = i < t1;
+    fc[e][0] = fc[e][1] = fc[e][2] = 0;
+    if (!ok[e]) continue;
+    int32_t c[3];
+    unpack_key(src[i], c[0], c[1], c[2]);
+    int64_t f[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) f[a] = floor_div(c[a], s) * s;
+    if (!in_range(f[0]) || !in_range(f[1]) || !in_range(f[2])) {
+      const int axis = !in_range(f[0]) ? 0 : (!in_range(f[1]) ? 1 : 2);
+      const int64_t j = src_idx ? src_idx[i] : i;
+      atomicMin(&flags->bad_floor, static_cast<unsigned long long>(j * 3 + axis));
+      continue;  // the build fails on the host; the key is irrelevant
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      fc[e][a] = static_cast<int32_t>(f[a]);
+      mn[a] = min(mn[a], fc[e][a]);
+      mx[a] = max(mx[a], fc[e][a]);
+    }
+  }
+  {  // CTA-reduced bbox: one atomic per bound per CTA
+    __shared__ int s_box[kCoopThreads / 32][6];
+    const int lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        mn[a] = min(mn[a], __shfl_xor_sync(0xFFFFFFFFu, mn[a], o));
+        mx[a] = max(mx[a], __shfl_xor_sync(0xFFFFFFFFu, mx[a], o));
+      }
+    if (lane == 0)
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        s_box[warp][a] = mn[a];
+        s_box[warp][3 + a] = mx[a];
+      }
+    __syncthreads();
+    if (tid < 6) {
+      int v = s_box[0][tid];
+      for (int w = 1; w < kCoopThreads / 32; ++w) v = tid < 3 ? min(v, s_box[w][tid]) : max(v, s_box[w][tid]);
+      if (tid < 3 ? v != INT_MAX : v != INT_MIN) {
+        if (tid < 3)
+          atomicMin(&flags->fbox[tid], v);
+        else
+          atomicMax(&flags->fbox[tid], v);
+      }
+    }
+  }
+  grid_barrier(bar, G, target);
+  int box[6];
+#pragma unroll
+  for (int a = 0; a < 6; ++a) box[a] = __ldcg(&flags->fbox[a]);
+  const int bx = bits_for((int64_t{box[3]} - box[0]) / s), by = bits_for((int64_t{box[4]} - box[1]) / s),
+            bz = bits_for((int64_t{box[5]} - box[2]) / s);
+  if (bx + by + bz > 32) {  // uniform across the grid: every CTA read the same bbox
+    if (blockIdx.x == 0 && tid == 0) flags->fwide = 1;
+    return;
+  }
+  uint32_t key[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e)
+    key[e] = ok[e] ? static_cast<uint32_t>((static_cast<uint64_t>((fc[e][0] - box[0]) / s) << (by + bz)) |
+                                           (static_cast<uint64_t>((fc[e][1] - box[1]) / s) << bz) |
+                                           static_cast<uint64_t>((fc[e][2] - box[2]) / s))
+                   : 0u;
+  const int passes = max(1, (bx + by + bz + 7) / 8);
+  for (int pass = 0; pass < passes; ++pass) {
+    if (pass > 0) {
+      const uint32_t* ki = (pass - 1) % 2 == 0 ? buf0 : buf1;
+#pragma unroll
+      for (int e = 0; e < E; ++e)
+        if (ok[e]) key[e] = __ldcg(ki + t0 + e * kCoopThreads + tid);
+    }
+    int pos[E];
+    lsd_pass_positions<E>(key, ok, 8 * pass, pos, cnt, tot, bar, target);
+    uint32_t* ko = pass % 2 == 0 ? buf0 : buf1;
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+      if (ok[e]) ko[pos[e]] = key[e];
+    grid_barrier(bar, G, target);
+  }
+  const uint32_t* sorted = (passes - 1) % 2 == 0 ? buf0 : buf1;
+  int rank[E], carry = 0;
+  bool first[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int64_t i = t0 + e * kCoopThreads + tid;
+    key[e] = ok[e] ? __ldcg(sorted + i) : 0u;
+    first[e] = ok[e] && (i == 0 || __ldcg(sorted + i - 1) != key[e]);
+    int excl;
+    const int total = block_exclusive_scan(first[e] ? 1 : 0, excl);
+    rank[e] = carry + excl;
+    carry += total;
+  }
+  if (tid == 0) cnt[blockIdx.x] = carry;  // unique keys starting in this tile
+  grid_barrier(bar, G, target);
+  int local = 0;
+  for (unsigned c = tid; c < blockIdx.x; c += kCoopThreads) local += __ldcg(cnt + c);
+  int dummy;
+  const int base = block_exclusive_scan(local, dummy);
+  const uint64_t ymask = (1ull << by) - 1ull, zmask = (1ull << bz) - 1ull;
+#pragma unroll
+  for (int e = 0; e < E; ++e)
+    if (first[e]) {
+      const uint64_t c = key[e];
+      const int32_t x = box[0] + static_cast<int32_t>(c >> (by + bz)) * s;
+      const int32_t y = box[1] + static_cast<int32_t>((c >> bz) & ymask) * s;
+      const int32_t z = box[2] + static_cast<int32_t>(c & zmask) * s;
+      q_out[base + rank[e]] = pack_key_unchecked(x, y, z);
+    }
+  if (blockIdx.x == G - 1 && tid == 0) *nsel = base + carry;
 }
 
 __global__ void k_floor_expand(const uint32_t* __restrict__ ck, const int64_t* __restrict__ count, int s,
@@ -1000,7 +1139,7 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
   bool need_nout_sync = false;
   DevBuf fl, fs;  // strided: floored keys / sort scratch (function scope: the wide fallback reuses them)
   std::function<void()> strided_wide;
-  DevBuf nsel;
+  DevBuf nsel, coop_aux;
   DevBuf target_xyz_dev;
   if (cfg.transposed) {
     if (!target) fail(SCONV_ERR_ARG, "transposed layer needs target coordinates");
@@ -1035,6 +1174,45 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
     if (n > 0) {
       // Eq. 1 on device: floor -> 32-bit bbox-relative compact keys (4 radix passes instead of 8)
       // -> sort -> unique -> expand; the 64-bit path below runs only if the compact key is wide.
+      static const int coop_cap = [] {
+        int per_sm = 0, dev = 0, sms = 0, coop = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_floor_unique<kCoopMaxE>, kCoopThreads, 0) !=
+            cudaSuccess)
+          per_sm = 0;
+        return coop ? per_sm * sms : 0;
+      }();
+      const bool one_launch = coop_cap > 0 && n <= static_cast<int64_t>(coop_cap) * kCoopThreads * kCoopMaxE &&
+                              !(std::getenv("SCONV_FLOOR_CUB") && std::getenv("SCONV_FLOOR_CUB")[0] == '1');
+      if (one_launch) {  // everything below in one cooperative launch
+        int e = 1;
+        while (ceil_div<int64_t>(n, int64_t{kCoopThreads} * e) > coop_cap) e *= 2;
+        const int tile = kCoopThreads * e;
+        const unsigned G = static_cast<unsigned>(ceil_div<int64_t>(n, tile));
+        coop_aux.alloc(sizeof(int) * (256 * static_cast<size_t>(G) + 256 + 4), st);
+        int* cnt = coop_aux.get<int>();
+        int* tot = cnt + 256 * static_cast<size_t>(G);
+        unsigned* bar = reinterpret_cast<unsigned*>(tot + 256);
+        SCONV_CUDA(cudaMemsetAsync(bar, 0, 4 * sizeof(unsigned), st));
+        uint32_t* b0 = reinterpret_cast<uint32_t*>(fs.get<uint64_t>());  // fs is 8n bytes: two u32 arrays
+        uint32_t* b1 = b0 + n;
+        int64_t nn = n;
+        int sv = cfg.out_stride, tilev = tile;
+        uint64_t* qo = m->q_keys->get<uint64_t>();
+        int64_t* ns = nsel.get<int64_t>();
+        MapFlags* fl_ = flags;
+        const int32_t* si = src_idx;
+        const uint64_t* sk = src;
+        void* args[] = {&sk, &si, &nn, &sv, &tilev, &fl_, &b0, &b1, &cnt, &tot, &bar, &qo, &ns};
+        const void* fn = e == 1   ? reinterpret_cast<const void*>(k_floor_unique<1>)
+                         : e == 2 ? reinterpret_cast<const void*>(k_floor_unique<2>)
+                                  : reinterpret_cast<const void*>(k_floor_unique<4>);
+        ctx.launch("k_floor_unique", [&] {
+          SCONV_CUDA(cudaLaunchCooperativeKernel(fn, dim3(G), dim3(kCoopThreads), args, 0, st));
+        });
+      } else {
       ctx.launch("k_floor_keys", [&] {
         k_floor_bbox<<<grid_for(n), kThreads, 0, st>>>(src, src_idx, n, cfg.out_stride, fl.get<uint64_t>(), flags);
       });
@@ -1062,6 +1240,7 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
         k_floor_expand<<<grid_for(n), kThreads, 0, st>>>(u32, nsel.get<int64_t>(), cfg.out_stride, flags,
                                                           m->q_keys->get<uint64_t>());
       });
+      }
       need_nout_sync = true;
       strided_wide = [&, n] {  // exact 64-bit fallback (coordinate span beyond 32 compact bits)
         ctx.launch("k_floor_keys", [&] {

@@ -121,6 +121,21 @@ def test_map_range_edges(ctx, oracle):
     assert_map_equal(gpu, ora)
 
 
+@pytest.mark.parametrize("s", [2, 4])
+def test_strided_wide_span_fallback(ctx, oracle, s):
+    """Eq. 1 output coordinates whose bbox-relative compact key needs > 32 bits (a cloud
+    spanning most of the coordinate range): the one-launch floor/sort/unique kernel flags it and
+    the 64-bit path rebuilds the coordinates; the map must equal the oracle's."""
+    rng = np.random.default_rng(s)
+    lo, hi = -(2 ** 20) + 8, 2 ** 20 - 8
+    xyz = np.unique(rng.integers(lo, hi, size=(3000, 3)).astype(np.int32), axis=0)
+    near = xyz[:200] + rng.integers(-3, 4, size=(200, 3)).astype(np.int32)  # neighbours to find
+    xyz = np.unique(np.concatenate([xyz, near]), axis=0)
+    xyz = xyz[rng.permutation(len(xyz))]
+    got = sc.KernelMap.build(ctx, xyz, False, 3, s, s).read()
+    assert_map_equal(got, oracle.layer_map(xyz, False, 3, s, s))
+
+
 def test_map_sort_fallbacks(ctx, oracle):
     """Compact 32-bit keys with an oversized bucket (> 4096 keys share the top 16 bits)
     force the exact CUB fallback; the map must not change."""
