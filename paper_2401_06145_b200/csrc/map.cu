@@ -1036,6 +1036,9 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
   if (cfg.block_C < 1 || cfg.block_C > 4096) fail(SCONV_ERR_ARG, "query block size C must be in [1, 4096]");
   if (!cfg.transposed && cfg.out_stride < 1) fail(SCONV_ERR_ARG, "stride must be positive");
   if (P.n < 0 || P.n > INT32_MAX / 2) fail(SCONV_ERR_ARG, "point count out of supported range");
+  // coordinates given as xyz need the flags readback (range / order checks) before the map is
+  // used, so such a build syncs; the canonical lists can still be deferred
+  const bool defer_canonical = lazy;
   if (lazy && (!P.keys || (cfg.transposed && (!target || !target->keys)))) lazy = false;
   auto m = std::make_unique<MapData>();
   m->cfg = cfg;
@@ -1298,6 +1301,9 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
     SCONV_CUDA(cudaMemcpyAsync(&pin[1], nsel.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     static_assert(2 * sizeof(MapFlags) <= Ctx::kPinFlagsBytes, "pinned flags region");
     ctx.sync();
+    // the input sort's compact key was too wide: P's keys are not valid yet, so nothing derived
+    // from them (floors, their range errors) is either; redo with the exact 64-bit sort first
+    if (!force_wide && (pin[0].wide || pin[0].big_bucket)) return build_map(ctx, P, cfg, target, true, defer_canonical);
     check_flags(pin[0]);
     if (pin[0].fwide && strided_wide) {  // rare: redo the output coordinates with 64-bit keys
       strided_wide();
@@ -1398,9 +1404,20 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
     pd.ntiles = ntiles;
     pd.ngroups = ngroups;
     pd.qpl = qpl;
-    if (!lazy) launch_canonical(ctx, *m);
+    if (!defer_canonical) launch_canonical(ctx, *m);
   }
   if (lazy) {  // canonical lists + readback deferred to ensure_canonical()
+    m->canonical = false;
+    m->total = -1;
+    m->pending.flags = std::move(flags_buf);
+    return m;
+  }
+  if (defer_canonical) {  // flags only (one sync), canonical lists on demand
+    SCONV_CUDA(cudaMemcpyAsync(pin, flags, sizeof(MapFlags), cudaMemcpyDeviceToHost, st));
+    ctx.sync();
+    const MapFlags f = pin[0];
+    if (!force_wide && (f.wide || f.big_bucket)) return build_map(ctx, P, cfg, target, true, true);  // exact fallback
+    check_flags(f);
     m->canonical = false;
     m->total = -1;
     m->pending.flags = std::move(flags_buf);
@@ -1410,8 +1427,8 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
   MapFlags f;
   read_starts(ctx, *m, flags, &f);
   m->pending = MapData::Pending{};
+  if (!force_wide && (f.wide || f.big_bucket)) return build_map(ctx, P, cfg, target, true);  // exact fallback: CUB 64-bit sort
   check_flags(f);
-  if (f.wide || f.big_bucket) return build_map(ctx, P, cfg, target, true);  // exact fallback: CUB 64-bit sort
   return m;
 }
 
