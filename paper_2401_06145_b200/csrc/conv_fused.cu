@@ -946,7 +946,7 @@ void prepare_fused_layout(Ctx& ctx, MapData& m) {
   if (one_launch) {
     // one row per thread when the co-resident grid allows (measured: a grid capped near one CTA
     // per SM, 4 rows per thread, is 1.6x slower: serial rank rounds, fewer loads in flight)
-    int e = 1;
+    int e = coop_rows_per_thread();
     while (ceil_div<int64_t>(n, int64_t{kCoopThreads} * e) > coop_cap) e *= 2;
     const int tile = kCoopThreads * e;
     const unsigned G = static_cast<unsigned>(ceil_div<int64_t>(n, tile));

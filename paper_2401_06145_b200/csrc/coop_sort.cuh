@@ -6,10 +6,22 @@
 // [b*tile, b*tile + tile); element e of thread t is row b*tile + e*kCoopThreads + t.
 #pragma once
 #include <cstdint>
+#include <cstdlib>
 
 namespace sconvb {
 
 constexpr int kCoopThreads = 256, kCoopMaxE = 4;
+
+// rows per thread to start from (1, 2 or 4; SCONV_COOP_E for experiments): the host doubles it
+// until the grid fits the co-resident CTAs
+inline int coop_rows_per_thread() {
+  static const int e = [] {
+    const char* v = std::getenv("SCONV_COOP_E");
+    const int x = v ? std::atoi(v) : 1;
+    return x >= 4 ? 4 : (x >= 2 ? 2 : 1);
+  }();
+  return e;
+}
 
 // all CTAs of the grid; `target` counts this launch's barriers (bar zeroed before the launch)
 __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks, unsigned& target) {

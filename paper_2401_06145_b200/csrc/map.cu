@@ -657,15 +657,22 @@ __global__ void __launch_bounds__(kSearchThreads) k_search(
   const int64_t c = blockIdx.x / ngroups;
   const int grp = static_cast<int>(blockIdx.x - c * ngroups);
   const int k = grp + warp * ngroups;  // this warp's offset
-  if (k >= K3) return;
+  const int64_t lo = c * CQ;
+  const int len = static_cast<int>(min(static_cast<int64_t>(CQ), n_q - lo));
+  // the chunk's query keys, staged once per CTA (every warp needs all of them), stored
+  // lane-major-transposed: lane L's u-th key (chunk position L*QPL + u) at [u][L], so the
+  // per-lane reads below are bank-conflict free
+  __shared__ uint64_t s_q[CQ];
+  for (int t = threadIdx.x; t < CQ; t += kSearchThreads)
+    s_q[(t % QPL) * 32 + t / QPL] = t < len ? __ldg(q + lo + t) : ~uint64_t{0};
+  __syncthreads();
+  if (k >= K3) return;  // no CTA barrier below
   uint64_t* bar = &s_bar[warp];
   if (lane == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncwarp();
-  const int64_t lo = c * CQ;
-  const int len = static_cast<int>(min(static_cast<int64_t>(CQ), n_q - lo));
   const int3 d = og.at(k);
   // lane-contiguous queries: lane L owns chunk positions [L*QPL, (L+1)*QPL), so a lane's
   // consecutive sorted queries can be merged against the sorted block (galloping)
@@ -674,10 +681,11 @@ __global__ void __launch_bounds__(kSearchThreads) k_search(
   int res[QPL];
 #pragma unroll
   for (int u = 0; u < QPL; ++u) {
-    key[u] = qb + u < len ? segment_key(__ldg(q + lo + qb + u), d) : ~uint64_t{0};
+    key[u] = qb + u < len ? segment_key(s_q[u * 32 + lane], d) : ~uint64_t{0};
     res[u] = -1;
   }
-  const uint64_t key_lo = segment_key(__ldg(q + lo), d), key_hi = segment_key(__ldg(q + lo + len - 1), d);
+  const uint64_t key_lo = segment_key(s_q[0], d),
+                 key_hi = segment_key(s_q[((len - 1) % QPL) * 32 + (len - 1) / QPL], d);
   const int64_t nb = (n_src + B - 1) / B;
   const int64_t blo =
       warp_first_pivot_ge(src, n_src, B, 0, nb, key_lo, lane, ((lo * n_src) / max(n_q, int64_t{1})) / B);
@@ -718,24 +726,28 @@ __global__ void __launch_bounds__(kSearchThreads) k_search(
     for (int u = 0; u < QPL; ++u) {
       if (blk[u] < 0) continue;
       const int w0 = blk[u] * B, end = w0 + min(B, wlen - w0);
-      bool bsearch = blk[u] != pblk;
-      if (!bsearch) {
-        int steps = 0;
-        while (p < end - 1 && s_win[p] < key[u] && steps < 6) {
-          ++p;
-          ++steps;
+      int base = w0, n = end - w0;  // lower bound of key[u] in [base, base + n), clamped to the last
+      if (blk[u] == pblk) {  // same block as the lane's previous (smaller) query: exponential search from p
+        if (p < end - 1 && s_win[p] < key[u]) {  // invariant: s_win[lo_] < key
+          int lo_ = p, hi_ = p + 1, step = 1;
+          while (hi_ < end - 1 && s_win[hi_] < key[u]) {
+            lo_ = hi_;
+            step <<= 1;
+            hi_ = min(p + step, end - 1);
+          }
+          base = lo_ + 1;
+          n = hi_ - lo_;
+        } else {
+          n = 1;
+          base = p;
         }
-        bsearch = p < end - 1 && s_win[p] < key[u];
       }
-      if (bsearch) {
-        int base = blk[u] != pblk ? w0 : p, n = end - base;
-        while (n > 1) {
-          const int h = n >> 1;
-          base += s_win[base + h - 1] < key[u] ? h : 0;
-          n -= h;
-        }
-        p = base;
+      while (n > 1) {
+        const int h = n >> 1;
+        base += s_win[base + h - 1] < key[u] ? h : 0;
+        n -= h;
       }
+      p = base;
       pblk = blk[u];
       if (s_win[p] == key[u]) res[u] = src_idx ? s_widx[p] : static_cast<int32_t>(g0 + p);
     }
@@ -1190,7 +1202,7 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
       const bool one_launch = coop_cap > 0 && n <= static_cast<int64_t>(coop_cap) * kCoopThreads * kCoopMaxE &&
                               !(std::getenv("SCONV_FLOOR_CUB") && std::getenv("SCONV_FLOOR_CUB")[0] == '1');
       if (one_launch) {  // everything below in one cooperative launch
-        int e = 1;
+        int e = coop_rows_per_thread();
         while (ceil_div<int64_t>(n, int64_t{kCoopThreads} * e) > coop_cap) e *= 2;
         const int tile = kCoopThreads * e;
         const unsigned G = static_cast<unsigned>(ceil_div<int64_t>(n, tile));
