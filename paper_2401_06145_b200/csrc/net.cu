@@ -183,9 +183,38 @@ void NetData::make_plan() {
   }
 }
 
+NetData::~NetData() {
+  maps.clear();  // frees enqueued on the streams the buffers were allocated on
+  coordsets.clear();
+  tensors.clear();
+  if (map_stream) {
+    cudaStreamSynchronize(map_stream);
+    cudaStreamDestroy(map_stream);
+  }
+  if (ev_order) cudaEventDestroy(ev_order);
+}
+
 void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f_dtype, int f_mem, int c_in) {
   if (f_dtype != SCONV_F32) fail(SCONV_ERR_ARG, "network input features must be fp32");
   const cudaStream_t st = ctx.stream;
+  static const bool use_map_stream = [] {
+    const char* e = std::getenv("SCONV_NET_MAP_STREAM");
+    return !(e && e[0] == '0');
+  }();
+  if (!ev_order) SCONV_CUDA(cudaEventCreateWithFlags(&ev_order, cudaEventDisableTiming));
+  if (use_map_stream && !map_stream) {
+    int lo = 0, hi = 0;
+    SCONV_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    SCONV_CUDA(cudaStreamCreateWithPriority(&map_stream, cudaStreamNonBlocking, hi));
+  }
+  const cudaStream_t ms = use_map_stream ? map_stream : st;
+  // the map stream starts after everything already on the context stream: the input
+  // coordinates may be produced there, and the previous forward's maps (freed below, on the
+  // map stream) may still be in use by its convs
+  if (ms != st) {
+    SCONV_CUDA(cudaEventRecord(ev_order, st));
+    SCONV_CUDA(cudaStreamWaitEvent(ms, ev_order));
+  }
   if (!planned) {
     make_plan();
     planned = true;
@@ -256,8 +285,22 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
           T.sorted = true;
         }
         // maps over the network's own (already validated) coordinate sets skip the canonical
-        // lists and the end-of-build sync unless a GMaS conv asks for them
-        auto m = build_map(ctx, P, mcfg, o.transposed ? &T : nullptr, false, /*lazy=*/true);
+        // lists and the end-of-build sync unless a GMaS conv asks for them; built on the map
+        // stream (with the fused row order when a fused conv may use them)
+        std::unique_ptr<MapData> m;
+        ctx.stream = ms;
+        try {
+          m = build_map(ctx, P, mcfg, o.transposed ? &T : nullptr, false, /*lazy=*/true);
+          if (pl.dataflow != SCONV_DATAFLOW_GMAS) prepare_fused_layout(ctx, *m);
+        } catch (...) {
+          ctx.stream = st;
+          throw;
+        }
+        ctx.stream = st;
+        if (ms != st) {
+          SCONV_CUDA(cudaEventRecord(ev_order, ms));
+          SCONV_CUDA(cudaStreamWaitEvent(st, ev_order));
+        }
         ++maps_built;
         if (!coordsets[a.coordset].keys && coordsets[a.coordset].sorted)
           coordsets[a.coordset].keys = m->src_keys;  // sorted raw input: its packed keys, same row order
@@ -394,6 +437,10 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
       out.ld = out.channels;
       out.feats = std::move(nb);
     }
+  }
+  if (ms != st) {  // readers of the forward's coordinates (map-stream buffers) use the context stream
+    SCONV_CUDA(cudaEventRecord(ev_order, ms));
+    SCONV_CUDA(cudaStreamWaitEvent(st, ev_order));
   }
 }
 

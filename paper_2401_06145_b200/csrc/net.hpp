@@ -73,7 +73,17 @@ struct NetData {
   // per CONV op of the last forward: n_in, n_out, |M|, R_pad (0 when fused), c_in, c_out, k_pad, K3,
   // dataflow, residual folded (0/1)
   std::vector<std::array<int64_t, 10>> conv_stats;
+  // Kernel maps depend on coordinates only: they are built (and their fused row order
+  // prepared) on a second, high-priority stream, so a map build and its host syncs overlap the
+  // previous layers' convs; the context stream waits on an event before the first conv using
+  // the map. SCONV_NET_MAP_STREAM=0 builds them on the context stream (A/B).
+  cudaStream_t map_stream = nullptr;
+  cudaEvent_t ev_order = nullptr;
 
+  NetData() = default;
+  NetData(const NetData&) = delete;
+  NetData& operator=(const NetData&) = delete;
+  ~NetData();
   void check_ops() const;
   void make_plan();
   void forward(Ctx& ctx, const MapSource& input, const void* feats, int f_dtype, int f_mem, int c_in);
