@@ -25,6 +25,7 @@ launching stream, summed, max over ranks.
 SPEC's Map/GMaS on its geometry) on all host threads, same workload, bounded sample.
 """
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -79,6 +80,9 @@ class ClockSampler:
     def __init__(self, index):
         self.samples, self.reasons, self.stop_ev = [], set(), threading.Event()
         self.ok = False
+        # NVML calls take driver locks and the GIL: polled too often they stall the forward's
+        # host syncs (measured: sporadic 5-8 ms steps at a 5 ms interval)
+        self.interval = float(os.environ.get("BENCH_CLOCK_INTERVAL", "0.05"))
         try:
             import pynvml as nv
             nv.nvmlInit()
@@ -100,7 +104,7 @@ class ClockSampler:
                         self.reasons.add(k)
             except Exception:
                 pass
-            time.sleep(0.005)
+            time.sleep(self.interval)
 
     def __enter__(self):
         if self.ok:
@@ -397,6 +401,10 @@ def main():
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
+    # a generational GC pass (~30 ms with torch loaded) inside a step stalls the host syncs of
+    # the forward and shows up as one slow step: collect now, none inside the timed loops
+    gc.collect()
+    gc.disable()
     with ClockSampler(local) as clk:
         for a, b in ev:
             ctx.flush_l2(256 << 20)
@@ -408,7 +416,9 @@ def main():
     prof = ctx.profile()
     ctx.set_profiling(False)
     ctx.set_profile_filter(None)
-    total_ms = sum(a.elapsed_time(b) for a, b in ev)
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = sum(step_ms)
+    print("step ms: " + " ".join(f"{t:.3f}" for t in step_ms), file=sys.stderr)
     t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
     if dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -428,6 +438,7 @@ def main():
     if dist:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     e2e_pps = world * wl.points / float(e2e_t.item())
+    gc.enable()
 
     # roofline of the dominant kernel: algorithmic bytes / measured duration
     hbm, _, peak_kind = load_peaks()
