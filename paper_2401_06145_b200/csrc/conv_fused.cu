@@ -983,9 +983,10 @@ void prepare_fused_layout(Ctx& ctx, MapData& m) {
   SCONV_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp, keys.get<uint32_t>(), keys_sorted.get<uint32_t>(),
                                              idx.get<int32_t>(), m.row_perm.get<int32_t>(), static_cast<int>(n),
                                              begin_bit, K3, st));
-  ctx.scratch_misc.reserve(temp, st);
+  DevBuf cub_temp;  // own scratch: networks run this on a stream beside the map builds
+  cub_temp.alloc(std::max<size_t>(temp, 16), st);
   ctx.launch("cub_radix_sort_masks", [&] {
-    cub::DeviceRadixSort::SortPairs(ctx.scratch_misc.get(), temp, keys.get<uint32_t>(), keys_sorted.get<uint32_t>(),
+    cub::DeviceRadixSort::SortPairs(cub_temp.get(), temp, keys.get<uint32_t>(), keys_sorted.get<uint32_t>(),
                                     idx.get<int32_t>(), m.row_perm.get<int32_t>(), static_cast<int>(n), begin_bit, K3,
                                     st);
   });

@@ -187,10 +187,11 @@ NetData::~NetData() {
   maps.clear();  // frees enqueued on the streams the buffers were allocated on
   coordsets.clear();
   tensors.clear();
-  if (map_stream) {
-    cudaStreamSynchronize(map_stream);
-    cudaStreamDestroy(map_stream);
-  }
+  for (cudaStream_t* sp : {&map_stream, &layout_stream})
+    if (*sp) {
+      cudaStreamSynchronize(*sp);
+      cudaStreamDestroy(*sp);
+    }
   if (ev_order) cudaEventDestroy(ev_order);
 }
 
@@ -206,14 +207,17 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
     int lo = 0, hi = 0;
     SCONV_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     SCONV_CUDA(cudaStreamCreateWithPriority(&map_stream, cudaStreamNonBlocking, hi));
+    SCONV_CUDA(cudaStreamCreateWithPriority(&layout_stream, cudaStreamNonBlocking, hi));
   }
   const cudaStream_t ms = use_map_stream ? map_stream : st;
+  const cudaStream_t ls = use_map_stream ? layout_stream : st;
   // the map stream starts after everything already on the context stream: the input
   // coordinates may be produced there, and the previous forward's maps (freed below, on the
   // map stream) may still be in use by its convs
   if (ms != st) {
     SCONV_CUDA(cudaEventRecord(ev_order, st));
     SCONV_CUDA(cudaStreamWaitEvent(ms, ev_order));
+    SCONV_CUDA(cudaStreamWaitEvent(ls, ev_order));
   }
   if (!planned) {
     make_plan();
@@ -291,14 +295,20 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
         ctx.stream = ms;
         try {
           m = build_map(ctx, P, mcfg, o.transposed ? &T : nullptr, false, /*lazy=*/true);
+          if (ms != st) {  // the row order runs beside the coordinate chain (next level's map)
+            SCONV_CUDA(cudaEventRecord(ev_order, ms));
+            SCONV_CUDA(cudaStreamWaitEvent(ls, ev_order));
+            SCONV_CUDA(cudaStreamWaitEvent(st, ev_order));
+          }
+          ctx.stream = ls;
           if (pl.dataflow != SCONV_DATAFLOW_GMAS) prepare_fused_layout(ctx, *m);
         } catch (...) {
           ctx.stream = st;
           throw;
         }
         ctx.stream = st;
-        if (ms != st) {
-          SCONV_CUDA(cudaEventRecord(ev_order, ms));
+        if (ls != st) {
+          SCONV_CUDA(cudaEventRecord(ev_order, ls));
           SCONV_CUDA(cudaStreamWaitEvent(st, ev_order));
         }
         ++maps_built;
@@ -440,6 +450,8 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
   }
   if (ms != st) {  // readers of the forward's coordinates (map-stream buffers) use the context stream
     SCONV_CUDA(cudaEventRecord(ev_order, ms));
+    SCONV_CUDA(cudaStreamWaitEvent(st, ev_order));
+    SCONV_CUDA(cudaEventRecord(ev_order, ls));
     SCONV_CUDA(cudaStreamWaitEvent(st, ev_order));
   }
 }

@@ -78,6 +78,7 @@ struct NetData {
   // previous layers' convs; the context stream waits on an event before the first conv using
   // the map. SCONV_NET_MAP_STREAM=0 builds them on the context stream (A/B).
   cudaStream_t map_stream = nullptr;
+  cudaStream_t layout_stream = nullptr;  // fused row order (mask sort): off the coordinate chain
   cudaEvent_t ev_order = nullptr;
 
   NetData() = default;
