@@ -303,6 +303,27 @@ def test_fused_matches_gmas(ctx):
     np.testing.assert_array_equal(b, c)  # deterministic
 
 
+@pytest.mark.parametrize("n", [450_000, 800_000])
+def test_large_fused_layout_and_strided_coords(ctx, n):
+    """Row counts beyond one row per thread of the co-resident grid (~3e5 on a B200): the
+    one-launch mask sort and Eq. 1 kernels then hold 2 or 4 rows per thread. Strided output
+    coordinates must equal numpy's floor + unique, and the fused layer (mask-sorted rows) must
+    match the GMaS dataflow on the same map."""
+    rng = np.random.default_rng(n)
+    xyz = random_cloud(rng, n, 160, origin=-80)
+    m2 = sc.KernelMap.build(ctx, xyz, False, 2, 1, 2)
+    q = m2.read()[0]
+    fl = np.unique(np.floor_divide(xyz.astype(np.int64), 2) * 2, axis=0)
+    np.testing.assert_array_equal(q, fl.astype(np.int32))
+    F = rng.random((len(xyz), 16), dtype=np.float32)
+    W = ((rng.random((27, 16, 16)) * 0.2 - 0.1)).astype(np.float32)
+    m = sc.KernelMap.build(ctx, xyz, False, 3, 1, 1)
+    w = sc.Weights(ctx, W)
+    a = sc.layer_forward(ctx, m, w, F, sc.exec_cfg(partial_f16=0))
+    b = sc.layer_forward(ctx, m, w, F, sc.exec_cfg(dataflow=sc.DATAFLOW_FUSED))
+    assert rel_errors(b, a)[0] <= 5e-6
+
+
 def test_layer_bf16(ctx, oracle):
     rng = np.random.default_rng(3)
     xyz = random_cloud(rng, 5000, 30)
