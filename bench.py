@@ -233,6 +233,11 @@ class LayerWorkload:
         self.W = sc.generate_weights(1, 1, 27, self.c, self.c)
         self.w = sc.Weights(ctx, self.W, dtype)
         self.xyz_d, self.F_d = torch.from_numpy(self.xyz).cuda(), torch.from_numpy(self.F).cuda()
+        # e2e host buffers in pinned memory (inputs and results), as for the network workloads
+        pin = lambda a: torch.from_numpy(a).pin_memory().numpy()
+        self.xyz_h, self.F_h = pin(self.xyz), pin(self.F)
+        self.oxyz_h = torch.empty((self.N, 3), dtype=torch.int32).pin_memory().numpy()
+        self.of_h = torch.empty((self.N, self.c), dtype=torch.float32).pin_memory().numpy()
         self.out_d = torch.empty((self.N, self.c), dtype=torch.float32, device="cuda")
         self.points = self.N
         m = self._map()
@@ -276,8 +281,9 @@ class LayerWorkload:
         m.free()
 
     def e2e_step(self):
-        out = self.sc.sc_layer_forward(self.ctx, self.sc.PointCloud(self.xyz, self.F, False), self.W, 3, 1, self.cfg)
-        return self.xyz.nbytes + self.F.nbytes + self.W.nbytes, out.coords.nbytes + out.features.nbytes
+        out = self.sc.sc_layer_forward(self.ctx, self.sc.PointCloud(self.xyz_h, self.F_h, False), self.W, 3, 1,
+                                       self.cfg, out_coords=self.oxyz_h, out_features=self.of_h)
+        return self.xyz_h.nbytes + self.F_h.nbytes + self.W.nbytes, out.coords.nbytes + out.features.nbytes
 
     def extra(self):
         return {}

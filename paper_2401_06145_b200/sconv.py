@@ -404,19 +404,28 @@ def build_kernel_map_sorted(ctx: Context, P: PointCloud, K: int, s: int, B: int 
 
 
 def sc_layer_forward(ctx: Context, cloud: PointCloud, W: np.ndarray, K: int, s: int,
-                     cfg: Optional[ExecCfg] = None) -> PointCloud:
-    """SPEC sc_layer_forward through the one-shot C entry point."""
+                     cfg: Optional[ExecCfg] = None, out_coords: Optional[np.ndarray] = None,
+                     out_features: Optional[np.ndarray] = None) -> PointCloud:
+    """SPEC sc_layer_forward through the one-shot C entry point.
+    out_coords [n, 3] int32 / out_features [n, c_out] float32: optional caller buffers (e.g.
+    pinned host memory, so the device->host copies are DMA at full link speed)."""
     xyz = np.ascontiguousarray(cloud.coords, dtype=np.int32).reshape(-1, 3)
     f = np.ascontiguousarray(cloud.features, dtype=np.float32)
     W = np.ascontiguousarray(W, dtype=np.float32)
     c_in, c_out = W.shape[1], W.shape[2]
-    out_xyz = np.empty_like(xyz)
-    out_f = np.empty((len(xyz), c_out), np.float32)
+    out_xyz = np.empty_like(xyz) if out_coords is None else out_coords
+    out_f = np.empty((len(xyz), c_out), np.float32) if out_features is None else out_features
+    if out_xyz.shape != xyz.shape or out_xyz.dtype != np.int32 or not out_xyz.flags.c_contiguous:
+        raise InvalidArgument("out_coords must be a contiguous int32 [n, 3] array")
+    if out_f.shape != (len(xyz), c_out) or out_f.dtype != np.float32 or not out_f.flags.c_contiguous:
+        raise InvalidArgument("out_features must be a contiguous float32 [n, c_out] array")
     n_out = C.c_int64()
     cfg = cfg or exec_cfg()
     ctx.check(ctx.lib.sconv_sc_layer_forward(ctx.h, _ptr(xyz), len(xyz), int(cloud.sorted), _ptr(f), c_in, _ptr(W),
                                              c_out, K, s, C.byref(cfg), _ptr(out_xyz), C.byref(n_out), _ptr(out_f)))
     n = n_out.value
+    if out_coords is not None or out_features is not None:
+        return PointCloud(out_xyz[:n], out_f[:n], True)  # views of the caller's buffers
     return PointCloud(out_xyz[:n].copy(), out_f[:n].copy(), True)
 
 
