@@ -338,6 +338,16 @@ sconv_status sconv_ctx_create(int device, sconv_ctx** out) {
     SCONV_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
     uint64_t threshold = UINT64_MAX;
     SCONV_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
+    {  // pre-grow the pool: later stream-ordered allocations (three streams in a network
+       // forward) are carved from retained memory instead of mapping new physical pages
+       // mid-forward (a sporadic multi-ms stall)
+      void* warm = nullptr;
+      if (cudaMallocAsync(&warm, size_t{4} << 30, ctx->own_stream) == cudaSuccess) {
+        cudaFreeAsync(warm, ctx->own_stream);
+        cudaStreamSynchronize(ctx->own_stream);
+      }
+      cudaGetLastError();
+    }
     SCONV_CUDA(cudaMalloc(reinterpret_cast<void**>(&ctx->done), 64));
     SCONV_CUDA(cudaMemset(ctx->done, 0, 64));
     const size_t sort_bytes = sizeof(int) * (3 * 65536 + 8);

@@ -691,6 +691,55 @@ __global__ void __launch_bounds__(kCoopThreads) k_mask_sort(
   }
 }
 
+// Small kernels (K^3 <= 8: the K=2 stride-2 down / transposed up maps) are grouped by
+// neighbour mask with a 256-bin bucket sort: an up-sampling output has exactly one of the 8
+// offsets, so an unsorted 128-row tile gathers all 8 (7/8 of it zero rows). Pass 1: mask per
+// row + global histogram. Pass 2: each CTA scans the histogram, reserves its per-bin ranges
+// with one atomic per bin, and scatters rows and their nbr entries. The order inside a bin is
+// not deterministic, and need not be: rows are independent (each output row's sum is the same
+// whatever rows share its tile: absent offsets add exact zeros), and the fused kernel writes
+// each row back to its original position.
+constexpr int kBucketThreads = 256;
+__global__ void __launch_bounds__(kBucketThreads) k_bucket_count(const int32_t* __restrict__ nbr, int64_t n, int K3,
+                                                                 uint8_t* __restrict__ masks, int* __restrict__ hist) {
+  __shared__ int s_hist[256];
+  s_hist[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t i = blockIdx.x * int64_t{kBucketThreads} + threadIdx.x;
+  if (i < n) {
+    uint32_t mk = 0;
+    for (int k = 0; k < K3; ++k) mk |= static_cast<uint32_t>(__ldg(nbr + int64_t{k} * n + i) >= 0) << k;
+    masks[i] = static_cast<uint8_t>(mk);
+    atomicAdd(&s_hist[mk], 1);
+  }
+  __syncthreads();
+  if (s_hist[threadIdx.x]) atomicAdd(&hist[threadIdx.x], s_hist[threadIdx.x]);
+}
+
+__global__ void __launch_bounds__(kBucketThreads) k_bucket_scatter(const int32_t* __restrict__ nbr, int64_t n, int K3,
+                                                                   const uint8_t* __restrict__ masks,
+                                                                   const int* __restrict__ hist, int* __restrict__ cursor,
+                                                                   int32_t* __restrict__ perm, int32_t* __restrict__ nbr_perm) {
+  __shared__ int s_start[256], s_cnt[256];
+  const int tid = threadIdx.x;
+  int start;
+  block_exclusive_scan(__ldg(hist + tid), start);  // bin b -> rows with neighbour mask b
+  s_start[tid] = start;
+  s_cnt[tid] = 0;
+  __syncthreads();
+  const int64_t i = blockIdx.x * int64_t{kBucketThreads} + tid;
+  const int mk = i < n ? masks[i] : 0;
+  const int rank = i < n ? atomicAdd(&s_cnt[mk], 1) : 0;
+  __syncthreads();
+  if (s_cnt[tid]) s_start[tid] += atomicAdd(&cursor[tid], s_cnt[tid]);
+  __syncthreads();
+  if (i < n) {
+    const int64_t pos = s_start[mk] + rank;
+    perm[pos] = static_cast<int32_t>(i);
+    for (int k = 0; k < K3; ++k) nbr_perm[int64_t{k} * n + pos] = __ldg(nbr + int64_t{k} * n + i);
+  }
+}
+
 // nbr_perm[k][r] = nbr_in[k][perm[r]] (coalesced writes; reads gathered from L2)
 __global__ void k_permute_nbr(const int32_t* __restrict__ nbr, const int32_t* __restrict__ perm, int64_t n, int K3,
                               int32_t* __restrict__ out) {
@@ -905,11 +954,39 @@ void prepare_fused_layout(Ctx& ctx, MapData& m) {
   // Only submanifold maps (stride 1, not transposed, K3 >= 27) are reordered: networks reuse
   // them for 4-8 convs, so the sort (~40 us at 1.2e5 rows) amortises; strided / transposed
   // maps serve a single conv.
-  m.permuted = K3 >= 27 && K3 <= 32 && m.cfg.out_stride == 1 && !m.cfg.transposed && n > 2 * 128 &&
-               n <= INT32_MAX;
+  // K3 <= 8 maps (K=2 down / up): cheap two-pass bucket order (SCONV_SMALL_PERMUTE=0: off). It
+  // pays only where the build runs off the critical path (networks: layout stream), so the
+  // single-layer API keeps these maps in order.
+  static const bool small_permute = [] {
+    const char* e = std::getenv("SCONV_SMALL_PERMUTE");
+    return !(e && e[0] == '0');
+  }();
+  const bool small = small_permute && m.layout_off_path && K3 >= 2 && K3 <= 8 && n > 2 * 128 && n <= INT32_MAX;
+  m.permuted = small || (K3 >= 27 && K3 <= 32 && m.cfg.out_stride == 1 && !m.cfg.transposed && n > 2 * 128 &&
+                         n <= INT32_MAX);
   if (const char* e = std::getenv("SCONV_NO_PERMUTE"); e && e[0] == '1') m.permuted = false;  // experiments
   if (const char* e = std::getenv("SCONV_PERMUTE_MIN"); e && n < std::atoll(e)) m.permuted = false;
   if (!m.permuted) return;
+  if (small) {
+    const cudaStream_t st = ctx.stream;
+    DevBuf masks, bins;
+    masks.alloc(n, st);
+    bins.alloc(2 * 256 * sizeof(int), st);
+    m.row_perm.alloc(4 * n, st);
+    m.nbr_perm.alloc(4 * n * K3, st);
+    SCONV_CUDA(cudaMemsetAsync(bins.get(), 0, 2 * 256 * sizeof(int), st));
+    const unsigned blocks = static_cast<unsigned>(ceil_div<int64_t>(n, kBucketThreads));
+    int* hist = bins.get<int>();
+    ctx.launch("k_bucket_count", [&] {
+      k_bucket_count<<<blocks, kBucketThreads, 0, st>>>(m.nbr_in.get<int32_t>(), n, K3, masks.get<uint8_t>(), hist);
+    });
+    ctx.launch("k_bucket_scatter", [&] {
+      k_bucket_scatter<<<blocks, kBucketThreads, 0, st>>>(m.nbr_in.get<int32_t>(), n, K3, masks.get<uint8_t>(), hist,
+                                                          hist + 256, m.row_perm.get<int32_t>(),
+                                                          m.nbr_perm.get<int32_t>());
+    });
+    return;
+  }
   // Bit position per offset: rarer offsets (larger L1 norm: corners, then edges, then faces,
   // the always-present centre last) in the more significant bits, so equal-or-similar masks
   // end up adjacent (KITTI scan: 25.4 -> 10.4 active offsets per 128-row tile).

@@ -36,7 +36,8 @@ struct MapData {
   // Canonical pair lists (scan + emit + one readback sync) are built lazily for network maps:
   // the fused dataflow needs only nbr_in (ensure_canonical() before using sizes/pairs/nbr_pos).
   bool canonical = true;
-  bool identity_pending = false;  // lazy 1x1 identity map: arrays not yet written (nbr_in[i] = i)
+  bool identity_pending = false;
+  bool layout_off_path = false;  // fused row order built beside the convs (network layout stream)  // lazy 1x1 identity map: arrays not yet written (nbr_in[i] = i)
   struct Pending {
     DevBuf counts, offs, tiles, flags;
     int64_t nchunk = 0, grid = 0, ntiles = 0;

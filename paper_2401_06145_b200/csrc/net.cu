@@ -231,6 +231,7 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
   }
   coordsets.clear();
   maps.clear();
+  int convs_issued = 0;
   maps_built = 0;
   conv_stats.clear();
   // coordinate set 0 = the raw input (may be unsorted)
@@ -301,6 +302,8 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
             SCONV_CUDA(cudaStreamWaitEvent(st, ev_order));
           }
           ctx.stream = ls;
+          // off the critical path only when convs are already queued ahead of this map's first use
+          m->layout_off_path = ls != st && convs_issued > 0;
           if (pl.dataflow != SCONV_DATAFLOW_GMAS) prepare_fused_layout(ctx, *m);
         } catch (...) {
           ctx.stream = st;
@@ -388,6 +391,7 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
       out.ld = o.c_out;
       out.feats = std::move(nb);
       if (pl.out != o.out) tensors.at(o.out).fused_away = true;
+      ++convs_issued;
       conv_stats.push_back({m.n_in, m.n_out, m.total, df == SCONV_DATAFLOW_FUSED ? 0 : m.buffer_length, w.c_in, w.c_out,
                             w.k_pad, m.K3, df, pl.res >= 0 ? 1 : 0});
     } else {
