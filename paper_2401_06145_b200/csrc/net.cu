@@ -211,6 +211,29 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
   }
   const cudaStream_t ms = use_map_stream ? map_stream : st;
   const cudaStream_t ls = use_map_stream ? layout_stream : st;
+  // SCONV_NET_WAIT_PROFILE=1: time how long the context stream waits for each map and row
+  // order (events around the wait; printed at the end of the forward). Measured r01q: ~205 us
+  // per MinkUNet42 forward, mostly the level 0-2 row orders; running the first conv of each
+  // level in output order instead removes the waits but not the time (that conv is ~2x slower)
+  static const bool wait_profile = [] {
+    const char* e = std::getenv("SCONV_NET_WAIT_PROFILE");
+    return e && e[0] == '1';
+  }();
+  std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>> waits;
+  auto wait_for = [&](cudaStream_t from, int op) {
+    SCONV_CUDA(cudaEventRecord(ev_order, from));
+    if (!wait_profile) {
+      SCONV_CUDA(cudaStreamWaitEvent(st, ev_order));
+      return;
+    }
+    cudaEvent_t a, b;
+    SCONV_CUDA(cudaEventCreate(&a));
+    SCONV_CUDA(cudaEventCreate(&b));
+    SCONV_CUDA(cudaEventRecord(a, st));
+    SCONV_CUDA(cudaStreamWaitEvent(st, ev_order));
+    SCONV_CUDA(cudaEventRecord(b, st));
+    waits.emplace_back(op, a, b);
+  };
   // the map stream starts after everything already on the context stream: the input
   // coordinates may be produced there, and the previous forward's maps (freed below, on the
   // map stream) may still be in use by its convs
@@ -299,7 +322,7 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
           if (ms != st) {  // the row order runs beside the coordinate chain (next level's map)
             SCONV_CUDA(cudaEventRecord(ev_order, ms));
             SCONV_CUDA(cudaStreamWaitEvent(ls, ev_order));
-            SCONV_CUDA(cudaStreamWaitEvent(st, ev_order));
+            wait_for(ms, oi);
           }
           ctx.stream = ls;
           // off the critical path only when convs are already queued ahead of this map's first use
@@ -310,10 +333,7 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
           throw;
         }
         ctx.stream = st;
-        if (ls != st) {
-          SCONV_CUDA(cudaEventRecord(ev_order, ls));
-          SCONV_CUDA(cudaStreamWaitEvent(st, ev_order));
-        }
+        if (ls != st) wait_for(ls, 1000 + oi);
         ++maps_built;
         if (!coordsets[a.coordset].keys && coordsets[a.coordset].sorted)
           coordsets[a.coordset].keys = m->src_keys;  // sorted raw input: its packed keys, same row order
@@ -457,6 +477,20 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
     SCONV_CUDA(cudaStreamWaitEvent(st, ev_order));
     SCONV_CUDA(cudaEventRecord(ev_order, ls));
     SCONV_CUDA(cudaStreamWaitEvent(st, ev_order));
+  }
+  if (!waits.empty()) {  // SCONV_NET_WAIT_PROFILE
+    SCONV_CUDA(cudaStreamSynchronize(st));
+    double total = 0;
+    for (auto& [op, a, b] : waits) {
+      float ms_ = 0;
+      cudaEventElapsedTime(&ms_, a, b);
+      total += ms_;
+      if (ms_ > 0.001f)
+        std::fprintf(stderr, "[sconv wait] op %d %s %.1f us\n", op % 1000, op >= 1000 ? "layout" : "map", 1e3 * ms_);
+      cudaEventDestroy(a);
+      cudaEventDestroy(b);
+    }
+    std::fprintf(stderr, "[sconv wait] total %.1f us over %zu waits\n", 1e3 * total, waits.size());
   }
 }
 
