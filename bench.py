@@ -205,8 +205,10 @@ class NetWorkload:
         """Per launch, averaged over the network's convs (the roofline divides by the average
         launch duration of the dominant kernel type)."""
         tot = self.net.algo_bytes()
-        nconv = len(self.g.convs()) * len(self.scenes)
-        return {k: v * len(self.scenes) / nconv for k, v in tot.items()}
+        nconv = len(self.g.convs())
+        per = {k: v / nconv for k, v in tot.items() if not k.startswith("_") and k != "k_search"}
+        per["k_search"] = tot["k_search"] / max(1, tot["_k_search_launches"])  # one launch per map
+        return per
 
     def cpu_sample(self, workers, budget_s=20.0):
         """Oracle network on a crop of scene 0, grown until ~budget_s/3 of CPU work."""

@@ -257,15 +257,19 @@ class Network:
         16-bit activations, 16-bit gather buffer, `part_bytes` GEMM partials, 16-bit outputs).
         Fused convs: input rows read once (2*ci*n), the nbr table (4*K3*q), output (+residual) once."""
         g = e = s = f = 0
+        maps = {}  # distinct searched maps (identity 1x1 maps need no search): SURVEY §8d Map bytes
         for st in self.conv_stats():
             n, q, M, R, ci, co, kp, K3, df, res = (st[k] for k in self.STAT_KEYS)
+            if K3 > 1:
+                maps[(n, q, M, K3)] = 8 * n + 8 * q + 8 * M + 4 * K3
             if df == 1:
                 f += 2 * ci * n + 4 * K3 * q + 2 * co * q * (2 if res else 1)
                 continue
             g += 2 * ci * n + 2 * kp * R + 4 * M
             e += 2 * kp * R + part_bytes * co * R + 2 * K3 * ci * co
             s += part_bytes * co * M + 4 * K3 * q + 2 * co * q * (2 if res else 1)
-        return {"k_gather": g, "k_gemm_grouped": e, "k_scatter": s, "k_conv_fused": f}
+        return {"k_gather": g, "k_gemm_grouped": e, "k_scatter": s, "k_conv_fused": f,
+                "k_search": sum(maps.values()), "_k_search_launches": len(maps)}
 
     def free(self):
         if self.h:
