@@ -319,10 +319,10 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
         ctx.stream = ms;
         try {
           m = build_map(ctx, P, mcfg, o.transposed ? &T : nullptr, false, /*lazy=*/true);
-          if (ms != st) {  // the row order runs beside the coordinate chain (next level's map)
+          if (ms != st) {  // the row order runs beside the coordinate chain (next level's map);
+            // the context stream waits on the layout stream below, which implies this map
             SCONV_CUDA(cudaEventRecord(ev_order, ms));
             SCONV_CUDA(cudaStreamWaitEvent(ls, ev_order));
-            wait_for(ms, oi);
           }
           ctx.stream = ls;
           // off the critical path only when convs are already queued ahead of this map's first use
