@@ -10,19 +10,25 @@ ms_per_step = latency of one step. Workloads (BASELINE.json configs):
                        geometry + GMaS for all 49 convs (42 SC + 7 1x1) + residual/concat ops
   c1_layer_100k        (configs[0]) one submanifold 3^3 layer, 32->32, 100k voxels in 400^3
   c3_resnet21d_s3dis   (configs[2]) SparseResNet21D (width x2) on an S3DIS-shaped room
-  c4_unet_pair_shapenet (configs[3]) K=2 s=2 down + transposed pair on ShapeNet-shaped objects
+  c4_unet_pair_shapenet (configs[3]) K=2 s=2 down + transposed pair on 8 ShapeNet-shaped
+                       objects batched in the coordinates
+  c5_minkunet42_batch64 (configs[4]) MinkUNet42 on 64 KITTI-shaped scans; a step runs this
+                       rank's contiguous share (64/N scans) and gathers every result to rank 0
 
-Multi-GPU (configs[4] shape): one process per GPU, each rank runs its OWN scene
-(scene seed = base + rank): scene sharding with no data-path collective -> weak scaling;
-NCCL carries the one-time weight broadcast from rank 0 (shard.broadcast_weights), the
-barrier and the max-over-ranks timing.
+Inputs, graphs and weights come from paper_2401_06145_b200/workloads.py (shared with the
+CPU reference arm and the full-size parity tests). Multi-GPU: one process per GPU; scenes
+are independent units (no data-path collective; weak scaling). NCCL carries the one-time
+weight broadcast from rank 0 (shard.broadcast_weights), the c5 result gather
+(shard.SceneResultGather: per-scene isend/irecv overlapped with the next scene), the barrier
+and the max-over-ranks timing. At N > 1 the c2 workload runs scan r of the batch on rank r.
 
 Inputs are device resident before the timed region; L2 (126 MB) is flushed by a 256 MB
 memset between timed steps, outside the events. Timing: CUDA events per step on the
 launching stream, summed, max over ranks.
 
 --impl reference: the CPU oracle (oracle/liboracle.so — the restatement of the reference
-SPEC's Map/GMaS on its geometry) on all host threads, same workload, bounded sample.
+SPEC's Map/GMaS on its geometry) on all host threads, on the GPU arm's own step input (c5:
+one whole scan per step); it imports nothing from the engine package.
 """
 import argparse
 import gc
@@ -49,7 +55,8 @@ def parse():
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--workload", default=DEFAULT_WORKLOAD,
-                   choices=["c2_minkunet42_kitti", "c1_layer_100k", "c3_resnet21d_s3dis", "c4_unet_pair_shapenet"])
+                   choices=["c2_minkunet42_kitti", "c1_layer_100k", "c3_resnet21d_s3dis", "c4_unet_pair_shapenet",
+                            "c5_minkunet42_batch64"])
     p.add_argument("--dtype", default="f16", choices=["f16", "bf16"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--B", type=int, default=256, help="source block size (SPEC default 256)")
@@ -123,79 +130,88 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- workloads
-def scene(name, seed):
-    from paper_2401_06145_b200 import datasets as D
-    if name == "c2_minkunet42_kitti":
-        return D.kitti_scan(seed)
-    if name == "c3_resnet21d_s3dis":
-        return D.s3dis_room(seed, n_points=870_000)
-    if name == "c4_unet_pair_shapenet":
-        return D.shapenet_object(seed)
-    raise ValueError(name)
-
-
-def graph(name):
-    from paper_2401_06145_b200 import network as N
-    return {"c2_minkunet42_kitti": N.minkunet42, "c3_resnet21d_s3dis": N.sparse_resnet21d,
-            "c4_unet_pair_shapenet": N.unet_pair}[name]()
-
-
 def oracle_crop(c, f, n):
-    """The n voxels closest to the scene's median point (a bounded CPU sample)."""
+    """The n voxels closest to the scene's median point (profiling tools only)."""
     ctr = np.median(c, axis=0)
     idx = np.sort(np.argsort(np.linalg.norm((c - ctr).astype(np.float64), axis=1), kind="stable")[:n])
     return c[idx], f[idx]
 
 
 class NetWorkload:
-    """A whole network forward per step; C4 runs a batch of objects (one after another)."""
+    """A whole network forward per scene; a step runs every scene of this rank's share.
 
-    def __init__(self, name, ctx, torch, seed, dtype, B, C, dist=None):
+    c2/c3: one scene per step on every rank (weak scaling: rank r runs scene r of the KITTI
+    batch for c2, the same room for c3); c4: the 8-object batch as one sparse tensor;
+    c5: this rank's contiguous share of the 64 scans, each result copied into a device slot
+    and gathered to rank 0 (NCCL isend/irecv overlapped with the next scene)."""
+
+    def __init__(self, name, ctx, torch, dtype, B, C, world, rank, dist=None):
         import paper_2401_06145_b200 as sc
         from paper_2401_06145_b200 import network as N
-        self.name, self.sc = name, sc
-        self.g = graph(name)
+        from paper_2401_06145_b200 import workloads as WL
+        self.name, self.sc, self.torch = name, sc, torch
+        self.g = WL.graph(name)
         if dist is not None:  # scene sharding: weights made on rank 0, one NCCL broadcast (SURVEY §8e)
             from paper_2401_06145_b200.shard import broadcast_weights
             shapes = {o.weight: (o.K ** 3, o.c_in, o.c_out) for o in self.g.convs()}
-            w0 = N.init_weights(self.g, 1) if dist.get_rank() == 0 else None
+            w0 = N.init_weights(self.g, WL.WEIGHT_SEED) if dist.get_rank() == 0 else None
             self.w = broadcast_weights(w0, shapes, src=0, device=torch.device("cuda", torch.cuda.current_device()))
         else:
-            self.w = N.init_weights(self.g, 1)
+            self.w = N.init_weights(self.g, WL.WEIGHT_SEED)
         self.net = N.Network(ctx, self.g, self.w, sc.exec_cfg(compute_dtype=dtype), B, C)
-        n_obj = 8 if name == "c4_unet_pair_shapenet" else 1
-        self.scenes = [scene(name, seed * 100 + i) for i in range(n_obj)]
-        if n_obj > 1:  # small objects: one forward over the batch encoded in the coordinates
-            from paper_2401_06145_b200 import datasets as D
-            c, f, _ = D.batch_clouds(self.scenes)
-            self.scenes = [(c, f)]
+        if name == "c2_minkunet42_kitti" and world > 1:
+            self.scenes = [WL.kitti_scene(rank)]  # each rank its own scan (rank 0: the C2 scan)
+        else:
+            self.scenes = WL.scenes(name, world, rank)
+        self.scene_ids = list(range(*WL.shard_range(WL.C5_SCENES, rank, world))) if name == "c5_minkunet42_batch64" \
+            else list(range(len(self.scenes)))
         self.dev = [(torch.from_numpy(c).cuda(), torch.from_numpy(f).cuda()) for c, f in self.scenes]
         # e2e leg: inputs and the result live in pinned host memory (page-locked numpy views)
         pin = lambda a: torch.from_numpy(a).pin_memory().numpy()  # noqa: E731
         self.pinned = [(pin(c), pin(f)) for c, f in self.scenes]
-        self.out_pinned = None
-        self.points = sum(len(c) for c, _ in self.scenes)
-        self.config = {"model": {"c2_minkunet42_kitti": "MinkUNet42", "c3_resnet21d_s3dis": "SparseResNet21D-w2",
-                                 "c4_unet_pair_shapenet": "UNetPair(K2s2 down+transposed)"}[name],
-                       "scenes_per_step": n_obj, "voxels_per_step": self.points,
-                       "batching": "batch-in-coordinates (x shifted by 256 per object)" if n_obj > 1 else "none",
+        self.out_pinned = {}
+        self.points = WL.total_points(self.scenes)
+        self.gather = None
+        if name == "c5_minkunet42_batch64":
+            from paper_2401_06145_b200.shard import SceneResultGather
+            if dist is None:
+                import types
+                dist = types.SimpleNamespace(get_rank=lambda: 0, get_world_size=lambda: 1,
+                                             all_gather_object=lambda out, obj: out.__setitem__(0, obj))
+                import paper_2401_06145_b200.shard as SH
+                SH._dist = lambda: dist  # noqa: E731  (single process: local slots only)
+            self.gather = SceneResultGather([len(c) for c, _ in self.scenes], WL.C5_SCENES,
+                                            self.g.channels[self.g.output], dtype=torch.float16,
+                                            device=torch.device("cuda", torch.cuda.current_device()))
+        model = WL.NETWORKS[name][0]
+        self.config = {"model": model, "scenes_per_step": len(self.scenes), "voxels_per_step": self.points,
+                       "batching": "batch-in-coordinates (x shifted by 256 per object)" if name.startswith("c4")
+                       else ("scene-sharded: scenes %d..%d of 64 on this rank, results gathered to rank 0"
+                             % (self.scene_ids[0], self.scene_ids[-1]) if self.gather else "none"),
                        "convs": len(self.g.convs()), "in_channels": self.g.in_channels}
 
     def step(self):
-        for xyz, f in self.dev:
+        if self.gather:
+            self.gather.begin_step()
+        for sid, (xyz, f) in zip(self.scene_ids, self.dev):
             self.net.forward(device_xyz=xyz.data_ptr(), device_feats=f.data_ptr(), n=xyz.shape[0], sorted_=True)
+            if self.gather:
+                self.net.copy_tensor(self.g.output, self.gather.slot(sid).data_ptr(), self.sc.F16)
+                self.gather.produced(sid)
+        if self.gather:
+            self.gather.end_step()
 
     def e2e_step(self):
-        import torch
+        torch = self.torch
         h2d = d2h = 0
-        for c, f in self.pinned:
+        for i, (c, f) in enumerate(self.pinned):
             self.net.forward(c, f, True)
             n, ch, _ = self.net.info(self.g.output)
-            if self.out_pinned is None or self.out_pinned.shape != (n, ch):
-                self.out_pinned = torch.empty((n, ch), dtype=torch.float32, pin_memory=True).numpy()
-            self.net.read(self.g.output, feats_out=self.out_pinned, coords=False)  # output coords = input coords
+            if self.out_pinned.get(i) is None or self.out_pinned[i].shape != (n, ch):
+                self.out_pinned[i] = torch.empty((n, ch), dtype=torch.float32, pin_memory=True).numpy()
+            self.net.read(self.g.output, feats_out=self.out_pinned[i], coords=False)  # output coords = input coords
             h2d += c.nbytes + f.nbytes
-            d2h += self.out_pinned.nbytes
+            d2h += self.out_pinned[i].nbytes
         return h2d, d2h
 
     def extra(self):
@@ -210,20 +226,26 @@ class NetWorkload:
         per["k_search"] = tot["k_search"] / max(1, tot["_k_search_launches"])  # one launch per map
         return per
 
+    def algo_flops(self):
+        """Useful flops per launch of the conv kernels (2 C_in C_out |M|)."""
+        st = self.net.conv_stats()
+        tot = sum(2 * s["c_in"] * s["c_out"] * s["M"] for s in st)
+        return tot / max(1, len(st))
+
     def cpu_sample(self, workers, budget_s=20.0):
-        """Oracle network on a crop of scene 0, grown until ~budget_s/3 of CPU work."""
+        """The CPU oracle on this workload's first scene, whole (same input as the GPU step)."""
         sys.path.insert(0, os.path.join(ROOT, "tests"))
-        from test_gpu_network import oracle_graph  # the oracle graph runner (test infrastructure)
+        from oracle_net import oracle_graph, oracle_weights  # the checker / CPU baseline (test infrastructure)
         c, f = self.scenes[0]
-        n = min(len(c), 5000)
-        while True:
-            cc, ff = oracle_crop(c, f, n)
+        w = oracle_weights(self.g, 1)
+        times = []
+        while not times or (sum(times) < budget_s / 2 and len(times) < 3):
             t0 = time.perf_counter()
-            oracle_graph(self.g, self.w, cc, ff)
-            dt = time.perf_counter() - t0
-            if dt > budget_s / 3 or n >= len(c):
-                return n / dt, f"oracle {self.config['model']} on a {n}-voxel crop of scene 0 ({dt:.1f}s)"
-            n = min(len(c), int(n * min(4.0, max(1.5, budget_s / 3 / max(dt, 1e-3)))))
+            oracle_graph(self.g, w, c, f, workers=workers)
+            times.append(time.perf_counter() - t0)
+        return len(c) / statistics.median(times), (
+            f"oracle {self.config['model']} forward on the whole first scene of the step ({len(c)} voxels, "
+            f"{len(times)} runs, median {statistics.median(times):.1f} s)")
 
 
 class LayerWorkload:
@@ -311,50 +333,70 @@ class LayerWorkload:
         return self.N / statistics.median(times), f"{len(times)} full C1 layers on the oracle, median"
 
 
-def make_workload(args, ctx, torch, rank, dist=None):
+def make_workload(args, ctx, torch, world, rank, dist=None):
     dtype = 1 if args.dtype == "f16" else 2
     if args.workload == "c1_layer_100k":
         return LayerWorkload(args.workload, ctx, torch, 1 + rank, dtype, args.B, args.C)
-    return NetWorkload(args.workload, ctx, torch, rank, dtype, args.B, args.C, dist)
+    return NetWorkload(args.workload, ctx, torch, dtype, args.B, args.C, world, rank, dist)
 
 
 # ---------------------------------------------------------------- reference arm (CPU oracle)
 def reference_arm(args):
+    """The reference's CPU path (the oracle restatement of SPEC Map + GMaS on the reference's
+    geometry; the reference ships no runnable Map/GMaS code) on the SAME inputs as the GPU arm,
+    all host threads. Imports nothing from the engine package: scenes, graphs and weights come
+    from the pure-Python workload modules (loaded by path) and the oracle's own PRNG."""
     if int(os.environ.get("RANK", "0")) != 0:
         return
     workers = os.cpu_count() or 1
     sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_lib import load_oracle
+    from oracle_net import load_pure, oracle_graph, oracle_weights
+    o = load_oracle()
+    WL = load_pure("workloads")
     if args.workload == "c1_layer_100k":
-        import paper_2401_06145_b200 as sc
-        from oracle_lib import load_oracle
-        o = load_oracle()
-        xyz, F = sc.generate_synthetic(100000, 400, 32, 1)
-        W = sc.generate_weights(1, 1, 27, 32, 32)
-        run = lambda: o.layer_forward(xyz, False, F, W, 3, 1, 1, workers=workers)  # noqa: E731
-        pts, sample = 100000, "full C1 layer per step"
+        xyz, F = o.generate_synthetic(100000, 400, 32, 1)
+        W = o.generate_weights(1, 1, 27, 32, 32)
+        units = [lambda: o.layer_forward(xyz, False, F, W, 3, 1, 1, B=args.B, Cq=args.C, workers=workers)]
+        pts = [100000]
+        sample = "the full C1 layer (100k voxels, K=3, 32->32) per step"
     else:
-        from paper_2401_06145_b200 import network as N
-        from test_gpu_network import oracle_graph
-        g = graph(args.workload)
-        w = N.init_weights(g, 1)
-        c, f = oracle_crop(*scene(args.workload, 0), 20000)
-        run = lambda: oracle_graph(g, w, c, f)  # noqa: E731
-        pts, sample = len(c), f"{len(c)}-voxel crop of scene 0 per step (the full scene is too slow on the CPU)"
-    for _ in range(min(args.warmup, 1)):
-        run()
-    times = []
-    for _ in range(args.steps):
+        g = WL.graph(args.workload)
+        w = oracle_weights(g, WL.WEIGHT_SEED)
+        if args.workload == "c5_minkunet42_batch64":
+            # 64 scans x ~6 s on the CPU do not fit a bench run: step i runs scan i of the batch
+            # (whole, same input as the GPU arm's scene i)
+            scenes = [WL.kitti_scene(i) for i in range(min(args.steps, WL.C5_SCENES))]
+            sample = "one whole scan of the 64-scan batch per step (scan i at step i)"
+        else:
+            scenes = WL.scenes(args.workload)
+            sample = "the whole workload per step (the GPU arm's step input)"
+        units = [(lambda c=c, f=f: oracle_graph(g, w, c, f, workers=workers)) for c, f in scenes]
+        pts = [len(c) for c, _ in scenes]
+    per_step = len(units) == 1 or args.workload != "c5_minkunet42_batch64"
+
+    def step(i):
+        if per_step:
+            for u in units:
+                u()
+            return sum(pts)
+        units[i % len(units)]()
+        return pts[i % len(units)]
+
+    for i in range(args.warmup):
+        step(i)
+    times, done = [], 0
+    for i in range(args.steps):
         t0 = time.perf_counter()
-        run()
+        done += step(i)
         times.append(time.perf_counter() - t0)
-        if sum(times) > 120:
-            break
-    pps = pts * len(times) / sum(times)
+    pps = done / sum(times)
     print(json.dumps({
         "metric": METRIC, "value": pps, "unit": "points/s", "n_gpus": args.gpus, "steps": len(times),
         "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32 (fp64 accumulate)", "data": "synthetic",
-        "config": {"workload": args.workload}, "impl": "reference",
+        "config": {"workload": args.workload, "voxels_per_step": done // max(1, len(times)), "B": args.B,
+                   "C": args.C, "same_input_as_gpu_arm": True}, "impl": "reference",
         "cpu_baseline": {"value": pps, "unit": "points/s", "cores": workers, "kind": "port", "sample": sample},
         "e2e": {"value": pps, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
@@ -387,7 +429,7 @@ def main():
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
-    wl = make_workload(args, ctx, torch, rank, dist)
+    wl = make_workload(args, ctx, torch, world, rank, dist)
     for _ in range(args.warmup):
         wl.step()
     torch.cuda.synchronize()
@@ -431,7 +473,11 @@ def main():
     if dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     max_total_ms = float(t.item())
-    pps = world * wl.points * args.steps / (max_total_ms / 1e3)
+    pts = torch.tensor([float(wl.points)], dtype=torch.float64, device="cuda")  # ranks' scenes may differ in size
+    if dist:
+        dist.all_reduce(pts, op=dist.ReduceOp.SUM)
+    job_points = float(pts.item())
+    pps = job_points * args.steps / (max_total_ms / 1e3)
 
     # end-to-end through the public API with host buffers (H2D + D2H inside the timing)
     e2e_times, h2d, d2h = [], 0, 0
@@ -445,7 +491,7 @@ def main():
     e2e_t = torch.tensor([statistics.median(e2e_times)], dtype=torch.float64, device="cuda")
     if dist:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-    e2e_pps = world * wl.points / float(e2e_t.item())
+    e2e_pps = job_points / float(e2e_t.item())
     gc.enable()
 
     # roofline of the dominant kernel: algorithmic bytes / measured duration

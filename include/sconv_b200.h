@@ -214,6 +214,12 @@ sconv_status sconv_net_read_tensor(sconv_ctx* ctx, const sconv_net* net, int ten
 /* Device view of a tensor's features: pointer, dtype (sconv_dtype) and row stride in elements
  * (valid until the next forward). */
 sconv_status sconv_net_tensor_device(const sconv_net* net, int tensor, const void** feats, int* dtype, int64_t* ld);
+/* Copy a tensor's features (n x channels, dense rows) into a caller buffer, converted to
+ * dst_dtype (sconv_dtype). Device destination: asynchronous on the context stream (e.g. a
+ * per-scene result slot that a scene-sharded runner sends to rank 0 while the next scene
+ * runs); host destination: synchronous. */
+sconv_status sconv_net_copy_tensor(sconv_ctx* ctx, const sconv_net* net, int tensor, void* dst, int dst_dtype,
+                                   int dst_mem);
 sconv_status sconv_net_stats(const sconv_net* net, int* maps_built, int* convs);
 /* Per CONV op (execution order) of the last forward: {n_in, n_out, |M|, R_pad (0 if fused), c_in, c_out,
  * k_pad, K3, dataflow, residual_folded}. */

@@ -30,6 +30,24 @@ void parallel_for(std::int64_t n, int workers, Fn&& fn) {
   for (auto& th : pool) th.join();
 }
 
+// Dynamic partition (atomic work counter) for items whose results do not depend on which
+// thread runs them: load balance only, outputs unchanged.
+template <class Fn>
+void parallel_for_chunked(std::int64_t n, int workers, Fn&& fn) {
+  if (workers <= 1 || n <= 1) {
+    for (std::int64_t i = 0; i < n; ++i) fn(i);
+    return;
+  }
+  std::atomic<std::int64_t> next{0};
+  const int w = static_cast<int>(std::min<std::int64_t>(workers, n));
+  std::vector<std::thread> pool;
+  for (int t = 0; t < w; ++t)
+    pool.emplace_back([&] {
+      for (std::int64_t i; (i = next.fetch_add(1, std::memory_order_relaxed)) < n;) fn(i);
+    });
+  for (auto& th : pool) th.join();
+}
+
 std::int64_t ceil_log2_plus1(std::int64_t n) {  // ceil(log2(n + 1))
   std::int64_t b = 0;
   while ((std::int64_t{1} << b) < n + 1) ++b;
@@ -423,18 +441,55 @@ Matrix gemm_execute(const Matrix& in, const WeightSet& w, const GemmGroupPlan& p
   if (in.cols() != w.c_in || in.rows() != plan.buffer_length)
     throw std::invalid_argument("gemm shape mismatch");
   Matrix out(in.rows(), w.c_out);
-  parallel_for(static_cast<std::int64_t>(plan.groups.size()), width, [&](std::int64_t gi, int) {
-    const GemmGroup& g = plan.groups[gi];
+  // Work items: (group member k, block of kRows buffer rows); groups are independent
+  // ("width"), and so are the row blocks of one member. Every output element is
+  // the fp64 sum over c ascending of in(r, c) * W_k[c][n], whatever the loop
+  // nesting, so this row-blocked form gives the same bits as a per-element dot product.
+  constexpr std::int64_t kRows = 4;
+  struct Item {
+    int k;
+    std::int64_t r0, r1;
+  };
+  std::vector<Item> items;
+  for (const GemmGroup& g : plan.groups)
     for (int p = g.begin; p < g.end; ++p) {
       const int k = plan.offset_order[p];
-      const float* W = w.matrix(k);
-      for (std::int64_t r = plan.buffer_offsets[k]; r < plan.buffer_offsets[k] + g.padded_height; ++r)
-        for (int n = 0; n < w.c_out; ++n) {
-          double acc = 0.0;
-          for (int c = 0; c < w.c_in; ++c) acc += static_cast<double>(in(r, c)) * W[c * w.c_out + n];
-          out(r, n) = static_cast<float>(acc);
-        }
+      for (std::int64_t r = 0; r < g.padded_height; r += kRows)
+        items.push_back({k, plan.buffer_offsets[k] + r,
+                         plan.buffer_offsets[k] + std::min<std::int64_t>(g.padded_height, r + kRows)});
     }
+  const int Cin = w.c_in, Cout = w.c_out;
+  std::vector<double> wd(static_cast<std::size_t>(w.num_offsets) * Cin * Cout);
+  for (std::size_t e = 0; e < wd.size(); ++e) wd[e] = static_cast<double>(w.w[e]);
+  parallel_for_chunked(static_cast<std::int64_t>(items.size()), std::max(1, width), [&](std::int64_t t) {
+    const Item& it = items[static_cast<std::size_t>(t)];
+    const double* W = wd.data() + static_cast<std::size_t>(it.k) * Cin * Cout;
+    const std::int64_t nr = it.r1 - it.r0;
+    const float* rows[kRows];
+    for (std::int64_t i = 0; i < kRows; ++i) rows[i] = in.row(it.r0 + std::min(i, nr - 1));
+    int n0 = 0;
+    for (; n0 + 8 <= Cout; n0 += 8) {  // 4 rows x 8 columns of fp64 accumulators in registers
+      double a0[8] = {}, a1[8] = {}, a2[8] = {}, a3[8] = {};
+      for (int c = 0; c < Cin; ++c) {
+        const double* w8 = W + static_cast<std::size_t>(c) * Cout + n0;
+        const double x0 = rows[0][c], x1 = rows[1][c], x2 = rows[2][c], x3 = rows[3][c];
+        for (int q = 0; q < 8; ++q) {
+          a0[q] += x0 * w8[q];
+          a1[q] += x1 * w8[q];
+          a2[q] += x2 * w8[q];
+          a3[q] += x3 * w8[q];
+        }
+      }
+      double* acc[kRows] = {a0, a1, a2, a3};
+      for (std::int64_t i = 0; i < nr; ++i)
+        for (int q = 0; q < 8; ++q) out(it.r0 + i, n0 + q) = static_cast<float>(acc[i][q]);
+    }
+    for (; n0 < Cout; ++n0)  // column tail
+      for (std::int64_t i = 0; i < nr; ++i) {
+        double a = 0.0;
+        for (int c = 0; c < Cin; ++c) a += static_cast<double>(rows[i][c]) * W[static_cast<std::size_t>(c) * Cout + n0];
+        out(it.r0 + i, n0) = static_cast<float>(a);
+      }
   });
   return out;
 }

@@ -787,6 +787,32 @@ sconv_status sconv_net_read_tensor(sconv_ctx* ctx, const sconv_net* net, int ten
   });
 }
 
+sconv_status sconv_net_copy_tensor(sconv_ctx* ctx, const sconv_net* net, int tensor, void* dst, int dst_dtype,
+                                   int dst_mem) {
+  return guarded(ctx, [&] {
+    if (!net || tensor < 0 || tensor >= static_cast<int>(net->tensors.size())) fail(SCONV_ERR_ARG, "bad tensor");
+    if (dst_dtype != SCONV_F32 && dst_dtype != SCONV_F16 && dst_dtype != SCONV_BF16) fail(SCONV_ERR_ARG, "bad dtype");
+    const NetTensor& t = net->tensors[tensor];
+    if (t.fused_away) fail(SCONV_ERR_STATE, "tensor was folded into a fused residual epilogue");
+    if (t.coordset < 0) fail(SCONV_ERR_STATE, "tensor not produced");
+    if (t.n == 0) return;
+    const size_t esz = dst_dtype == SCONV_F32 ? 4 : 2;
+    const size_t bytes = esz * static_cast<size_t>(t.n) * t.channels;
+    if (dst_mem == SCONV_MEM_DEVICE) {
+      if (dst_dtype == t.dtype && t.ld == t.channels)
+        SCONV_CUDA(cudaMemcpyAsync(dst, t.feats.get(), bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+      else
+        convert_rows(*ctx, t.feats.get(), t.dtype, t.n, t.channels, t.ld, dst, dst_dtype, t.channels);
+      return;  // asynchronous on the context stream
+    }
+    auto* n = const_cast<sconv_net*>(net);
+    n->readback.reserve(bytes, ctx->stream);
+    convert_rows(*ctx, t.feats.get(), t.dtype, t.n, t.channels, t.ld, n->readback.get(), dst_dtype, t.channels);
+    SCONV_CUDA(cudaMemcpyAsync(dst, n->readback.get(), bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->sync();
+  });
+}
+
 sconv_status sconv_net_tensor_device(const sconv_net* net, int tensor, const void** feats, int* dtype, int64_t* ld) {
   if (!net || tensor < 0 || tensor >= static_cast<int>(net->tensors.size()) || !feats) return SCONV_ERR_ARG;
   const NetTensor& t = net->tensors[tensor];

@@ -359,6 +359,9 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
         res = &tensors.at(pl.res);
         if (res->coordset < 0) fail(SCONV_ERR_STATE, "residual operand not produced yet");
         if (res->channels != o.c_out || res->n != m.n_out) fail(SCONV_ERR_ARG, "add operands need the same shape");
+        // as the unfused ADD below: both operands on one coordinate set (equal row counts alone
+        // could add misaligned rows)
+        if (res->coordset != it->second.out_cs) fail(SCONV_ERR_ARG, "add/concat operands need the same coordinates");
       }
       // the output buffer may be read below (residual or input of a re-used tensor id): fresh allocation
       DevBuf nb;

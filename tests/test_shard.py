@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 
 from paper_2401_06145_b200 import network as N
-from paper_2401_06145_b200.shard import broadcast_weights, gather_results, run_shard, shard_range
+from paper_2401_06145_b200.shard import SceneResultGather, broadcast_weights, gather_results, run_shard, shard_range
 
 
 @pytest.mark.parametrize("n,world", [(64, 1), (64, 2), (64, 8), (7, 3), (3, 8), (0, 2)])
@@ -53,8 +53,25 @@ def _worker(rank, world, port, n_scenes, out_dir):
             ok_g = len(res) == n_scenes and all(np.array_equal(res[s], fake_scene(s)) for s in range(n_scenes))
         else:
             ok_g = res is None
+        # the overlapped per-scene gather of bench.py's C5 step (same code path, host tensors on gloo)
+        import torch
+        lo, hi = shard_range(n_scenes, rank, world)
+        rg = SceneResultGather([5 + 3 * s for s in range(lo, hi)], n_scenes, 6, dtype=torch.float32)
+        ok_s = True
+        for step in range(2):
+            rg.begin_step()
+            for s in range(lo, hi):
+                rg.slot(s).copy_(torch.from_numpy(fake_scene(s)) + step)
+                rg.produced(s)
+            rg.end_step()
+            if rank == 0:
+                got = rg.results()
+                ok_s &= len(got) == n_scenes and all(np.array_equal(got[s].numpy(), fake_scene(s) + step)
+                                                     for s in range(n_scenes))
+            else:
+                ok_s &= rg.results() is None
         with open(os.path.join(out_dir, f"rank{rank}.txt"), "w") as f:
-            f.write(f"{int(ok_w)} {int(ok_g)}")
+            f.write(f"{int(ok_w)} {int(ok_g and ok_s)}")
     finally:
         dist.destroy_process_group()
 
