@@ -31,8 +31,13 @@ clean:
 
 # Reference-typed adapter test (needs the reference headers at build time; the binary travels)
 REF_INC ?= /root/reference/proj/include
-tests/cpp/test_adapter: tests/cpp/test_adapter.cpp include/sconv_b200.hpp include/sconv_b200.h $(LIB)
-	g++ -std=c++20 -O2 -I$(REF_INC) -Iinclude -o $@ $< -L$(PKG) -lsconv_b200 -Wl,-rpath,'$$ORIGIN/../../$(PKG)'
+# (links the reference-header oracle build as the checker: test infrastructure)
+tests/cpp/test_adapter: tests/cpp/test_adapter.cpp include/sconv_b200.hpp include/sconv_b200.h $(LIB) oracle/_ref/liboracle_ref.so
+	g++ -std=c++20 -O2 -DSCONV_ORACLE_USE_REFERENCE -I$(REF_INC) -Iinclude -Ioracle -o $@ $< -L$(PKG) -lsconv_b200 \
+	  -Loracle/_ref -loracle_ref -Wl,-rpath,'$$ORIGIN/../../$(PKG)' -Wl,-rpath,'$$ORIGIN/../../oracle/_ref'
+
+oracle/_ref/liboracle_ref.so:
+	$(MAKE) -C oracle ref
 
 adapter: tests/cpp/test_adapter
 .PHONY: adapter

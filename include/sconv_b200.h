@@ -68,7 +68,12 @@ typedef struct {
  * HASH: the SPEC's hash-table baseline (capacity = smallest power of two >= 2N, 64-bit
  * Fibonacci multiplicative hash, linear probing) on the GPU. Both produce the
  * identical canonical KernelMap (SPEC.md:367 backend equivalence). */
-typedef enum { SCONV_MAP_SORTED = 0, SCONV_MAP_HASH = 1 } sconv_map_backend;
+/* SORTED_SPEC: the same sorted search with the SPEC's literal work decomposition
+ * (backward_partition per (offset, source block) -> balance_blocks: ceil(L/C) near-equal ranges
+ * -> forward_block_search per range with the block staged in shared memory)
+ * and its SearchCounters (sconv_map_search_counters), equal to the oracle's. SORTED is this
+ * engine's warp-window redesign of that search (faster; no comparison counters). */
+typedef enum { SCONV_MAP_SORTED = 0, SCONV_MAP_HASH = 1, SCONV_MAP_SORTED_SPEC = 2 } sconv_map_backend;
 
 /* GMaS configuration (SPEC.md:359 config{grouping policy, eps, max_batch, tiles}). */
 typedef struct {
@@ -136,6 +141,30 @@ sconv_status sconv_map_build(sconv_ctx* ctx, const int32_t* xyz, int64_t n, int 
 /* Chain: P = the output coordinates of `prev` (device-resident, sorted; SPEC.md:528 reuse). */
 sconv_status sconv_map_build_chained(sconv_ctx* ctx, const sconv_map* prev, const sconv_map_cfg* cfg,
                                      const sconv_map* target_of, sconv_map** out);
+/* SPEC-literal build_kernel_map_sorted(P, Q, offsets, B, C): an arbitrary
+ * sorted unique query list Q (n_q x 3, "query coordinates must be sorted and unique") and an
+ * arbitrary offset list (n_offsets x 3 int32, SPEC: sorted once per layer); P as in
+ * sconv_map_build. Map index j = row of P as given, i = row of Q; K3 = n_offsets. backend:
+ * sconv_map_backend (SORTED_SPEC fills the comparison counters). */
+sconv_status sconv_map_build_explicit(sconv_ctx* ctx, const int32_t* p_xyz, int64_t n_p, int p_mem, int p_sorted,
+                                     const int32_t* q_xyz, int64_t n_q, int q_mem, const int32_t* offsets_xyz,
+                                     int n_offsets, int block_B, int block_C, int backend, sconv_map** out);
+/* SearchCounters of a map build. sorts = coordinate-array sorts the build
+ * performed (0 when P was flagged sorted and the stride is 1, acceptance #7).
+ * The comparison tallies are filled (counted = 1) by the SORTED_SPEC backend, whose work
+ * decomposition is the SPEC's; they equal the oracle's exactly. */
+typedef struct {
+  uint64_t backward_comparisons;
+  uint64_t forward_comparisons;
+  uint64_t source_elements_loaded;
+  uint64_t queries_executed;
+  uint64_t sorts;
+  int32_t counted;
+} sconv_search_counters;
+sconv_status sconv_map_search_counters(sconv_ctx* ctx, const sconv_map* map, sconv_search_counters* out);
+/* theoretical_hyperparams(|P|, |Q|) -> (B, C) (Eq. 4): advisory; the runtime
+ * defaults stay B = 256, C = 512. Errors: ARG "point counts must be positive". */
+sconv_status sconv_theoretical_hyperparams(int64_t num_inputs, int64_t num_outputs, int* block_B, int* block_C);
 sconv_status sconv_map_get_info(sconv_ctx* ctx, const sconv_map* map, sconv_map_info* info);
 /* KernelMap readback in canonical order (per offset k, sorted by output index i;
  * SPEC.md:109). sizes: num_offsets; in_idx/out_idx: total_matches; out_xyz: num_outputs x 3.
@@ -221,6 +250,11 @@ sconv_status sconv_net_tensor_device(const sconv_net* net, int tensor, const voi
 sconv_status sconv_net_copy_tensor(sconv_ctx* ctx, const sconv_net* net, int tensor, void* dst, int dst_dtype,
                                    int dst_mem);
 sconv_status sconv_net_stats(const sconv_net* net, int* maps_built, int* convs);
+/* Coordinate-array sorts of the last forward: 1 for an unsorted input (0 when flagged sorted)
+ * plus one Eq. 1 sort per distinct strided map; stride-1 layers reuse the sorted keys
+ * (acceptance #7: a 5-layer stride-1 chain sorts once, strides [1,2,1,2,1]
+ * three times). */
+sconv_status sconv_net_sort_count(const sconv_net* net, int64_t* sorts);
 /* Per CONV op (execution order) of the last forward: {n_in, n_out, |M|, R_pad (0 if fused), c_in, c_out,
  * k_pad, K3, dataflow, residual_folded}. */
 sconv_status sconv_net_conv_stats(const sconv_net* net, int conv, int64_t* out10);

@@ -7,8 +7,10 @@
 // std::invalid_argument for arguments, std::logic_error for invariant violations).
 //
 //   sconv::gpu::Context ctx(0);
-//   auto [Q, map] = sconv::gpu::build_kernel_map_sorted(ctx, P, K, s);
+//   auto [Q, map] = sconv::gpu::build_kernel_map_sorted(ctx, P, K, s);       // SPEC.md:235 (layer form)
+//   auto [km, counters] = sconv::gpu::build_kernel_map_sorted(ctx, P, Q, offsets, 256, 512);  // SPEC form
 //   sconv::PointCloud out = sconv::gpu::sc_layer_forward(ctx, P, W, K, s);
+//   auto res = sconv::gpu::forward_network(ctx, spec, P, cfg, seed);
 #pragma once
 
 #include <cstdint>
@@ -115,6 +117,78 @@ inline std::pair<CoordsPtr, KernelMap> build_kernel_map_sorted(Context& ctx, con
   return {Q, std::move(km)};
 }
 
+// SearchCounters. The comparison tallies are filled (counted) by the
+// SORTED_SPEC backend, whose work decomposition is the SPEC's; sorts by every backend.
+struct SearchCounters {
+  std::uint64_t backward_comparisons = 0, forward_comparisons = 0, source_elements_loaded = 0, queries_executed = 0;
+  std::uint64_t sorts = 0;
+  bool counted = false;
+};
+
+// build_kernel_map_sorted(P, Q, offsets, B, C) -> (KernelMap, SearchCounters):
+// arbitrary sorted unique queries Q and any OffsetSet (reference OffsetSet, geometry.hpp:123-148).
+// Errors as the reference: std::out_of_range for out-of-range coordinates, std::invalid_argument
+// for unsorted queries or bad B / C.
+inline std::pair<KernelMap, SearchCounters> build_kernel_map_sorted(Context& ctx, const PointCloud& P,
+                                                                    const CoordList& Q, const OffsetSet& offsets,
+                                                                    int B = 256, int C = 512,
+                                                                    int backend = SCONV_MAP_SORTED_SPEC) {
+  const auto pxyz = detail::flatten(*P.coords);
+  const auto qxyz = detail::flatten(Q);
+  const auto oxyz = detail::flatten(offsets.offsets);
+  sconv_map* m = nullptr;
+  ctx.check_status(sconv_map_build_explicit(ctx.get(), pxyz.data(), P.size(), SCONV_MEM_HOST, P.sorted ? 1 : 0,
+                                            qxyz.data(), static_cast<std::int64_t>(Q.size()), SCONV_MEM_HOST,
+                                            oxyz.data(), static_cast<int>(offsets.offsets.size()), B, C, backend, &m));
+  sconv_map_info info;
+  sconv_search_counters c;
+  sconv_status st = sconv_map_get_info(ctx.get(), m, &info);
+  if (st == SCONV_OK) st = sconv_map_search_counters(ctx.get(), m, &c);
+  std::vector<std::int32_t> in(static_cast<std::size_t>(st == SCONV_OK ? info.total_matches : 0)), out(in.size());
+  std::vector<std::int64_t> sizes(static_cast<std::size_t>(st == SCONV_OK ? info.num_offsets : 0));
+  if (st == SCONV_OK) st = sconv_map_read(ctx.get(), m, nullptr, sizes.data(), in.data(), out.data());
+  if (st != SCONV_OK) {
+    const std::string msg = sconv_last_error(ctx.get());
+    sconv_map_free(ctx.get(), m);
+    check(st, msg.c_str());
+  }
+  sconv_map_free(ctx.get(), m);
+  KernelMap km;
+  km.offsets = offsets;
+  km.matches.resize(sizes.size());
+  std::size_t pos = 0;
+  for (std::size_t k = 0; k < sizes.size(); ++k)
+    for (std::int64_t r = 0; r < sizes[k]; ++r, ++pos) km.matches[k].emplace_back(in[pos], out[pos]);
+  SearchCounters sc;
+  sc.backward_comparisons = c.backward_comparisons;
+  sc.forward_comparisons = c.forward_comparisons;
+  sc.source_elements_loaded = c.source_elements_loaded;
+  sc.queries_executed = c.queries_executed;
+  sc.sorts = c.sorts;
+  sc.counted = c.counted != 0;
+  return {std::move(km), sc};
+}
+
+// theoretical_hyperparams(|P|, |Q|) -> (B, C) (Eq. 4); advisory.
+inline std::pair<int, int> theoretical_hyperparams(std::int64_t P, std::int64_t Q) {
+  int B = 0, C = 0;
+  check(sconv_theoretical_hyperparams(P, Q, &B, &C), sconv_global_last_error());
+  return {B, C};
+}
+
+// WeightSet: per offset k a C_in x C_out fp32 matrix W_k, flattened [k][cin][cout].
+struct WeightSet {
+  int num_offsets = 0, c_in = 0, c_out = 0;
+  std::vector<float> w;
+  const float* matrix(int k) const { return w.data() + static_cast<std::size_t>(k) * c_in * c_out; }
+  // Rng(stream_seed(seed, stream)), U[-0.1, 0.1] (bit-identical to the oracle)
+  static WeightSet generate(std::uint64_t seed, std::uint64_t stream, int num_offsets, int c_in, int c_out) {
+    WeightSet ws{num_offsets, c_in, c_out, std::vector<float>(static_cast<std::size_t>(num_offsets) * c_in * c_out)};
+    check(sconv_generate_weights(seed, stream, num_offsets, c_in, c_out, ws.w.data()), sconv_global_last_error());
+    return ws;
+  }
+};
+
 // voxelize (geometry.hpp:180-255) on the GPU: same voxels, same mean-merged features, bit for bit.
 inline PointCloud voxelize(Context& ctx, const std::vector<std::array<double, 3>>& points, const Matrix& features,
                            double resolution) {
@@ -199,6 +273,75 @@ inline PointCloud sc_layer_forward(Context& ctx, const PointCloud& cloud, const 
     for (int c = 0; c < c_out; ++c) trimmed(r, c) = out(r, c);
   CoordsPtr Q = (s == 1 && cloud.sorted) ? cloud.coords : make_coords(detail::unflatten(oxyz, n_out));
   return PointCloud{Q, std::move(trimmed), true};
+}
+
+// sc_layer_forward with a WeightSet.
+inline PointCloud sc_layer_forward(Context& ctx, const PointCloud& cloud, const WeightSet& W, int K, int s,
+                                   const LayerConfig& cfg = {}) {
+  if (W.c_in != cloud.channels()) throw std::invalid_argument("feature channels do not match weights");
+  return sc_layer_forward(ctx, cloud, W.w, W.c_out, K, s, cfg);
+}
+
+// NetworkSpec: ordered (K, s, C_in, C_out) layers.
+struct NetLayer {
+  int K, s, c_in, c_out;
+};
+struct NetworkSpec {
+  std::vector<NetLayer> layers;
+};
+struct NetworkResult {
+  PointCloud output;
+  std::uint64_t sorts = 0;  // coordinate sorts performed (1 + strided layers)
+};
+
+// forward_network(spec, cloud, config, seed) on the GPU network driver: layer
+// l is the SPEC-literal SC layer (offsets weight_offsets(K, s), Eq. 1 stride s) with weights
+// Rng(stream_seed(seed, l + 1)) U[-0.1, 0.1]; layer l+1 reads layer l's sorted output
+// coordinates (sort reuse). Activations between layers in cfg.compute_dtype (16-bit).
+inline NetworkResult forward_network(Context& ctx, const NetworkSpec& spec, const PointCloud& cloud,
+                                     const LayerConfig& cfg, std::uint64_t seed) {
+  if (spec.layers.empty()) throw std::invalid_argument("empty network");
+  if (cloud.channels() != spec.layers.front().c_in) throw std::invalid_argument("network input channels mismatch");
+  for (std::size_t l = 1; l < spec.layers.size(); ++l)
+    if (spec.layers[l - 1].c_out != spec.layers[l].c_in)
+      throw std::invalid_argument("network layers are not channel compatible");
+  const int L = static_cast<int>(spec.layers.size());
+  std::vector<std::int32_t> ops;
+  for (int l = 0; l < L; ++l) {
+    const NetLayer& y = spec.layers[static_cast<std::size_t>(l)];
+    ops.insert(ops.end(), {1, l + 1, l, -1, y.K, y.s, y.s, 0, y.c_in, y.c_out, l, 0});
+  }
+  sconv_exec_cfg ec{cfg.policy,       cfg.epsilon,       cfg.max_batch,   cfg.gather_tile,
+                    cfg.scatter_tile, cfg.compute_dtype, cfg.partial_f16, SCONV_DATAFLOW_AUTO, 1};
+  sconv_net* net = nullptr;
+  ctx.check_status(sconv_net_create(ctx.get(), ops.data(), L, L + 1, 0, L, &ec, cfg.B, cfg.C, &net));
+  struct Guard {
+    Context& c;
+    sconv_net* n;
+    ~Guard() { sconv_net_free(c.get(), n); }
+  } guard{ctx, net};
+  for (int l = 0; l < L; ++l) {
+    const NetLayer& y = spec.layers[static_cast<std::size_t>(l)];
+    const WeightSet w = WeightSet::generate(seed, static_cast<std::uint64_t>(l + 1), y.K * y.K * y.K, y.c_in, y.c_out);
+    ctx.check_status(sconv_net_set_weights(ctx.get(), net, l, w.w.data(), SCONV_MEM_HOST, w.num_offsets, w.c_in,
+                                           w.c_out));
+  }
+  const auto xyz = detail::flatten(*cloud.coords);
+  ctx.check_status(sconv_net_forward(ctx.get(), net, xyz.data(), cloud.size(), SCONV_MEM_HOST, cloud.sorted ? 1 : 0,
+                                     cloud.size() ? cloud.features.row(0) : nullptr, SCONV_MEM_HOST,
+                                     static_cast<int>(cloud.channels())));
+  std::int64_t n = 0;
+  int ch = 0, cs = 0;
+  ctx.check_status(sconv_net_tensor_info(ctx.get(), net, L, &n, &ch, &cs));
+  std::vector<std::int32_t> oxyz(static_cast<std::size_t>(3 * n));
+  Matrix f(n, ch);
+  ctx.check_status(sconv_net_read_tensor(ctx.get(), net, L, oxyz.data(), n ? f.row(0) : nullptr));
+  std::int64_t sorts = 0;
+  ctx.check_status(sconv_net_sort_count(net, &sorts));
+  NetworkResult r;
+  r.output = PointCloud{make_coords(detail::unflatten(oxyz, n)), std::move(f), true};
+  r.sorts = static_cast<std::uint64_t>(sorts);
+  return r;
 }
 
 }  // namespace sconv::gpu

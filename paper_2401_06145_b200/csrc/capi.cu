@@ -502,6 +502,65 @@ sconv_status sconv_map_build_chained(sconv_ctx* ctx, const sconv_map* prev, cons
   });
 }
 
+sconv_status sconv_map_build_explicit(sconv_ctx* ctx, const int32_t* p_xyz, int64_t n_p, int p_mem, int p_sorted,
+                                     const int32_t* q_xyz, int64_t n_q, int q_mem, const int32_t* offsets_xyz,
+                                     int n_offsets, int block_B, int block_C, int backend, sconv_map** out) {
+  return guarded(ctx, [&] {
+    if (!out) fail(SCONV_ERR_ARG, "null argument");
+    if ((n_p > 0 && !p_xyz) || (n_q > 0 && !q_xyz)) fail(SCONV_ERR_ARG, "null coordinates");
+    if (n_offsets < 1 || !offsets_xyz) fail(SCONV_ERR_ARG, "offset count must be in [1, 4096]");
+    if (n_q < 0 || n_q > INT32_MAX / 2) fail(SCONV_ERR_ARG, "point count out of supported range");
+    std::vector<int3> offs(static_cast<size_t>(n_offsets));
+    for (int k = 0; k < n_offsets; ++k) offs[k] = make_int3(offsets_xyz[3 * k], offsets_xyz[3 * k + 1], offsets_xyz[3 * k + 2]);
+    MapSource P;
+    P.xyz = p_xyz;
+    P.n = n_p;
+    P.mem = p_mem;
+    P.sorted = p_sorted != 0;
+    MapSource T;
+    T.xyz = q_xyz;
+    T.n = n_q;
+    T.mem = q_mem;
+    T.sorted = true;
+    // kernel_size / scale describe no geometry here (the offsets are explicit); stride 1
+    sconv_map_cfg cfg{1, 1, 1, 0, block_B, block_C, backend};
+    *out = wrap(build_map(*ctx, P, cfg, &T, false, false, &offs));
+  });
+}
+
+sconv_status sconv_map_search_counters(sconv_ctx* ctx, const sconv_map* m, sconv_search_counters* c) {
+  return guarded(ctx, [&] {
+    if (!m || !c) fail(SCONV_ERR_ARG, "null argument");
+    *c = sconv_search_counters{};
+    c->sorts = static_cast<uint64_t>(m->sorts);
+    c->counted = m->counted ? 1 : 0;
+    if (m->counted) {
+      uint64_t v[4];
+      SCONV_CUDA(cudaMemcpyAsync(v, m->counters.get(), sizeof(v), cudaMemcpyDeviceToHost, ctx->stream));
+      ctx->sync();
+      c->backward_comparisons = v[0];
+      c->forward_comparisons = v[1];
+      c->source_elements_loaded = v[2];
+      c->queries_executed = v[3];
+    }
+  });
+}
+
+sconv_status sconv_theoretical_hyperparams(int64_t num_inputs, int64_t num_outputs, int* block_B, int* block_C) {
+  return guarded(nullptr, [&] {
+  if (num_inputs < 1 || num_outputs < 1) fail(SCONV_ERR_ARG, "point counts must be positive");
+  if (!block_B || !block_C) fail(SCONV_ERR_ARG, "null argument");
+  // SPEC.md:244-252 (Eq. 4): B = max(1, round(|P|/|Q| log2|Q|)),
+  // C = max(1, round(sqrt(|Q| / (|P| log2 B)) B)) with log2 B floored at 1
+  const double ratio = static_cast<double>(num_inputs) / static_cast<double>(num_outputs);
+  const int B = std::max(1, static_cast<int>(std::lround(ratio * std::log2(static_cast<double>(num_outputs)))));
+  const double lb = std::max(1.0, std::log2(static_cast<double>(B)));
+  *block_B = B;
+  *block_C = std::max(1, static_cast<int>(std::lround(
+                             std::sqrt(static_cast<double>(num_outputs) / (static_cast<double>(num_inputs) * lb)) * B)));
+  });
+}
+
 sconv_status sconv_map_get_info(sconv_ctx* ctx, const sconv_map* m, sconv_map_info* info) {
   return guarded(ctx, [&] {
     if (!m || !info) fail(SCONV_ERR_ARG, "null argument");
@@ -820,6 +879,12 @@ sconv_status sconv_net_tensor_device(const sconv_net* net, int tensor, const voi
   *feats = t.feats.get();
   if (dtype) *dtype = t.dtype;
   if (ld) *ld = t.ld;
+  return SCONV_OK;
+}
+
+sconv_status sconv_net_sort_count(const sconv_net* net, int64_t* sorts) {
+  if (!net || !sorts) return SCONV_ERR_ARG;
+  *sorts = net->sorts;
   return SCONV_OK;
 }
 

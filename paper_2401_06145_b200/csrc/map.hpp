@@ -24,6 +24,10 @@ struct MapData {
   DevBuf nbr_in;             // int32 x K3 x n_out: input row j of (k, i) or -1 (fused dataflow)
   std::vector<int3> delta;   // search offsets (host copy)
   DevBuf hash_keys, hash_vals;  // hash backend index, kept for inspection
+  DevBuf delta_dev;             // explicit offset list (SPEC build_kernel_map_sorted(P, Q, offsets, B, C))
+  DevBuf counters;              // SORTED_SPEC backend: u64 {backward, forward, loaded, executed}
+  bool counted = false;
+  int sorts = 0;                // coordinate sorts this build performed (acceptance #7)
   // Fused-dataflow row order (built lazily, conv_fused.cu prepare_fused_layout): output rows
   // sorted by their neighbour bitmask so a 128-row tile touches few offsets.
   bool fused_ready = false;
@@ -64,8 +68,11 @@ struct MapSource {
 
 // lazy: skip the canonical lists and the end-of-build sync (only for maps over existing sorted
 // device keys, whose coordinates were validated when they were first built).
+// explicit_offsets: SPEC build_kernel_map_sorted(P, Q, offsets, B, C) with an arbitrary offset
+// list and Q = *target (sorted unique queries).
 std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map_cfg& cfg, const MapSource* target,
-                                   bool force_wide = false, bool lazy = false);
+                                   bool force_wide = false, bool lazy = false,
+                                   const std::vector<int3>* explicit_offsets = nullptr);
 // Builds the canonical pair lists of a lazily built map (no-op otherwise): scan + emit + sync.
 void ensure_canonical(Ctx& ctx, MapData& m);
 

@@ -256,6 +256,7 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
   maps.clear();
   int convs_issued = 0;
   maps_built = 0;
+  sorts = 0;
   conv_stats.clear();
   // coordinate set 0 = the raw input (may be unsorted)
   coordsets.push_back({input.keys, input.n, input.sorted, true});
@@ -335,6 +336,7 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
         ctx.stream = st;
         if (ls != st) wait_for(ls, 1000 + oi);
         ++maps_built;
+        sorts += m->sorts;
         if (!coordsets[a.coordset].keys && coordsets[a.coordset].sorted)
           coordsets[a.coordset].keys = m->src_keys;  // sorted raw input: its packed keys, same row order
         int out_cs;

@@ -66,6 +66,7 @@ struct NetData {
   MapSource raw_input;
   DevBuf input_xyz;  // device copy of host input coordinates
   int maps_built = 0;
+  int64_t sorts = 0;  // coordinate sorts of the last forward (acceptance #7)
   std::vector<OpPlan> plan;
   bool planned = false;
   std::vector<std::array<double, 2>> auto_ms;  // per op: GMaS / fused ms of the tuning forward

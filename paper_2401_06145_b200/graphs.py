@@ -155,6 +155,41 @@ def unet_pair(c_in=32, c_mid=64) -> Graph:
     return g
 
 
+# SPEC netdef presets (oracle preset_network): (K, s, c_in, c_out) per layer
+PRESETS = {
+    "resnet_like": [(3, 1, 4, 16), (3, 1, 16, 16), (3, 2, 16, 32), (3, 1, 32, 32), (3, 2, 32, 64), (3, 1, 64, 64),
+                    (3, 2, 64, 128), (3, 1, 128, 128)],
+    "unet_like": [(3, 1, 4, 32), (3, 2, 32, 64), (3, 1, 64, 64), (3, 2, 64, 128), (3, 1, 128, 128), (3, 1, 128, 64),
+                  (3, 1, 64, 32)],
+}
+
+
+def spec_chain(layers) -> Graph:
+    """SPEC NetworkSpec: a sequential chain of SPEC-literal SC layers (K, s,
+    c_in, c_out) — offsets weight_offsets(K, s), Eq. 1 stride s, no nonlinearity — where layer
+    l+1's input coordinates are layer l's sorted output (sort reuse). Weight id l."""
+    layers = [tuple(int(v) for v in L) for L in layers]
+    if not layers:
+        raise ValueError("empty network")
+    for a, b in zip(layers, layers[1:]):
+        if a[3] != b[2]:
+            raise ValueError("network layers are not channel compatible")
+    g = Graph(in_channels=layers[0][2])
+    x = g.tensor(layers[0][2], 1)
+    g.input = x
+    for w, (K, s, ci, co) in enumerate(layers):
+        y = g.tensor(co, 1)
+        g.ops.append(Op(CONV, y, x, -1, K, s, s, 0, ci, co, w, 0))
+        x = y
+    g.output = x
+    return g
+
+
+def spec_weights(g: Graph, seed: int, generate: Callable) -> dict:
+    """layer l's WeightSet from Rng(stream_seed(seed, l + 1)), U[-0.1, 0.1]."""
+    return {o.weight: generate(seed, o.weight + 1, o.K ** 3, o.c_in, o.c_out) for o in g.convs()}
+
+
 def weight_scale(g: Graph, o: Op) -> float:
     """Factor applied to the SPEC's U[-0.1, 0.1] draw: a / 0.1 with a = sqrt(3 / (nbr * c_in))."""
     return float(np.sqrt(3.0 / (g.nbr[o.weight] * o.c_in)) / 0.1)

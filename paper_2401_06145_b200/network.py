@@ -8,13 +8,28 @@ from typing import Optional
 import numpy as np
 
 from . import sconv as S
-from .graphs import ADD, CONCAT, CONV, Graph, Op, minkunet42, sparse_resnet21d, unet_pair, weight_scale  # noqa: F401
+from .graphs import (ADD, CONCAT, CONV, PRESETS, Graph, Op, minkunet42, sparse_resnet21d, spec_chain,  # noqa: F401
+                     unet_pair, weight_scale)
 from . import graphs as _graphs
 
 
 def init_weights(g: Graph, seed: int):
     """graphs.init_weights with the engine's SPEC PRNG (sconv_generate_weights)."""
     return _graphs.init_weights(g, seed, S.generate_weights)
+
+
+def forward_network(ctx: S.Context, layers, cloud: S.PointCloud, seed: int, cfg: Optional[S.ExecCfg] = None,
+                    B: int = 256, Cq: int = 512):
+    """SPEC forward_network(spec, cloud, config, seed): the sequential chain
+    `layers` [(K, s, c_in, c_out), ...] with SPEC weights (stream l+1, U[-0.1, 0.1]) on the GPU.
+    Returns (output PointCloud (sorted), coordinate sorts performed)."""
+    g = spec_chain(layers)
+    net = Network(ctx, g, _graphs.spec_weights(g, seed, S.generate_weights), cfg, B, Cq)
+    net.forward(cloud.coords, cloud.features, cloud.sorted)
+    xyz, f = net.read(g.output)
+    sorts = net.sort_count()
+    net.free()
+    return S.PointCloud(xyz, f, True), sorts
 
 
 class Network:
@@ -76,6 +91,12 @@ class Network:
         """Features of tensor t into a caller buffer (n x channels, dense): asynchronous on the
         context stream for a device destination (sconv_net_copy_tensor)."""
         self.ctx.check(self.ctx.lib.sconv_net_copy_tensor(self.ctx.h, self.h, t, dst_ptr, dtype, mem))
+
+    def sort_count(self):
+        """Coordinate sorts of the last forward (acceptance #7 accounting)."""
+        v = C.c_int64()
+        self.ctx.check(self.ctx.lib.sconv_net_sort_count(self.h, C.byref(v)))
+        return v.value
 
     def stats(self):
         mb, nc = C.c_int(), C.c_int()

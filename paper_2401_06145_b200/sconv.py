@@ -30,7 +30,7 @@ MEM_HOST, MEM_DEVICE = 0, 1
 F32, F16, BF16 = 0, 1, 2
 GROUP_MAP_ORDER, GROUP_SORTED = 0, 1
 DATAFLOW_GMAS, DATAFLOW_FUSED, DATAFLOW_AUTO = 0, 1, 2
-MAP_SORTED, MAP_HASH = 0, 1
+MAP_SORTED, MAP_HASH, MAP_SORTED_SPEC = 0, 1, 2
 
 
 class SconvError(RuntimeError):
@@ -92,6 +92,9 @@ SIGNATURES = [
     ("sconv_device_free", _I, [_P, _P]),
     ("sconv_memcpy", _I, [_P, _P, _P, _S, _I]),
     ("sconv_map_build", _I, [_P, _P, _I64, _I, _I, C.POINTER(MapCfg), _P, _I64, _I, C.POINTER(_P)]),
+    ("sconv_map_build_explicit", _I, [_P, _P, _I64, _I, _I, _P, _I64, _I, _P, _I, _I, _I, _I, C.POINTER(_P)]),
+    ("sconv_map_search_counters", _I, [_P, _P, C.c_void_p]),
+    ("sconv_theoretical_hyperparams", _I, [_I64, _I64, C.POINTER(_I), C.POINTER(_I)]),
     ("sconv_map_build_chained", _I, [_P, _P, C.POINTER(MapCfg), _P, C.POINTER(_P)]),
     ("sconv_map_get_info", _I, [_P, _P, C.POINTER(MapInfo)]),
     ("sconv_map_read", _I, [_P, _P, _P, _P, _P, _P]),
@@ -112,6 +115,7 @@ SIGNATURES = [
     ("sconv_net_read_tensor", _I, [_P, _P, _I, _P, _P]),
     ("sconv_net_tensor_device", _I, [_P, _I, C.POINTER(_P), C.POINTER(_I), C.POINTER(_I64)]),
     ("sconv_net_copy_tensor", _I, [_P, _P, _I, _P, _I, _I]),
+    ("sconv_net_sort_count", _I, [_P, C.POINTER(_I64)]),
     ("sconv_net_conv_timings", _I, [_P, _I, C.POINTER(_D), C.POINTER(_D)]),
     ("sconv_voxelize", _I, [_P, _P, _I64, _I, _P, _I64, _I, _D, _P, _P, _I, C.POINTER(_I64)]),
     ("sconv_net_stats", _I, [_P, C.POINTER(_I), C.POINTER(_I)]),
@@ -236,6 +240,12 @@ def exec_cfg(policy=GROUP_SORTED, epsilon=0.25, max_batch=16, gather_tile=0, sca
                    -1 if dataflow is None else dataflow, fuse_residual)
 
 
+class SearchCountersC(C.Structure):
+    _fields_ = [("backward_comparisons", C.c_uint64), ("forward_comparisons", C.c_uint64),
+                ("source_elements_loaded", C.c_uint64), ("queries_executed", C.c_uint64), ("sorts", C.c_uint64),
+                ("counted", C.c_int32)]
+
+
 class KernelMap:
     """Device-resident kernel map + sorted output coordinates."""
 
@@ -274,6 +284,26 @@ class KernelMap:
         i = MapInfo()
         self.ctx.check(self.ctx.lib.sconv_map_get_info(self.ctx.h, self.h, C.byref(i)))
         return i
+
+    @classmethod
+    def build_explicit(cls, ctx: Context, P, P_sorted: bool, Q, offsets, B=256, Cq=512,
+                       backend=0) -> "KernelMap":
+        """SPEC build_kernel_map_sorted(P, Q, offsets, B, C): arbitrary sorted
+        unique queries Q and an arbitrary offset list (host arrays)."""
+        P = np.ascontiguousarray(P, np.int32).reshape(-1, 3)
+        Q = np.ascontiguousarray(Q, np.int32).reshape(-1, 3)
+        offs = np.ascontiguousarray(offsets, np.int32).reshape(-1, 3)
+        h = C.c_void_p()
+        ctx.check(ctx.lib.sconv_map_build_explicit(ctx.h, _ptr(P), len(P), MEM_HOST, int(P_sorted), _ptr(Q), len(Q),
+                                                   MEM_HOST, _ptr(offs), len(offs), B, Cq, backend, C.byref(h)))
+        return cls(ctx, h)
+
+    def search_counters(self) -> dict:
+        """SearchCounters: comparison tallies when built with MAP_SORTED_SPEC,
+        plus the coordinate sorts the build performed."""
+        c = SearchCountersC()
+        self.ctx.check(self.ctx.lib.sconv_map_search_counters(self.ctx.h, self.h, C.byref(c)))
+        return {f: getattr(c, f) for f, _ in SearchCountersC._fields_}
 
     def read(self):
         """(output coords [n_out,3], sizes [K3], in_idx [|M|], out_idx [|M|]) in canonical order."""
@@ -402,6 +432,31 @@ def build_kernel_map_sorted(ctx: Context, P: PointCloud, K: int, s: int, B: int 
         pos += n
     m.free()
     return q, lists
+
+
+def build_kernel_map_sorted_explicit(ctx: Context, P: "PointCloud", Q, offsets, B: int = 256, Cq: int = 512,
+                                     backend: int = MAP_SORTED_SPEC):
+    """SPEC build_kernel_map_sorted(P, Q, offsets, B, C) -> (KernelMap, SearchCounters): list of
+    per-offset (j, i) arrays sorted by i, and the counters dict."""
+    m = KernelMap.build_explicit(ctx, P.coords, P.sorted, Q, offsets, B, Cq, backend)
+    _, sizes, j, i = m.read()
+    lists, pos = [], 0
+    for n in sizes:
+        lists.append(np.stack([j[pos:pos + n], i[pos:pos + n]], 1))
+        pos += n
+    cnt = m.search_counters()
+    m.free()
+    return lists, cnt
+
+
+def theoretical_hyperparams(num_inputs: int, num_outputs: int):
+    """SPEC theoretical_hyperparams(|P|, |Q|) -> (B, C); advisory."""
+    b, c = C.c_int(), C.c_int()
+    lib = load()
+    st = lib.sconv_theoretical_hyperparams(int(num_inputs), int(num_outputs), C.byref(b), C.byref(c))
+    if st != OK:
+        _raise(st, lib.sconv_global_last_error().decode())
+    return b.value, c.value
 
 
 def sc_layer_forward(ctx: Context, cloud: PointCloud, W: np.ndarray, K: int, s: int,

@@ -18,3 +18,9 @@ def ctx():
     c = sc.Context(0)
     yield c
     c.close()
+
+
+@pytest.fixture(scope="session")
+def oracle():
+    from oracle_lib import load_oracle
+    return load_oracle()

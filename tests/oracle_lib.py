@@ -154,6 +154,36 @@ class Oracle:
                                         _p(counters)))
         return self._read_map(h, counters)
 
+    def map_build(self, P, P_sorted, Q, offsets, backend=0, B=256, Cq=512, workers=1):
+        """build_kernel_map_sorted(P, Q, offsets, B, C) over explicit queries and offsets; backend
+        0 sorted (counters), 1 hash, 2 brute force. Returns (Q, sizes, j, i, counters[5])."""
+        P = np.ascontiguousarray(P, np.int32).reshape(-1, 3)
+        Q = np.ascontiguousarray(Q, np.int32).reshape(-1, 3)
+        offs = np.ascontiguousarray(offsets, np.int32).reshape(-1, 3)
+        h = C.c_void_p()
+        counters = np.zeros(5, np.uint64)
+        self._chk(self.lib.so_map_build(_p(P), len(P), int(P_sorted), _p(Q), len(Q), _p(offs), len(offs), backend, B,
+                                        Cq, workers, C.byref(h), _p(counters)))
+        return self._read_map(h, counters)
+
+    def forward_network(self, layers, xyz, sorted_, feats, seed, workers=1):
+        """SPEC forward_network over a sequential NetworkSpec (K, s, c_in, c_out) per layer ->
+        (coords, feats, sorts)."""
+        L = np.ascontiguousarray(layers, np.int32).reshape(-1, 4)
+        xyz = np.ascontiguousarray(xyz, np.int32).reshape(-1, 3)
+        feats = np.ascontiguousarray(feats, np.float32)
+        oxyz = np.empty((max(len(xyz), 1), 3), np.int32)
+        of = np.empty((max(len(xyz), 1), int(L[-1, 3])), np.float32)
+        n, sorts = C.c_int64(), C.c_uint64()
+        self._chk(self.lib.so_forward_network(_p(L), len(L), _p(xyz), len(xyz), int(sorted_), _p(feats), seed, 0,
+                                              workers, _p(oxyz), _p(of), C.byref(n), C.byref(sorts)))
+        return oxyz[: n.value], of[: n.value], sorts.value
+
+    def theoretical_hyperparams(self, P, Q):
+        b, c = C.c_int(), C.c_int()
+        self._chk(self.lib.so_theoretical_hyperparams(P, Q, C.byref(b), C.byref(c)))
+        return b.value, c.value
+
     def group_gemms(self, sizes, policy=1, eps=0.25, max_batch=16):
         sizes = np.ascontiguousarray(sizes, np.int64)
         n = len(sizes)

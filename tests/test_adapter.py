@@ -13,7 +13,8 @@ REF_INC = "/root/reference/proj/include"
 
 @pytest.mark.skipif(not os.path.isdir(REF_INC), reason="reference headers only exist on the build machine")
 def test_adapter_compiles_against_reference_headers(tmp_path):
-    r = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", f"-I{REF_INC}", f"-I{ROOT}/include",
+    r = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-DSCONV_ORACLE_USE_REFERENCE", f"-I{REF_INC}",
+                        f"-I{ROOT}/include", f"-I{ROOT}/oracle",
                         os.path.join(ROOT, "tests", "cpp", "test_adapter.cpp")], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
 
@@ -24,4 +25,4 @@ def test_adapter_runs_on_gpu():
         pytest.skip("adapter binary not built (needs the reference headers at build time)")
     r = subprocess.run([EXE], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
-    assert "threw=1" in r.stdout
+    assert "threw=1" in r.stdout and "failures 0" in r.stdout
