@@ -93,3 +93,16 @@ def test_no_cpu_fallback_when_library_missing(tmp_path):
             mod.load(str(tmp_path / "missing.so"))
         finally:
             mod._lib = saved
+
+
+def test_theoretical_hyperparams_matches_oracle():
+    """SPEC.md:244-252 (Eq. 4) through the C ABI (no GPU needed): equal to the oracle, the
+    SPEC's worked example |P| = |Q| = 2^16 -> B = 16, and its argument error."""
+    o = load_oracle()
+    assert sc.theoretical_hyperparams(1 << 16, 1 << 16)[0] == 16
+    rng = np.random.default_rng(4)
+    for p, q in [(1, 1), (2, 1), (1, 2), (100000, 100000), (123457, 40001)] + [
+            tuple(int(v) for v in rng.integers(1, 10 ** 7, 2)) for _ in range(200)]:
+        assert sc.theoretical_hyperparams(p, q) == o.theoretical_hyperparams(p, q), (p, q)
+    with pytest.raises(sc.InvalidArgument, match="point counts must be positive"):
+        sc.theoretical_hyperparams(0, 5)
