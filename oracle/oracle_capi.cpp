@@ -238,7 +238,11 @@ int so_layer_map(const std::int32_t* p, std::int64_t np, int p_sorted, int K, in
     P.coords = make_coords(to_coords(p, np));
     P.sorted = p_sorted != 0;
     const LayerGeometry g = to_geometry(K, offset_scale, out_stride, transposed, target, ntarget);
-    PointCloud Q = g.transposed ? PointCloud{g.target, Matrix{}, true} : layer_output_coords(P, out_stride, &m->counters);
+    // Q's own sort counts only for Eq. 1 (stride > 1); the sort of P that a stride-1 Q reuses is
+    // counted once, by build_layer_map's source array (one array sorted)
+    SearchCounters qc;
+    PointCloud Q = g.transposed ? PointCloud{g.target, Matrix{}, true} : layer_output_coords(P, out_stride, &qc);
+    if (!g.transposed && out_stride != 1) ++m->counters.sorts;
     LayerConfig cfg = to_config(backend, 1, 0.25, 16, 0, 0, B, C, workers);
     m->map = build_layer_map(P, Q, g, cfg, &m->counters);
     m->q = Q.coords;

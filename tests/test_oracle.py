@@ -174,3 +174,13 @@ def test_candidate_tiles_and_hyperparams(oracle):
     B, Cq = C.c_int(), C.c_int()
     assert oracle.lib.so_theoretical_hyperparams(2 ** 16, 2 ** 16, C.byref(B), C.byref(Cq)) == 0
     assert B.value == 16
+
+
+@pytest.mark.parametrize("sorted_,s,expect", [(False, 1, 1), (True, 1, 0), (False, 2, 2), (True, 2, 1)])
+def test_layer_map_sort_accounting(oracle, sorted_, s, expect):
+    """a stride-1 layer sorts its one coordinate array once (none when flagged
+    sorted); Eq. 1 adds one sort."""
+    xyz, _ = oracle.generate_synthetic(3000, 30, 0, 4)
+    if sorted_:
+        xyz = xyz[np.lexsort((xyz[:, 2], xyz[:, 1], xyz[:, 0]))]
+    assert int(oracle.layer_map(xyz, sorted_, 3, s, s)[4][4]) == expect
