@@ -83,8 +83,10 @@ typedef struct {
   int gather_tile;    /* T_g channels per work item; 0 = autotuned / heuristic */
   int scatter_tile;   /* T_s; 0 = autotuned / heuristic */
   int compute_dtype;  /* GEMM operand type: SCONV_F16 (default) or SCONV_BF16 */
-  int partial_f16;    /* 1 (default): per-offset GEMM partials stored as f16 when compute is f16;
-                         0: fp32 partials ("stored as 32-bit") */
+  int partial_f16;    /* 0 (default): per-offset GEMM partials stored as fp32 ("stored as
+                         32-bit"); 1: f16 partials when compute is f16 (halves partial traffic; the
+                         extra rounding per offset can exceed SURVEY 8(c)'s per-element bound on
+                         outputs near zero, so it is opt-in) */
   int dataflow;       /* sconv_dataflow, default GMAS for layers, AUTO for networks */
   int fuse_residual;  /* network driver: fold ADD (+ReLU) into the producing conv's epilogue (default 1) */
 } sconv_exec_cfg;

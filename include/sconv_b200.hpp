@@ -69,7 +69,7 @@ struct LayerConfig {  // SPEC.md:359 config{grouping policy, eps, max_batch, til
   int gather_tile = 0, scatter_tile = 0;  // 0 = tuned / heuristic
   int B = 256, C = 512;
   int compute_dtype = SCONV_F16;
-  int partial_f16 = 1;
+  int partial_f16 = 0;
   int dataflow = SCONV_DATAFLOW_GMAS;  // SCONV_DATAFLOW_FUSED: one output-stationary kernel
 };
 

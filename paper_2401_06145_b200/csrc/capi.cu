@@ -97,7 +97,7 @@ sconv_exec_cfg normalize(const sconv_exec_cfg* cfg, int default_dataflow = SCONV
   c.gather_tile = 0;
   c.scatter_tile = 0;
   c.compute_dtype = SCONV_F16;
-  c.partial_f16 = 1;
+  c.partial_f16 = 0;
   c.dataflow = default_dataflow;
   c.fuse_residual = 1;
   if (cfg) c = *cfg;

@@ -233,7 +233,7 @@ def map_cfg(K=3, offset_scale=1, out_stride=1, transposed=False, B=256, Cq=512, 
 
 
 def exec_cfg(policy=GROUP_SORTED, epsilon=0.25, max_batch=16, gather_tile=0, scatter_tile=0,
-             compute_dtype=F16, partial_f16=1, dataflow=None, fuse_residual=1) -> ExecCfg:
+             compute_dtype=F16, partial_f16=0, dataflow=None, fuse_residual=1) -> ExecCfg:
     """dataflow: GMAS (Minuet gather/GEMM/scatter), FUSED (one output-stationary kernel) or
     AUTO (networks: per-conv choice by timing); None = GMAS for layers, AUTO for networks."""
     return ExecCfg(policy, epsilon, max_batch, gather_tile, scatter_tile, compute_dtype, partial_f16,

@@ -222,10 +222,13 @@ def test_layer_parity(ctx, oracle, K, s, n, extent, cin, cout):
     assert_north_star(out.features, of, "fp32 partials")
     _, of32, _ = oracle.layer_forward(xyz, False, F, W, K, s, s)
     assert elementwise_errors(out.features, of32)[2] <= 2e-3
-    # default: f16 partials (halved partial traffic) -> still within the north_star tolerance
-    out16 = sc.sc_layer_forward(ctx, sc.PointCloud(xyz, F, False), W, K, s)
-    assert_north_star(out16.features, of, "f16 partials")
-    assert elementwise_errors(out16.features, of32)[2] <= 2e-3
+    # default: fp32 partials -> identical to the explicit setting above
+    np.testing.assert_array_equal(sc.sc_layer_forward(ctx, sc.PointCloud(xyz, F, False), W, K, s).features,
+                                  out.features)
+    # opt-in f16 partials (halved partial traffic): one extra rounding per offset -> bounded in
+    # the Frobenius norm only (near-zero outputs can exceed the per-element 8(c) bound)
+    out16 = sc.sc_layer_forward(ctx, sc.PointCloud(xyz, F, False), W, K, s, sc.exec_cfg(partial_f16=1))
+    assert elementwise_errors(out16.features, of)[2] <= 2e-3
     assert rel_errors(out16.features, of)[0] <= 2e-3
 
 
