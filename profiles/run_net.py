@@ -27,5 +27,5 @@ coords, feats = WL.scenes(a.workload)[0]
 net = N.Network(ctx, g, N.init_weights(g, WL.WEIGHT_SEED), sc.exec_cfg(dataflow=df))
 for _ in range(a.forwards):
     net.forward(coords, feats, True)
-ctx.sync()
+ctx.synchronize()
 print("convs", len(net.conv_stats()))
