@@ -114,6 +114,11 @@ sconv_status sconv_ctx_synchronize(sconv_ctx* ctx);
 /* Kernel launches issued by this context so far (gpu_launches accounting). */
 int64_t sconv_ctx_launch_count(const sconv_ctx* ctx);
 /* Per-kernel CUDA-event timing on the context stream (0 = off). */
+/* Gather IMT-lookup counter (SPEC.md:332-340 counter; acceptance #6: lookups = (C_in / T) * |M|):
+ * while enabled every GMaS gather adds its lookups; sconv_ctx_lookup_count returns the total since
+ * the last read and resets it (synchronises the context stream). */
+sconv_status sconv_ctx_set_lookup_counting(sconv_ctx* ctx, int enabled);
+sconv_status sconv_ctx_lookup_count(sconv_ctx* ctx, unsigned long long* count);
 sconv_status sconv_ctx_set_profiling(sconv_ctx* ctx, int enabled);
 /* Restrict profiling events to launches with this label (NULL / "" = all). */
 sconv_status sconv_ctx_set_profile_filter(sconv_ctx* ctx, const char* kernel_label);
@@ -263,6 +268,22 @@ sconv_status sconv_net_conv_stats(const sconv_net* net, int conv, int64_t* out10
 /* AUTO dataflow measurements of the tuning forward for op index `op` (ms; -1 when the op was
  * not tuned): Minuet GMaS vs the fused kernel. */
 sconv_status sconv_net_conv_timings(const sconv_net* net, int op, double* gmas_ms, double* fused_ms);
+/* autotune_network(layers, dataset sample, R) (Alg. 2): runs the network on each
+ * of the n_samples clouds (host xyz n_i x 3 int32, sorted[i], fp32 features n_i x c_in); at every
+ * CONV op profiles each candidate gather tile (supported divisors of C_in) and scatter tile
+ * (divisors of C_out) of the GMaS dataflow, 1 warm-up + `rounds` measured runs, median of the
+ * kernel's CUDA-event times; medians are summed over the samples and the argmin
+ * (smallest tile on ties) is kept for the network's later GMaS convs. tiles_out
+ * (optional, 2 per op): {T_g, T_s}, 0 for non-CONV ops. Errors: n_samples < 1 -> ARG
+ * ("sample must be nonempty"), rounds < 1 -> ARG. Tuning time is outside any benchmark. */
+sconv_status sconv_net_autotune(sconv_ctx* ctx, sconv_net* net, int n_samples, const int32_t* const* xyz,
+                                const int64_t* n, const int* sorted, const float* const* feats, int c_in, int rounds,
+                                int* tiles_out);
+/* TunedLayerConfig.latencies of op `op` from the last autotune: summed medians (ms) per candidate,
+ * gather candidates then scatter candidates, ascending tiles. tiles/ms hold `cap` entries;
+ * *n_gather / *n_scatter receive the candidate counts. */
+sconv_status sconv_net_tune_latencies(const sconv_net* net, int op, int* tiles, double* ms, int cap, int* n_gather,
+                                      int* n_scatter);
 void sconv_net_free(sconv_ctx* ctx, sconv_net* net);
 
 /* ---------------- voxelization (the step before the path) ----------------

@@ -350,6 +350,8 @@ sconv_status sconv_ctx_create(int device, sconv_ctx** out) {
     }
     SCONV_CUDA(cudaMalloc(reinterpret_cast<void**>(&ctx->done), 64));
     SCONV_CUDA(cudaMemset(ctx->done, 0, 64));
+    SCONV_CUDA(cudaMalloc(reinterpret_cast<void**>(&ctx->lookup_counter), 8));
+    SCONV_CUDA(cudaMemset(ctx->lookup_counter, 0, 8));
     const size_t sort_bytes = sizeof(int) * (3 * 65536 + 8);
     SCONV_CUDA(cudaMalloc(reinterpret_cast<void**>(&ctx->sort_state), sort_bytes));
     SCONV_CUDA(cudaMemset(ctx->sort_state, 0, sort_bytes));
@@ -377,6 +379,7 @@ void sconv_ctx_destroy(sconv_ctx* ctx) {
     ctx->gemm_out.release();
     ctx->plan_dev.release();
     ctx->fused_counter.release();  // every Ctx-owned DevBuf: freed on the stream before it dies
+    ctx->fused_ws.release();
   }
   cudaStreamSynchronize(ctx->stream);
   for (auto& p : ctx->pending) {
@@ -386,6 +389,7 @@ void sconv_ctx_destroy(sconv_ctx* ctx) {
   for (auto e : ctx->event_pool) cudaEventDestroy(e);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   if (ctx->done) cudaFree(ctx->done);
+  if (ctx->lookup_counter) cudaFree(ctx->lookup_counter);
   if (ctx->sort_state) cudaFree(ctx->sort_state);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
@@ -407,6 +411,19 @@ sconv_status sconv_ctx_synchronize(sconv_ctx* ctx) {
   });
 }
 int64_t sconv_ctx_launch_count(const sconv_ctx* ctx) { return ctx->launches; }
+sconv_status sconv_ctx_set_lookup_counting(sconv_ctx* ctx, int enabled) {
+  return guarded(ctx, [&] { ctx->count_lookups = enabled != 0; });
+}
+
+sconv_status sconv_ctx_lookup_count(sconv_ctx* ctx, unsigned long long* count) {
+  return guarded(ctx, [&] {
+    if (!count) fail(SCONV_ERR_ARG, "null argument");
+    SCONV_CUDA(cudaMemcpyAsync(count, ctx->lookup_counter, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    SCONV_CUDA(cudaMemsetAsync(ctx->lookup_counter, 0, 8, ctx->stream));
+    ctx->sync();
+  });
+}
+
 sconv_status sconv_ctx_set_profiling(sconv_ctx* ctx, int enabled) {
   return guarded(ctx, [&] {
     ctx->resolve_profile();
@@ -909,6 +926,66 @@ sconv_status sconv_net_conv_timings(const sconv_net* net, int op, double* gmas_m
   if (!net || op < 0 || op >= static_cast<int>(net->auto_ms.size())) return SCONV_ERR_ARG;
   if (gmas_ms) *gmas_ms = net->auto_ms[op][0];
   if (fused_ms) *fused_ms = net->auto_ms[op][1];
+  return SCONV_OK;
+}
+
+sconv_status sconv_net_autotune(sconv_ctx* ctx, sconv_net* net, int n_samples, const int32_t* const* xyz,
+                                const int64_t* n, const int* sorted, const float* const* feats, int c_in, int rounds,
+                                int* tiles_out) {
+  return guarded(ctx, [&] {
+    if (!net) fail(SCONV_ERR_ARG, "null argument");
+    if (n_samples < 1) fail(SCONV_ERR_ARG, "sample must be nonempty");
+    if (rounds < 1) fail(SCONV_ERR_ARG, "rounds must be positive");
+    if (!xyz || !n || !feats) fail(SCONV_ERR_ARG, "null argument");
+    NetTune t;
+    t.rounds = rounds;
+    struct Reset {
+      NetData* net;
+      ~Reset() { net->tune = nullptr; }
+    } reset{net};
+    net->tune = &t;
+    for (int i = 0; i < n_samples; ++i) {
+      MapSource P;
+      P.n = n[i];
+      P.sorted = sorted ? sorted[i] != 0 : false;
+      DevBuf staged;
+      if (P.n > 0) {
+        staged.alloc(sizeof(int32_t) * 3 * P.n, ctx->stream);
+        SCONV_CUDA(cudaMemcpyAsync(staged.get(), xyz[i], sizeof(int32_t) * 3 * P.n, cudaMemcpyHostToDevice, ctx->stream));
+        net->input_xyz = std::move(staged);
+        P.xyz = net->input_xyz.get<int32_t>();
+        P.mem = SCONV_MEM_DEVICE;
+      }
+      net->forward(*ctx, P, feats[i], SCONV_F32, SCONV_MEM_HOST, c_in);
+      ctx->sync();
+    }
+    net->finish_tune();
+    net->last_tune = t;
+    if (tiles_out)
+      for (size_t o = 0; o < net->ops.size(); ++o) {
+        tiles_out[2 * o] = net->plan.empty() ? 0 : net->plan[o].gather_tile;
+        tiles_out[2 * o + 1] = net->plan.empty() ? 0 : net->plan[o].scatter_tile;
+      }
+  });
+}
+
+sconv_status sconv_net_tune_latencies(const sconv_net* net, int op, int* tiles, double* ms, int cap, int* n_gather,
+                                      int* n_scatter) {
+  if (!net || op < 0) return SCONV_ERR_ARG;
+  const NetTune& t = net->last_tune;
+  const auto g = t.gather_ms.find(op), s = t.scatter_ms.find(op);
+  int i = 0;
+  auto put = [&](const std::map<int, double>& c) {
+    for (const auto& [tile, v] : c) {
+      if (i < cap && tiles) tiles[i] = tile;
+      if (i < cap && ms) ms[i] = v;
+      ++i;
+    }
+  };
+  if (g != t.gather_ms.end()) put(g->second);
+  if (n_gather) *n_gather = g != t.gather_ms.end() ? static_cast<int>(g->second.size()) : 0;
+  if (s != t.scatter_ms.end()) put(s->second);
+  if (n_scatter) *n_scatter = s != t.scatter_ms.end() ? static_cast<int>(s->second.size()) : 0;
   return SCONV_OK;
 }
 

@@ -152,10 +152,42 @@ struct FusedParams {
   int target_occ;  // resident CTAs per SM the ring was sized for
   unsigned long long* trace;  // debug 5: CTA 0 event timeline {kind<<56 | seq<<32 | t_lo}
   int debug;   // profiling experiments only (SCONV_FUSED_DEBUG bits): 1 no gather copies, 2 no MMAs,
-               // 4 no weight TMA (plain arrive), 8 CTA-0 timeline trace, 256 no epilogue
+               // 4 no weight TMA (plain arrive), 8 CTA-0 timeline trace, 256 no epilogue, with 1|2|4 only:
+               // 1024 producers skip the free-stage wait, 2048 MMA skips the full wait, 4096 no producer arrive
   uint32_t tmem_cols;
   int bf16;
+  int wait_mode;  // experiments (SCONV_FUSED_WAIT): how producers wait for a free stage
+  unsigned long long* spans;  // debug 8192: per CTA {start, setup done, end, tiles} (globaltimer ns)
+  // work-item kernel (k_conv_items)
+  const unsigned long long* tile_mask;
+  const void* items;  // int4 (null: one item per row block)
+  const int* item_ws;  // workspace slot per item (-1: tile not split)
+  const int* n_items;
+  int* item_counters;
+  float* ws;
+  int num_rb;
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// producers wait for a free stage (released by tcgen05.commit): 0 try_wait by every thread,
+// 1 test_wait polling by every thread, 2 lane 0 polls (test_wait) then __syncwarp,
+// 3 try_wait with a 20 ns suspend hint
+__device__ __forceinline__ void stage_wait(const FusedParams& p, uint64_t* bar, uint32_t parity) {
+  switch (p.wait_mode) {
+    case 1: sm100::mbar_wait_test(bar, parity); break;
+    case 2:
+      if ((threadIdx.x & 31) == 0) sm100::mbar_wait_test(bar, parity);
+      __syncwarp();
+      break;
+    case 3: sm100::mbar_wait_hint(bar, parity, 20); break;
+    default: sm100::mbar_wait(bar, parity); break;
+  }
+}
 
 // debug 5 timeline: each event kind owns a 1024-slot region, written with plain stores by a
 // single thread (no atomics: the trace must not perturb the pipeline)
@@ -202,10 +234,11 @@ __global__ void __launch_bounds__(kThreads, NK == 0 ? 4 : 2) k_conv_fused(const 
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_tq + 4);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int K3 = p.K3;
+  if (p.spans && threadIdx.x == 0) p.spans[blockIdx.x * 4] = gtimer();
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], (p.debug & 16) ? 4 + 1 : kProducers + 1);
+      mbar_init(&full[s], kProducers + 1);
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -223,7 +256,9 @@ __global__ void __launch_bounds__(kThreads, NK == 0 ? 4 : 2) k_conv_fused(const 
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  unsigned tr1 = 0, tr2 = 0, tr3 = 0, tr4 = 0, tr5 = 0, tr6 = 0, tr7 = 0;  // debug-8 trace cursors
+  unsigned tr0 = 0, tr1 = 0, tr2 = 0, tr3 = 0, tr4 = 0, tr5 = 0, tr6 = 0, tr7 = 0;  // debug-8 trace cursors
+  if (threadIdx.x == 0) trace_ev(p, 0, 0, tr0);  // CTA start (after TMEM allocation)
+  if (p.spans && threadIdx.x == 0) p.spans[blockIdx.x * 4 + 1] = gtimer();
 
   if (REG && warp < 4) {
     // ------------------------------------------------------------ gather producers, register indices
@@ -271,6 +306,8 @@ __global__ void __launch_bounds__(kThreads, NK == 0 ? 4 : 2) k_conv_fused(const 
     int it = 0;
     for (; t >= 0; ++it) {
       const int buf = it & 1;
+      if (tid == 0) trace_ev(p, 1, it, tr1);
+      if (p.spans && tid == 0) p.spans[blockIdx.x * 4 + 3] = it + 1;
       if (it > 0) named_bar(1, kProducers);
       if (tid == 0) s_tq[(it + 1) & 3] = grab();
       const int nb = t % p.n_blocks;
@@ -325,21 +362,31 @@ __global__ void __launch_bounds__(kThreads, NK == 0 ? 4 : 2) k_conv_fused(const 
         const int b_row = k * p.n_pad + b_row0;
         for (int kb = 0; kb < p.num_kb; ++kb) {
           if (in_stage == 0) {
-            mbar_wait(&empty[stage], phase ^ 1u);
+            if (tid == 0) trace_ev(p, 7, stage, tr7);  // about to wait for a free stage
+            if (!(p.debug & 1024)) stage_wait(p, &empty[stage], phase ^ 1u);
             stage_units = min(p.G, units_left);
             slot32 = smem_base + static_cast<uint32_t>(stage) * p.stage_bytes;
-            if (tid == 0) mbar_expect_tx(&full[stage], static_cast<uint32_t>(stage_units) * p.b_bytes);
+            if (tid == 0) {
+              if (p.debug & 4)
+                mbar_arrive(&full[stage]);
+              else
+                mbar_expect_tx(&full[stage], static_cast<uint32_t>(stage_units) * p.b_bytes);
+            }
           }
-          if (tid == 0) tma_load_2d(smem + (slot32 - smem_base) + p.a_bytes, &tmB, kb * KC, b_row, &full[stage]);
+          if (tid == 0 && !(p.debug & 4))
+            tma_load_2d(smem + (slot32 - smem_base) + p.a_bytes, &tmB, kb * KC, b_row, &full[stage]);
           const unsigned char* col = src_col + kb * (KC * 2);
+          if (!(p.debug & 1)) {
 #pragma unroll
-          for (int q = 0; q < CPR; ++q)
-            cp_async16(slot32 + a_off[q], col + static_cast<int64_t>(j[q] >= 0 ? j[q] : 0) * p.ld_in_bytes,
-                       j[q] >= 0 ? 16u : 0u);
+            for (int q = 0; q < CPR; ++q)
+              cp_async16(slot32 + a_off[q], col + static_cast<int64_t>(j[q] >= 0 ? j[q] : 0) * p.ld_in_bytes,
+                         j[q] >= 0 ? 16u : 0u);
+          }
           --units_left;
           slot32 += p.unit_bytes;
           if (++in_stage == stage_units) {
-            cp_async_arrive_noinc(&full[stage]);
+            if (!(p.debug & 4096)) cp_async_arrive_noinc(&full[stage]);
+            if (tid == 0) trace_ev(p, 2, stage, tr2);
             in_stage = 0;
             if (++stage == S) {
               stage = 0;
@@ -421,6 +468,7 @@ __global__ void __launch_bounds__(kThreads, NK == 0 ? 4 : 2) k_conv_fused(const 
       const uint32_t hi = __reduce_or_sync(0xFFFFFFFFu, static_cast<uint32_t>(mine >> 32));
       if (lane == 0) s_part[buf * 4 + warp] = (static_cast<uint64_t>(hi) << 32) | lo;
       named_bar(1, kProducers);  // index rows + partial masks of this tile are published
+      const int t_after = s_tq[(it + 2) & 3];  // the tile after next (written before the barrier)
       uint64_t mask = s_part[buf * 4] | s_part[buf * 4 + 1] | s_part[buf * 4 + 2] | s_part[buf * 4 + 3];
       if (mask == 0) mask = 1;  // no neighbour at all: one all-zero stage keeps the accumulator defined
       if (tid == 0) {
@@ -450,7 +498,7 @@ __global__ void __launch_bounds__(kThreads, NK == 0 ? 4 : 2) k_conv_fused(const 
         for (int kb = 0; kb < p.num_kb; ++kb) {
           if (in_stage == 0) {
             if (tid == 0) trace_ev(p, 7, stage, tr7);  // about to wait for a free stage
-            mbar_wait(&empty[stage], phase ^ 1u);
+            if (!(p.debug & 1024)) stage_wait(p, &empty[stage], phase ^ 1u);
             stage_units = min(p.G, units_left);
             slot32 = smem_base + static_cast<uint32_t>(stage) * p.stage_bytes;
             if (tid == 0) {
@@ -469,7 +517,7 @@ __global__ void __launch_bounds__(kThreads, NK == 0 ? 4 : 2) k_conv_fused(const 
           --units_left;
           slot32 += p.unit_bytes;
           if (++in_stage == stage_units) {
-            cp_async_arrive_noinc(&full[stage]);
+            if (!(p.debug & 4096)) cp_async_arrive_noinc(&full[stage]);
             if (tid == 0) trace_ev(p, 2, stage, tr2);
             in_stage = 0;
             if (++stage == S) {
@@ -480,6 +528,7 @@ __global__ void __launch_bounds__(kThreads, NK == 0 ? 4 : 2) k_conv_fused(const 
         }
       }
       t = t_next;
+      t_next = t_after;
     }
     if (tid == 0) {  // end-of-work marker for the MMA and the epilogue
       const int slot = it % kInfo;
@@ -510,7 +559,7 @@ __global__ void __launch_bounds__(kThreads, NK == 0 ? 4 : 2) k_conv_fused(const 
         uint32_t accumulate = 0;
         for (int units_left = __popcll(mask) * p.num_kb; units_left > 0;) {
           const int su = min(p.G, units_left);
-          mbar_wait(&full[stage], phase);
+          if (!(p.debug & 2048)) mbar_wait(&full[stage], phase);
           trace_ev(p, 3, stage, tr3);
           if (!(p.debug & 1)) fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tensor core reads
           tc_fence_after();
@@ -608,10 +657,434 @@ __global__ void __launch_bounds__(kThreads, NK == 0 ? 4 : 2) k_conv_fused(const 
   }
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) trace_ev(p, 0, 1, tr0);  // CTA end
+  if (p.spans && threadIdx.x == 0) p.spans[blockIdx.x * 4 + 2] = gtimer();
   if (warp == 8) {
     tc_fence_after();
     tmem_dealloc(tmem_base, p.tmem_cols);
   }
+}
+
+// ================================================================ work-item fused kernel
+// Same arithmetic and warp roles as k_conv_fused, with the tile bookkeeping moved off the
+// pipeline (measured r02: with every copy, MMA, handshake and epilogue disabled the old kernel
+// still spent 15-30 us per launch on its dynamic tile queue, per-tile index publication and
+// tile-info ring, and the slowest CTA ran 1.25-1.34x the average one: a few 27-offset tiles per
+// CTA do not balance).
+//   * work items are precomputed once per map (build_fused_items): item = (128-row tile, a
+//     range of <= kItemMaxOffsets of its active offsets), densest tiles first; tiles with more
+//     active offsets than the per-map cap are split into near-equal ranges, so items are of
+//     bounded size and a wide few-row layer still spreads over every SM (split-K over offsets);
+//   * static schedule: CTA b runs items b, b + grid, ...; producers, MMA issuer and epilogue
+//     walk the same list independently (no atomics, no tile-info ring, no producer barriers);
+//   * row indices in registers: thread t of the producers loads nbr[k][tile row t] for every
+//     offset of the NEXT item while the current one streams (one item of look-ahead), and the
+//     item descriptor two items ahead; warp shuffles hand each copy lane its row's index;
+//   * split items: each part writes its fp32 partial (column-major [bn][128], coalesced) to a
+//     workspace slot, the last part to finish (per-tile counter, self-resetting) sums the parts
+//     in part order -- the result does not depend on which part finishes last (deterministic).
+constexpr int kItemMaxOffsets = 28, kItemHead = 8;
+
+// work item {row block, part | parts << 8, offset mask lo, hi}: the mask holds exactly this
+// part's offsets, so one 16-byte load describes the item (no dependent loads)
+struct ItemView {
+  int rb, part, parts;
+  uint64_t mask;
+};
+// snake (boustrophedon) static schedule: round r hands items r*G .. r*G + G - 1 to CTAs 0..G-1
+// on even rounds and G-1..0 on odd ones, so with densest-first items no CTA takes the heaviest
+// item of every round
+__device__ __forceinline__ int work_of(int r) {
+  const int G = gridDim.x, b = blockIdx.x;
+  return r * G + ((r & 1) ? G - 1 - b : b);
+}
+__device__ __forceinline__ ItemView load_item(const int4* items, int i) {
+  if (!items) return ItemView{i, 0, 1, 1ull};  // 1x1 identity map: one offset per tile
+  const int4 v = __ldg(items + i);
+  return ItemView{v.x, v.y & 0xFF, v.y >> 8,
+                  (static_cast<uint64_t>(static_cast<uint32_t>(v.w)) << 32) | static_cast<uint32_t>(v.z)};
+}
+
+template <int KC, class TOut>
+__global__ void __launch_bounds__(kThreads, 2) k_conv_items(const __grid_constant__ CUtensorMap tmB,
+                                                         const __grid_constant__ FusedParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  const int S = p.stages;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.bar_off);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int* s_last = reinterpret_cast<int*>(tmem_slot + 1);  // [2] epilogue: this part finished its tile
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (p.spans && threadIdx.x == 0) p.spans[blockIdx.x * 4] = gtimer();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], kProducers + 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], kEpiWarps);
+    }
+    mbar_fence_init();
+  }
+  if (warp == 8) tmem_alloc(tmem_slot, p.tmem_cols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  if (p.spans && threadIdx.x == 0) p.spans[blockIdx.x * 4 + 1] = gtimer();
+  const int4* items = reinterpret_cast<const int4*>(p.items);
+  const int n_items = p.n_items ? __ldg(p.n_items) : p.num_rb;
+  const int n_work = n_items * p.n_blocks;
+  const int G = gridDim.x;
+
+  if (warp < 4) {
+    // ------------------------------------------------------------ gather producers
+    constexpr int CPR = KC / 8, RPI = 32 / CPR;  // 16-byte chunks per row, rows per copy instruction
+    constexpr int KM = kItemMaxOffsets;
+    const int tid = threadIdx.x;
+    const int chunk = lane % CPR, rsub = lane / CPR;
+    uint32_t a_off[CPR];
+#pragma unroll
+    for (int q = 0; q < CPR; ++q) a_off[q] = swizzled_offset<KC>(32 * warp + rsub + q * RPI, chunk);
+    const unsigned char* src_col = p.f_in + chunk * 16;
+    if (tid == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+    // software pipeline: item descriptor two items ahead; row indices of the first kItemHead
+    // offsets one item ahead, the rest at the item start (consumed kItemHead offsets later)
+    constexpr int KH = kItemHead;
+    int idx_cur[KM], idx_nxt[KH];
+    auto load_desc = [&](int w) -> ItemView {
+      return w < n_work ? load_item(items, w / p.n_blocks) : ItemView{0, 0, 1, 0ull};
+    };
+    auto nbr_of = [&](int k, int64_t row, bool ok) -> int32_t {
+      return ok ? (p.nbr ? __ldg(p.nbr + static_cast<int64_t>(k) * p.n_out + row) : static_cast<int32_t>(row)) : -1;
+    };
+    auto load_head = [&](const ItemView& it, int (&dst)[KH]) {
+      uint64_t m = it.mask;
+      const int64_t row = static_cast<int64_t>(it.rb) * 128 + tid;
+      const bool ok = row < p.n_out;
+#pragma unroll
+      for (int u = 0; u < KH; ++u)
+        if (m) {
+          dst[u] = nbr_of(__ffsll(static_cast<long long>(m)) - 1, row, ok);
+          m &= m - 1;
+        }
+    };
+    auto load_tail = [&](const ItemView& it) {
+      uint64_t m = it.mask;
+#pragma unroll
+      for (int u = 0; u < KH; ++u) m &= m - 1;
+      const int64_t row = static_cast<int64_t>(it.rb) * 128 + tid;
+      const bool ok = row < p.n_out;
+#pragma unroll
+      for (int u = KH; u < KM; ++u)
+        if (m) {
+          idx_cur[u] = nbr_of(__ffsll(static_cast<long long>(m)) - 1, row, ok);
+          m &= m - 1;
+        }
+    };
+    int r = 0, w = work_of(0);
+    ItemView it_cur = load_desc(w), it_nxt = load_desc(work_of(1));
+    load_head(it_cur, idx_nxt);
+    int stage = 0;
+    uint32_t phase = 0;
+    const uint32_t smem_base = smem_u32(smem);
+    for (; w < n_work; w = work_of(++r)) {
+#pragma unroll
+      for (int u = 0; u < KH; ++u) idx_cur[u] = idx_nxt[u];
+      load_tail(it_cur);                              // offsets >= KH of this item
+      const ItemView it_nn = load_desc(work_of(r + 2));  // consumed two items from now
+      load_head(it_nxt, idx_nxt);                    // consumed at the next item
+      const int nb = w % p.n_blocks;
+      const int b_row0 = nb * p.block_n;
+      uint64_t m = it_cur.mask;
+      int units_left = __popcll(it_cur.mask) * p.num_kb, in_stage = 0, stage_units = 0;
+      uint32_t slot32 = 0;
+#pragma unroll
+      for (int u = 0; u < KM; ++u) {
+        if (m == 0) break;
+        const int k = __ffsll(static_cast<long long>(m)) - 1;
+        m &= m - 1;
+        int32_t j[CPR];
+#pragma unroll
+        for (int q = 0; q < CPR; ++q) j[q] = __shfl_sync(0xFFFFFFFFu, idx_cur[u], rsub + q * RPI);
+        const int b_row = k * p.n_pad + b_row0;
+#pragma unroll 1
+        for (int kb = 0; kb < p.num_kb; ++kb) {
+          if (in_stage == 0) {
+            mbar_wait(&empty[stage], phase ^ 1u);
+            stage_units = min(p.G, units_left);
+            slot32 = smem_base + static_cast<uint32_t>(stage) * p.stage_bytes;
+            if (tid == 0) mbar_expect_tx(&full[stage], static_cast<uint32_t>(stage_units) * p.b_bytes);
+          }
+          if (tid == 0) tma_load_2d(smem + (slot32 - smem_base) + p.a_bytes, &tmB, kb * KC, b_row, &full[stage]);
+          const unsigned char* col = src_col + kb * (KC * 2);
+#pragma unroll
+          for (int q = 0; q < CPR; ++q)
+            cp_async16(slot32 + a_off[q], col + static_cast<int64_t>(j[q] >= 0 ? j[q] : 0) * p.ld_in_bytes,
+                       j[q] >= 0 ? 16u : 0u);
+          --units_left;
+          slot32 += p.unit_bytes;
+          if (++in_stage == stage_units) {
+            cp_async_arrive_noinc(&full[stage]);
+            in_stage = 0;
+            if (++stage == S) {
+              stage = 0;
+              phase ^= 1u;
+            }
+          }
+        }
+      }
+      it_cur = it_nxt;
+      it_nxt = it_nn;
+    }
+  } else if (warp == 8) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      int stage = 0, acc = 0;
+      uint32_t phase = 0, acc_phase = 0;
+      auto count_of = [&](int w) { return w < n_work ? __popcll(load_item(items, w / p.n_blocks).mask) : 0; };
+      int cnt_next = count_of(work_of(0));
+      for (int r = 0, w = work_of(0); w < n_work; w = work_of(++r)) {
+        const int cnt = cnt_next;
+        cnt_next = count_of(work_of(r + 1));
+        const int nb = w % p.n_blocks;
+        const int n_tile = min(p.block_n, p.n_pad - nb * p.block_n);
+        const uint32_t idesc = idesc_f16(p.bf16, n_tile);
+        mbar_wait(&tempty[acc], acc_phase ^ 1u);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * p.block_n);
+        uint32_t accumulate = 0;
+        for (int units_left = cnt * p.num_kb; units_left > 0;) {
+          const int su = min(p.G, units_left);
+          mbar_wait(&full[stage], phase);
+          fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tensor core reads
+          tc_fence_after();
+          uint32_t sa = smem_u32(smem + stage * p.stage_bytes);
+          for (int u = 0; u < su; ++u, sa += p.unit_bytes) {
+            const uint32_t sb = sa + p.a_bytes;
+#pragma unroll
+            for (int kk = 0; kk < KC / 16; ++kk) {
+              tc_mma(d_tmem, smem_desc<KC>(sa + kk * 32), smem_desc<KC>(sb + kk * 32), idesc, accumulate);
+              accumulate = 1;
+            }
+          }
+          tc_commit(&empty[stage]);
+          units_left -= su;
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+        tc_commit(&tfull[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1u;
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int q = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    TOut* out = static_cast<TOut*>(p.out);
+    const TOut* res = static_cast<const TOut*>(p.res);
+    int i = 0;
+    ItemView it_next = work_of(0) < n_work ? load_item(items, work_of(0) / p.n_blocks) : ItemView{};
+    for (int r = 0, w = work_of(0); w < n_work; w = work_of(++r), ++i) {
+      const int ii = w / p.n_blocks, nb = w % p.n_blocks;
+      const ItemView it = it_next;
+      if (work_of(r + 1) < n_work) it_next = load_item(items, work_of(r + 1) / p.n_blocks);
+      const int n0 = nb * p.block_n;
+      const int n_tile = min(p.block_n, p.n_pad - n0);
+      const int64_t trow = static_cast<int64_t>(it.rb) * 128 + q * 32 + lane;
+      const bool valid = trow < p.n_out;
+      const int64_t orow = valid && p.perm ? static_cast<int64_t>(__ldg(p.perm + trow)) : trow;
+      const int ncols = min(n_tile, p.c_out - n0);
+      mbar_wait_backoff(&tfull[acc], acc_phase);
+      tc_fence_after();
+      auto finish = [&](int c0, float (&x)[16]) {  // residual, ReLU, store 16 columns of this row
+        TOut* op = out + orow * p.ld_out + n0;
+        const TOut* rp = res ? res + orow * p.ld_res + n0 : nullptr;
+        const bool full16 = p.vec && c0 + 16 <= ncols;
+        if (rp) {
+          if (full16) {
+            float rv[16];
+            OutCvt<TOut>::load16(rp + c0, rv);
+#pragma unroll
+            for (int e = 0; e < 16; ++e) x[e] += rv[e];
+          } else {
+#pragma unroll
+            for (int e = 0; e < 16; ++e)
+              if (e < ncols - c0) x[e] += OutCvt<TOut>::to(rp[c0 + e]);
+          }
+        }
+        if (p.relu)
+#pragma unroll
+          for (int e = 0; e < 16; ++e) x[e] = fmaxf(x[e], 0.f);
+        if (full16)
+          OutCvt<TOut>::store16(op + c0, x);
+        else
+#pragma unroll
+          for (int e = 0; e < 16; ++e)
+            if (e < ncols - c0) op[c0 + e] = OutCvt<TOut>::from(x[e]);
+      };
+      const bool direct = it.parts == 1;
+      const size_t slot_elems = static_cast<size_t>(128) * p.block_n;
+      const float4* base = nullptr;  // split tile: part 0's workspace slot
+      size_t pstride = 0;
+      bool last = direct;
+      if (!direct) {
+        // split tile: partial -> workspace slot ([bn / 4][128 rows][4] fp32: each float4 access of a
+        // warp covers 512 contiguous bytes); the last part to finish sums all parts in part order
+        const int ws0 = __ldg(p.item_ws + ii) - it.part;
+        base = reinterpret_cast<const float4*>(p.ws + (static_cast<size_t>(ws0) * p.n_blocks + nb) * slot_elems) +
+               q * 32 + lane;
+        pstride = static_cast<size_t>(p.n_blocks) * slot_elems / 4;
+        float4* mine = const_cast<float4*>(base) + it.part * pstride;
+        for (int c0 = 0; c0 < n_tile; c0 += 16) {
+          uint32_t v[16];
+          tmem_ld16(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * p.block_n + c0), v);
+#pragma unroll
+          for (int g = 0; g < 4; ++g)
+            __stcg(mine + static_cast<size_t>(c0 / 4 + g) * 128,
+                   make_float4(__uint_as_float(v[4 * g]), __uint_as_float(v[4 * g + 1]), __uint_as_float(v[4 * g + 2]),
+                               __uint_as_float(v[4 * g + 3])));
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);  // the accumulator is free once read
+        __threadfence();
+        named_bar(2, 32 * kEpiWarps);
+        if (warp == 4 && lane == 0) {
+          int* ctr = p.item_counters + static_cast<int64_t>(it.rb) * p.n_blocks + nb;
+          const int done = atomicAdd(ctr, 1) == it.parts - 1;
+          if (done) *ctr = 0;  // self-resetting for the next launch on this map
+          s_last[i & 1] = done;
+        }
+        named_bar(2, 32 * kEpiWarps);
+        last = s_last[i & 1];
+        if (last) __threadfence();
+      }
+      if (last) {
+        for (int c0 = 0; c0 < n_tile; c0 += 16) {
+          float x[16];
+          if (direct) {
+            uint32_t v[16];
+            tmem_ld16(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * p.block_n + c0), v);
+#pragma unroll
+            for (int e = 0; e < 16; ++e) x[e] = __uint_as_float(v[e]);
+          } else {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) x[e] = 0.f;
+            if (valid && c0 < ncols)
+              for (int pp = 0; pp < it.parts; ++pp) {  // fixed part order: deterministic sum
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                  const float4 y = __ldcg(base + pp * pstride + static_cast<size_t>(c0 / 4 + g) * 128);
+                  x[4 * g] += y.x;
+                  x[4 * g + 1] += y.y;
+                  x[4 * g + 2] += y.z;
+                  x[4 * g + 3] += y.w;
+                }
+              }
+          }
+          if (valid && c0 < ncols) finish(c0, x);
+        }
+        if (direct) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
+      }
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1u;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (p.spans && threadIdx.x == 0) {
+    p.spans[blockIdx.x * 4 + 2] = gtimer();
+    p.spans[blockIdx.x * 4 + 3] = (n_work - blockIdx.x + G - 1) / G;
+  }
+  if (warp == 8) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, p.tmem_cols);
+  }
+}
+
+// tile_mask[rb] = OR over the tile's rows of their neighbour masks (1 if empty: one all-zero
+// offset keeps the accumulator defined)
+__global__ void __launch_bounds__(128) k_tile_masks(const int32_t* __restrict__ nbr, int64_t n, int K3,
+                                                    unsigned long long* __restrict__ tile_mask) {
+  __shared__ unsigned long long s_m[4];
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * 128 + threadIdx.x;
+  uint64_t m = 0;
+  if (row < n)
+    for (int k = 0; k < K3; ++k) m |= static_cast<uint64_t>(__ldg(nbr + static_cast<int64_t>(k) * n + row) >= 0) << k;
+  const uint32_t lo = __reduce_or_sync(0xFFFFFFFFu, static_cast<uint32_t>(m));
+  const uint32_t hi = __reduce_or_sync(0xFFFFFFFFu, static_cast<uint32_t>(m >> 32));
+  if ((threadIdx.x & 31) == 0) s_m[threadIdx.x >> 5] = (static_cast<uint64_t>(hi) << 32) | lo;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint64_t t = s_m[0] | s_m[1] | s_m[2] | s_m[3];
+    tile_mask[blockIdx.x] = t ? t : 1ull;
+  }
+}
+
+// One CTA: per-map offset budget opp = clamp(ceil(total active offsets / slots), 4, 28) (about
+// one item per CTA slot); a tile (densest = last row block first when `reverse`) with more than
+// opp active offsets is split into kItemMaxParts near-equal offset ranges, emitted in order. Split
+// parts get compact workspace slots (item_ws[i] = slot, -1 unsplit): fewer than 2 * total / opp
+// <= 2 * slots (plus 3 per tile when K3 > 2 * 28). Zeroes the split tiles' counters.
+constexpr int kItemThreads = 1024;
+__global__ void __launch_bounds__(kItemThreads) k_build_items(const unsigned long long* __restrict__ tile_mask,
+                                                              int num_rb, int slots, int reverse, int4* __restrict__ items,
+                                                              int* __restrict__ item_ws, int* __restrict__ n_items,
+                                                              int* __restrict__ counters, int n_counters) {
+  using Scan = cub::BlockScan<int, kItemThreads>;
+  __shared__ typename Scan::TempStorage tmp;
+  const int tid = threadIdx.x;
+  int pop_sum = 0;
+  for (int t = tid; t < num_rb; t += kItemThreads) pop_sum += __popcll(tile_mask[t]);
+  int total = 0, excl = 0;
+  Scan(tmp).ExclusiveSum(pop_sum, excl, total);
+  const int opp = max(4, min(kItemMaxOffsets, (total + slots - 1) / slots));
+  int carry = 0, ws_carry = 0;
+  for (int base = 0; base < num_rb; base += kItemThreads) {
+    const int ti = base + tid;
+    const int t = reverse ? num_rb - 1 - ti : ti;
+    const int pop = ti < num_rb ? __popcll(tile_mask[t]) : 0;
+    const int parts = ti < num_rb ? max(pop > opp ? 2 : 1, (pop + kItemMaxOffsets - 1) / kItemMaxOffsets) : 0;
+    int off = 0, blk = 0, woff = 0, wblk = 0;
+    __syncthreads();
+    Scan(tmp).ExclusiveSum(parts, off, blk);
+    __syncthreads();
+    Scan(tmp).ExclusiveSum(parts > 1 ? parts : 0, woff, wblk);
+    uint64_t m = ti < num_rb ? tile_mask[t] : 0;
+    for (int pp = 0; pp < parts; ++pp) {
+      const int cnt = (pp + 1) * pop / parts - pp * pop / parts;
+      uint64_t pm = 0;  // the next cnt active offsets
+      for (int c = 0; c < cnt; ++c) {
+        pm |= m & (~m + 1);
+        m &= m - 1;
+      }
+      const int i = carry + off + pp;
+      items[i] = make_int4(t, pp | (parts << 8), static_cast<int>(static_cast<uint32_t>(pm)),
+                           static_cast<int>(static_cast<uint32_t>(pm >> 32)));
+      item_ws[i] = parts > 1 ? ws_carry + woff + pp : -1;
+    }
+    carry += blk;
+    ws_carry += wblk;
+  }
+  if (tid == 0) *n_items = carry;
+  for (int c = tid; c < n_counters; c += kItemThreads) counters[c] = 0;
 }
 
 // neighbour-mask sort keys: bit pos[k] set when output i has a neighbour at offset k
@@ -629,7 +1102,8 @@ __global__ void k_mask_keys(const int32_t* __restrict__ nbr, int64_t n, int K3, 
 // The neighbour-mask permutation of a submanifold map in ONE cooperative launch instead of
 // mask kernel + CUB radix sort (histogram, scan, 3 onesweep passes) + permute kernel: every
 // one of those is latency bound at these sizes (~70 us per map whatever n). Stable LSD radix
-// sort of the 24 mask bits [begin_bit, begin_bit + 24) in three 8-bit passes, keys and values
+// sort of the 24 mask bits [begin_bit, begin_bit + 24) in three 8-bit passes (npass = 1: the
+// 8-offset maps' whole mask in one pass), keys and values
 // in registers (tile of <= 256 * kCoopMaxE rows per CTA), grid barriers between the phases:
 //   rank     stable rank of each row among its tile's rows with the same digit (warp match +
 //            per-warp digit counts, tile order = element e of thread t at e*256 + t)
@@ -642,8 +1116,8 @@ __global__ void k_mask_keys(const int32_t* __restrict__ nbr, int64_t n, int K3, 
 template <int E>
 __global__ void __launch_bounds__(kCoopThreads) k_mask_sort(
     const int32_t* __restrict__ nbr, int64_t n, int K3, const __grid_constant__ MaskOrder ord, int begin_bit,
-    int tile, uint32_t* keys0, int32_t* vals0, uint32_t* keys1, int32_t* vals1, int* cnt, int* tot, unsigned* bar,
-    int32_t* __restrict__ perm, int32_t* __restrict__ nbr_perm) {
+    int npass, int tile, uint32_t* keys0, int32_t* vals0, uint32_t* keys1, int32_t* vals1, int* cnt, int* tot,
+    unsigned* bar, int32_t* __restrict__ perm, int32_t* __restrict__ nbr_perm) {
   const int tid = threadIdx.x;
   const unsigned G = gridDim.x;
   const int64_t t0 = static_cast<int64_t>(blockIdx.x) * tile, t1 = min(n, t0 + tile);
@@ -660,7 +1134,7 @@ __global__ void __launch_bounds__(kCoopThreads) k_mask_sort(
     if (ok[e])
       for (int k = 0; k < K3; ++k) key[e] |= static_cast<uint32_t>(__ldg(nbr + int64_t{k} * n + i) >= 0) << ord.pos[k];
   }
-  for (int pass = 0; pass < 3; ++pass) {
+  for (int pass = 0; pass < npass; ++pass) {
     if (pass > 0) {
       const uint32_t* ki = pass == 1 ? keys1 : keys0;
       const int32_t* vi = pass == 1 ? vals1 : vals0;
@@ -679,7 +1153,7 @@ __global__ void __launch_bounds__(kCoopThreads) k_mask_sort(
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       if (!ok[e]) continue;
-      if (pass < 2) {
+      if (pass < npass - 1) {
         ko[pos[e]] = key[e];
         vo[pos[e]] = val[e];
       } else {
@@ -687,56 +1161,7 @@ __global__ void __launch_bounds__(kCoopThreads) k_mask_sort(
         for (int k = 0; k < K3; ++k) nbr_perm[int64_t{k} * n + pos[e]] = __ldg(nbr + int64_t{k} * n + val[e]);
       }
     }
-    if (pass < 2) grid_barrier(bar, G, target);
-  }
-}
-
-// Small kernels (K^3 <= 8: the K=2 stride-2 down / transposed up maps) are grouped by
-// neighbour mask with a 256-bin bucket sort: an up-sampling output has exactly one of the 8
-// offsets, so an unsorted 128-row tile gathers all 8 (7/8 of it zero rows). Pass 1: mask per
-// row + global histogram. Pass 2: each CTA scans the histogram, reserves its per-bin ranges
-// with one atomic per bin, and scatters rows and their nbr entries. The order inside a bin is
-// not deterministic, and need not be: rows are independent (each output row's sum is the same
-// whatever rows share its tile: absent offsets add exact zeros), and the fused kernel writes
-// each row back to its original position.
-constexpr int kBucketThreads = 256;
-__global__ void __launch_bounds__(kBucketThreads) k_bucket_count(const int32_t* __restrict__ nbr, int64_t n, int K3,
-                                                                 uint8_t* __restrict__ masks, int* __restrict__ hist) {
-  __shared__ int s_hist[256];
-  s_hist[threadIdx.x] = 0;
-  __syncthreads();
-  const int64_t i = blockIdx.x * int64_t{kBucketThreads} + threadIdx.x;
-  if (i < n) {
-    uint32_t mk = 0;
-    for (int k = 0; k < K3; ++k) mk |= static_cast<uint32_t>(__ldg(nbr + int64_t{k} * n + i) >= 0) << k;
-    masks[i] = static_cast<uint8_t>(mk);
-    atomicAdd(&s_hist[mk], 1);
-  }
-  __syncthreads();
-  if (s_hist[threadIdx.x]) atomicAdd(&hist[threadIdx.x], s_hist[threadIdx.x]);
-}
-
-__global__ void __launch_bounds__(kBucketThreads) k_bucket_scatter(const int32_t* __restrict__ nbr, int64_t n, int K3,
-                                                                   const uint8_t* __restrict__ masks,
-                                                                   const int* __restrict__ hist, int* __restrict__ cursor,
-                                                                   int32_t* __restrict__ perm, int32_t* __restrict__ nbr_perm) {
-  __shared__ int s_start[256], s_cnt[256];
-  const int tid = threadIdx.x;
-  int start;
-  block_exclusive_scan(__ldg(hist + tid), start);  // bin b -> rows with neighbour mask b
-  s_start[tid] = start;
-  s_cnt[tid] = 0;
-  __syncthreads();
-  const int64_t i = blockIdx.x * int64_t{kBucketThreads} + tid;
-  const int mk = i < n ? masks[i] : 0;
-  const int rank = i < n ? atomicAdd(&s_cnt[mk], 1) : 0;
-  __syncthreads();
-  if (s_cnt[tid]) s_start[tid] += atomicAdd(&cursor[tid], s_cnt[tid]);
-  __syncthreads();
-  if (i < n) {
-    const int64_t pos = s_start[mk] + rank;
-    perm[pos] = static_cast<int32_t>(i);
-    for (int k = 0; k < K3; ++k) nbr_perm[int64_t{k} * n + pos] = __ldg(nbr + int64_t{k} * n + i);
+    if (pass < npass - 1) grid_barrier(bar, G, target);
   }
 }
 
@@ -758,6 +1183,45 @@ __global__ void k_convert_rows(const TS* __restrict__ src, int64_t n, int c, int
   const int col = static_cast<int>(g - r * ld_dst);
   const float v = col < c ? OutCvt<TS>::to(src[r * ld_src + col]) : 0.f;
   dst[g] = OutCvt<TD>::from(v);
+}
+
+template <int KC, class TOut>
+void launch_items_t(Ctx& ctx, const FusedParams& prm, size_t smem, const CUtensorMap& tB, int64_t max_work) {
+  auto kern = k_conv_items<KC, TOut>;
+  static thread_local std::map<int, int> regs_cache;
+  int regs;
+  if (const auto hit = regs_cache.find(ctx.device); hit != regs_cache.end()) {
+    regs = hit->second;
+  } else {
+    SCONV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    SCONV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    cudaFuncAttributes fa{};
+    SCONV_CUDA(cudaFuncGetAttributes(&fa, kern));
+    regs = fa.numRegs;
+    regs_cache[ctx.device] = regs;
+  }
+  const int by_smem = static_cast<int>((228u * 1024u) / (smem + 1024u));
+  const int by_regs = 65536 / std::max(1, ((regs * 32 + 255) / 256 * 256) * (kThreads / 32));
+  const int occ = std::max(1, std::min({by_smem, by_regs, static_cast<int>(512u / prm.tmem_cols), 2}));
+  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(max_work, int64_t{ctx.num_sms} * occ)));
+  if (const char* dbg = std::getenv("SCONV_DEBUG_SYNC"); (dbg && dbg[0] == '1') || (prm.debug & 8192)) {
+    int api_occ = -1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&api_occ, kern, kThreads, smem);
+    std::fprintf(stderr, "[sconv] k_conv_items<%d> max_work=%lld grid=%d occ=%d (api %d) regs=%d smem=%zu stages=%d G=%d bn=%d cols=%u\n",
+                 KC, static_cast<long long>(max_work), grid, occ, api_occ, regs, smem, prm.stages, prm.G, prm.block_n,
+                 prm.tmem_cols);
+  }
+  ctx.launch("k_conv_fused", [&] { kern<<<grid, kThreads, smem, ctx.stream>>>(tB, prm); });
+}
+
+template <class TOut>
+void launch_items_kc(Ctx& ctx, const FusedParams& prm, size_t smem, const CUtensorMap& tB, int64_t max_work, int kc) {
+  if (kc == 64)
+    launch_items_t<64, TOut>(ctx, prm, smem, tB, max_work);
+  else if (kc == 32)
+    launch_items_t<32, TOut>(ctx, prm, smem, tB, max_work);
+  else
+    launch_items_t<16, TOut>(ctx, prm, smem, tB, max_work);
 }
 
 template <int NK, int KC, class TOut>
@@ -828,6 +1292,108 @@ void launch_kc(Ctx& ctx, const FusedArgs& a, const FusedParams& prm, size_t smem
 
 }  // namespace
 
+namespace {
+// Work-item kernel launch (k_conv_items): one pipeline per CTA, 1-2 CTAs per SM.
+void launch_conv_items(Ctx& ctx, const FusedArgs& a, int kc, int64_t row_blocks) {
+  const WeightData& w = *a.w;
+  const int bn = std::min(w.n_pad, 256);  // widest accumulator: A is gathered once per n block
+  FusedParams prm{};
+  prm.f_in = static_cast<const unsigned char*>(a.f_in);
+  prm.ld_in_bytes = a.ld_in * 2;
+  prm.nbr = a.nbr;
+  prm.perm = a.perm;
+  prm.n_out = a.n_out;
+  prm.K3 = w.K3;
+  prm.num_kb = w.k_pad / kc;
+  prm.block_n = bn;
+  prm.n_pad = w.n_pad;
+  prm.n_blocks = ceil_div(w.n_pad, bn);
+  prm.c_out = w.c_out;
+  prm.out = a.out;
+  prm.ld_out = a.ld_out;
+  prm.res = a.res;
+  prm.ld_res = a.ld_res;
+  prm.relu = a.relu;
+  prm.tile_mask = a.tile_mask;
+  prm.items = a.items;
+  prm.item_ws = a.item_ws;
+  prm.n_items = a.n_items;
+  prm.item_counters = a.item_counters;
+  prm.num_rb = static_cast<int>(row_blocks);
+  if (const char* e = std::getenv("SCONV_FUSED_DEBUG")) prm.debug = std::atoi(e);
+  {
+    const int64_t align = a.out_dtype == SCONV_F32 ? 4 : 8;  // elements per 16 bytes
+    prm.vec = a.ld_out % align == 0 && (!a.res || a.ld_res % align == 0) &&
+              reinterpret_cast<uintptr_t>(a.out) % 16 == 0 && reinterpret_cast<uintptr_t>(a.res) % 16 == 0;
+  }
+  prm.bf16 = w.dtype == SCONV_BF16;
+  prm.a_bytes = 128u * kc * 2u;
+  prm.b_bytes = static_cast<uint32_t>(bn) * kc * 2u;
+  prm.unit_bytes = (prm.a_bytes + prm.b_bytes + 1023u) & ~1023u;
+  prm.G = std::max(1, static_cast<int>((32u * 1024u) / prm.unit_bytes));
+  if (const char* e = std::getenv("SCONV_FUSED_G")) prm.G = std::max(1, std::atoi(e));
+  prm.stage_bytes = static_cast<uint32_t>(prm.G) * prm.unit_bytes;
+  const uint32_t fixed = 1024u + (2 * kMaxStages + 4) * 8u + 64u;
+  int target = 2;
+  if (const char* e = std::getenv("SCONV_FUSED_OCC")) target = std::max(1, std::min(2, std::atoi(e)));
+  const uint32_t half = (227u * 1024u) / static_cast<uint32_t>(target) - 1024u, whole = 227u * 1024u;
+  int stages = fixed < half ? static_cast<int>((half - fixed) / prm.stage_bytes) : 0;
+  if (stages < 3) stages = static_cast<int>((whole - fixed) / prm.stage_bytes);
+  stages = std::min(stages, kMaxStages);
+  if (stages < 2) fail(SCONV_ERR_ARG, "fused layer tile does not fit in shared memory");
+  prm.stages = stages;
+  prm.bar_off = static_cast<uint32_t>(stages) * prm.stage_bytes;
+  uint32_t cols = 32;
+  while (cols < 2u * static_cast<uint32_t>(bn)) cols <<= 1;
+  prm.tmem_cols = cols;
+  const size_t smem = 1024 + prm.bar_off + (2 * stages + 4) * 8 + 16;
+  if (smem > 227 * 1024) fail(SCONV_ERR_ARG, "fused layer tile does not fit in shared memory");
+  const int64_t max_items = a.items ? a.max_items : row_blocks;
+  const int64_t max_work = max_items * prm.n_blocks;
+  DevBuf spans;
+  if (prm.debug & 8192) {
+    spans.alloc(size_t{4} * 8 * 148 * 8, ctx.stream);
+    SCONV_CUDA(cudaMemsetAsync(spans.get(), 0, size_t{4} * 8 * 148 * 8, ctx.stream));
+    prm.spans = spans.get<unsigned long long>();
+  }
+  if (a.items) {  // split items' partials: one [bn][128] fp32 slot per split part and n block
+    ctx.fused_ws.reserve(static_cast<size_t>(a.max_ws_slots) * prm.n_blocks * 128 * bn * sizeof(float), ctx.stream);
+    prm.ws = ctx.fused_ws.get<float>();
+  }
+  if (prm.n_blocks > 4) fail(SCONV_ERR_ARG, "fused dataflow supports at most 1024 output channels");
+  const CUtensorMap tB = make_tensor_map_2d(w.buf.get(), w.dtype, w.k_pad, static_cast<uint64_t>(w.K3) * w.n_pad, kc,
+                                            static_cast<uint32_t>(bn), kc);
+  if (a.out_dtype == SCONV_F32)
+    launch_items_kc<float>(ctx, prm, smem, tB, max_work, kc);
+  else if (a.out_dtype == SCONV_F16)
+    launch_items_kc<__half>(ctx, prm, smem, tB, max_work, kc);
+  else
+    launch_items_kc<__nv_bfloat16>(ctx, prm, smem, tB, max_work, kc);
+  if (prm.spans) {  // debug 8192 summary (synchronises)
+    std::vector<unsigned long long> h(4 * 8 * 148);
+    SCONV_CUDA(cudaMemcpyAsync(h.data(), spans.get(), h.size() * 8, cudaMemcpyDeviceToHost, ctx.stream));
+    SCONV_CUDA(cudaStreamSynchronize(ctx.stream));
+    unsigned long long t0 = ~0ull, t1 = 0;
+    double life = 0, life_max = 0;
+    int n = 0;
+    for (size_t b = 0; b < h.size() / 4; ++b)
+      if (h[4 * b]) {
+        ++n;
+        t0 = std::min(t0, h[4 * b]);
+        t1 = std::max(t1, h[4 * b + 2]);
+        const double l = (h[4 * b + 2] - h[4 * b]) * 1e-3;
+        life += l;
+        life_max = std::max(life_max, l);
+      }
+    std::vector<int> sh(8, 0);  // CTA start offsets in 5 us bins
+    for (size_t b = 0; b < h.size() / 4; ++b)
+      if (h[4 * b]) ++sh[std::min<size_t>(7, (h[4 * b] - t0) / 5000)];
+    std::fprintf(stderr, "[spans] items ctas=%d span=%.2f us life avg=%.2f max=%.2f starts/5us: %d %d %d %d %d %d %d %d\n", n,
+                 (t1 - t0) * 1e-3, life / std::max(1, n), life_max, sh[0], sh[1], sh[2], sh[3], sh[4], sh[5], sh[6], sh[7]);
+  }
+}
+}  // namespace
+
 bool fused_supported(int K3, int c_in, int c_out) { return K3 >= 1 && K3 <= 64 && c_in >= 1 && c_out >= 1; }
 
 void launch_conv_fused(Ctx& ctx, const FusedArgs& a) {
@@ -840,6 +1406,14 @@ void launch_conv_fused(Ctx& ctx, const FusedArgs& a) {
   const int kc = w.k_pad % 64 == 0 ? 64 : (w.k_pad % 32 == 0 ? 32 : 16);
   const int64_t row_blocks = ceil_div<int64_t>(a.n_out, 128);
   if (row_blocks > INT32_MAX / 16) fail(SCONV_ERR_ARG, "layer too large");
+  static const bool v1 = [] {
+    const char* e = std::getenv("SCONV_FUSED_V1");  // A/B: the previous tile-queue kernel
+    return e && e[0] == '1';
+  }();
+  if (!v1 && (a.items || !a.nbr)) {
+    launch_conv_items(ctx, a, kc, row_blocks);
+    return;
+  }
   // block_n: widest multiple of 16 (<= 256) that still gives ~2 tiles per SM; narrower
   // blocks re-gather A from L2 once per extra n block.
   int bn = a.block_n;
@@ -872,7 +1446,13 @@ void launch_conv_fused(Ctx& ctx, const FusedArgs& a) {
   prm.ld_res = a.ld_res;
   prm.relu = a.relu;
   if (const char* e = std::getenv("SCONV_FUSED_DEBUG")) prm.debug = std::atoi(e);
-  DevBuf trace;
+  if (const char* e = std::getenv("SCONV_FUSED_WAIT")) prm.wait_mode = std::atoi(e);
+  DevBuf trace, spans;
+  if (prm.debug & 8192) {
+    spans.alloc(size_t{4} * 8 * 148 * 8, ctx.stream);
+    SCONV_CUDA(cudaMemsetAsync(spans.get(), 0, size_t{4} * 8 * 148 * 8, ctx.stream));
+    prm.spans = spans.get<unsigned long long>();
+  }
   if (prm.debug & 8) {
     trace.alloc(8192 * 8, ctx.stream);
     SCONV_CUDA(cudaMemsetAsync(trace.get(), 0, 8192 * 8, ctx.stream));
@@ -938,6 +1518,40 @@ void launch_conv_fused(Ctx& ctx, const FusedArgs& a) {
                      (e >> 32) & 0xFFFFFF);
     }
   } dump{ctx, trace};
+  struct SpanDump {  // debug 8192: kernel span, CTA start skew, lifetimes, tiles per CTA
+    Ctx& ctx;
+    DevBuf& buf;
+    ~SpanDump() {
+      if (!buf.get()) return;
+      std::vector<unsigned long long> h(4 * 8 * 148);
+      cudaMemcpyAsync(h.data(), buf.get(), h.size() * 8, cudaMemcpyDeviceToHost, ctx.stream);
+      cudaStreamSynchronize(ctx.stream);
+      unsigned long long t0 = ~0ull, t1 = 0, skew = 0;
+      double life = 0, life_max = 0, setup = 0;
+      int n = 0, tiles_max = 0;
+      for (size_t b = 0; b < h.size() / 4; ++b) {
+        if (!h[4 * b]) continue;
+        ++n;
+        t0 = std::min(t0, h[4 * b]);
+        t1 = std::max(t1, h[4 * b + 2]);
+      }
+      std::vector<int> hist(16, 0);
+      for (size_t b = 0; b < h.size() / 4; ++b) {
+        if (!h[4 * b]) continue;
+        skew = std::max(skew, h[4 * b] - t0);
+        const double l = (h[4 * b + 2] - h[4 * b]) * 1e-3;
+        life += l;
+        life_max = std::max(life_max, l);
+        setup += (h[4 * b + 1] - h[4 * b]) * 1e-3;
+        tiles_max = std::max(tiles_max, static_cast<int>(h[4 * b + 3]));
+        ++hist[std::min<int>(15, static_cast<int>(h[4 * b + 3]))];
+      }
+      std::fprintf(stderr, "[spans] ctas=%d span=%.2f us start_skew=%.2f us life avg=%.2f max=%.2f setup=%.2f us tiles max=%d hist",
+                   n, (t1 - t0) * 1e-3, skew * 1e-3, life / std::max(1, n), life_max, setup / std::max(1, n), tiles_max);
+      for (int i = 0; i <= tiles_max && i < 16; ++i) std::fprintf(stderr, " %d:%d", i, hist[i]);
+      std::fprintf(stderr, "\n");
+    }
+  } sdump{ctx, spans};
   if (a.out_dtype == SCONV_F32)
     launch_kc<float>(ctx, a, prm, smem, tB, kc);
   else if (a.out_dtype == SCONV_F16)
@@ -946,17 +1560,63 @@ void launch_conv_fused(Ctx& ctx, const FusedArgs& a) {
     launch_kc<__nv_bfloat16>(ctx, a, prm, smem, tB, kc);
 }
 
+namespace {
+void order_fused_rows(Ctx& ctx, MapData& m);
+}  // namespace
+
+// Work items of a map (k_tile_masks + k_build_items on the current stream, no host sync): the
+// item count stays on the device; the host bound max_items sizes grids and the workspace.
+void build_fused_items(Ctx& ctx, MapData& m) {
+  if (m.items_ready) return;
+  m.items_ready = true;
+  const int64_t n = m.n_out;
+  if (n == 0 || m.identity_pending) return;  // identity map: implicit single-offset items
+  const int64_t num_rb = ceil_div<int64_t>(n, 128);
+  const int slots = 2 * ctx.num_sms;
+  // split parts: < 4 slots (+ 2 per tile when K3 > 32), see k_build_items; items <= tiles + that
+  m.max_ws_slots = 4 * int64_t{slots} + (m.K3 > 2 * kItemMaxOffsets ? 3 * num_rb : 0);
+  m.max_items = num_rb + m.max_ws_slots;
+  const cudaStream_t st = ctx.stream;
+  m.tile_mask.alloc(8 * num_rb, st);
+  m.items.alloc(16 * m.max_items, st);
+  m.item_ws.alloc(4 * m.max_items, st);
+  m.n_items.alloc(sizeof(int), st);
+  m.item_counters.alloc(sizeof(int) * 4 * num_rb, st);  // (row block, n block <= 4)
+  const int32_t* nbr = m.permuted ? m.nbr_perm.get<int32_t>() : m.nbr_in.get<int32_t>();
+  const int K3 = m.K3;
+  ctx.launch("k_tile_masks", [&] {
+    k_tile_masks<<<static_cast<unsigned>(num_rb), 128, 0, st>>>(nbr, n, K3, m.tile_mask.get<unsigned long long>());
+  });
+  ctx.launch("k_build_items", [&] {
+    k_build_items<<<1, kItemThreads, 0, st>>>(m.tile_mask.get<unsigned long long>(), static_cast<int>(num_rb), slots,
+                                              m.permuted ? 1 : 0, m.items.get<int4>(), m.item_ws.get<int>(),
+                                              m.n_items.get<int>(), m.item_counters.get<int>(),
+                                              static_cast<int>(4 * num_rb));
+  });
+}
+
 void prepare_fused_layout(Ctx& ctx, MapData& m) {
   if (m.fused_ready) return;
   m.fused_ready = true;
+  order_fused_rows(ctx, m);
+  static const bool v1 = [] {
+    const char* e = std::getenv("SCONV_FUSED_V1");
+    return e && e[0] == '1';
+  }();
+  if (!v1) build_fused_items(ctx, m);
+}
+
+namespace {
+void order_fused_rows(Ctx& ctx, MapData& m) {
   const int64_t n = m.n_out;
   const int K3 = m.K3;
   // Only submanifold maps (stride 1, not transposed, K3 >= 27) are reordered: networks reuse
   // them for 4-8 convs, so the sort (~40 us at 1.2e5 rows) amortises; strided / transposed
   // maps serve a single conv.
-  // K3 <= 8 maps (K=2 down / up): cheap two-pass bucket order (SCONV_SMALL_PERMUTE=0: off). It
-  // pays only where the build runs off the critical path (networks: layout stream), so the
-  // single-layer API keeps these maps in order.
+  // K3 <= 8 maps (K=2 down / up): one stable 8-bit pass (SCONV_SMALL_PERMUTE=0: off): an
+  // up-sampling output has exactly one of the 8 offsets, so an unordered 128-row tile gathers
+  // all 8. It pays only where the build runs off the critical path (networks: layout stream),
+  // so the single-layer API keeps these maps in order.
   static const bool small_permute = [] {
     const char* e = std::getenv("SCONV_SMALL_PERMUTE");
     return !(e && e[0] == '0');
@@ -967,26 +1627,6 @@ void prepare_fused_layout(Ctx& ctx, MapData& m) {
   if (const char* e = std::getenv("SCONV_NO_PERMUTE"); e && e[0] == '1') m.permuted = false;  // experiments
   if (const char* e = std::getenv("SCONV_PERMUTE_MIN"); e && n < std::atoll(e)) m.permuted = false;
   if (!m.permuted) return;
-  if (small) {
-    const cudaStream_t st = ctx.stream;
-    DevBuf masks, bins;
-    masks.alloc(n, st);
-    bins.alloc(2 * 256 * sizeof(int), st);
-    m.row_perm.alloc(4 * n, st);
-    m.nbr_perm.alloc(4 * n * K3, st);
-    SCONV_CUDA(cudaMemsetAsync(bins.get(), 0, 2 * 256 * sizeof(int), st));
-    const unsigned blocks = static_cast<unsigned>(ceil_div<int64_t>(n, kBucketThreads));
-    int* hist = bins.get<int>();
-    ctx.launch("k_bucket_count", [&] {
-      k_bucket_count<<<blocks, kBucketThreads, 0, st>>>(m.nbr_in.get<int32_t>(), n, K3, masks.get<uint8_t>(), hist);
-    });
-    ctx.launch("k_bucket_scatter", [&] {
-      k_bucket_scatter<<<blocks, kBucketThreads, 0, st>>>(m.nbr_in.get<int32_t>(), n, K3, masks.get<uint8_t>(), hist,
-                                                          hist + 256, m.row_perm.get<int32_t>(),
-                                                          m.nbr_perm.get<int32_t>());
-    });
-    return;
-  }
   // Bit position per offset: rarer offsets (larger L1 norm: corners, then edges, then faces,
   // the always-present centre last) in the more significant bits, so equal-or-similar masks
   // end up adjacent (KITTI scan: 25.4 -> 10.4 active offsets per 128-row tile).
@@ -995,7 +1635,7 @@ void prepare_fused_layout(Ctx& ctx, MapData& m) {
   for (int k = 0; k < K3; ++k) order[k] = k;
   auto norm = [&](int k) { return std::abs(m.delta[k].x) + std::abs(m.delta[k].y) + std::abs(m.delta[k].z); };
   std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return norm(a) < norm(b); });
-  for (int p = 0; p < K3; ++p) ord.pos[order[p]] = p;
+  for (int p = 0; p < K3; ++p) ord.pos[order[p]] = small ? order[p] : p;  // small maps: bit k = offset k
   const cudaStream_t st = ctx.stream;
   DevBuf keys, keys_sorted, idx;
   keys.alloc(4 * n, st);
@@ -1017,7 +1657,10 @@ void prepare_fused_layout(Ctx& ctx, MapData& m) {
       per_sm = 0;
     return coop ? per_sm * sms : 0;
   }();
-  const bool one_launch = mask_bits == 24 && K3 >= 24 && coop_cap > 0 &&
+  // 8-offset maps: their whole 8-bit mask in one stable pass (the same one-launch sort, so the
+  // row order -- and with it the work items and any split-part summation -- is deterministic)
+  const int npass = small ? 1 : 3;
+  const bool one_launch = (small || (mask_bits == 24 && K3 >= 24)) && coop_cap > 0 &&
                           n <= static_cast<int64_t>(coop_cap) * kCoopThreads * kCoopMaxE &&
                           !(std::getenv("SCONV_MASK_SORT_CUB") && std::getenv("SCONV_MASK_SORT_CUB")[0] == '1');
   if (one_launch) {
@@ -1035,12 +1678,12 @@ void prepare_fused_layout(Ctx& ctx, MapData& m) {
     unsigned* bar = reinterpret_cast<unsigned*>(tot + 256);
     SCONV_CUDA(cudaMemsetAsync(bar, 0, 4 * sizeof(unsigned), st));
     const int32_t* nbr = m.nbr_in.get<int32_t>();
-    int begin_bit = K3 - 24, K3v = K3, tilev = tile;
+    int begin_bit = small ? 0 : K3 - 24, K3v = K3, tilev = tile, np = npass;
     int64_t nn = n;
     uint32_t *k0 = keys.get<uint32_t>(), *k1 = keys_sorted.get<uint32_t>();
     int32_t *v0 = idx.get<int32_t>(), *v1 = v1buf.get<int32_t>();
     int32_t *perm = m.row_perm.get<int32_t>(), *nperm = m.nbr_perm.get<int32_t>();
-    void* args[] = {&nbr, &nn, &K3v, &ord, &begin_bit, &tilev, &k0, &v0, &k1, &v1, &cnt, &tot, &bar, &perm, &nperm};
+    void* args[] = {&nbr, &nn, &K3v, &ord, &begin_bit, &np, &tilev, &k0, &v0, &k1, &v1, &cnt, &tot, &bar, &perm, &nperm};
     const void* fn = e == 1   ? reinterpret_cast<const void*>(k_mask_sort<1>)
                      : e == 2 ? reinterpret_cast<const void*>(k_mask_sort<2>)
                               : reinterpret_cast<const void*>(k_mask_sort<4>);
@@ -1056,7 +1699,7 @@ void prepare_fused_layout(Ctx& ctx, MapData& m) {
   size_t temp = 0;
   // sort on the top 24 key bits only (3 radix passes instead of 4): the dropped low bits are
   // the centre and two face offsets, the most common ones (KITTI: 10.32 -> 10.59 offsets/tile)
-  const int begin_bit = std::max(0, K3 - mask_bits);
+  const int begin_bit = small ? 0 : std::max(0, K3 - mask_bits);
   SCONV_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp, keys.get<uint32_t>(), keys_sorted.get<uint32_t>(),
                                              idx.get<int32_t>(), m.row_perm.get<int32_t>(), static_cast<int>(n),
                                              begin_bit, K3, st));
@@ -1073,6 +1716,8 @@ void prepare_fused_layout(Ctx& ctx, MapData& m) {
                                       m.nbr_perm.get<int32_t>());
   });
 }
+
+}  // namespace
 
 void convert_rows(Ctx& ctx, const void* src, int src_dtype, int64_t n, int c, int64_t ld_src, void* dst, int dst_dtype,
                   int64_t ld_dst) {

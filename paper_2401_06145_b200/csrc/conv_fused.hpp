@@ -22,11 +22,21 @@ struct FusedArgs {
   int64_t ld_res = 0;
   int relu = 0;
   int block_n = 0;  // 0 = choose (fill the SMs)
+  // work items (MapData::items; null with the 1x1 identity map: one single-offset item per tile)
+  const unsigned long long* tile_mask = nullptr;
+  const int4* items = nullptr;
+  const int* item_ws = nullptr;
+  const int* n_items = nullptr;
+  int* item_counters = nullptr;
+  int64_t max_items = 0, max_ws_slots = 0;
 };
 
 struct MapData;
-// Lazily orders the map's output rows by neighbour bitmask for the fused kernel (once per map).
+// Lazily orders the map's output rows by neighbour bitmask for the fused kernel and builds its
+// work items (once per map).
 void prepare_fused_layout(Ctx& ctx, MapData& m);
+// The work items alone (no-op once built; prepare_fused_layout builds them after the row order).
+void build_fused_items(Ctx& ctx, MapData& m);
 
 // true when the fused kernel supports this layer (K3 <= 64, 16-bit operands)
 bool fused_supported(int K3, int c_in, int c_out);

@@ -117,6 +117,7 @@ struct Ctx {
   DevBuf scratch_sort, scratch_misc, flush_buf;
   DevBuf gather_buf, gemm_out, plan_dev;
   DevBuf fused_counter;  // dynamic tile queue of the fused kernel
+  DevBuf fused_ws;       // split work items' fp32 partials (fused kernel)
   // (sconv_ctx_destroy releases every DevBuf above before destroying the stream)
   // Pinned host staging, carved into fixed regions, used ONLY for device->host readbacks that
   // are followed by a stream sync (map sizes / flags). Host->device inputs of a map build are
@@ -129,6 +130,9 @@ struct Ctx {
   void* pin_plan() { return pinned + kPinFlagsBytes + kPinReadbackBytes; }
 
   std::map<TuneKey, std::pair<int, int>> tuned;  // (T_g, T_s)
+  // gather IMT-lookup counter (SPEC.md:340 counter; acceptance #6), on when count_lookups
+  bool count_lookups = false;
+  unsigned long long* lookup_counter = nullptr;  // device, allocated with the context
   unsigned* done = nullptr;  // zero-initialised "last CTA" counter, reset by its user kernel
   unsigned* done_counter() { return done; }
   // bucket-sort state: histogram (kept zeroed by its scan kernel) + starts + cursors

@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(256) k_gather(const TIn* __restrict__ f_in, in
                                                 const __grid_constant__ LayerPlan plan,
                                                 const int32_t* __restrict__ map_start,
                                                 const int32_t* __restrict__ pair_in, int64_t rows, int k_pad,
-                                                TOp* __restrict__ buf) {
+                                                TOp* __restrict__ buf, unsigned long long* __restrict__ lookups) {
   __shared__ int4 s_mem[kMaxOffsets];
   const int num_members = plan.nm;
   for (int t = threadIdx.x; t < num_members; t += blockDim.x) s_mem[t] = plan.members[t];
@@ -115,6 +115,10 @@ __global__ void __launch_bounds__(256) k_gather(const TIn* __restrict__ f_in, in
   const int4 mb = s_mem[lo];
   const int64_t r = s - mb.y;
   TOp* dst = buf + s * k_pad + t * T;
+  if (lookups) {  // IMT-lookup counter ((C_in / T) * |M|), one atomic per warp
+    const unsigned hit = __ballot_sync(__activemask(), r < mb.z);
+    if ((threadIdx.x & 31) == __ffs(__activemask()) - 1) atomicAdd(lookups, static_cast<unsigned long long>(__popc(hit)));
+  }
   float v[T];
   if (r < mb.z) {
     const int32_t j = __ldg(pair_in + __ldg(map_start + mb.x) + r);
@@ -401,7 +405,8 @@ void gather_dispatch(Ctx& ctx, int T, const void* f_in, int c_in, int64_t ld_in,
   auto go = [&](auto kern) {
     ctx.launch("k_gather", [&] {
       kern<<<blocks_for(work), kBlock, 0, ctx.stream>>>(static_cast<const TIn*>(f_in), c_in, ld_in, plan, starts,
-                                                        pair_in, rows, k_pad, static_cast<TOp*>(buf));
+                                                        pair_in, rows, k_pad, static_cast<TOp*>(buf),
+                                                        ctx.count_lookups ? ctx.lookup_counter : nullptr);
     });
   };
   switch (T) {
@@ -699,7 +704,17 @@ void fused_forward(Ctx& ctx, MapData& m, const WeightData& w, const LayerIO& io)
   a.ld_in = ld;
   a.n_in = m.n_in;
   prepare_fused_layout(ctx, m);
+  if (m.fused_ready && !m.identity_pending && !m.items_ready) build_fused_items(ctx, m);  // identity materialised later
   a.nbr = m.identity_pending ? nullptr : (m.permuted ? m.nbr_perm.get<int32_t>() : m.nbr_in.get<int32_t>());
+  if (m.items.get()) {
+    a.tile_mask = m.tile_mask.get<unsigned long long>();
+    a.items = m.items.get<int4>();
+    a.item_ws = m.item_ws.get<int>();
+    a.n_items = m.n_items.get<int>();
+    a.item_counters = m.item_counters.get<int>();
+    a.max_items = m.max_items;
+    a.max_ws_slots = m.max_ws_slots;
+  }
   a.perm = m.permuted ? m.row_perm.get<int32_t>() : nullptr;
   a.n_out = m.n_out;
   a.w = &w;

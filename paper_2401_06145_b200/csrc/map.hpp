@@ -34,6 +34,13 @@ struct MapData {
   bool permuted = false;     // false: identity order (nbr_perm unused, nbr_in is read directly)
   DevBuf row_perm;           // int32 x n_out: tile row r -> output row
   DevBuf nbr_perm;           // int32 x K3 x n_out: nbr_in[k][row_perm[r]]
+  // Fused work items (conv_fused.cu build_fused_items, once per map): each 128-row tile's mask
+  // of active offsets and the work items {tile, first offset rank, offset count, part | parts << 8}
+  // in descending density; tiles with more active offsets than the per-item cap are split into
+  // near-equal offset ranges whose fp32 partials are summed in part order by the last to finish.
+  bool items_ready = false;
+  DevBuf tile_mask, items, item_ws, n_items, item_counters;
+  int64_t max_items = 0, max_ws_slots = 0;
   std::vector<int64_t> sizes;      // n_k (host)
   std::vector<int32_t> starts;     // map_start (host copy)
   int64_t total = 0;

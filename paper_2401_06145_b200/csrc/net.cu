@@ -379,6 +379,7 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
       io.res = res ? res->feats.get() : nullptr;
       io.ld_res = res ? res->ld : 0;
       io.relu = pl.relu;
+      if (tune) tune_conv(ctx, oi, m, w, io);
       int df = pl.dataflow;
       if (df == SCONV_DATAFLOW_AUTO) {
         // time both dataflows once on this input (1 warm-up + 2 timed runs each, min)
@@ -389,7 +390,10 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
         for (int rep = 0; rep < 3; ++rep)
           for (int d = 0; d < 2; ++d) {
             SCONV_CUDA(cudaEventRecord(e0, st));
-            layer_forward_dev(ctx, m, w, cfg, d == 0 ? SCONV_DATAFLOW_GMAS : SCONV_DATAFLOW_FUSED, io);
+            sconv_exec_cfg tcfg = cfg;
+            if (pl.gather_tile > 0) tcfg.gather_tile = pl.gather_tile;
+            if (pl.scatter_tile > 0) tcfg.scatter_tile = pl.scatter_tile;
+            layer_forward_dev(ctx, m, w, tcfg, d == 0 ? SCONV_DATAFLOW_GMAS : SCONV_DATAFLOW_FUSED, io);
             SCONV_CUDA(cudaEventRecord(e1, st));
             SCONV_CUDA(cudaEventSynchronize(e1));
             float ms = 0;
@@ -402,7 +406,10 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
         pl.dataflow = best[1] <= best[0] ? SCONV_DATAFLOW_FUSED : SCONV_DATAFLOW_GMAS;
         df = pl.dataflow;
       }
-      layer_forward_dev(ctx, m, w, cfg, df, io);
+      sconv_exec_cfg ccfg = cfg;  // autotuned GMaS tiles of this op (Alg. 2)
+      if (pl.gather_tile > 0) ccfg.gather_tile = pl.gather_tile;
+      if (pl.scatter_tile > 0) ccfg.scatter_tile = pl.scatter_tile;
+      layer_forward_dev(ctx, m, w, ccfg, df, io);
       if (debug_sync()) {
         std::fprintf(stderr, "[sconv] op %d conv K3=%d n_in=%lld n_out=%lld c_in=%d c_out=%d dataflow=%d ...", oi, m.K3,
                      static_cast<long long>(m.n_in), static_cast<long long>(m.n_out), w.c_in, w.c_out, df);
@@ -497,6 +504,59 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
     }
     std::fprintf(stderr, "[sconv wait] total %.1f us over %zu waits\n", 1e3 * total, waits.size());
   }
+}
+
+// Alg. 2 on one conv of a tuning forward: every candidate tile (divisors of C_in for gather,
+// C_out for scatter) runs the GMaS dataflow 1 + rounds times on this conv's
+// actual map and input; the median of the kernel's CUDA-event times is added
+// to the op's per-tile sum over the samples. The other kernel keeps the default tile.
+void NetData::tune_conv(Ctx& ctx, int op, MapData& m, const WeightData& w, const LayerIO& io) {
+  if (m.n_out == 0) return;
+  const bool was = ctx.profiling;
+  ctx.resolve_profile();
+  ctx.profiling = true;
+  DevBuf out;
+  out.alloc(static_cast<size_t>(m.n_out) * w.c_out * 2, ctx.stream);
+  LayerIO tio = io;
+  tio.f_out = out.get();
+  tio.res = nullptr;  // the epilogue does not depend on the tile
+  auto time_kernel = [&](const char* name, int tg, int ts) {
+    sconv_exec_cfg c = cfg;
+    c.gather_tile = tg;
+    c.scatter_tile = ts;
+    std::vector<double> samples;
+    for (int r = 0; r <= tune->rounds; ++r) {  // 1 warm-up + R measured
+      ctx.last_records.clear();
+      layer_forward_dev(ctx, m, w, c, SCONV_DATAFLOW_GMAS, tio);
+      ctx.resolve_profile();
+      double ms = 0;
+      for (auto& rec : ctx.last_records)
+        if (rec.first == name) ms += rec.second;
+      if (r > 0) samples.push_back(ms);
+    }
+    std::sort(samples.begin(), samples.end());
+    const size_t n = samples.size();
+    return n % 2 ? samples[n / 2] : 0.5 * (samples[n / 2 - 1] + samples[n / 2]);
+  };
+  for (int t : candidate_tiles(w.c_in)) tune->gather_ms[op][t] += time_kernel("k_gather", t, default_tile(w.c_out, false));
+  for (int t : candidate_tiles(w.c_out)) tune->scatter_ms[op][t] += time_kernel("k_scatter", default_tile(w.c_in, true), t);
+  ctx.last_records.clear();
+  ctx.profiling = was;
+}
+
+void NetData::finish_tune() {
+  auto pick = [](const std::map<int, double>& c) {
+    int best = 0;
+    double best_ms = 0;
+    for (const auto& [t, ms] : c)  // ascending tiles, strict '<': the smallest tile wins ties
+      if (best == 0 || ms < best_ms) {
+        best = t;
+        best_ms = ms;
+      }
+    return best;
+  };
+  for (auto& [op, c] : tune->gather_ms) plan.at(op).gather_tile = pick(c);
+  for (auto& [op, c] : tune->scatter_ms) plan.at(op).scatter_tile = pick(c);
 }
 
 }  // namespace sconvb

@@ -39,6 +39,14 @@ struct OpPlan {
   int res = -1;       // residual tensor added in the epilogue (-1: none)
   int relu = 0;
   int dataflow = -1;  // resolved per conv (AUTO: timed on the first forward)
+  int gather_tile = 0, scatter_tile = 0;  // autotune_network's pick for GMaS (0: context default)
+};
+
+// autotune_network (Alg. 2) state: per CONV op and candidate tile, the median
+// gather / scatter latency summed over the sample clouds.
+struct NetTune {
+  int rounds = 5;
+  std::map<int, std::map<int, double>> gather_ms, scatter_ms;
 };
 
 struct CoordSet {
@@ -89,6 +97,12 @@ struct NetData {
   void check_ops() const;
   void make_plan();
   void forward(Ctx& ctx, const MapSource& input, const void* feats, int f_dtype, int f_mem, int c_in);
+  // autotune_network: tuning forwards over the samples (profiling every candidate tile of every
+  // conv on the GMaS dataflow), then the per-op argmin (smallest tile on ties) into the plan
+  NetTune* tune = nullptr;
+  NetTune last_tune;
+  void tune_conv(Ctx& ctx, int op, MapData& m, const WeightData& w, const struct LayerIO& io);
+  void finish_tune();
 };
 
 }  // namespace sconvb

@@ -127,6 +127,49 @@ class Network:
             out[i] = (a.value, b.value)
         return out
 
+    def autotune(self, samples, rounds: int = 5):
+        """SPEC autotune_network(layers, sample, R) (Alg. 2): `samples` is a list
+        of (coords int32 [n,3], feats f32 [n,c_in], sorted) clouds. Every CONV op's GMaS gather /
+        scatter tiles are profiled on each sample (1 warm-up + R rounds, median), medians summed
+        over the samples, argmin kept (smallest tile on ties) and used by later GMaS forwards.
+        Returns {op index: TunedLayerConfig dict(gather_tile, scatter_tile, gather_ms{T: ms},
+        scatter_ms{T: ms})}."""
+        keep = []
+        xyz_p, n_v, srt, f_p = [], [], [], []
+        for c, f, srt_i in samples:
+            c = np.ascontiguousarray(c, np.int32)
+            f = np.ascontiguousarray(f, np.float32)
+            keep += [c, f]
+            xyz_p.append(c.ctypes.data)
+            f_p.append(f.ctypes.data)
+            n_v.append(len(c))
+            srt.append(int(srt_i))
+        k = len(samples)
+        arr_p = (C.c_void_p * max(1, k))(*xyz_p)
+        arr_f = (C.c_void_p * max(1, k))(*f_p)
+        arr_n = (C.c_int64 * max(1, k))(*n_v)
+        arr_s = (C.c_int * max(1, k))(*srt)
+        tiles = np.zeros(2 * len(self.g.ops), np.int32)
+        self.ctx.check(self.ctx.lib.sconv_net_autotune(self.ctx.h, self.h, k, C.cast(arr_p, C.c_void_p),
+                                                       C.cast(arr_n, C.c_void_p), C.cast(arr_s, C.c_void_p),
+                                                       C.cast(arr_f, C.c_void_p), self.g.in_channels, rounds,
+                                                       S._ptr(tiles)))
+        out = {}
+        for i, o in enumerate(self.g.ops):
+            if o.kind != CONV:
+                continue
+            cap = 64
+            t = np.zeros(cap, np.int32)
+            ms = np.zeros(cap, np.float64)
+            ng, ns = C.c_int(), C.c_int()
+            self.ctx.check(self.ctx.lib.sconv_net_tune_latencies(self.h, i, S._ptr(t), S._ptr(ms), cap, C.byref(ng),
+                                                                 C.byref(ns)))
+            g, s_ = ng.value, ns.value
+            out[i] = dict(gather_tile=int(tiles[2 * i]), scatter_tile=int(tiles[2 * i + 1]),
+                          gather_ms={int(a): float(b) for a, b in zip(t[:g], ms[:g])},
+                          scatter_ms={int(a): float(b) for a, b in zip(t[g:g + s_], ms[g:g + s_])})
+        return out
+
     def algo_bytes(self, part_bytes=2):
         """Algorithmic bytes per kernel type summed over the convs (SURVEY §8d with this path's dtypes:
         16-bit activations, 16-bit gather buffer, `part_bytes` GEMM partials, 16-bit outputs).

@@ -82,6 +82,8 @@ SIGNATURES = [
     ("sconv_ctx_stream", _P, [_P]),
     ("sconv_ctx_synchronize", _I, [_P]),
     ("sconv_ctx_launch_count", _I64, [_P]),
+    ("sconv_ctx_set_lookup_counting", _I, [_P, _I]),
+    ("sconv_ctx_lookup_count", _I, [_P, C.POINTER(_U64)]),
     ("sconv_ctx_set_profiling", _I, [_P, _I]),
     ("sconv_ctx_set_profile_filter", _I, [_P, C.c_char_p]),
     ("sconv_ctx_profile_count", _I, [_P]),
@@ -120,6 +122,8 @@ SIGNATURES = [
     ("sconv_voxelize", _I, [_P, _P, _I64, _I, _P, _I64, _I, _D, _P, _P, _I, C.POINTER(_I64)]),
     ("sconv_net_stats", _I, [_P, C.POINTER(_I), C.POINTER(_I)]),
     ("sconv_net_conv_stats", _I, [_P, _I, _P]),
+    ("sconv_net_autotune", _I, [_P, _P, _I, _P, _P, _P, _P, _I, _I, _P]),
+    ("sconv_net_tune_latencies", _I, [_P, _I, _P, _P, _I, C.POINTER(_I), C.POINTER(_I)]),
     ("sconv_net_free", None, [_P, _P]),
     ("sconv_cloud_file_info", _I, [C.c_char_p, C.POINTER(_I), C.POINTER(_I64), C.POINTER(_I64)]),
     ("sconv_mpc_read", _I, [C.c_char_p, _P, _P, _I64, _I64]),
@@ -200,6 +204,16 @@ class Context:
 
     def synchronize(self):
         self.check(self.lib.sconv_ctx_synchronize(self.h))
+
+    def count_lookups(self, enabled: bool = True):
+        """Gather IMT-lookup counting on / off (SPEC.md:340 counter)."""
+        self.check(self.lib.sconv_ctx_set_lookup_counting(self.h, int(enabled)))
+
+    def lookup_count(self) -> int:
+        """IMT lookups since the last call (resets; synchronises)."""
+        v = C.c_uint64()
+        self.check(self.lib.sconv_ctx_lookup_count(self.h, C.byref(v)))
+        return int(v.value)
 
     @property
     def launch_count(self) -> int:

@@ -290,6 +290,19 @@ def test_fused_even_kernel_and_transposed(ctx, oracle, transposed):
     assert rel_errors(got, gm)[0] <= 5e-6
 
 
+def test_fused_runtime_offset_count(ctx, oracle):
+    """64 offsets (K=4, even-K extension): the fused kernel's runtime-K3 producer variant (row
+    indices through shared memory, no compile-time offset count) against the oracle."""
+    rng = np.random.default_rng(44)
+    xyz = sort_rows(random_cloud(rng, 6000, 25))
+    m = sc.KernelMap.build(ctx, xyz, True, 4, 1, 1)
+    F = rng.random((len(xyz), 32), dtype=np.float32)
+    W = ((rng.random((64, 32, 32)) * 0.2 - 0.1)).astype(np.float32)
+    got = sc.layer_forward(ctx, m, sc.Weights(ctx, W), F, sc.exec_cfg(dataflow=sc.DATAFLOW_FUSED))
+    _, of, _ = oracle.layer_forward(xyz, True, f16(F), f16(W), 4, 1, 1)
+    assert rel_errors(got, of)[0] <= 5e-6
+
+
 def test_fused_matches_gmas(ctx):
     """Both dataflows on one map: fp32-partial GMaS and the fused kernel agree to fp32 rounding."""
     rng = np.random.default_rng(21)
