@@ -444,7 +444,8 @@ def main():
     breakdown = ctx.profile()
     dominant = max(breakdown.items(), key=lambda kv: kv[1][1])[0] if breakdown else None
     ctx.profile_reset()
-    ctx.set_profile_filter(dominant)  # timed region: events only around the dominant kernel
+    ctx.set_profiling(False)  # timed region: no per-kernel events (an event between two convs
+    # would serialise their programmatic dependent launch); the roofline pass below times them
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     launches0 = ctx.launch_count
@@ -463,10 +464,19 @@ def main():
             b.record(stream)
         torch.cuda.synchronize()
     launches = ctx.launch_count - launches0
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    # roofline pass: the same K steps again with CUDA events around the dominant kernel only
+    # (on the library's stream), giving its average launch duration
+    ctx.set_profiling(True)
+    ctx.set_profile_filter(dominant)
+    ctx.profile_reset()
+    for _ in range(args.steps):
+        ctx.flush_l2(256 << 20)
+        wl.step()
+    torch.cuda.synchronize()
     prof = ctx.profile()
     ctx.set_profiling(False)
     ctx.set_profile_filter(None)
-    step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = sum(step_ms)
     print("step ms: " + " ".join(f"{t:.3f}" for t in step_ms), file=sys.stderr)
     t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
@@ -495,18 +505,32 @@ def main():
     gc.enable()
 
     # roofline of the dominant kernel: algorithmic bytes / measured duration
-    hbm, _, peak_kind = load_peaks()
+    hbm, tc, peak_kind = load_peaks()
     roofline = None
     if dominant and dominant in prof:
         n_launch, tot = prof[dominant]
         avg_ms = tot / n_launch
         algo = wl.algo_bytes().get(dominant)
+        flops = wl.algo_flops() if dominant == "k_conv_fused" and hasattr(wl, "algo_flops") else 0.0
         ach = algo / (avg_ms / 1e3) / 1e9 if algo else None
-        roofline = {"kernel": dominant, "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
-                    "frac": (ach / hbm) if ach else None, "traffic": load_traffic().get(dominant),
-                    "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})", "avg_launch_ms": avg_ms,
-                    "launches_per_step": n_launch / args.steps, "algorithmic_bytes_per_launch": algo,
-                    "share_of_step": tot / total_ms}
+        hbm_b = {"achieved": ach, "peak": hbm, "unit": "GB/s", "frac": (ach / hbm) if ach else None,
+                 "t_min_ms": algo / hbm / 1e6 if algo else None}
+        tfs = flops / (avg_ms / 1e3) / 1e12 if flops else None
+        tc_b = {"achieved": tfs, "peak": tc, "unit": "TFLOP/s", "frac": tfs / tc if tfs else None,
+                "t_min_ms": flops / tc / 1e9 if flops else None}
+        # the binding bound: the one whose attainable time (algorithmic bytes / HBM peak vs useful
+        # flops / tensor peak) is longer
+        bind = "tensor" if flops and tc_b["t_min_ms"] > (hbm_b["t_min_ms"] or 0) else "hbm"
+        b = tc_b if bind == "tensor" else hbm_b
+        roofline = {"kernel": dominant, "bound": bind, "achieved": b["achieved"], "peak": b["peak"],
+                    "unit": b["unit"], "frac": b["frac"], "traffic": load_traffic().get(dominant),
+                    "peak_source": f"MEASURED_PEAKS.json {'bf16_tflops' if bind == 'tensor' else 'hbm_gbs'} "
+                                   f"({peak_kind})",
+                    "avg_launch_ms": avg_ms, "launches_per_step": n_launch / args.steps,
+                    "algorithmic_bytes_per_launch": algo, "useful_flops_per_launch": flops or None,
+                    "bounds": {"hbm": hbm_b, "tensor": tc_b if flops else None},
+                    "timing": "CUDA events around each launch on the library stream, a second pass over "
+                              "the K timed steps", "share_of_step": tot / total_ms}
     phases = {k: {"launches_per_step": n / n_bd, "us_per_step": 1e3 * ms / n_bd}
               for k, (n, ms) in sorted(breakdown.items(), key=lambda kv: -kv[1][1])}
 

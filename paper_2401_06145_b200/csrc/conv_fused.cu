@@ -152,11 +152,9 @@ struct FusedParams {
   int target_occ;  // resident CTAs per SM the ring was sized for
   unsigned long long* trace;  // debug 5: CTA 0 event timeline {kind<<56 | seq<<32 | t_lo}
   int debug;   // profiling experiments only (SCONV_FUSED_DEBUG bits): 1 no gather copies, 2 no MMAs,
-               // 4 no weight TMA (plain arrive), 8 CTA-0 timeline trace, 256 no epilogue, with 1|2|4 only:
-               // 1024 producers skip the free-stage wait, 2048 MMA skips the full wait, 4096 no producer arrive
+               // 4 no weight TMA (plain arrive), 8 CTA-0 timeline trace, 256 no epilogue, 8192 CTA spans
   uint32_t tmem_cols;
   int bf16;
-  int wait_mode;  // experiments (SCONV_FUSED_WAIT): how producers wait for a free stage
   unsigned long long* spans;  // debug 8192: per CTA {start, setup done, end, tiles} (globaltimer ns)
   // work-item kernel (k_conv_items)
   const unsigned long long* tile_mask;
@@ -172,21 +170,6 @@ __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
-}
-
-// producers wait for a free stage (released by tcgen05.commit): 0 try_wait by every thread,
-// 1 test_wait polling by every thread, 2 lane 0 polls (test_wait) then __syncwarp,
-// 3 try_wait with a 20 ns suspend hint
-__device__ __forceinline__ void stage_wait(const FusedParams& p, uint64_t* bar, uint32_t parity) {
-  switch (p.wait_mode) {
-    case 1: sm100::mbar_wait_test(bar, parity); break;
-    case 2:
-      if ((threadIdx.x & 31) == 0) sm100::mbar_wait_test(bar, parity);
-      __syncwarp();
-      break;
-    case 3: sm100::mbar_wait_hint(bar, parity, 20); break;
-    default: sm100::mbar_wait(bar, parity); break;
-  }
 }
 
 // debug 5 timeline: each event kind owns a 1024-slot region, written with plain stores by a
@@ -256,6 +239,12 @@ __global__ void __launch_bounds__(kThreads, NK == 0 ? 4 : 2) k_conv_fused(const 
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // PDL: setup above overlapped the previous kernel's tail; its outputs (our input rows, the
+  // residual, the tile queue it reset) are visible past this point. Dependents may launch once
+  // every CTA got here (each already holds its TMEM, so a dependent's allocation can only wait
+  // on CTAs that make progress).
+  grid_dep_wait();
+  if (threadIdx.x == 0) grid_dep_launch();
   unsigned tr0 = 0, tr1 = 0, tr2 = 0, tr3 = 0, tr4 = 0, tr5 = 0, tr6 = 0, tr7 = 0;  // debug-8 trace cursors
   if (threadIdx.x == 0) trace_ev(p, 0, 0, tr0);  // CTA start (after TMEM allocation)
   if (p.spans && threadIdx.x == 0) p.spans[blockIdx.x * 4 + 1] = gtimer();
@@ -306,8 +295,6 @@ __global__ void __launch_bounds__(kThreads, NK == 0 ? 4 : 2) k_conv_fused(const 
     int it = 0;
     for (; t >= 0; ++it) {
       const int buf = it & 1;
-      if (tid == 0) trace_ev(p, 1, it, tr1);
-      if (p.spans && tid == 0) p.spans[blockIdx.x * 4 + 3] = it + 1;
       if (it > 0) named_bar(1, kProducers);
       if (tid == 0) s_tq[(it + 1) & 3] = grab();
       const int nb = t % p.n_blocks;
@@ -362,31 +349,21 @@ __global__ void __launch_bounds__(kThreads, NK == 0 ? 4 : 2) k_conv_fused(const 
         const int b_row = k * p.n_pad + b_row0;
         for (int kb = 0; kb < p.num_kb; ++kb) {
           if (in_stage == 0) {
-            if (tid == 0) trace_ev(p, 7, stage, tr7);  // about to wait for a free stage
-            if (!(p.debug & 1024)) stage_wait(p, &empty[stage], phase ^ 1u);
+            mbar_wait(&empty[stage], phase ^ 1u);
             stage_units = min(p.G, units_left);
             slot32 = smem_base + static_cast<uint32_t>(stage) * p.stage_bytes;
-            if (tid == 0) {
-              if (p.debug & 4)
-                mbar_arrive(&full[stage]);
-              else
-                mbar_expect_tx(&full[stage], static_cast<uint32_t>(stage_units) * p.b_bytes);
-            }
+            if (tid == 0) mbar_expect_tx(&full[stage], static_cast<uint32_t>(stage_units) * p.b_bytes);
           }
-          if (tid == 0 && !(p.debug & 4))
-            tma_load_2d(smem + (slot32 - smem_base) + p.a_bytes, &tmB, kb * KC, b_row, &full[stage]);
+          if (tid == 0) tma_load_2d(smem + (slot32 - smem_base) + p.a_bytes, &tmB, kb * KC, b_row, &full[stage]);
           const unsigned char* col = src_col + kb * (KC * 2);
-          if (!(p.debug & 1)) {
 #pragma unroll
-            for (int q = 0; q < CPR; ++q)
-              cp_async16(slot32 + a_off[q], col + static_cast<int64_t>(j[q] >= 0 ? j[q] : 0) * p.ld_in_bytes,
-                         j[q] >= 0 ? 16u : 0u);
-          }
+          for (int q = 0; q < CPR; ++q)
+            cp_async16(slot32 + a_off[q], col + static_cast<int64_t>(j[q] >= 0 ? j[q] : 0) * p.ld_in_bytes,
+                       j[q] >= 0 ? 16u : 0u);
           --units_left;
           slot32 += p.unit_bytes;
           if (++in_stage == stage_units) {
-            if (!(p.debug & 4096)) cp_async_arrive_noinc(&full[stage]);
-            if (tid == 0) trace_ev(p, 2, stage, tr2);
+            cp_async_arrive_noinc(&full[stage]);
             in_stage = 0;
             if (++stage == S) {
               stage = 0;
@@ -498,7 +475,7 @@ __global__ void __launch_bounds__(kThreads, NK == 0 ? 4 : 2) k_conv_fused(const 
         for (int kb = 0; kb < p.num_kb; ++kb) {
           if (in_stage == 0) {
             if (tid == 0) trace_ev(p, 7, stage, tr7);  // about to wait for a free stage
-            if (!(p.debug & 1024)) stage_wait(p, &empty[stage], phase ^ 1u);
+            mbar_wait(&empty[stage], phase ^ 1u);
             stage_units = min(p.G, units_left);
             slot32 = smem_base + static_cast<uint32_t>(stage) * p.stage_bytes;
             if (tid == 0) {
@@ -517,7 +494,7 @@ __global__ void __launch_bounds__(kThreads, NK == 0 ? 4 : 2) k_conv_fused(const 
           --units_left;
           slot32 += p.unit_bytes;
           if (++in_stage == stage_units) {
-            if (!(p.debug & 4096)) cp_async_arrive_noinc(&full[stage]);
+            cp_async_arrive_noinc(&full[stage]);
             if (tid == 0) trace_ev(p, 2, stage, tr2);
             in_stage = 0;
             if (++stage == S) {
@@ -559,7 +536,7 @@ __global__ void __launch_bounds__(kThreads, NK == 0 ? 4 : 2) k_conv_fused(const 
         uint32_t accumulate = 0;
         for (int units_left = __popcll(mask) * p.num_kb; units_left > 0;) {
           const int su = min(p.G, units_left);
-          if (!(p.debug & 2048)) mbar_wait(&full[stage], phase);
+          mbar_wait(&full[stage], phase);
           trace_ev(p, 3, stage, tr3);
           if (!(p.debug & 1)) fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tensor core reads
           tc_fence_after();
@@ -659,6 +636,16 @@ __global__ void __launch_bounds__(kThreads, NK == 0 ? 4 : 2) k_conv_fused(const 
   __syncthreads();
   if (threadIdx.x == 0) trace_ev(p, 0, 1, tr0);  // CTA end
   if (p.spans && threadIdx.x == 0) p.spans[blockIdx.x * 4 + 2] = gtimer();
+  if (threadIdx.x == 0) {
+    // the last CTA out resets the tile queue for the next launch (every CTA has drawn its
+    // end-of-queue ticket before exiting), so no memset node sits between two convs
+    __threadfence();
+    if (atomicAdd(p.tile_counter + 1, 1) == static_cast<int>(gridDim.x) - 1) {
+      p.tile_counter[0] = 0;
+      p.tile_counter[1] = 0;
+      __threadfence();
+    }
+  }
   if (warp == 8) {
     tc_fence_after();
     tmem_dealloc(tmem_base, p.tmem_cols);
@@ -789,6 +776,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_conv_items(const __grid_constan
     int r = 0, w = work_of(0);
     ItemView it_cur = load_desc(w), it_nxt = load_desc(work_of(1));
     load_head(it_cur, idx_nxt);
+    // PDL: the map-only loads above overlapped the previous kernel's tail; the input rows are
+    // its output. Dependents may launch once every CTA got here (TMEM already held).
+    grid_dep_wait();
+    if (tid == 0) grid_dep_launch();
     int stage = 0;
     uint32_t phase = 0;
     const uint32_t smem_base = smem_u32(smem);
@@ -888,6 +879,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_conv_items(const __grid_constan
     }
   } else {
     // ------------------------------------------------------------ epilogue
+    grid_dep_wait();  // PDL: output / residual / split-tile counters of the previous kernel
     const int q = warp & 3;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -1185,6 +1177,28 @@ __global__ void k_convert_rows(const TS* __restrict__ src, int64_t n, int c, int
   dst[g] = OutCvt<TD>::from(v);
 }
 
+// Launch with programmatic stream serialization (PDL): the kernel's prologue overlaps the tail
+// of the previous kernel on the stream (the kernels call grid_dep_wait before touching its
+// outputs). SCONV_PDL=0 launches plainly (A/B).
+template <class K>
+void launch_pdl(K kern, int grid, size_t smem, cudaStream_t st, const CUtensorMap& tB, const FusedParams& prm) {
+  static const bool pdl = [] {
+    const char* e = std::getenv("SCONV_PDL");
+    return !(e && e[0] == '0');
+  }();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  SCONV_CUDA(cudaLaunchKernelEx(&cfg, kern, tB, prm));
+}
+
 template <int KC, class TOut>
 void launch_items_t(Ctx& ctx, const FusedParams& prm, size_t smem, const CUtensorMap& tB, int64_t max_work) {
   auto kern = k_conv_items<KC, TOut>;
@@ -1211,7 +1225,7 @@ void launch_items_t(Ctx& ctx, const FusedParams& prm, size_t smem, const CUtenso
                  KC, static_cast<long long>(max_work), grid, occ, api_occ, regs, smem, prm.stages, prm.G, prm.block_n,
                  prm.tmem_cols);
   }
-  ctx.launch("k_conv_fused", [&] { kern<<<grid, kThreads, smem, ctx.stream>>>(tB, prm); });
+  ctx.launch("k_conv_fused", [&] { launch_pdl(kern, grid, smem, ctx.stream, tB, prm); });
 }
 
 template <class TOut>
@@ -1262,7 +1276,7 @@ void launch_t(Ctx& ctx, const FusedArgs& a, const FusedParams& prm, size_t smem,
   if (const char* dbg = std::getenv("SCONV_DEBUG_SYNC"); dbg && dbg[0] == '1')
     std::fprintf(stderr, "[sconv] k_conv_fused<%d,%d> tiles=%d grid=%d occ=%d smem=%zu stages=%d bn=%d cols=%u\n", NK, KC,
                  prm.num_tiles, grid, occ, smem, prm.stages, prm.block_n, prm.tmem_cols);
-  ctx.launch("k_conv_fused", [&] { kern<<<grid, kThreads, smem, ctx.stream>>>(tB, prm); });
+  ctx.launch("k_conv_fused", [&] { launch_pdl(kern, grid, smem, ctx.stream, tB, prm); });
 }
 
 template <int KC, class TOut>
@@ -1394,6 +1408,18 @@ void launch_conv_items(Ctx& ctx, const FusedArgs& a, int kc, int64_t row_blocks)
 }
 }  // namespace
 
+// SCONV_FUSED_ITEMS: 0 = tile-queue kernel only, 1 = work-item kernel wherever items exist,
+// unset / 2 = per conv (few-tile wide layers: work items)
+int fused_items_mode() {
+  static const int mode = [] {
+    const char* e = std::getenv("SCONV_FUSED_ITEMS");
+    if (e && (e[0] == '0' || e[0] == '1')) return e[0] - '0';
+    const char* v1 = std::getenv("SCONV_FUSED_V1");  // older A/B switch: tile-queue only
+    return v1 && v1[0] == '1' ? 0 : 2;
+  }();
+  return mode;
+}
+
 bool fused_supported(int K3, int c_in, int c_out) { return K3 >= 1 && K3 <= 64 && c_in >= 1 && c_out >= 1; }
 
 void launch_conv_fused(Ctx& ctx, const FusedArgs& a) {
@@ -1406,11 +1432,15 @@ void launch_conv_fused(Ctx& ctx, const FusedArgs& a) {
   const int kc = w.k_pad % 64 == 0 ? 64 : (w.k_pad % 32 == 0 ? 32 : 16);
   const int64_t row_blocks = ceil_div<int64_t>(a.n_out, 128);
   if (row_blocks > INT32_MAX / 16) fail(SCONV_ERR_ARG, "layer too large");
-  static const bool v1 = [] {
-    const char* e = std::getenv("SCONV_FUSED_V1");  // A/B: the previous tile-queue kernel
-    return e && e[0] == '1';
-  }();
-  if (!v1 && (a.items || !a.nbr)) {
+  // Kernel choice (measured per conv, r02s vs r02q): the work-item kernel wins only where a
+  // layer has fewer 128-row tiles than half the SMs AND wide (>= 256-channel) inputs: its split
+  // items spread a few long tiles over every SM (C2 7,780-row 256->256: 63 -> 52 us; C3 5,512
+  // rows: 62 -> 51 us); on the big layers the tile-queue kernel's dynamic densest-first queue
+  // balances better (e.g. 119k rows 128->96: 68 vs 90 us).
+  const int mode = fused_items_mode();
+  const bool items = a.items && (mode == 1 || (mode == 2 && w.k_pad >= 256 && w.K3 >= 27 &&
+                                                  row_blocks * 2 < ctx.num_sms));
+  if (items) {
     launch_conv_items(ctx, a, kc, row_blocks);
     return;
   }
@@ -1446,7 +1476,6 @@ void launch_conv_fused(Ctx& ctx, const FusedArgs& a) {
   prm.ld_res = a.ld_res;
   prm.relu = a.relu;
   if (const char* e = std::getenv("SCONV_FUSED_DEBUG")) prm.debug = std::atoi(e);
-  if (const char* e = std::getenv("SCONV_FUSED_WAIT")) prm.wait_mode = std::atoi(e);
   DevBuf trace, spans;
   if (prm.debug & 8192) {
     spans.alloc(size_t{4} * 8 * 148 * 8, ctx.stream);
@@ -1496,8 +1525,12 @@ void launch_conv_fused(Ctx& ctx, const FusedArgs& a) {
   if (smem > 227 * 1024) fail(SCONV_ERR_ARG, "fused layer tile does not fit in shared memory");
   const CUtensorMap tB = make_tensor_map_2d(w.buf.get(), w.dtype, w.k_pad, static_cast<uint64_t>(w.K3) * w.n_pad, kc,
                                             static_cast<uint32_t>(bn), kc);
-  ctx.fused_counter.reserve(16, ctx.stream);
-  SCONV_CUDA(cudaMemsetAsync(ctx.fused_counter.get(), 0, sizeof(int), ctx.stream));
+  {  // {queue, exited CTAs}: zeroed when (re)allocated, then reset by each launch's last CTA
+    const void* before = ctx.fused_counter.get();
+    ctx.fused_counter.reserve(16, ctx.stream);
+    if (ctx.fused_counter.get() != before)
+      SCONV_CUDA(cudaMemsetAsync(ctx.fused_counter.get(), 0, 16, ctx.stream));
+  }
   prm.tile_counter = ctx.fused_counter.get<int>();
   struct TraceDump {  // debug 5: print CTA 0's timeline after the launch
     Ctx& ctx;
@@ -1571,6 +1604,8 @@ void build_fused_items(Ctx& ctx, MapData& m) {
   m.items_ready = true;
   const int64_t n = m.n_out;
   if (n == 0 || m.identity_pending) return;  // identity map: implicit single-offset items
+  const int mode = fused_items_mode();
+  if (mode == 0 || (mode == 2 && ceil_div<int64_t>(n, 128) * 2 >= ctx.num_sms)) return;  // tile-queue kernel
   const int64_t num_rb = ceil_div<int64_t>(n, 128);
   const int slots = 2 * ctx.num_sms;
   // split parts: < 4 slots (+ 2 per tile when K3 > 32), see k_build_items; items <= tiles + that
@@ -1599,11 +1634,7 @@ void prepare_fused_layout(Ctx& ctx, MapData& m) {
   if (m.fused_ready) return;
   m.fused_ready = true;
   order_fused_rows(ctx, m);
-  static const bool v1 = [] {
-    const char* e = std::getenv("SCONV_FUSED_V1");
-    return e && e[0] == '1';
-  }();
-  if (!v1) build_fused_items(ctx, m);
+  build_fused_items(ctx, m);
 }
 
 namespace {

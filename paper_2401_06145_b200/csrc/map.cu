@@ -37,6 +37,7 @@ struct MapFlags {
   int big_bucket;                // a sort bucket exceeds kMaxBucket: rebuild with the 64-bit CUB sort
   int fbox[6];                   // bbox of the Eq. 1 floored coordinates (strided maps)
   int fwide;                     // floored compact key needs > 32 bits: redo with 64-bit keys
+  int reserved;                  // explicit tail (the struct is copied to the host whole)
 };
 
 // ---------------------------------------------------------------- key packing
@@ -77,6 +78,7 @@ __global__ void k_init_flags(MapFlags* f) {
     f->fbox[0] = f->fbox[1] = f->fbox[2] = INT_MAX;
     f->fbox[3] = f->fbox[4] = f->fbox[5] = INT_MIN;
     f->fwide = 0;
+    f->reserved = 0;
   }
 }
 
@@ -1140,7 +1142,12 @@ void read_starts(Ctx& ctx, MapData& m, const void* flags, MapFlags* f) {
   const int K3 = m.K3;
   if (sizeof(MapFlags) + sizeof(int32_t) * (K3 + 1) > Ctx::kPinReadbackBytes) fail(SCONV_ERR_ARG, "kernel too large");
   auto* pin2 = static_cast<unsigned char*>(ctx.pin_readback());
-  SCONV_CUDA(cudaMemcpyAsync(pin2, flags, sizeof(MapFlags), cudaMemcpyDeviceToHost, ctx.stream));
+  if (flags) {
+    SCONV_CUDA(cudaMemcpyAsync(pin2, flags, sizeof(MapFlags), cudaMemcpyDeviceToHost, ctx.stream));
+  } else {  // lazy map over validated keys: its flags were never initialised (nothing to check)
+    std::memset(pin2, 0, sizeof(MapFlags));
+    std::memset(pin2, 0xFF, 3 * sizeof(unsigned long long));
+  }
   SCONV_CUDA(cudaMemcpyAsync(pin2 + sizeof(MapFlags), m.map_start.get(), sizeof(int32_t) * (K3 + 1),
                              cudaMemcpyDeviceToHost, ctx.stream));
   ctx.sync();
@@ -1169,7 +1176,7 @@ void ensure_canonical(Ctx& ctx, MapData& m) {
   if (m.canonical) return;
   if (m.pending.grid > 0) launch_canonical(ctx, m);
   MapFlags f;
-  read_starts(ctx, m, m.pending.flags.get(), &f);  // lazy maps carry no coordinate checks
+  read_starts(ctx, m, m.pending.flags_init ? m.pending.flags.get() : nullptr, &f);  // lazy: no coordinate checks
   m.pending = MapData::Pending{};
   m.canonical = true;
 }
@@ -1613,6 +1620,7 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
     m->canonical = false;
     m->total = -1;
     m->pending.flags = std::move(flags_buf);
+    m->pending.flags_init = flags_used;
     return m;
   }
   if (defer_canonical) {  // flags only (one sync), canonical lists on demand
@@ -1624,6 +1632,7 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
     m->canonical = false;
     m->total = -1;
     m->pending.flags = std::move(flags_buf);
+    m->pending.flags_init = flags_used;
     return m;
   }
   // ---- readback: flags + canonical list starts (one sync per map)

@@ -53,6 +53,7 @@ struct MapData {
     DevBuf counts, offs, tiles, flags;
     int64_t nchunk = 0, grid = 0, ntiles = 0;
     int ngroups = 0, qpl = 0;
+    bool flags_init = false;  // k_init_flags ran on `flags`
   } pending;
   // last GMaS stats
   int64_t buffer_length = 0;

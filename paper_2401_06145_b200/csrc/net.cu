@@ -22,6 +22,7 @@
 // (SPEC.md:528 sort reuse), so only the raw input and strided layers ever sort. Map builds
 // sync once each (sizes + error flags); GMaS launches never sync.
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -220,6 +221,18 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
     return e && e[0] == '1';
   }();
   std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>> waits;
+  // SCONV_NET_HOST_PROFILE=1: host timestamps (us since the forward started) of each op's map
+  // build / row order / launch, printed at the end (compare with a kernel timeline)
+  static const bool host_profile = [] {
+    const char* e = std::getenv("SCONV_NET_HOST_PROFILE");
+    return e && e[0] == '1';
+  }();
+  const auto h0 = std::chrono::steady_clock::now();
+  std::vector<std::tuple<int, const char*, double>> hmarks;
+  auto hmark = [&](int op, const char* what) {
+    if (host_profile)
+      hmarks.emplace_back(op, what, std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h0).count());
+  };
   auto wait_for = [&](cudaStream_t from, int op) {
     SCONV_CUDA(cudaEventRecord(ev_order, from));
     if (!wait_profile) {
@@ -318,8 +331,10 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
         // stream (with the fused row order when a fused conv may use them)
         std::unique_ptr<MapData> m;
         ctx.stream = ms;
+        hmark(oi, "map build");
         try {
           m = build_map(ctx, P, mcfg, o.transposed ? &T : nullptr, false, /*lazy=*/true);
+          hmark(oi, "map built");
           if (ms != st) {  // the row order runs beside the coordinate chain (next level's map);
             // the context stream waits on the layout stream below, which implies this map
             SCONV_CUDA(cudaEventRecord(ev_order, ms));
@@ -329,6 +344,7 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
           // off the critical path only when convs are already queued ahead of this map's first use
           m->layout_off_path = ls != st && convs_issued > 0;
           if (pl.dataflow != SCONV_DATAFLOW_GMAS) prepare_fused_layout(ctx, *m);
+          hmark(oi, "layout queued");
         } catch (...) {
           ctx.stream = st;
           throw;
@@ -410,6 +426,7 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
       if (pl.gather_tile > 0) ccfg.gather_tile = pl.gather_tile;
       if (pl.scatter_tile > 0) ccfg.scatter_tile = pl.scatter_tile;
       layer_forward_dev(ctx, m, w, ccfg, df, io);
+      hmark(oi, "conv queued");
       if (debug_sync()) {
         std::fprintf(stderr, "[sconv] op %d conv K3=%d n_in=%lld n_out=%lld c_in=%d c_out=%d dataflow=%d ...", oi, m.K3,
                      static_cast<long long>(m.n_in), static_cast<long long>(m.n_out), w.c_in, w.c_out, df);
@@ -489,6 +506,10 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
     SCONV_CUDA(cudaStreamWaitEvent(st, ev_order));
     SCONV_CUDA(cudaEventRecord(ev_order, ls));
     SCONV_CUDA(cudaStreamWaitEvent(st, ev_order));
+  }
+  if (host_profile) {
+    hmark(-1, "forward returns");
+    for (auto& [op, what, us] : hmarks) std::fprintf(stderr, "[sconv host] %8.1f us op %d %s\n", us, op, what);
   }
   if (!waits.empty()) {  // SCONV_NET_WAIT_PROFILE
     SCONV_CUDA(cudaStreamSynchronize(st));

@@ -173,7 +173,8 @@ class Network:
     def algo_bytes(self, part_bytes=2):
         """Algorithmic bytes per kernel type summed over the convs (SURVEY §8d with this path's dtypes:
         16-bit activations, 16-bit gather buffer, `part_bytes` GEMM partials, 16-bit outputs).
-        Fused convs: input rows read once (2*ci*n), the nbr table (4*K3*q), output (+residual) once."""
+        Fused convs: input rows read once (2*ci*n), the nbr table (4*K3*q), output (+residual) once,
+        the weights once (2*K3*ci*co)."""
         g = e = s = f = 0
         maps = {}  # distinct searched maps (identity 1x1 maps need no search): SURVEY §8d Map bytes
         for st in self.conv_stats():
@@ -181,7 +182,7 @@ class Network:
             if K3 > 1:
                 maps[(n, q, M, K3)] = 8 * n + 8 * q + 8 * M + 4 * K3
             if df == 1:
-                f += 2 * ci * n + 4 * K3 * q + 2 * co * q * (2 if res else 1)
+                f += 2 * ci * n + 4 * K3 * q + 2 * co * q * (2 if res else 1) + 2 * K3 * ci * co
                 continue
             g += 2 * ci * n + 2 * kp * R + 4 * M
             e += 2 * kp * R + part_bytes * co * R + 2 * K3 * ci * co

@@ -8,6 +8,8 @@ the layer's max |output|), (b) SURVEY §8(c)'s per-element metric against that o
 (c) the effect of rounding inputs and weights to 16 bits, against the plain fp32 oracle
 (Frobenius-relative <= 2e-3).
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -301,6 +303,53 @@ def test_fused_runtime_offset_count(ctx, oracle):
     got = sc.layer_forward(ctx, m, sc.Weights(ctx, W), F, sc.exec_cfg(dataflow=sc.DATAFLOW_FUSED))
     _, of, _ = oracle.layer_forward(xyz, True, f16(F), f16(W), 4, 1, 1)
     assert rel_errors(got, of)[0] <= 5e-6
+
+
+_VARIANT_SCRIPT = r"""
+import os, sys, json
+import numpy as np
+sys.path[:0] = [os.environ["REPO"], os.path.join(os.environ["REPO"], "tests")]
+import paper_2401_06145_b200 as sc
+from oracle_lib import load_oracle
+ctx = sc.Context(0)
+ora = load_oracle()
+rng = np.random.default_rng(5)
+res = {}
+for n, ext, cin, cout in [(3000, 24, 256, 256), (5000, 30, 384, 256), (2500, 22, 128, 96), (40000, 60, 64, 64)]:
+    flat = rng.choice(ext ** 3, size=n, replace=False)
+    xyz = np.stack(np.unravel_index(flat, (ext,) * 3), 1).astype(np.int32)
+    F = rng.random((n, cin), dtype=np.float32)
+    W = (rng.random((27, cin, cout)) * 0.2 - 0.1).astype(np.float32)
+    m = sc.KernelMap.build(ctx, xyz, False, 3, 1, 1)
+    w = sc.Weights(ctx, W)
+    cfg = sc.exec_cfg(dataflow=sc.DATAFLOW_FUSED)
+    a = sc.layer_forward(ctx, m, w, F, cfg)
+    b = sc.layer_forward(ctx, m, w, F, cfg)
+    h = lambda x: x.astype(np.float16).astype(np.float32)
+    _, of, _ = ora.layer_forward(xyz, False, h(F), h(W), 3, 1, 1)
+    res[f"{n}x{cin}->{cout}"] = {"err": float(np.abs(a - of).max() / np.abs(of).max()),
+                                  "deterministic": bool((a == b).all())}
+print(json.dumps(res))
+"""
+
+
+@pytest.mark.parametrize("mode", ["0", "1", "2"])
+def test_fused_kernel_variants(mode):
+    """Both fused kernels on the same layers (SCONV_FUSED_ITEMS: 0 tile-queue kernel, 1 work-item
+    kernel wherever items exist, 2 the per-conv default), incl. few-tile wide layers whose tiles
+    the work-item kernel splits over offsets (fp32 part sums in fixed part order): same-operand
+    parity with the oracle and bitwise-repeatable results."""
+    import json
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SCONV_FUSED_ITEMS=mode, REPO=repo)
+    r = subprocess.run([sys.executable, "-c", _VARIANT_SCRIPT], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    res = json.loads(r.stdout.strip().splitlines()[-1])
+    for k, v in res.items():
+        assert v["err"] <= 5e-6, (mode, k, v)
+        assert v["deterministic"], (mode, k)
 
 
 def test_fused_matches_gmas(ctx):
