@@ -1181,8 +1181,26 @@ void ensure_canonical(Ctx& ctx, MapData& m) {
   m.canonical = true;
 }
 
+void check_deferred_map_flags(const void* flags_host, const MapSource& P) {
+  static_assert(sizeof(MapFlags) <= kDeferredFlagsBytes, "deferred flags slot");
+  MapFlags f;
+  std::memcpy(&f, flags_host, sizeof(f));
+  if (f.bad_coord != ULLONG_MAX) {
+    const int64_t i = static_cast<int64_t>(f.bad_coord / 3);
+    const int axis = static_cast<int>(f.bad_coord % 3);
+    int32_t c[3];
+    if (P.mem == SCONV_MEM_HOST)
+      std::memcpy(c, P.xyz + 3 * i, sizeof(c));
+    else
+      SCONV_CUDA(cudaMemcpy(c, P.xyz + 3 * i, sizeof(c), cudaMemcpyDeviceToHost));
+    fail(SCONV_ERR_RANGE, coord_error("xyz"[axis], c[axis]));
+  }
+  if (f.unsorted) fail(SCONV_ERR_ARG, "input coordinates flagged sorted are not strictly increasing");
+}
+
 std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map_cfg& cfg, const MapSource* target,
-                                   bool force_wide, bool lazy, const std::vector<int3>* explicit_offsets) {
+                                   bool force_wide, bool lazy, const std::vector<int3>* explicit_offsets,
+                                   void* defer_flags) {
   if (cfg.block_B < 4 || cfg.block_B > 1024 || cfg.block_B % 4 != 0)
     fail(SCONV_ERR_ARG, "block size B must be a multiple of 4 in [4, 1024]");
   if (cfg.block_C < 1 || cfg.block_C > 4096) fail(SCONV_ERR_ARG, "query block size C must be in [1, 4096]");
@@ -1617,6 +1635,16 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
     if (!defer_canonical) launch_canonical(ctx, *m);
   }
   if (lazy) {  // canonical lists + readback deferred to ensure_canonical()
+    m->canonical = false;
+    m->total = -1;
+    m->pending.flags = std::move(flags_buf);
+    m->pending.flags_init = flags_used;
+    return m;
+  }
+  if (defer_canonical && defer_flags && P.sorted && !P.keys && !target && !need_nout_sync) {
+    // sorted raw coordinates: only range / order flags, no fallback -> checked by the caller
+    SCONV_CUDA(cudaMemcpyAsync(defer_flags, flags, sizeof(MapFlags), cudaMemcpyDeviceToHost, st));
+    m->flags_deferred = true;
     m->canonical = false;
     m->total = -1;
     m->pending.flags = std::move(flags_buf);

@@ -47,6 +47,7 @@ struct MapData {
   // Canonical pair lists (scan + emit + one readback sync) are built lazily for network maps:
   // the fused dataflow needs only nbr_in (ensure_canonical() before using sizes/pairs/nbr_pos).
   bool canonical = true;
+  bool flags_deferred = false;  // build_map(defer_flags): coordinate checks pending at the caller
   bool identity_pending = false;
   bool layout_off_path = false;  // fused row order built beside the convs (network layout stream)  // lazy 1x1 identity map: arrays not yet written (nbr_in[i] = i)
   struct Pending {
@@ -80,7 +81,13 @@ struct MapSource {
 // list and Q = *target (sorted unique queries).
 std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map_cfg& cfg, const MapSource* target,
                                    bool force_wide = false, bool lazy = false,
-                                   const std::vector<int3>* explicit_offsets = nullptr);
+                                   const std::vector<int3>* explicit_offsets = nullptr, void* defer_flags = nullptr);
+// defer_flags (pinned host, >= kDeferredFlagsBytes): a map over SORTED raw coordinates (no sort
+// fallback exists) skips its flags sync; the flags are copied there asynchronously on the build
+// stream and the caller checks them with check_deferred_map_flags once that copy completed
+// (networks: at the end of the forward, after every launch is queued).
+constexpr size_t kDeferredFlagsBytes = 128;
+void check_deferred_map_flags(const void* flags_host, const MapSource& P);
 // Builds the canonical pair lists of a lazily built map (no-op otherwise): scan + emit + sync.
 void ensure_canonical(Ctx& ctx, MapData& m);
 

@@ -194,6 +194,7 @@ NetData::~NetData() {
       cudaStreamDestroy(*sp);
     }
   if (ev_order) cudaEventDestroy(ev_order);
+  if (ev_flags) cudaEventDestroy(ev_flags);
 }
 
 void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f_dtype, int f_mem, int c_in) {
@@ -204,6 +205,7 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
     return !(e && e[0] == '0');
   }();
   if (!ev_order) SCONV_CUDA(cudaEventCreateWithFlags(&ev_order, cudaEventDisableTiming));
+  if (!ev_flags) SCONV_CUDA(cudaEventCreateWithFlags(&ev_flags, cudaEventDisableTiming));
   if (use_map_stream && !map_stream) {
     int lo = 0, hi = 0;
     SCONV_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -266,7 +268,11 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
     t.fused_away = false;
   }
   coordsets.clear();
-  maps.clear();
+  // the previous forward's maps are freed at the END of this forward: ~180 stream-ordered
+  // frees here would delay the first launches by ~80 us of host time (the GPU idles then)
+  std::map<MapKey, MapEntry> old_maps;
+  old_maps.swap(maps);
+  const void* deferred_flags = nullptr;  // raw sorted input: coordinate checks after the launches
   int convs_issued = 0;
   maps_built = 0;
   sorts = 0;
@@ -333,7 +339,12 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
         ctx.stream = ms;
         hmark(oi, "map build");
         try {
-          m = build_map(ctx, P, mcfg, o.transposed ? &T : nullptr, false, /*lazy=*/true);
+          void* dflags = cs.raw && !cs.keys ? static_cast<char*>(ctx.pin_flags()) + Ctx::kPinFlagsBytes / 2 : nullptr;
+          m = build_map(ctx, P, mcfg, o.transposed ? &T : nullptr, false, /*lazy=*/true, nullptr, dflags);
+          if (m->flags_deferred) {
+            deferred_flags = dflags;
+            SCONV_CUDA(cudaEventRecord(ev_flags, ms));
+          }
           hmark(oi, "map built");
           if (ms != st) {  // the row order runs beside the coordinate chain (next level's map);
             // the context stream waits on the layout stream below, which implies this map
@@ -506,6 +517,11 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
     SCONV_CUDA(cudaStreamWaitEvent(st, ev_order));
     SCONV_CUDA(cudaEventRecord(ev_order, ls));
     SCONV_CUDA(cudaStreamWaitEvent(st, ev_order));
+  }
+  old_maps.clear();  // frees enqueued behind this forward's work on the map / layout streams
+  if (deferred_flags) {  // the copy was queued right after the input's key packing: long done
+    SCONV_CUDA(cudaEventSynchronize(ev_flags));
+    check_deferred_map_flags(deferred_flags, raw_input);
   }
   if (host_profile) {
     hmark(-1, "forward returns");

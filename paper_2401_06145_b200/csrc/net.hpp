@@ -89,6 +89,7 @@ struct NetData {
   cudaStream_t map_stream = nullptr;
   cudaStream_t layout_stream = nullptr;  // fused row order (mask sort): off the coordinate chain
   cudaEvent_t ev_order = nullptr;
+  cudaEvent_t ev_flags = nullptr;  // deferred raw-input coordinate checks (copy done)
 
   NetData() = default;
   NetData(const NetData&) = delete;
