@@ -769,6 +769,135 @@ __global__ void __launch_bounds__(kSearchThreads) k_search(
   if (lane == 0) chunk_count[int64_t{k} * nchunk + c] = cnt;
 }
 
+// Column variant of k_search for the cubic offset sets (K = 2, 3; no explicit offset list).
+// The K offsets sharing (dx, dy) -- a "column" -- differ only in z, and within one (x, y)
+// column of a sorted key array z is the last key field: their segment keys are consecutive
+// keys of the column. So a warp owns a COLUMN (K^2 warps per CTA instead of K^3 warp tasks):
+// it stages one window [q_first + (dx, dy, zmin), q_last + (dx, dy, zmax)] (per-warp bulk copy,
+// sliced as in k_search), finds each query's lower bound of its smallest-z key by galloping
+// from the lane's previous query, and resolves the K z-offsets by a merge walk (keys between
+// two z-offsets of a lattice-aligned set do not exist, so the walk is <= K + a few steps).
+// A third of the searches and window copies of k_search and no per-block backward pass; the
+// same dense k-major table and per-(k, chunk) hit counts as k_search.
+template <int QPL, int KZ>
+__global__ void __launch_bounds__(32 * KZ * KZ, KZ == 3 ? 2 : 4) k_search_col(
+    const uint64_t* __restrict__ src, const int32_t* __restrict__ src_idx, int64_t n_src, int B,
+    const uint64_t* __restrict__ q, int64_t n_q, int scale, int64_t nchunk, int cap_blocks,
+    int32_t* __restrict__ nbr, int32_t* __restrict__ chunk_count) {
+  constexpr int CQ = 32 * QPL, kWarps = KZ * KZ;
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ __align__(8) uint64_t s_bar[kWarps];
+  __shared__ uint64_t s_q[CQ];
+  const int lane = threadIdx.x & 31, col = threadIdx.x >> 5;
+  const int cap = cap_blocks * B;
+  uint64_t* s_win = reinterpret_cast<uint64_t*>(smem) + int64_t{col} * cap;
+  int32_t* s_widx = reinterpret_cast<int32_t*>(reinterpret_cast<uint64_t*>(smem) + int64_t{kWarps} * cap) +
+                    int64_t{col} * cap;
+  const int64_t c = blockIdx.x;
+  const int64_t lo = c * CQ;
+  const int len = static_cast<int>(min(static_cast<int64_t>(CQ), n_q - lo));
+  for (int t = threadIdx.x; t < CQ; t += 32 * kWarps)
+    s_q[(t % QPL) * 32 + t / QPL] = t < len ? __ldg(q + lo + t) : ~uint64_t{0};
+  __syncthreads();
+  uint64_t* bar = &s_bar[col];
+  if (lane == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  constexpr int zlo = (KZ % 2 == 1) ? -(KZ / 2) : 0;
+  const int dx = (col / KZ + zlo) * scale, dy = (col % KZ + zlo) * scale;
+  // z-ascending order of the column's offsets: zi -> tz (scale < 0 for transposed maps)
+  auto tz_of = [&](int zi) { return scale > 0 ? zi : KZ - 1 - zi; };
+  auto ekey = [&](uint64_t qk, int zi) { return segment_key(qk, make_int3(dx, dy, (tz_of(zi) + zlo) * scale)); };
+  const int qb = lane * QPL;
+  uint64_t key[QPL];
+  int res[QPL][KZ];
+  int zn[QPL];  // next unresolved z-offset of each query (KZ: done)
+#pragma unroll
+  for (int u = 0; u < QPL; ++u) {
+    key[u] = s_q[u * 32 + lane];
+    zn[u] = qb + u < len ? 0 : KZ;
+#pragma unroll
+    for (int z = 0; z < KZ; ++z) res[u][z] = -1;
+  }
+  const uint64_t key_lo = ekey(s_q[0], 0), key_hi = ekey(s_q[((len - 1) % QPL) * 32 + (len - 1) / QPL], KZ - 1);
+  const int64_t nb = (n_src + B - 1) / B;
+  const int64_t blo =
+      warp_first_pivot_ge(src, n_src, B, 0, nb, key_lo, lane, ((lo * n_src) / max(n_q, int64_t{1})) / B);
+  const int64_t bhi =
+      blo >= nb ? blo : min(warp_first_pivot_ge(src, n_src, B, blo, nb, key_hi, lane, blo + (len + B - 1) / B), nb - 1);
+  uint32_t phase = 0;
+  for (int64_t sb = blo; sb < nb && sb <= bhi; sb += cap_blocks) {
+    const int nblk = static_cast<int>(min(static_cast<int64_t>(cap_blocks), bhi - sb + 1));
+    const int64_t g0 = sb * B;
+    const int wlen = static_cast<int>(min(static_cast<int64_t>(nblk) * B, n_src - g0));
+    if (lane == 0) {
+      const uint32_t kb = static_cast<uint32_t>((wlen + 3) & ~3);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                   "r"(kb * 8u + (src_idx ? kb * 4u : 0u))
+                   : "memory");
+      bulk_g2s(s_win, src + g0, kb * 8u, bar);
+      if (src_idx) bulk_g2s(s_widx, src_idx + g0, kb * 4u, bar);
+    }
+    mbar_wait_parity(bar, phase);
+    phase ^= 1u;
+    const uint64_t last = s_win[wlen - 1];
+    int pprev = 0;  // lower bound of the lane's previous query's smallest-z key (sorted queries)
+#pragma unroll
+    for (int u = 0; u < QPL; ++u) {
+      if (zn[u] >= KZ) continue;
+      uint64_t e = ekey(key[u], zn[u]);
+      if (e > last) continue;  // beyond this slice
+      // lower bound of e in [base, wlen): gallop from the previous query's position
+      int base = zn[u] == 0 ? pprev : 0;
+      if (s_win[base] < e) {
+        int lo_ = base, hi_ = base + 1, step = 1;  // invariant s_win[lo_] < e
+        while (hi_ < wlen - 1 && s_win[hi_] < e) {
+          lo_ = hi_;
+          step <<= 1;
+          hi_ = min(base + step, wlen - 1);
+        }
+        int b = lo_ + 1, n = hi_ - lo_;  // answer in [lo_ + 1, hi_]; s_win[wlen - 1] >= e
+        while (n > 1) {
+          const int h = n >> 1;
+          b += s_win[b + h - 1] < e ? h : 0;
+          n -= h;
+        }
+        base = b;
+      }
+      if (zn[u] == 0) pprev = base;
+      int p = base;
+      const int z0 = zn[u];
+#pragma unroll
+      for (int zi = 0; zi < KZ; ++zi) {
+        if (zi < z0) continue;
+        if (zi > z0) e = ekey(key[u], zi);
+        while (p < wlen && s_win[p] < e) ++p;
+        if (p == wlen) break;  // the rest lies in the next slice
+        if (s_win[p] == e) {
+          res[u][zi] = src_idx ? s_widx[p] : static_cast<int32_t>(g0 + p);  // z order (static index)
+          ++p;
+        }
+        zn[u] = zi + 1;
+      }
+    }
+    __syncwarp();  // the next slice overwrites the window
+  }
+#pragma unroll
+  for (int zi = 0; zi < KZ; ++zi) {
+    const int k = col * KZ + tz_of(zi);
+    int32_t* row = nbr + int64_t{k} * n_q + lo + qb;
+    int cnt = 0;
+#pragma unroll
+    for (int u = 0; u < QPL; ++u) {
+      if (qb + u < len) row[u] = res[u][zi];
+      cnt += __popc(__ballot_sync(0xFFFFFFFFu, res[u][zi] >= 0));
+    }
+    if (lane == 0) chunk_count[int64_t{k} * nchunk + c] = cnt;
+  }
+}
+
 // Exclusive scan of the (k, chunk) hit counts in canonical order: each CTA scans a tile of
 // kScanTile counts (tile-local offsets + tile total); the last CTA to finish scans the tile
 // totals and writes the canonical list starts map_start[k] (= offset of (k, chunk 0)).
@@ -1527,7 +1656,13 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
     if (lazy) return m;  // nothing pending; flags were not touched
   } else {
     // Work item = one CTA per chunk of CQ = 32*QPL sorted queries (CQ <= C), all offsets.
-    const int qpl = C >= 256 ? 8 : (C >= 128 ? 4 : (C >= 64 ? 2 : 1));
+    static const bool col_search = [] {
+      const char* e = std::getenv("SCONV_SEARCH_COL");  // A/B: 0 = one warp per offset
+      return !(e && e[0] == '0');
+    }();
+    const bool use_col = col_search && !explicit_q && (cfg.kernel_size == 2 || cfg.kernel_size == 3) && C >= 128 &&
+                         cfg.backend == SCONV_MAP_SORTED;
+    const int qpl = use_col ? 4 : (C >= 256 ? 8 : (C >= 128 ? 4 : (C >= 64 ? 2 : 1)));
     const int CQ = 32 * qpl;
     const int64_t nchunk2 = ceil_div<int64_t>(n_out, CQ);
     const int64_t grid2 = nchunk2 * K3;
@@ -1607,6 +1742,25 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
         return e ? std::max(4, std::atoi(e)) : 768;
       }();
       const int cap_blocks = std::max(1, cap_keys / B);
+      if (use_col) {
+        const int kz = cfg.kernel_size;
+        // a 128-query chunk's column window spans ~1-2 blocks of 256: 2-block slices
+        const int cap_col = std::max(1, std::min(cap_blocks, 512 / B));
+        const size_t smem = size_t{12} * kz * kz * cap_col * B;
+        const int scale = cfg.transposed ? -cfg.offset_scale : cfg.offset_scale;
+        auto go = [&](auto kern) {
+          SCONV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+          ctx.launch("k_search", [&] {
+            kern<<<static_cast<unsigned>(nchunk2), 32 * kz * kz, smem, st>>>(
+                src, src_idx, n, B, q, n_out, scale, nchunk2, cap_col, m->nbr_in.get<int32_t>(),
+                counts.get<int32_t>());
+          });
+        };
+        if (kz == 3)
+          go(k_search_col<4, 3>);
+        else
+          go(k_search_col<4, 2>);
+      } else {
       const size_t smem = size_t{12} * (kSearchThreads / 32) * cap_blocks * B;
       auto go = [&](auto kern) {
         SCONV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
@@ -1621,6 +1775,7 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
         case 2: go(k_search<2>); break;
         case 4: go(k_search<4>); break;
         default: go(k_search<8>); break;
+      }
       }
     }
     auto& pd = m->pending;

@@ -93,7 +93,13 @@ for i, f_ in enumerate(fw):
     names = collections.defaultdict(float)
     for k in cs:
         names[k["name"].replace("(anonymous namespace)::", "").replace("sconvb::", "").split("(")[0][-40:]] += k["end"] - k["start"]
-    rec = {"forward": i, "span_us": t1 - t0, "launches": len(f_), "conv_stream": conv_stream,
+    alln = collections.defaultdict(lambda: [0, 0.0])
+    for k in f_:
+        nm = k["name"].replace("(anonymous namespace)::", "").replace("sconvb::", "").split("(")[0][-40:]
+        alln[nm][0] += 1
+        alln[nm][1] += k["end"] - k["start"]
+    rec = {"forward": i, "all_kernels": {n: {"launches": c, "us": round(t, 1)} for n, (c, t) in
+                                         sorted(alln.items(), key=lambda kv: -kv[1][1])}, "span_us": t1 - t0, "launches": len(f_), "conv_stream": conv_stream,
            "busy_us": {str(s): v for s, v in busy.items()},
            "conv_stream_idle_us": sum(g_[0] for g_ in gaps), "conv_stream_gaps": len(gaps),
            "top_gaps": [{"us": round(g_[0], 1), "before": g_[1], "at_us": round(g_[2], 1)}
@@ -108,6 +114,9 @@ for i, f_ in enumerate(fw):
     for g_ in rec["top_gaps"][:8]:
         print(f"   gap {g_['us']:7.1f} us at {g_['at_us']:7.1f} before {g_['before']}")
 if out:
+    print("kernel totals of the last forward (all streams):")
+    for n, v in out[-1]["all_kernels"].items():
+        print(f"  {n:44s} {v['launches']:3d} {v['us']:8.1f} us")
     print("timeline of the last forward (first 60 kernels): t0 t1 stream name")
     for k in out[-1]["first_kernels"]:
         print(f"  {k['t0']:8.1f} {k['t1']:8.1f} {k['stream']:4d} {k['name']}")
