@@ -195,9 +195,13 @@ __device__ __forceinline__ int32_t nbr_at(const FusedParams& p, int k, int64_t i
 }
 
 // NK = compile-time offset count (registers prefetch the next tile's index rows), 0 = runtime
-template <int NK, int KC, class TOut, bool REG = false>
+// DENSE (1x1 identity maps only: input row i of output row i, no row permutation): the A tile
+// is a plain 128-row box of the input, TMA-loaded with the same swizzle as the weights by one
+// producer thread (no per-row cp.async gathers), so the layer is a TMA-fed tcgen05 GEMM.
+template <int NK, int KC, class TOut, bool REG = false, bool DENSE = false>
 __global__ void __launch_bounds__(kThreads, NK == 0 ? 4 : 2) k_conv_fused(const __grid_constant__ CUtensorMap tmB,
-                                                           const __grid_constant__ FusedParams p) {
+                                                           const __grid_constant__ FusedParams p,
+                                                           const __grid_constant__ CUtensorMap tmA) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte aligned base (SW128 atoms) derived by OFFSET from the __shared__ array, so the
   // compiler keeps the shared address space (LDS/STS, not generic LD/ST) for every access
@@ -221,7 +225,7 @@ __global__ void __launch_bounds__(kThreads, NK == 0 ? 4 : 2) k_conv_fused(const 
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], kProducers + 1);
+      mbar_init(&full[s], DENSE ? 1 : kProducers + 1);
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -249,7 +253,48 @@ __global__ void __launch_bounds__(kThreads, NK == 0 ? 4 : 2) k_conv_fused(const 
   if (threadIdx.x == 0) trace_ev(p, 0, 0, tr0);  // CTA start (after TMEM allocation)
   if (p.spans && threadIdx.x == 0) p.spans[blockIdx.x * 4 + 1] = gtimer();
 
-  if (REG && warp < 4) {
+  if (DENSE && warp < 4) {
+    // ------------------------------------------------------------ dense producer (one thread)
+    if (threadIdx.x == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+      const uint32_t smem_base = smem_u32(smem);
+      int stage = 0, it = 0;
+      uint32_t phase = 0;
+      for (;; ++it) {
+        const int q = atomicAdd(p.tile_counter, 1);
+        const int t = q < p.num_tiles ? q : -1;
+        const int slot = it % kInfo;
+        mbar_wait(&iempty[slot], ((it / kInfo) & 1) ^ 1);
+        s_mask[slot] = 1;
+        s_tile[slot] = t;
+        mbar_arrive(&ifull[slot]);
+        if (t < 0) break;
+        const int rb = t / p.n_blocks, nb = t % p.n_blocks;
+        int units_left = p.num_kb, in_stage = 0, stage_units = 0;
+        uint32_t slot32 = 0;
+        for (int kb = 0; kb < p.num_kb; ++kb) {
+          if (in_stage == 0) {
+            mbar_wait(&empty[stage], phase ^ 1u);
+            stage_units = min(p.G, units_left);
+            slot32 = smem_base + static_cast<uint32_t>(stage) * p.stage_bytes;
+            mbar_expect_tx(&full[stage], static_cast<uint32_t>(stage_units) * (p.a_bytes + p.b_bytes));
+          }
+          tma_load_2d(smem + (slot32 - smem_base), &tmA, kb * KC, rb * 128, &full[stage]);
+          tma_load_2d(smem + (slot32 - smem_base) + p.a_bytes, &tmB, kb * KC, nb * p.block_n, &full[stage]);
+          --units_left;
+          slot32 += p.unit_bytes;
+          if (++in_stage == stage_units) {
+            in_stage = 0;
+            if (++stage == S) {
+              stage = 0;
+              phase ^= 1u;
+            }
+          }
+        }
+      }
+    }
+  } else if (REG && warp < 4) {
     // ------------------------------------------------------------ gather producers, register indices
     // Thread tid owns tile row tid: its K3 input-row indices are loaded at the tile start
     // (independent LDGs, all in flight together) and published to the warp's own columns of
@@ -1180,8 +1225,8 @@ __global__ void k_convert_rows(const TS* __restrict__ src, int64_t n, int c, int
 // Launch with programmatic stream serialization (PDL): the kernel's prologue overlaps the tail
 // of the previous kernel on the stream (the kernels call grid_dep_wait before touching its
 // outputs). SCONV_PDL=0 launches plainly (A/B).
-template <class K>
-void launch_pdl(K kern, int grid, size_t smem, cudaStream_t st, const CUtensorMap& tB, const FusedParams& prm) {
+template <class K, class... Args>
+void launch_pdl(K kern, int grid, size_t smem, cudaStream_t st, const Args&... args) {
   static const bool pdl = [] {
     const char* e = std::getenv("SCONV_PDL");
     return !(e && e[0] == '0');
@@ -1196,7 +1241,7 @@ void launch_pdl(K kern, int grid, size_t smem, cudaStream_t st, const CUtensorMa
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
-  SCONV_CUDA(cudaLaunchKernelEx(&cfg, kern, tB, prm));
+  SCONV_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
 }
 
 template <int KC, class TOut>
@@ -1239,7 +1284,8 @@ void launch_items_kc(Ctx& ctx, const FusedParams& prm, size_t smem, const CUtens
 }
 
 template <int NK, int KC, class TOut>
-void launch_t(Ctx& ctx, const FusedArgs& a, const FusedParams& prm, size_t smem, const CUtensorMap& tB) {
+void launch_t(Ctx& ctx, const FusedArgs& a, const FusedParams& prm, size_t smem, const CUtensorMap& tB,
+              const CUtensorMap& tA) {
   auto kern = k_conv_fused<NK, KC, TOut>;
   int variant = 0;
   if constexpr (NK > 0) {  // register-resident row indices (SCONV_FUSED_REG=0: shared-memory variant)
@@ -1252,12 +1298,22 @@ void launch_t(Ctx& ctx, const FusedArgs& a, const FusedParams& prm, size_t smem,
       variant = 1;
     }
   }
+  if constexpr (NK == 1) {  // 1x1 identity map, rows in order: TMA-fed dense GEMM (SCONV_FUSED_DENSE=0: gathers)
+    static const bool dense = [] {
+      const char* e = std::getenv("SCONV_FUSED_DENSE");
+      return !(e && e[0] == '0');
+    }();
+    if (dense && !a.nbr && !a.perm) {
+      kern = k_conv_fused<1, KC, TOut, false, true>;
+      variant = 2;
+    }
+  }
   // Resident CTAs per SM from the kernel's own budget (the runtime occupancy query reported 1
   // where ncu's launch statistics show 2): 228 KB shared memory (1 KB reserved per CTA), the
   // register file, and TMEM (512 columns). Attributes are set once per instantiation/device.
   static thread_local std::map<int, int> regs_cache;
   int regs;
-  const int cache_key = ctx.device * 2 + variant;
+  const int cache_key = ctx.device * 4 + variant;
   const auto hit = regs_cache.find(cache_key);
   if (hit != regs_cache.end()) {
     regs = hit->second;
@@ -1276,32 +1332,34 @@ void launch_t(Ctx& ctx, const FusedArgs& a, const FusedParams& prm, size_t smem,
   if (const char* dbg = std::getenv("SCONV_DEBUG_SYNC"); dbg && dbg[0] == '1')
     std::fprintf(stderr, "[sconv] k_conv_fused<%d,%d> tiles=%d grid=%d occ=%d smem=%zu stages=%d bn=%d cols=%u\n", NK, KC,
                  prm.num_tiles, grid, occ, smem, prm.stages, prm.block_n, prm.tmem_cols);
-  ctx.launch("k_conv_fused", [&] { launch_pdl(kern, grid, smem, ctx.stream, tB, prm); });
+  ctx.launch("k_conv_fused", [&] { launch_pdl(kern, grid, smem, ctx.stream, tB, prm, tA); });
 }
 
 template <int KC, class TOut>
-void launch_nk(Ctx& ctx, const FusedArgs& a, const FusedParams& prm, size_t smem, const CUtensorMap& tB) {
+void launch_nk(Ctx& ctx, const FusedArgs& a, const FusedParams& prm, size_t smem, const CUtensorMap& tB,
+               const CUtensorMap& tA) {
   switch (prm.K3) {
     case 27:
       if (prm.target_occ > 2)
-        launch_t<0, KC, TOut>(ctx, a, prm, smem, tB);
+        launch_t<0, KC, TOut>(ctx, a, prm, smem, tB, tA);
       else
-        launch_t<27, KC, TOut>(ctx, a, prm, smem, tB);
+        launch_t<27, KC, TOut>(ctx, a, prm, smem, tB, tA);
       break;
-    case 8: launch_t<8, KC, TOut>(ctx, a, prm, smem, tB); break;
-    case 1: launch_t<1, KC, TOut>(ctx, a, prm, smem, tB); break;
-    default: launch_t<0, KC, TOut>(ctx, a, prm, smem, tB); break;
+    case 8: launch_t<8, KC, TOut>(ctx, a, prm, smem, tB, tA); break;
+    case 1: launch_t<1, KC, TOut>(ctx, a, prm, smem, tB, tA); break;
+    default: launch_t<0, KC, TOut>(ctx, a, prm, smem, tB, tA); break;
   }
 }
 
 template <class TOut>
-void launch_kc(Ctx& ctx, const FusedArgs& a, const FusedParams& prm, size_t smem, const CUtensorMap& tB, int kc) {
+void launch_kc(Ctx& ctx, const FusedArgs& a, const FusedParams& prm, size_t smem, const CUtensorMap& tB,
+               const CUtensorMap& tA, int kc) {
   if (kc == 64)
-    launch_nk<64, TOut>(ctx, a, prm, smem, tB);
+    launch_nk<64, TOut>(ctx, a, prm, smem, tB, tA);
   else if (kc == 32)
-    launch_nk<32, TOut>(ctx, a, prm, smem, tB);
+    launch_nk<32, TOut>(ctx, a, prm, smem, tB, tA);
   else
-    launch_nk<16, TOut>(ctx, a, prm, smem, tB);
+    launch_nk<16, TOut>(ctx, a, prm, smem, tB, tA);
 }
 
 }  // namespace
@@ -1585,12 +1643,17 @@ void launch_conv_fused(Ctx& ctx, const FusedArgs& a) {
       std::fprintf(stderr, "\n");
     }
   } sdump{ctx, spans};
+  // A operand of the dense (1x1 identity) variant: 128-row boxes of the input, same swizzle as B
+  const CUtensorMap tA = !a.nbr && !a.perm && w.K3 == 1
+                             ? make_tensor_map_2d_strided(a.f_in, w.dtype, w.k_pad, static_cast<uint64_t>(a.n_in),
+                                                          static_cast<uint64_t>(a.ld_in) * 2, kc, 128, kc)
+                             : tB;
   if (a.out_dtype == SCONV_F32)
-    launch_kc<float>(ctx, a, prm, smem, tB, kc);
+    launch_kc<float>(ctx, a, prm, smem, tB, tA, kc);
   else if (a.out_dtype == SCONV_F16)
-    launch_kc<__half>(ctx, a, prm, smem, tB, kc);
+    launch_kc<__half>(ctx, a, prm, smem, tB, tA, kc);
   else
-    launch_kc<__nv_bfloat16>(ctx, a, prm, smem, tB, kc);
+    launch_kc<__nv_bfloat16>(ctx, a, prm, smem, tB, tA, kc);
 }
 
 namespace {

@@ -13,6 +13,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <climits>
 #include <cstdlib>
 #include <cstring>
@@ -1330,6 +1331,18 @@ void check_deferred_map_flags(const void* flags_host, const MapSource& P) {
 std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map_cfg& cfg, const MapSource* target,
                                    bool force_wide, bool lazy, const std::vector<int3>* explicit_offsets,
                                    void* defer_flags) {
+  // SCONV_MAP_HOST_PROFILE=1: host-side phase timestamps of each build (us since entry)
+  static const bool hprof = [] {
+    const char* e = std::getenv("SCONV_MAP_HOST_PROFILE");
+    return e && e[0] == '1';
+  }();
+  const auto h0 = std::chrono::steady_clock::now();
+  auto hmark = [&](const char* what) {
+    if (hprof)
+      std::fprintf(stderr, "[sconv map host] %7.1f us %s (n=%lld K=%d s=%d)\n",
+                   std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h0).count(), what,
+                   static_cast<long long>(P.n), cfg.kernel_size, cfg.out_stride);
+  };
   if (cfg.block_B < 4 || cfg.block_B > 1024 || cfg.block_B % 4 != 0)
     fail(SCONV_ERR_ARG, "block size B must be a multiple of 4 in [4, 1024]");
   if (cfg.block_C < 1 || cfg.block_C > 4096) fail(SCONV_ERR_ARG, "query block size C must be in [1, 4096]");
@@ -1578,6 +1591,7 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
     }
   }
 
+  hmark("source + Q queued");
   // ---- error checks that must precede any use of the keys (one sync when needed)
   auto check_flags = [&](const MapFlags& f) {
     auto report = [&](unsigned long long code, const int32_t* base, int mem) {
@@ -1628,6 +1642,7 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
     std::memcpy(&nout, &pin[1], sizeof(int64_t));
     m->n_out = nout;
   }
+  hmark("after n_out sync");
   const int64_t n_out = m->n_out;
   const uint64_t* q = m->q_keys_ptr();
 
@@ -1778,6 +1793,7 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
       }
       }
     }
+    hmark("search queued");
     auto& pd = m->pending;
     pd.counts = std::move(counts);
     pd.offs = std::move(offs);

@@ -266,6 +266,22 @@ def test_fused_layer_parity(ctx, oracle, K, s, n, extent, cin, cout):
     assert elementwise_errors(out.features, of32)[2] <= 2e-3
 
 
+@pytest.mark.parametrize("n,cin,cout", [(1000, 32, 48), (8000, 128, 256), (300, 4, 16), (5000, 96, 96),
+                                         (20000, 384, 256)])
+def test_fused_dense_identity(ctx, oracle, n, cin, cout):
+    """1x1 conv on sorted coordinates (identity map, rows in order): the TMA-fed dense variant of
+    the fused kernel (A = 128-row input boxes, out-of-range rows zero-filled by TMA) against the
+    oracle on the same 16-bit operands, incl. K padding (C_in = 4) and a partial last tile."""
+    rng = np.random.default_rng(n + cin)
+    xyz = sort_rows(random_cloud(rng, n, 40))
+    m = sc.KernelMap.build(ctx, xyz, True, 1, 1, 1)
+    F = rng.random((len(xyz), cin), dtype=np.float32)
+    W = ((rng.random((1, cin, cout)) * 0.2 - 0.1)).astype(np.float32)
+    got = sc.layer_forward(ctx, m, sc.Weights(ctx, W), F, sc.exec_cfg(dataflow=sc.DATAFLOW_FUSED))
+    _, of, _ = oracle.layer_forward(xyz, True, f16(F), f16(W), 1, 1, 1)
+    assert rel_errors(got, of)[0] <= 5e-6
+
+
 @pytest.mark.parametrize("transposed", [False, True])
 def test_fused_even_kernel_and_transposed(ctx, oracle, transposed):
     """K=2 s=2 down-sampling and its transposed map (U-Net up-conv) through the fused kernel
