@@ -226,6 +226,10 @@ class NetWorkload:
         per["k_search"] = tot["k_search"] / max(1, tot["_k_search_launches"])  # one launch per map
         return per
 
+    def map_algo_bytes(self):
+        """SURVEY §8d Map bytes of one step: the distinct maps of every scene of the step."""
+        return self.net.algo_bytes()["k_search"] * len(self.scenes)
+
     def algo_flops(self):
         """Useful flops per launch of the conv kernels (2 C_in C_out |M|)."""
         st = self.net.conv_stats()
@@ -311,6 +315,10 @@ class LayerWorkload:
 
     def extra(self):
         return {}
+
+    def map_algo_bytes(self):  # 8|P| + 8|Q| + 8|M| + 4 K^3 (stride 1: Q = P)
+        i = self.info
+        return 8 * self.N + 8 * i.num_outputs + 8 * i.total_matches + 4 * 27
 
     def algo_bytes(self):  # per launch (SURVEY §8d with this path's dtypes)
         i, N, c, K3 = self.info, self.N, self.c, 27
@@ -533,6 +541,19 @@ def main():
                               "the K timed steps", "share_of_step": tot / total_ms}
     phases = {k: {"launches_per_step": n / n_bd, "us_per_step": 1e3 * ms / n_bd}
               for k, (n, ms) in sorted(breakdown.items(), key=lambda kv: -kv[1][1])}
+    # the Map step: every kernel that builds the kernel maps of a step (key packing /
+    # sorting, Eq. 1 output coordinates, search, canonical lists), event-timed in the breakdown
+    # pass, against the algorithmic bytes of the step's distinct maps
+    map_kernels = ("k_search", "k_floor", "k_pack", "k_init_flags", "k_bbox", "k_hist_scan", "k_bucket_scatter",
+                   "k_bucket_rank", "k_scan_counts", "k_emit", "k_identity_map", "k_hash", "cub_")
+    map_us = sum(v["us_per_step"] for k, v in phases.items() if k.startswith(map_kernels))
+    map_b = wl.map_algo_bytes() if hasattr(wl, "map_algo_bytes") else None
+    map_roof = None
+    if map_us > 0 and map_b:
+        gbs = map_b / (map_us * 1e-6) / 1e9
+        map_roof = {"algorithmic_bytes_per_step": map_b, "kernel_us_per_step": map_us, "achieved": gbs,
+                    "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
+                    "kernels": "event-timed sum of the map-building kernels (breakdown pass), serialised"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -554,6 +575,7 @@ def main():
             "gpu_launches": launches,
             "roofline": roofline,
             "phases": phases,
+            "map_roofline": map_roof,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
         }

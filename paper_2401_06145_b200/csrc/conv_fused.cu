@@ -1332,7 +1332,9 @@ void launch_t(Ctx& ctx, const FusedArgs& a, const FusedParams& prm, size_t smem,
   if (const char* dbg = std::getenv("SCONV_DEBUG_SYNC"); dbg && dbg[0] == '1')
     std::fprintf(stderr, "[sconv] k_conv_fused<%d,%d> tiles=%d grid=%d occ=%d smem=%zu stages=%d bn=%d cols=%u\n", NK, KC,
                  prm.num_tiles, grid, occ, smem, prm.stages, prm.block_n, prm.tmem_cols);
+  ctx.hmark("conv: launch");
   ctx.launch("k_conv_fused", [&] { launch_pdl(kern, grid, smem, ctx.stream, tB, prm, tA); });
+  ctx.hmark("conv: launched");
 }
 
 template <int KC, class TOut>
@@ -1481,6 +1483,7 @@ int fused_items_mode() {
 bool fused_supported(int K3, int c_in, int c_out) { return K3 >= 1 && K3 <= 64 && c_in >= 1 && c_out >= 1; }
 
 void launch_conv_fused(Ctx& ctx, const FusedArgs& a) {
+  ctx.hmark("conv: enter");
   const WeightData& w = *a.w;
   if (!fused_supported(w.K3, w.c_in, w.c_out)) fail(SCONV_ERR_ARG, "fused dataflow supports at most 64 offsets");
   if (a.n_out == 0) return;
@@ -1581,8 +1584,10 @@ void launch_conv_fused(Ctx& ctx, const FusedArgs& a) {
   prm.tmem_cols = cols;
   const size_t smem = 1024 + prm.bar_off + (2 * stages + 4 + 3 * kInfo + 8) * 8 + (kInfo + 4 + 1) * 4 + 16;
   if (smem > 227 * 1024) fail(SCONV_ERR_ARG, "fused layer tile does not fit in shared memory");
+  ctx.hmark("conv: params");
   const CUtensorMap tB = make_tensor_map_2d(w.buf.get(), w.dtype, w.k_pad, static_cast<uint64_t>(w.K3) * w.n_pad, kc,
                                             static_cast<uint32_t>(bn), kc);
+  ctx.hmark("conv: tensor map");
   {  // {queue, exited CTAs}: zeroed when (re)allocated, then reset by each launch's last CTA
     const void* before = ctx.fused_counter.get();
     ctx.fused_counter.reserve(16, ctx.stream);
@@ -1696,7 +1701,9 @@ void build_fused_items(Ctx& ctx, MapData& m) {
 void prepare_fused_layout(Ctx& ctx, MapData& m) {
   if (m.fused_ready) return;
   m.fused_ready = true;
+  ctx.hmark("layout: enter");
   order_fused_rows(ctx, m);
+  ctx.hmark("layout: row order queued");
   build_fused_items(ctx, m);
 }
 
@@ -1731,6 +1738,7 @@ void order_fused_rows(Ctx& ctx, MapData& m) {
   std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return norm(a) < norm(b); });
   for (int p = 0; p < K3; ++p) ord.pos[order[p]] = small ? order[p] : p;  // small maps: bit k = offset k
   const cudaStream_t st = ctx.stream;
+  ctx.hmark("layout: allocs");
   DevBuf keys, keys_sorted, idx;
   keys.alloc(4 * n, st);
   keys_sorted.alloc(4 * n, st);
@@ -1781,9 +1789,11 @@ void order_fused_rows(Ctx& ctx, MapData& m) {
     const void* fn = e == 1   ? reinterpret_cast<const void*>(k_mask_sort<1>)
                      : e == 2 ? reinterpret_cast<const void*>(k_mask_sort<2>)
                               : reinterpret_cast<const void*>(k_mask_sort<4>);
+    ctx.hmark("layout: coop launch");
     ctx.launch("k_mask_sort", [&] {
       SCONV_CUDA(cudaLaunchCooperativeKernel(fn, dim3(G), dim3(kCoopThreads), args, 0, st));
     });
+    ctx.hmark("layout: coop launched");
     return;
   }
   const unsigned b1 = static_cast<unsigned>(ceil_div<int64_t>(n, 256));

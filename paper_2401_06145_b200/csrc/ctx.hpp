@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <chrono>
+#include <cstdlib>
 #include <map>
 #include <tuple>
 #include <stdexcept>
@@ -141,6 +143,22 @@ struct Ctx {
 
   cudaEvent_t take_event();
   void resolve_profile();
+
+  // host-side phase trace (SCONV_HOST_TRACE=1): (label, us since the trace epoch), buffered
+  // and printed by the network forward at its end (printing inline would distort the times)
+  std::vector<std::pair<const char*, double>> htrace;
+  std::chrono::steady_clock::time_point htrace_t0 = std::chrono::steady_clock::now();
+  static bool htrace_on() {
+    static const bool on = [] {
+      const char* e = std::getenv("SCONV_HOST_TRACE");
+      return e && e[0] == '1';
+    }();
+    return on;
+  }
+  void hmark(const char* what) {
+    if (htrace_on())
+      htrace.emplace_back(what, std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - htrace_t0).count());
+  }
 
   template <class F>
   void launch(const char* name, F&& f) {

@@ -18,6 +18,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <map>
+#include <mutex>
 #include <string>
 
 #include "common.cuh"
@@ -1195,6 +1197,20 @@ __global__ void k_hash_query(const uint64_t* __restrict__ q, int64_t n_q, Offset
   if (threadIdx.x == 0) counts[int64_t{k} * nchunk + c] = hits;
 }
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, size): a driver call per
+// launch costs host time on the map stream's critical path
+void set_max_smem(const void* kern, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> done;  // (kernel, device) -> largest size set
+  int dev = 0;
+  SCONV_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& cur = done[{kern, dev}];
+  if (smem <= cur) return;
+  SCONV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  cur = smem;
+}
+
 constexpr int kThreads = 256;
 // Key / index arrays carry slack so 16-byte bulk copies may run past the last element.
 inline int64_t slack(int64_t n) { return ((n + 3) & ~int64_t{3}) + 4; }
@@ -1247,6 +1263,11 @@ namespace {
 void launch_canonical(Ctx& ctx, MapData& m) {
   auto& pd = m.pending;
   const cudaStream_t st = ctx.stream;
+  if (!m.nbr_pos.get()) m.nbr_pos.alloc(sizeof(int32_t) * std::max<int64_t>(1, int64_t{m.K3} * m.n_out), st);
+  if (!m.pair_in.get()) {
+    m.pair_in.alloc(sizeof(int32_t) * std::max<int64_t>(1, pd.max_pairs), st);
+    m.pair_out.alloc(sizeof(int32_t) * std::max<int64_t>(1, pd.max_pairs), st);
+  }
   ctx.launch("k_scan_counts", [&] {
     k_scan_counts<<<static_cast<unsigned>(pd.ntiles), kSearchThreads, 0, st>>>(
         pd.counts.get<int32_t>(), pd.grid, pd.offs.get<int32_t>(), pd.tiles.get<int32_t>(), pd.nchunk, m.K3,
@@ -1294,6 +1315,7 @@ void launch_identity(Ctx& ctx, MapData& m) {
   if (!m.identity_pending) return;
   m.identity_pending = false;
   const int64_t n = m.n_out;
+  if (!m.nbr_pos.get()) m.nbr_pos.alloc(sizeof(int32_t) * std::max<int64_t>(1, n), ctx.stream);
   ctx.launch("k_identity_map", [&] {
     k_identity_map<<<grid_for(n), kThreads, 0, ctx.stream>>>(n, m.nbr_in.get<int32_t>(), m.nbr_pos.get<int32_t>(),
                                                              m.pair_in.get<int32_t>(), m.pair_out.get<int32_t>(),
@@ -1309,6 +1331,27 @@ void ensure_canonical(Ctx& ctx, MapData& m) {
   read_starts(ctx, m, m.pending.flags_init ? m.pending.flags.get() : nullptr, &f);  // lazy: no coordinate checks
   m.pending = MapData::Pending{};
   m.canonical = true;
+}
+
+bool finish_coords(Ctx& ctx, MapData& m) {
+  if (m.n_out >= 0) return true;
+  auto* pin = reinterpret_cast<MapFlags*>(ctx.pin_flags());
+  SCONV_CUDA(cudaMemcpyAsync(pin, m.pending.flags.get(), sizeof(MapFlags), cudaMemcpyDeviceToHost, ctx.stream));
+  SCONV_CUDA(cudaMemcpyAsync(&pin[1], m.pend_nsel.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, ctx.stream));
+  ctx.sync();
+  const MapFlags f = pin[0];
+  if (f.fwide || f.wide || f.big_bucket) return false;  // the caller rebuilds with the exact path
+  if (f.bad_floor != ULLONG_MAX) {
+    const int64_t j = static_cast<int64_t>(f.bad_floor / 3);
+    const int axis = static_cast<int>(f.bad_floor % 3);
+    uint64_t key;
+    SCONV_CUDA(cudaMemcpy(&key, m.src_keys_ptr() + j, sizeof(key), cudaMemcpyDeviceToHost));
+    int32_t c[3];
+    unpack_key(key, c[0], c[1], c[2]);
+    fail(SCONV_ERR_RANGE, coord_error("xyz"[axis], floor_div(c[axis], m.cfg.out_stride) * m.cfg.out_stride));
+  }
+  std::memcpy(&m.n_out, &pin[1], sizeof(int64_t));
+  return true;
 }
 
 void check_deferred_map_flags(const void* flags_host, const MapSource& P) {
@@ -1330,19 +1373,9 @@ void check_deferred_map_flags(const void* flags_host, const MapSource& P) {
 
 std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map_cfg& cfg, const MapSource* target,
                                    bool force_wide, bool lazy, const std::vector<int3>* explicit_offsets,
-                                   void* defer_flags) {
-  // SCONV_MAP_HOST_PROFILE=1: host-side phase timestamps of each build (us since entry)
-  static const bool hprof = [] {
-    const char* e = std::getenv("SCONV_MAP_HOST_PROFILE");
-    return e && e[0] == '1';
-  }();
-  const auto h0 = std::chrono::steady_clock::now();
-  auto hmark = [&](const char* what) {
-    if (hprof)
-      std::fprintf(stderr, "[sconv map host] %7.1f us %s (n=%lld K=%d s=%d)\n",
-                   std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h0).count(), what,
-                   static_cast<long long>(P.n), cfg.kernel_size, cfg.out_stride);
-  };
+                                   void* defer_flags, bool coords_only, const MapSource* strided_q) {
+  auto hmark = [&](const char* what) { ctx.hmark(what); };
+  hmark("map: enter");
   if (cfg.block_B < 4 || cfg.block_B > 1024 || cfg.block_B % 4 != 0)
     fail(SCONV_ERR_ARG, "block size B must be a multiple of 4 in [4, 1024]");
   if (cfg.block_C < 1 || cfg.block_C > 4096) fail(SCONV_ERR_ARG, "query block size C must be in [1, 4096]");
@@ -1383,7 +1416,11 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
   // reused by the next build while this build's copies are still queued
   // flags are written only by coordinate packing / Eq. 1 floor (raw coordinates, strided
   // layers); chained stride-1 / transposed maps over existing keys skip the init launch
-  const bool flags_used = !lazy || !P.keys || (!cfg.transposed && cfg.out_stride != 1) ||
+  if (coords_only && (!P.keys || cfg.transposed || cfg.out_stride == 1 || explicit_offsets || target))
+    fail(SCONV_ERR_ARG, "coordinates-only builds need a strided map over existing sorted keys");
+  if (strided_q && (cfg.transposed || cfg.out_stride == 1 || explicit_offsets || target || !strided_q->keys))
+    fail(SCONV_ERR_ARG, "precomputed output coordinates need a strided, non-transposed map");
+  const bool flags_used = !lazy || !P.keys || (!cfg.transposed && cfg.out_stride != 1 && !strided_q) ||
                           (cfg.transposed && target && !target->keys);
   if (flags_used) ctx.launch("k_init_flags", [&] { k_init_flags<<<1, 1, 0, st>>>(flags); });
   auto* pin = reinterpret_cast<MapFlags*>(ctx.pin_flags());
@@ -1491,6 +1528,9 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
         });
     }
     m->n_out = target->n;
+  } else if (strided_q) {  // Eq. 1 output computed earlier (coords_only build + finish_coords)
+    m->q_keys = strided_q->keys;
+    m->n_out = strided_q->n;
   } else if (cfg.out_stride == 1) {
     m->q_keys = m->src_keys;  // stride-1 alias: one array serves as source and query
     m->n_out = n;
@@ -1592,6 +1632,13 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
   }
 
   hmark("source + Q queued");
+  if (coords_only) {  // Eq. 1 queued; |Q| and the flags are read by finish_coords
+    m->pending.flags = std::move(flags_buf);
+    m->pending.flags_init = true;
+    m->pend_nsel = std::move(nsel);
+    m->n_out = -1;
+    return m;
+  }
   // ---- error checks that must precede any use of the keys (one sync when needed)
   auto check_flags = [&](const MapFlags& f) {
     auto report = [&](unsigned long long code, const int32_t* base, int mem) {
@@ -1647,12 +1694,18 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
   const uint64_t* q = m->q_keys_ptr();
 
   // ---- search
+  hmark("map: search allocs");
   m->map_start.alloc(sizeof(int32_t) * (K3 + 1), st);
-  m->nbr_pos.alloc(sizeof(int32_t) * std::max<int64_t>(1, int64_t{K3} * n_out), st);
   m->nbr_in.alloc(sizeof(int32_t) * std::max<int64_t>(1, int64_t{K3} * n_out), st);
   const int B = cfg.block_B, C = cfg.block_C;
   // upper bound on the match count: every query hits at most once
   const int64_t max_pairs = std::min<int64_t>(int64_t{K3} * n_out, int64_t{K3} * n);
+  if (max_pairs > INT32_MAX) fail(SCONV_ERR_ARG, "kernel map too large: more than 2^31 - 1 pairs");
+  m->pending.max_pairs = max_pairs;
+  // canonical positions and pair lists: allocated with the canonical build (launch_canonical),
+  // so lazy network maps that never need them (fused convs) skip 3 allocations of up to K3 |Q|
+  if (!defer_canonical || n == 0 || n_out == 0)
+    m->nbr_pos.alloc(sizeof(int32_t) * std::max<int64_t>(1, int64_t{K3} * n_out), st);
   if (n == 0 || n_out == 0) {
     SCONV_CUDA(cudaMemsetAsync(m->map_start.get(), 0, sizeof(int32_t) * (K3 + 1), st));
     if (n_out > 0) SCONV_CUDA(cudaMemsetAsync(m->nbr_in.get(), 0xFF, sizeof(int32_t) * int64_t{K3} * n_out, st));
@@ -1684,11 +1737,15 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
     if (grid2 > INT32_MAX) fail(SCONV_ERR_ARG, "kernel map too large");
     DevBuf counts, offs, tiles;
     const int64_t ntiles = ceil_div<int64_t>(grid2, kScanTile);
+    hmark("map: table allocs done");
     counts.alloc(sizeof(int32_t) * grid2, st);
     offs.alloc(sizeof(int32_t) * grid2, st);
     tiles.alloc(sizeof(int32_t) * ntiles, st);
-    m->pair_in.alloc(sizeof(int32_t) * std::max<int64_t>(1, max_pairs), st);
-    m->pair_out.alloc(sizeof(int32_t) * std::max<int64_t>(1, max_pairs), st);
+    if (!defer_canonical) {
+      m->pair_in.alloc(sizeof(int32_t) * std::max<int64_t>(1, max_pairs), st);
+      m->pair_out.alloc(sizeof(int32_t) * std::max<int64_t>(1, max_pairs), st);
+    }
+    hmark("map: pair allocs done");
     const int ngroups = ceil_div(K3, kSearchThreads / 32);  // search / emit CTA = chunk x <= 8 offsets
     const OffsetGen og{cfg.kernel_size, cfg.transposed ? -cfg.offset_scale : cfg.offset_scale,
                        explicit_q ? m->delta_dev.get<int3>() : nullptr};
@@ -1764,7 +1821,7 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
         const size_t smem = size_t{12} * kz * kz * cap_col * B;
         const int scale = cfg.transposed ? -cfg.offset_scale : cfg.offset_scale;
         auto go = [&](auto kern) {
-          SCONV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+          set_max_smem(reinterpret_cast<const void*>(kern), smem);
           ctx.launch("k_search", [&] {
             kern<<<static_cast<unsigned>(nchunk2), 32 * kz * kz, smem, st>>>(
                 src, src_idx, n, B, q, n_out, scale, nchunk2, cap_col, m->nbr_in.get<int32_t>(),
@@ -1778,7 +1835,7 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
       } else {
       const size_t smem = size_t{12} * (kSearchThreads / 32) * cap_blocks * B;
       auto go = [&](auto kern) {
-        SCONV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        set_max_smem(reinterpret_cast<const void*>(kern), smem);
         ctx.launch("k_search", [&] {
           kern<<<static_cast<unsigned>(nchunk2 * ngroups), kSearchThreads, smem, st>>>(
               src, src_idx, n, B, q, n_out, og,

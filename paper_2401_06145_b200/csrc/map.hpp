@@ -48,6 +48,7 @@ struct MapData {
   // the fused dataflow needs only nbr_in (ensure_canonical() before using sizes/pairs/nbr_pos).
   bool canonical = true;
   bool flags_deferred = false;  // build_map(defer_flags): coordinate checks pending at the caller
+  DevBuf pend_nsel;             // coords_only builds: |Q| on the device until finish_coords
   bool identity_pending = false;
   bool layout_off_path = false;  // fused row order built beside the convs (network layout stream)  // lazy 1x1 identity map: arrays not yet written (nbr_in[i] = i)
   struct Pending {
@@ -55,6 +56,7 @@ struct MapData {
     int64_t nchunk = 0, grid = 0, ntiles = 0;
     int ngroups = 0, qpl = 0;
     bool flags_init = false;  // k_init_flags ran on `flags`
+    int64_t max_pairs = 0;    // pair-list capacity (allocated by the canonical build)
   } pending;
   // last GMaS stats
   int64_t buffer_length = 0;
@@ -81,7 +83,13 @@ struct MapSource {
 // list and Q = *target (sorted unique queries).
 std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map_cfg& cfg, const MapSource* target,
                                    bool force_wide = false, bool lazy = false,
-                                   const std::vector<int3>* explicit_offsets = nullptr, void* defer_flags = nullptr);
+                                   const std::vector<int3>* explicit_offsets = nullptr, void* defer_flags = nullptr,
+                                   bool coords_only = false, const MapSource* strided_q = nullptr);
+// coords_only: a strided map over existing sorted keys queues only its Eq. 1 output coordinates
+// (floor / sort / unique) and returns without a sync (n_out = -1); finish_coords then reads |Q|
+// and the flags (one sync on the build's stream; false: the compact-key path overflowed, rebuild
+// normally). strided_q: the strided map's Eq. 1 output computed that way (no second sort).
+bool finish_coords(Ctx& ctx, MapData& m);
 // defer_flags (pinned host, >= kDeferredFlagsBytes): a map over SORTED raw coordinates (no sort
 // fallback exists) skips its flags sync; the flags are copied there asynchronously on the build
 // stream and the caller checks them with check_deferred_map_flags once that copy completed

@@ -188,13 +188,15 @@ NetData::~NetData() {
   maps.clear();  // frees enqueued on the streams the buffers were allocated on
   coordsets.clear();
   tensors.clear();
-  for (cudaStream_t* sp : {&map_stream, &layout_stream})
+  pre_coords.clear();
+  for (cudaStream_t* sp : {&map_stream, &layout_stream, &coord_stream})
     if (*sp) {
       cudaStreamSynchronize(*sp);
       cudaStreamDestroy(*sp);
     }
   if (ev_order) cudaEventDestroy(ev_order);
   if (ev_flags) cudaEventDestroy(ev_flags);
+  if (ev_coords) cudaEventDestroy(ev_coords);
 }
 
 void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f_dtype, int f_mem, int c_in) {
@@ -211,7 +213,14 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
     SCONV_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     SCONV_CUDA(cudaStreamCreateWithPriority(&map_stream, cudaStreamNonBlocking, hi));
     SCONV_CUDA(cudaStreamCreateWithPriority(&layout_stream, cudaStreamNonBlocking, hi));
+    SCONV_CUDA(cudaStreamCreateWithPriority(&coord_stream, cudaStreamNonBlocking, hi));
   }
+  if (!ev_coords) SCONV_CUDA(cudaEventCreateWithFlags(&ev_coords, cudaEventDisableTiming));
+  static const bool coord_ahead = [] {
+    const char* e = std::getenv("SCONV_NET_COORD_AHEAD");
+    return !(e && e[0] == '0');
+  }();
+  const cudaStream_t cst = use_map_stream && coord_ahead ? coord_stream : nullptr;
   const cudaStream_t ms = use_map_stream ? map_stream : st;
   const cudaStream_t ls = use_map_stream ? layout_stream : st;
   // SCONV_NET_WAIT_PROFILE=1: time how long the context stream waits for each map and row
@@ -225,15 +234,16 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
   std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>> waits;
   // SCONV_NET_HOST_PROFILE=1: host timestamps (us since the forward started) of each op's map
   // build / row order / launch, printed at the end (compare with a kernel timeline)
-  static const bool host_profile = [] {
-    const char* e = std::getenv("SCONV_NET_HOST_PROFILE");
-    return e && e[0] == '1';
-  }();
-  const auto h0 = std::chrono::steady_clock::now();
-  std::vector<std::tuple<int, const char*, double>> hmarks;
+  const bool host_profile = Ctx::htrace_on();  // SCONV_HOST_TRACE=1
+  std::vector<std::tuple<int, size_t>> hops;  // (op, first trace entry of the op)
+  if (host_profile) {
+    ctx.htrace.clear();
+    ctx.htrace_t0 = std::chrono::steady_clock::now();
+  }
   auto hmark = [&](int op, const char* what) {
-    if (host_profile)
-      hmarks.emplace_back(op, what, std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h0).count());
+    if (!host_profile) return;
+    hops.emplace_back(op, ctx.htrace.size());
+    ctx.hmark(what);
   };
   auto wait_for = [&](cudaStream_t from, int op) {
     SCONV_CUDA(cudaEventRecord(ev_order, from));
@@ -256,7 +266,9 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
     SCONV_CUDA(cudaEventRecord(ev_order, st));
     SCONV_CUDA(cudaStreamWaitEvent(ms, ev_order));
     SCONV_CUDA(cudaStreamWaitEvent(ls, ev_order));
+    if (cst) SCONV_CUDA(cudaStreamWaitEvent(cst, ev_order));
   }
+  hmark(-1, "forward: streams joined");
   if (!planned) {
     make_plan();
     planned = true;
@@ -272,6 +284,53 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
   // frees here would delay the first launches by ~80 us of host time (the GPU idles then)
   std::map<MapKey, MapEntry> old_maps;
   old_maps.swap(maps);
+  pre_coords.clear();  // (unused look-ahead coordinates of the previous forward)
+  // queue the Eq. 1 output of the next strided conv over coordinate set cs_new (see net.hpp)
+  // (op `from` writes a tensor on cs_new; its output is not assigned yet when this runs)
+  auto prelaunch = [&](int cs_new, int from, bool wait_map_stream) {
+    if (!cst || !coordsets[cs_new].keys) return;
+    std::vector<int> tcs(num_tensors);
+    for (int t = 0; t < num_tensors; ++t) tcs[t] = tensors[t].coordset;
+    tcs[plan[from].out] = cs_new;
+    for (int j = from + 1; j < static_cast<int>(ops.size()); ++j) {
+      if (plan[j].skip) continue;
+      const NetOp& q = ops[j];
+      const int in = tcs[q.in];
+      int outc = in;
+      if (q.kind == kOpConv) {
+        if (q.transposed) {
+          outc = tcs[q.target];
+        } else if (q.out_stride != 1) {
+          if (in != cs_new) {
+            outc = -2;  // a coordinate set not created yet
+          } else {
+            const auto pk = std::make_pair(cs_new, q.out_stride);
+            if (!pre_coords.count(pk) && !maps.count(MapKey{cs_new, q.K, q.offset_scale, q.out_stride, 0, -1})) {
+              sconv_map_cfg c{q.K, q.offset_scale, q.out_stride, 0, block_B, block_C, SCONV_MAP_SORTED};
+              MapSource P;
+              P.keys = coordsets[cs_new].keys;
+              P.n = coordsets[cs_new].n;
+              P.sorted = true;
+              if (wait_map_stream) {  // the keys are still being produced on the map stream
+                SCONV_CUDA(cudaEventRecord(ev_coords, ms));
+                SCONV_CUDA(cudaStreamWaitEvent(cst, ev_coords));
+              }
+              ctx.stream = cst;
+              try {
+                pre_coords[pk] = build_map(ctx, P, c, nullptr, false, true, nullptr, nullptr, /*coords_only=*/true);
+              } catch (...) {
+                ctx.stream = st;
+                throw;
+              }
+              ctx.stream = st;
+            }
+            return;
+          }
+        }
+      }
+      tcs[plan[j].out] = outc;
+    }
+  };
   const void* deferred_flags = nullptr;  // raw sorted input: coordinate checks after the launches
   int convs_issued = 0;
   maps_built = 0;
@@ -286,6 +345,7 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
   tin.channels = c_in;
   tin.dtype = act;
   tin.ld = round_up(c_in, 16);  // zero padded: the fused gather reads whole 16-channel chunks
+  hmark(-1, "forward: tensors reset");
   tin.feats.reserve(std::max<size_t>(2 * input.n * tin.ld, 16), st);
   if (input.n > 0) {
     const float* src = static_cast<const float*>(feats);
@@ -297,6 +357,7 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
     }
     convert_rows(ctx, src, SCONV_F32, input.n, c_in, c_in, tin.feats.get(), act, tin.ld);
   }
+  hmark(-1, "forward: input converted");
   for (int oi = 0; oi < static_cast<int>(ops.size()); ++oi) {
     const NetOp& o = ops[oi];
     OpPlan& pl = plan[oi];
@@ -340,7 +401,28 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
         hmark(oi, "map build");
         try {
           void* dflags = cs.raw && !cs.keys ? static_cast<char*>(ctx.pin_flags()) + Ctx::kPinFlagsBytes / 2 : nullptr;
-          m = build_map(ctx, P, mcfg, o.transposed ? &T : nullptr, false, /*lazy=*/true, nullptr, dflags);
+          std::unique_ptr<MapData> pre;  // this strided map's coordinates, queued ahead
+          if (!o.transposed && o.out_stride != 1 && P.keys) {
+            auto f = pre_coords.find({a.coordset, o.out_stride});
+            if (f != pre_coords.end()) {
+              pre = std::move(f->second);
+              pre_coords.erase(f);
+              ctx.stream = cst;
+              const bool ok = finish_coords(ctx, *pre);  // |Q| (the floor ran long ago)
+              ctx.stream = ms;
+              if (!ok) pre.reset();  // compact keys overflowed: the normal build's exact path
+            }
+          }
+          if (pre) {
+            MapSource Q;
+            Q.keys = pre->q_keys;
+            Q.n = pre->n_out;
+            Q.sorted = true;
+            m = build_map(ctx, P, mcfg, nullptr, false, /*lazy=*/true, nullptr, nullptr, false, &Q);
+            m->sorts += pre->sorts;
+          } else {
+            m = build_map(ctx, P, mcfg, o.transposed ? &T : nullptr, false, /*lazy=*/true, nullptr, dflags);
+          }
           if (m->flags_deferred) {
             deferred_flags = dflags;
             SCONV_CUDA(cudaEventRecord(ev_flags, ms));
@@ -375,7 +457,14 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
           coordsets.push_back({m->q_keys, m->n_out, true, false});
           out_cs = static_cast<int>(coordsets.size()) - 1;
         }
+        // the raw input's keys were just packed (cs may dangle after the push_back above)
+        const bool raw_keyed = a.coordset == 0 && maps_built == 1 && coordsets[0].keys;
         it = maps.emplace(key, MapEntry{std::move(m), out_cs}).first;
+        // coordinate look-ahead: the next strided conv over a coordinate set created now
+        if (out_cs != a.coordset && !o.transposed)
+          prelaunch(out_cs, oi, false);  // (keys complete: this build synchronised on |Q|)
+        else if (raw_keyed)
+          prelaunch(a.coordset, oi, true);
       }
       MapData& m = *it->second.map;
       auto wt = weights.find(o.weight);
@@ -513,6 +602,10 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
     }
   }
   if (ms != st) {  // readers of the forward's coordinates (map-stream buffers) use the context stream
+    if (cst) {
+      SCONV_CUDA(cudaEventRecord(ev_order, cst));
+      SCONV_CUDA(cudaStreamWaitEvent(st, ev_order));
+    }
     SCONV_CUDA(cudaEventRecord(ev_order, ms));
     SCONV_CUDA(cudaStreamWaitEvent(st, ev_order));
     SCONV_CUDA(cudaEventRecord(ev_order, ls));
@@ -525,7 +618,12 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
   }
   if (host_profile) {
     hmark(-1, "forward returns");
-    for (auto& [op, what, us] : hmarks) std::fprintf(stderr, "[sconv host] %8.1f us op %d %s\n", us, op, what);
+    size_t h = 0;
+    int op = -1;
+    for (size_t i = 0; i < ctx.htrace.size(); ++i) {
+      while (h < hops.size() && std::get<1>(hops[h]) <= i) op = std::get<0>(hops[h++]);
+      std::fprintf(stderr, "[sconv host] %8.1f us op %d %s\n", ctx.htrace[i].second, op, ctx.htrace[i].first);
+    }
   }
   if (!waits.empty()) {  // SCONV_NET_WAIT_PROFILE
     SCONV_CUDA(cudaStreamSynchronize(st));

@@ -90,6 +90,13 @@ struct NetData {
   cudaStream_t layout_stream = nullptr;  // fused row order (mask sort): off the coordinate chain
   cudaEvent_t ev_order = nullptr;
   cudaEvent_t ev_flags = nullptr;  // deferred raw-input coordinate checks (copy done)
+  // Coordinate look-ahead: when a coordinate set is created, the Eq. 1 output of the next
+  // strided conv over it is queued at once on coord_stream (coords_only build); that conv's map
+  // build later only reads |Q| (long done), instead of queueing the floor / sort / unique behind
+  // the current level's searches and blocking the host on it. SCONV_NET_COORD_AHEAD=0: off.
+  cudaStream_t coord_stream = nullptr;
+  cudaEvent_t ev_coords = nullptr;
+  std::map<std::pair<int, int>, std::unique_ptr<MapData>> pre_coords;  // (coordinate set, stride)
 
   NetData() = default;
   NetData(const NetData&) = delete;

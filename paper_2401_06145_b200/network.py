@@ -180,7 +180,8 @@ class Network:
         for st in self.conv_stats():
             n, q, M, R, ci, co, kp, K3, df, res = (st[k] for k in self.STAT_KEYS)
             if K3 > 1:
-                maps[(n, q, M, K3)] = 8 * n + 8 * q + 8 * M + 4 * K3
+                # (+ 12|P| + 8|Q| for an Eq. 1 downsample, which creates the smaller output set)
+                maps[(n, q, M, K3)] = 8 * n + 8 * q + 8 * M + 4 * K3 + ((12 * n + 8 * q) if q < n else 0)
             if df == 1:
                 f += 2 * ci * n + 4 * K3 * q + 2 * co * q * (2 if res else 1) + 2 * K3 * ci * co
                 continue
