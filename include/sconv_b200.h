@@ -265,6 +265,9 @@ sconv_status sconv_net_sort_count(const sconv_net* net, int64_t* sorts);
 /* Per CONV op (execution order) of the last forward: {n_in, n_out, |M|, R_pad (0 if fused), c_in, c_out,
  * k_pad, K3, dataflow, residual_folded}. */
 sconv_status sconv_net_conv_stats(const sconv_net* net, int conv, int64_t* out10);
+/* Fills in |M| (out10[2], -1 for maps built lazily by the forward) of the last forward's convs:
+ * builds the canonical lists of those maps (synchronises; statistics only). */
+sconv_status sconv_net_resolve_stats(sconv_ctx* ctx, sconv_net* net);
 /* AUTO dataflow measurements of the tuning forward for op index `op` (ms; -1 when the op was
  * not tuned): Minuet GMaS vs the fused kernel. */
 sconv_status sconv_net_conv_timings(const sconv_net* net, int op, double* gmas_ms, double* fused_ms);

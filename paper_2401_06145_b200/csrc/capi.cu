@@ -922,6 +922,14 @@ sconv_status sconv_net_conv_stats(const sconv_net* net, int conv, int64_t* out10
   return SCONV_OK;
 }
 
+sconv_status sconv_net_resolve_stats(sconv_ctx* ctx, sconv_net* net) {
+  if (!net) return SCONV_ERR_ARG;
+  return guarded(ctx, [&] {
+    net->resolve_stats(*ctx);
+    ctx->sync();
+  });
+}
+
 sconv_status sconv_net_conv_timings(const sconv_net* net, int op, double* gmas_ms, double* fused_ms) {
   if (!net || op < 0 || op >= static_cast<int>(net->auto_ms.size())) return SCONV_ERR_ARG;
   if (gmas_ms) *gmas_ms = net->auto_ms[op][0];

@@ -901,6 +901,59 @@ __global__ void __launch_bounds__(32 * KZ * KZ, KZ == 3 ? 2 : 4) k_search_col(
   }
 }
 
+// ---------------------------------------------------------------- derived maps (networks)
+// K = 2, stride 2s down-sampling map of a fine set P on the s-lattice onto Q = Eq. 1 of P:
+// every p has exactly one parent q = floor(p / 2s) * 2s in Q and one offset (p - q) / s in
+// {0, 1}^3, so the map is a scatter, not a search: nbr[k(p)][index of q in Q] = p (one binary
+// search of q per fine point instead of 8 segment searches per coarse point).
+__global__ void k_down_map(const uint64_t* __restrict__ fine, int64_t nf, const uint64_t* __restrict__ coarse,
+                           int64_t nc, int s, int32_t* __restrict__ nbr) {
+  const int64_t i = blockIdx.x * int64_t{blockDim.x} + threadIdx.x;
+  if (i >= nf) return;
+  int32_t c[3];
+  unpack_key(__ldg(fine + i), c[0], c[1], c[2]);
+  const int64_t S = 2 * int64_t{s};
+  int32_t qc[3];
+  int k = 0;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    qc[a] = static_cast<int32_t>(floor_div(c[a], S) * S);
+    k = 2 * k + static_cast<int>((c[a] - qc[a]) / s);  // 0 or 1 on the s-lattice
+  }
+  const uint64_t key = pack_key_unchecked(qc[0], qc[1], qc[2]);
+  int64_t lo = 0, hi = nc;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (__ldg(coarse + mid) < key)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  if (lo < nc && __ldg(coarse + lo) == key) nbr[int64_t{k} * nc + lo] = static_cast<int32_t>(i);
+}
+
+// Transposed map from its forward map: the pairs are the same with input and output swapped
+// (offsets negated): dst[k][src[k][i]] = i.
+__global__ void k_transpose_map(const int32_t* __restrict__ src, int64_t n_src_out, int K3, int32_t* __restrict__ dst,
+                                int64_t n_dst_out) {
+  const int64_t g = blockIdx.x * int64_t{blockDim.x} + threadIdx.x;
+  if (g >= n_src_out * K3) return;
+  const int64_t k = g / n_src_out, i = g - k * n_src_out;
+  const int32_t j = __ldg(src + g);
+  if (j >= 0) dst[k * n_dst_out + j] = static_cast<int32_t>(i);
+}
+
+// Per-(k, chunk of CQ queries) hit counts of a dense table (what k_search writes alongside the
+// table), for the canonical lists of a derived map.
+__global__ void k_chunk_counts(const int32_t* __restrict__ nbr, int64_t n_q, int CQ, int64_t nchunk,
+                               int32_t* __restrict__ counts) {
+  const int64_t k = blockIdx.y, c = blockIdx.x;
+  const int64_t i = c * CQ + threadIdx.x;
+  const bool hit = threadIdx.x < CQ && i < n_q && __ldg(nbr + k * n_q + i) >= 0;
+  const int cnt = __syncthreads_count(hit);
+  if (threadIdx.x == 0) counts[k * nchunk + c] = cnt;
+}
+
 // Exclusive scan of the (k, chunk) hit counts in canonical order: each CTA scans a tile of
 // kScanTile counts (tile-local offsets + tile total); the last CTA to finish scans the tile
 // totals and writes the canonical list starts map_start[k] (= offset of (k, chunk 0)).
@@ -1263,6 +1316,13 @@ namespace {
 void launch_canonical(Ctx& ctx, MapData& m) {
   auto& pd = m.pending;
   const cudaStream_t st = ctx.stream;
+  if (pd.counts_from_nbr) {  // derived map: per-(k, chunk) counts from its table
+    const int CQ = 32 * pd.qpl;
+    ctx.launch("k_chunk_counts", [&] {
+      k_chunk_counts<<<dim3(static_cast<unsigned>(pd.nchunk), static_cast<unsigned>(m.K3)), CQ, 0, st>>>(
+          m.nbr_in.get<int32_t>(), m.n_out, CQ, pd.nchunk, pd.counts.get<int32_t>());
+    });
+  }
   if (!m.nbr_pos.get()) m.nbr_pos.alloc(sizeof(int32_t) * std::max<int64_t>(1, int64_t{m.K3} * m.n_out), st);
   if (!m.pair_in.get()) {
     m.pair_in.alloc(sizeof(int32_t) * std::max<int64_t>(1, pd.max_pairs), st);
@@ -1897,6 +1957,73 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
   m->pending = MapData::Pending{};
   if (!force_wide && (f.wide || f.big_bucket)) return build_map(ctx, P, cfg, target, true);  // exact fallback: CUB 64-bit sort
   check_flags(f);
+  return m;
+}
+
+
+namespace {
+// lazy map shell over sorted source / query keys with an all -1 table, canonical lists on demand
+std::unique_ptr<MapData> derived_shell(Ctx& ctx, const MapSource& P, const MapSource& Q, const sconv_map_cfg& cfg) {
+  auto m = std::make_unique<MapData>();
+  m->cfg = cfg;
+  m->n_in = P.n;
+  m->n_out = Q.n;
+  m->src_keys = P.keys;
+  m->q_keys = Q.keys;
+  m->src_identity = true;
+  m->delta = weight_offsets_ext(cfg.kernel_size, cfg.offset_scale);
+  if (cfg.transposed)
+    for (auto& d : m->delta) d = make_int3(-d.x, -d.y, -d.z);
+  m->K3 = static_cast<int>(m->delta.size());
+  const cudaStream_t st = ctx.stream;
+  const int64_t cells = std::max<int64_t>(1, int64_t{m->K3} * Q.n);
+  m->nbr_in.alloc(sizeof(int32_t) * cells, st);
+  SCONV_CUDA(cudaMemsetAsync(m->nbr_in.get(), 0xFF, sizeof(int32_t) * cells, st));
+  m->map_start.alloc(sizeof(int32_t) * (m->K3 + 1), st);
+  auto& pd = m->pending;
+  pd.qpl = 4;
+  pd.nchunk = ceil_div<int64_t>(Q.n, 32 * pd.qpl);
+  pd.grid = pd.nchunk * m->K3;
+  pd.ntiles = ceil_div<int64_t>(pd.grid, kScanTile);
+  pd.ngroups = ceil_div(m->K3, kSearchThreads / 32);
+  pd.counts.alloc(sizeof(int32_t) * std::max<int64_t>(1, pd.grid), st);
+  pd.offs.alloc(sizeof(int32_t) * std::max<int64_t>(1, pd.grid), st);
+  pd.tiles.alloc(sizeof(int32_t) * std::max<int64_t>(1, pd.ntiles), st);
+  pd.counts_from_nbr = true;
+  pd.max_pairs = std::min<int64_t>(int64_t{m->K3} * Q.n, int64_t{m->K3} * P.n);
+  m->canonical = false;
+  m->total = -1;
+  return m;
+}
+}  // namespace
+
+std::unique_ptr<MapData> derive_down_map(Ctx& ctx, const MapSource& P, const MapSource& Q, const sconv_map_cfg& cfg) {
+  if (cfg.kernel_size != 2 || cfg.transposed || cfg.out_stride != 2 * cfg.offset_scale || !P.keys || !Q.keys)
+    fail(SCONV_ERR_ARG, "derived down-sampling maps need K = 2, stride 2s over sorted keys");
+  auto m = derived_shell(ctx, P, Q, cfg);
+  if (P.n > 0 && Q.n > 0) {
+    const cudaStream_t st = ctx.stream;
+    ctx.launch("k_down_map", [&] {
+      k_down_map<<<grid_for(P.n), kThreads, 0, st>>>(m->src_keys_ptr(), P.n, m->q_keys_ptr(), Q.n, cfg.offset_scale,
+                                                     m->nbr_in.get<int32_t>());
+    });
+  }
+  return m;
+}
+
+std::unique_ptr<MapData> derive_transposed_map(Ctx& ctx, const MapData& fwd, const MapSource& P, const MapSource& T,
+                                               const sconv_map_cfg& cfg) {
+  if (!cfg.transposed || fwd.cfg.transposed || fwd.cfg.kernel_size != cfg.kernel_size ||
+      fwd.cfg.offset_scale != cfg.offset_scale || fwd.n_out != P.n || fwd.n_in != T.n || !fwd.nbr_in.get())
+    fail(SCONV_ERR_ARG, "a derived transposed map needs its forward map (same K and offset scale)");
+  auto m = derived_shell(ctx, P, T, cfg);
+  if (fwd.n_out > 0 && T.n > 0) {
+    const cudaStream_t st = ctx.stream;
+    ctx.launch("k_transpose_map", [&] {
+      k_transpose_map<<<grid_for(fwd.n_out * fwd.K3), kThreads, 0, st>>>(fwd.nbr_in.get<int32_t>(), fwd.n_out, fwd.K3,
+                                                                         m->nbr_in.get<int32_t>(), T.n);
+    });
+  }
   return m;
 }
 

@@ -57,6 +57,7 @@ struct MapData {
     int ngroups = 0, qpl = 0;
     bool flags_init = false;  // k_init_flags ran on `flags`
     int64_t max_pairs = 0;    // pair-list capacity (allocated by the canonical build)
+    bool counts_from_nbr = false;  // derived map: chunk counts computed from the table on demand
   } pending;
   // last GMaS stats
   int64_t buffer_length = 0;
@@ -90,6 +91,13 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
 // and the flags (one sync on the build's stream; false: the compact-key path overflowed, rebuild
 // normally). strided_q: the strided map's Eq. 1 output computed that way (no second sort).
 bool finish_coords(Ctx& ctx, MapData& m);
+// Derived network maps (no search), exact by construction where net.cu uses them:
+// derive_down_map: K = 2, stride 2s map of P (on the s-lattice) onto Q = Eq. 1 of P;
+// derive_transposed_map: the transposed map (P = fwd's output set, T = fwd's input set) from
+// its forward map fwd, pairs swapped.
+std::unique_ptr<MapData> derive_down_map(Ctx& ctx, const MapSource& P, const MapSource& Q, const sconv_map_cfg& cfg);
+std::unique_ptr<MapData> derive_transposed_map(Ctx& ctx, const MapData& fwd, const MapSource& P, const MapSource& T,
+                                               const sconv_map_cfg& cfg);
 // defer_flags (pinned host, >= kDeferredFlagsBytes): a map over SORTED raw coordinates (no sort
 // fallback exists) skips its flags sync; the flags are copied there asynchronously on the build
 // stream and the caller checks them with check_deferred_map_flags once that copy completed

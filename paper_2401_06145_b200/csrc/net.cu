@@ -216,6 +216,10 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
     SCONV_CUDA(cudaStreamCreateWithPriority(&coord_stream, cudaStreamNonBlocking, hi));
   }
   if (!ev_coords) SCONV_CUDA(cudaEventCreateWithFlags(&ev_coords, cudaEventDisableTiming));
+  static const bool derive_maps = [] {  // SCONV_NET_DERIVE=0: search every map (A/B)
+    const char* e = std::getenv("SCONV_NET_DERIVE");
+    return !(e && e[0] == '0');
+  }();
   static const bool coord_ahead = [] {
     const char* e = std::getenv("SCONV_NET_COORD_AHEAD");
     return !(e && e[0] == '0');
@@ -336,6 +340,7 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
   maps_built = 0;
   sorts = 0;
   conv_stats.clear();
+  conv_maps.clear();
   // coordinate set 0 = the raw input (may be unsorted)
   coordsets.push_back({input.keys, input.n, input.sorted, true});
   raw_input = input;
@@ -413,13 +418,31 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
               if (!ok) pre.reset();  // compact keys overflowed: the normal build's exact path
             }
           }
+          // K = 2, stride 2s down-sampling of a set on the s-lattice: the map is derived from the
+          // Eq. 1 output (a scatter, no search); its transposed up-sampling map from it in turn
+          const bool down_derivable = derive_maps && !o.transposed && o.K == 2 && o.out_stride == 2 * o.offset_scale &&
+                                      P.keys && coordsets[a.coordset].lattice % o.offset_scale == 0;
+          if (down_derivable && !pre) {  // no look-ahead coordinates: Eq. 1 now (one sync, as before)
+            pre = build_map(ctx, P, mcfg, nullptr, false, true, nullptr, nullptr, /*coords_only=*/true);
+            if (!finish_coords(ctx, *pre)) pre.reset();
+          }
+          const MapData* fwd = nullptr;
+          if (derive_maps && o.transposed && o.K == 2) {
+            auto f = maps.find(MapKey{tgt, o.K, o.offset_scale, 2 * o.offset_scale, 0, -1});
+            if (f != maps.end() && f->second.out_cs == a.coordset) fwd = f->second.map.get();
+          }
           if (pre) {
             MapSource Q;
             Q.keys = pre->q_keys;
             Q.n = pre->n_out;
             Q.sorted = true;
-            m = build_map(ctx, P, mcfg, nullptr, false, /*lazy=*/true, nullptr, nullptr, false, &Q);
+            if (down_derivable)
+              m = derive_down_map(ctx, P, Q, mcfg);
+            else
+              m = build_map(ctx, P, mcfg, nullptr, false, /*lazy=*/true, nullptr, nullptr, false, &Q);
             m->sorts += pre->sorts;
+          } else if (fwd) {
+            m = derive_transposed_map(ctx, *fwd, P, T, mcfg);
           } else {
             m = build_map(ctx, P, mcfg, o.transposed ? &T : nullptr, false, /*lazy=*/true, nullptr, dflags);
           }
@@ -454,7 +477,7 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
         } else if (o.out_stride == 1 && coordsets[a.coordset].keys) {
           out_cs = a.coordset;  // stride-1 alias
         } else {
-          coordsets.push_back({m->q_keys, m->n_out, true, false});
+          coordsets.push_back({m->q_keys, m->n_out, true, false, o.out_stride});
           out_cs = static_cast<int>(coordsets.size()) - 1;
         }
         // the raw input's keys were just packed (cs may dangle after the push_back above)
@@ -543,6 +566,7 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
       ++convs_issued;
       conv_stats.push_back({m.n_in, m.n_out, m.total, df == SCONV_DATAFLOW_FUSED ? 0 : m.buffer_length, w.c_in, w.c_out,
                             w.k_pad, m.K3, df, pl.res >= 0 ? 1 : 0});
+      conv_maps.push_back(&m);
     } else {
       NetTensor& b = tensors.at(o.b);
       if (b.coordset < 0) fail(SCONV_ERR_STATE, "op reads a tensor that was not produced yet");
@@ -677,6 +701,16 @@ void NetData::tune_conv(Ctx& ctx, int op, MapData& m, const WeightData& w, const
   for (int t : candidate_tiles(w.c_out)) tune->scatter_ms[op][t] += time_kernel("k_scatter", default_tile(w.c_in, true), t);
   ctx.last_records.clear();
   ctx.profiling = was;
+}
+
+// |M| of lazily built maps (the fused dataflow never needs it): canonical lists on demand, after
+// the forward (one sync per unresolved map; statistics / roofline only, never in a timed loop)
+void NetData::resolve_stats(Ctx& ctx) {
+  for (size_t c = 0; c < conv_stats.size() && c < conv_maps.size(); ++c) {
+    if (conv_stats[c][2] >= 0 || !conv_maps[c]) continue;
+    ensure_canonical(ctx, *conv_maps[c]);
+    conv_stats[c][2] = conv_maps[c]->total;
+  }
 }
 
 void NetData::finish_tune() {

@@ -54,6 +54,7 @@ struct CoordSet {
   int64_t n = 0;
   bool sorted = true;
   bool raw = false;
+  int lattice = 1;  // every coordinate is a multiple of this (Eq. 1 outputs: their stride)
 };
 
 using MapKey = std::tuple<int, int, int, int, int, int>;
@@ -82,6 +83,8 @@ struct NetData {
   // per CONV op of the last forward: n_in, n_out, |M|, R_pad (0 when fused), c_in, c_out, k_pad, K3,
   // dataflow, residual folded (0/1)
   std::vector<std::array<int64_t, 10>> conv_stats;
+  std::vector<MapData*> conv_maps;  // the map of each conv of the last forward (|M| on demand)
+  void resolve_stats(Ctx& ctx);
   // Kernel maps depend on coordinates only: they are built (and their fused row order
   // prepared) on a second, high-priority stream, so a map build and its host syncs overlap the
   // previous layers' convs; the context stream waits on an event before the first conv using

@@ -108,6 +108,7 @@ class Network:
     def conv_stats(self):
         """Per conv (execution order): n_in, n_out, M, R_pad (0 when fused), c_in, c_out, k_pad, K3,
         dataflow (0 GMaS / 1 fused), residual (ADD folded into the epilogue)."""
+        self.ctx.check(self.ctx.lib.sconv_net_resolve_stats(self.ctx.h, self.h))  # |M| of lazily built maps
         out = []
         for i in range(len(self.g.convs())):
             v = np.zeros(10, np.int64)

@@ -122,6 +122,7 @@ SIGNATURES = [
     ("sconv_voxelize", _I, [_P, _P, _I64, _I, _P, _I64, _I, _D, _P, _P, _I, C.POINTER(_I64)]),
     ("sconv_net_stats", _I, [_P, C.POINTER(_I), C.POINTER(_I)]),
     ("sconv_net_conv_stats", _I, [_P, _I, _P]),
+    ("sconv_net_resolve_stats", _I, [_P, _P]),
     ("sconv_net_autotune", _I, [_P, _P, _I, _P, _P, _P, _P, _I, _I, _P]),
     ("sconv_net_tune_latencies", _I, [_P, _I, _P, _P, _I, C.POINTER(_I), C.POINTER(_I)]),
     ("sconv_net_free", None, [_P, _P]),
