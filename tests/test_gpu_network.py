@@ -124,6 +124,24 @@ def test_minkunet42_end_to_end(ctx):
     assert elementwise_errors(outs["fused"], outs["gmas-unfolded"])[2] <= 2e-2
 
 
+def test_minkunet42_bf16_end_to_end(ctx):
+    """bf16 activations and weights (compute_dtype=BF16) through the whole network: fused
+    dataflow, folded residuals, derived K=2 maps; output coordinates exact, features against the
+    fp32 oracle graph (bf16 keeps 8 mantissa bits: the Frobenius bound is 8x the f16 one)."""
+    coords, feats = D.kitti_scan(3, n_azimuth=400)
+    g = N.minkunet42()
+    w = N.init_weights(g, 7)
+    q, ref = oracle_graph(g, w, coords, feats)
+    net = N.Network(ctx, g, w, sc.exec_cfg(dataflow=sc.DATAFLOW_FUSED, compute_dtype=sc.BF16))
+    net.forward(coords, feats)
+    xo, fo = net.read(g.output)
+    np.testing.assert_array_equal(xo, q)
+    mx, mean, fro = elementwise_errors(fo, ref)
+    print(f"MinkUNet42 bf16 end-to-end: max_rel={mx:.2e} mean_rel={mean:.2e} fro={fro:.2e}")
+    assert fro <= 1.6e-1, (mx, mean, fro)
+    assert sum(s["dataflow"] for s in net.conv_stats()) == 49
+
+
 @pytest.mark.parametrize("dataflow", [sc.DATAFLOW_GMAS, sc.DATAFLOW_FUSED])
 def test_sparse_resnet21d_small_room(ctx, dataflow):
     coords, feats = D.s3dis_room(2, n_points=60000, resolution=0.05)
