@@ -213,7 +213,8 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
     SCONV_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     SCONV_CUDA(cudaStreamCreateWithPriority(&map_stream, cudaStreamNonBlocking, hi));
     SCONV_CUDA(cudaStreamCreateWithPriority(&layout_stream, cudaStreamNonBlocking, hi));
-    SCONV_CUDA(cudaStreamCreateWithPriority(&coord_stream, cudaStreamNonBlocking, lo));  // look-ahead: least urgent
+    const char* cp = std::getenv("SCONV_COORD_PRIO");  // A/B: "hi" | "lo" (default)
+    SCONV_CUDA(cudaStreamCreateWithPriority(&coord_stream, cudaStreamNonBlocking, cp && cp[0] == 'h' ? hi : lo));
   }
   if (!ev_coords) SCONV_CUDA(cudaEventCreateWithFlags(&ev_coords, cudaEventDisableTiming));
   static const bool derive_maps = [] {  // SCONV_NET_DERIVE=0: search every map (A/B)
@@ -315,10 +316,14 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
               P.keys = coordsets[cs_new].keys;
               P.n = coordsets[cs_new].n;
               P.sorted = true;
-              if (wait_map_stream) {  // the keys are still being produced on the map stream: wait
-                // for the layout stream, which follows it and holds this level's row order (the
-                // first conv needs that; the next level's Eq. 1 does not need to compete with it)
-                SCONV_CUDA(cudaEventRecord(ev_coords, ls));
+              if (wait_map_stream) {  // the keys are still being produced on the map stream
+                // (measured r02ag, same box: waiting for the map stream 2.20 ms, for the layout
+                // stream 2.28 ms, look-ahead off 2.22 ms; A/B: SCONV_COORD_AFTER=layout)
+                static const bool after_map = [] {
+                  const char* e = std::getenv("SCONV_COORD_AFTER");
+                  return !(e && e[0] == 'l');
+                }();
+                SCONV_CUDA(cudaEventRecord(ev_coords, after_map ? ms : ls));
                 SCONV_CUDA(cudaStreamWaitEvent(cst, ev_coords));
               }
               ctx.stream = cst;
