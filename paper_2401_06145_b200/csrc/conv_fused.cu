@@ -1745,10 +1745,22 @@ void order_fused_rows(Ctx& ctx, MapData& m) {
   idx.alloc(4 * n, st);
   m.row_perm.alloc(4 * n, st);
   m.nbr_perm.alloc(4 * n * K3, st);
-  static const int mask_bits = [] {
-    const char* e = std::getenv("SCONV_MASK_BITS");  // experiments (16 bits: -78 us sort, +60 us convs)
-    return e ? std::max(1, std::min(32, std::atoi(e))) : 24;
+  // Sort-key width: networks pass a hint from the number of convs that use the map (net.cu:
+  // 24 bits = 3 passes when >= 6 convs amortise the sort, else 16 bits = 2 passes); otherwise
+  // 24 bits, 16 for maps of more than SCONV_MASK16_ROWS rows (default 200k). Same-box A/B r02ah: C2 (maps <= 119k rows)
+  // 24 bits 2.20 ms vs 16 bits 2.25 ms; C3 (level 0: 337k rows) 1.354 ms vs 1.309 ms with 16.
+  // SCONV_MASK_BITS forces one width.
+  static const int mask_bits_forced = [] {
+    const char* e = std::getenv("SCONV_MASK_BITS");
+    return e ? std::max(1, std::min(32, std::atoi(e))) : 0;
   }();
+  static const int64_t mask16_rows = [] {
+    const char* e = std::getenv("SCONV_MASK16_ROWS");
+    return e ? std::atoll(e) : int64_t{200000};
+  }();
+  const int mask_bits = mask_bits_forced     ? mask_bits_forced
+                        : m.mask_bits_hint ? m.mask_bits_hint
+                                           : (n > mask16_rows ? 16 : 24);
   // one cooperative launch when every row fits the co-resident CTAs' registers
   static const int coop_cap = [] {
     int per_sm = 0, dev = 0, sms = 0, coop = 0;
@@ -1761,8 +1773,9 @@ void order_fused_rows(Ctx& ctx, MapData& m) {
   }();
   // 8-offset maps: their whole 8-bit mask in one stable pass (the same one-launch sort, so the
   // row order -- and with it the work items and any split-part summation -- is deterministic)
-  const int npass = small ? 1 : 3;
-  const bool one_launch = (small || (mask_bits == 24 && K3 >= 24)) && coop_cap > 0 &&
+  // the top mask_bits bits (a multiple of 8) in mask_bits / 8 stable passes
+  const int npass = small ? 1 : mask_bits / 8;
+  const bool one_launch = (small || (mask_bits % 8 == 0 && mask_bits <= 24 && K3 >= mask_bits)) && coop_cap > 0 &&
                           n <= static_cast<int64_t>(coop_cap) * kCoopThreads * kCoopMaxE &&
                           !(std::getenv("SCONV_MASK_SORT_CUB") && std::getenv("SCONV_MASK_SORT_CUB")[0] == '1');
   if (one_launch) {
@@ -1780,7 +1793,7 @@ void order_fused_rows(Ctx& ctx, MapData& m) {
     unsigned* bar = reinterpret_cast<unsigned*>(tot + 256);
     SCONV_CUDA(cudaMemsetAsync(bar, 0, 4 * sizeof(unsigned), st));
     const int32_t* nbr = m.nbr_in.get<int32_t>();
-    int begin_bit = small ? 0 : K3 - 24, K3v = K3, tilev = tile, np = npass;
+    int begin_bit = small ? 0 : K3 - mask_bits, K3v = K3, tilev = tile, np = npass;
     int64_t nn = n;
     uint32_t *k0 = keys.get<uint32_t>(), *k1 = keys_sorted.get<uint32_t>();
     int32_t *v0 = idx.get<int32_t>(), *v1 = v1buf.get<int32_t>();

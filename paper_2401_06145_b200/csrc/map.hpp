@@ -50,6 +50,7 @@ struct MapData {
   bool flags_deferred = false;  // build_map(defer_flags): coordinate checks pending at the caller
   DevBuf pend_nsel;             // coords_only builds: |Q| on the device until finish_coords
   bool identity_pending = false;
+  int mask_bits_hint = 0;        // fused row order's key width chosen by the caller (0: default rule)
   bool layout_off_path = false;  // fused row order built beside the convs (network layout stream)  // lazy 1x1 identity map: arrays not yet written (nbr_in[i] = i)
   struct Pending {
     DevBuf counts, offs, tiles, flags;

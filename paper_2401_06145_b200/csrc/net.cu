@@ -290,6 +290,7 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
   std::map<MapKey, MapEntry> old_maps;
   old_maps.swap(maps);
   pre_coords.clear();  // (unused look-ahead coordinates of the previous forward)
+  plan_map_uses(input.sorted);
   // queue the Eq. 1 output of the next strided conv over coordinate set cs_new (see net.hpp)
   // (op `from` writes a tensor on cs_new; its output is not assigned yet when this runs)
   auto prelaunch = [&](int cs_new, int from, bool wait_map_stream) {
@@ -466,6 +467,11 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
           ctx.stream = ls;
           // off the critical path only when convs are already queued ahead of this map's first use
           m->layout_off_path = ls != st && convs_issued > 0;
+          // row-order key width from the number of convs that will use this map (plan_map_uses:
+          // the op graph alone, so every forward orders the rows alike): 3 sort passes pay off only
+          // when enough convs share the map (r02ai: C2 maps serve 6-8 convs, 24 bits best; C3's
+          // serve 4-5, 16 bits best)
+          if (oi < static_cast<int>(map_uses.size()) && map_uses[oi] > 0) m->mask_bits_hint = map_uses[oi] >= 6 ? 24 : 16;
           if (pl.dataflow != SCONV_DATAFLOW_GMAS) prepare_fused_layout(ctx, *m);
           hmark(oi, "layout queued");
         } catch (...) {
@@ -718,6 +724,51 @@ void NetData::resolve_stats(Ctx& ctx) {
     ensure_canonical(ctx, *conv_maps[c]);
     conv_stats[c][2] = conv_maps[c]->total;
   }
+}
+
+// Per op: how many convs of a forward use the map first built at that op, from the op graph alone
+// (the runtime's coordinate-set and map-cache rules replayed symbolically; input sortedness
+// decides whether the raw set aliases). Deterministic, so the row-order hint it feeds is the
+// same in every forward.
+void NetData::plan_map_uses(bool input_sorted) {
+  map_uses.assign(ops.size(), 0);
+  struct Sym {
+    bool keyed, sorted;
+  };
+  std::vector<Sym> cs{{false, input_sorted}};
+  std::vector<int> tcs(num_tensors, -1);
+  tcs[input_tensor] = 0;
+  std::map<MapKey, std::pair<int, int>> seen;  // key -> (first op, output set)
+  std::map<MapKey, int> uses;
+  for (int oi = 0; oi < static_cast<int>(ops.size()); ++oi) {
+    if (plan[oi].skip) continue;
+    const NetOp& o = ops[oi];
+    const int a = tcs[o.in];
+    if (a < 0) continue;
+    if (o.kind != kOpConv) {
+      tcs[plan[oi].out] = a;
+      continue;
+    }
+    const int tgt = o.transposed ? tcs[o.target] : -1;
+    const MapKey key{a, o.K, o.offset_scale, o.transposed ? 1 : o.out_stride, o.transposed, tgt};
+    auto it = seen.find(key);
+    if (it == seen.end()) {
+      if (!cs[a].keyed && cs[a].sorted) cs[a].keyed = true;
+      int out;
+      if (o.transposed) {
+        out = tgt;
+      } else if (o.out_stride == 1 && cs[a].keyed) {
+        out = a;
+      } else {
+        cs.push_back({true, true});
+        out = static_cast<int>(cs.size()) - 1;
+      }
+      it = seen.emplace(key, std::make_pair(oi, out)).first;
+    }
+    ++uses[key];
+    tcs[plan[oi].out] = it->second.second;
+  }
+  for (const auto& [k, v] : seen) map_uses[v.first] = uses[k];
 }
 
 void NetData::finish_tune() {

@@ -84,6 +84,8 @@ struct NetData {
   // dataflow, residual folded (0/1)
   std::vector<std::array<int64_t, 10>> conv_stats;
   std::vector<MapData*> conv_maps;  // the map of each conv of the last forward (|M| on demand)
+  std::vector<int> map_uses;  // per op: convs using the map first built at that op (plan_map_uses)
+  void plan_map_uses(bool input_sorted);
   void resolve_stats(Ctx& ctx);
   // Kernel maps depend on coordinates only: they are built (and their fused row order
   // prepared) on a second, high-priority stream, so a map build and its host syncs overlap the
