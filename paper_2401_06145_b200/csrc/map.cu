@@ -1433,7 +1433,8 @@ void check_deferred_map_flags(const void* flags_host, const MapSource& P) {
 
 std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map_cfg& cfg, const MapSource* target,
                                    bool force_wide, bool lazy, const std::vector<int3>* explicit_offsets,
-                                   void* defer_flags, bool coords_only, const MapSource* strided_q) {
+                                   void* defer_flags, bool coords_only, const MapSource* strided_q,
+                                   cudaEvent_t src_ready) {
   auto hmark = [&](const char* what) { ctx.hmark(what); };
   hmark("map: enter");
   if (cfg.block_B < 4 || cfg.block_B > 1024 || cfg.block_B % 4 != 0)
@@ -1558,6 +1559,7 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
       m->sorts = 1;
     }
   }
+  if (src_ready) SCONV_CUDA(cudaEventRecord(src_ready, st));  // sorted source keys complete
   const uint64_t* src = m->src_keys_ptr();
   const int32_t* src_idx = m->src_identity ? nullptr : m->src_idx.get<int32_t>();
 

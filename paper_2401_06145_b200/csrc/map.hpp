@@ -86,11 +86,13 @@ struct MapSource {
 std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map_cfg& cfg, const MapSource* target,
                                    bool force_wide = false, bool lazy = false,
                                    const std::vector<int3>* explicit_offsets = nullptr, void* defer_flags = nullptr,
-                                   bool coords_only = false, const MapSource* strided_q = nullptr);
+                                   bool coords_only = false, const MapSource* strided_q = nullptr,
+                                   cudaEvent_t src_ready = nullptr);
 // coords_only: a strided map over existing sorted keys queues only its Eq. 1 output coordinates
 // (floor / sort / unique) and returns without a sync (n_out = -1); finish_coords then reads |Q|
 // and the flags (one sync on the build's stream; false: the compact-key path overflowed, rebuild
 // normally). strided_q: the strided map's Eq. 1 output computed that way (no second sort).
+// src_ready: recorded on the build stream once the sorted source keys exist (before the search).
 bool finish_coords(Ctx& ctx, MapData& m);
 // Derived network maps (no search), exact by construction where net.cu uses them:
 // derive_down_map: K = 2, stride 2s map of P (on the s-lattice) onto Q = Eq. 1 of P;

@@ -221,6 +221,10 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
     const char* e = std::getenv("SCONV_NET_DERIVE");
     return !(e && e[0] == '0');
   }();
+  static const bool coord_after_pack = [] {  // SCONV_COORD_AFTER=pack: first Eq. 1 right after key packing
+    const char* e = std::getenv("SCONV_COORD_AFTER");
+    return e && e[0] == 'p';
+  }();
   static const bool coord_ahead = [] {
     const char* e = std::getenv("SCONV_NET_COORD_AHEAD");
     return !(e && e[0] == '0');
@@ -324,7 +328,7 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
                   const char* e = std::getenv("SCONV_COORD_AFTER");
                   return !(e && e[0] == 'l');
                 }();
-                SCONV_CUDA(cudaEventRecord(ev_coords, after_map ? ms : ls));
+                if (!coord_after_pack) SCONV_CUDA(cudaEventRecord(ev_coords, after_map ? ms : ls));
                 SCONV_CUDA(cudaStreamWaitEvent(cst, ev_coords));
               }
               ctx.stream = cst;
@@ -452,7 +456,9 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
           } else if (fwd) {
             m = derive_transposed_map(ctx, *fwd, P, T, mcfg);
           } else {
-            m = build_map(ctx, P, mcfg, o.transposed ? &T : nullptr, false, /*lazy=*/true, nullptr, dflags);
+            // the raw input's packed keys feed the look-ahead Eq. 1: event before this map's search
+            m = build_map(ctx, P, mcfg, o.transposed ? &T : nullptr, false, /*lazy=*/true, nullptr, dflags, false,
+                          nullptr, cs.raw && coord_after_pack ? ev_coords : nullptr);
           }
           if (m->flags_deferred) {
             deferred_flags = dflags;
