@@ -221,9 +221,12 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
     const char* e = std::getenv("SCONV_NET_DERIVE");
     return !(e && e[0] == '0');
   }();
-  static const bool coord_after_pack = [] {  // SCONV_COORD_AFTER=pack: first Eq. 1 right after key packing
+  // the first look-ahead Eq. 1 starts right after the raw input's key packing, beside the level-0
+  // search (same box r02ao: C2 2.207 -> 2.167 ms, C3 1.299 -> 1.268); SCONV_COORD_AFTER=map|layout
+  // waits for the level-0 search / row order instead
+  static const bool coord_after_pack = [] {
     const char* e = std::getenv("SCONV_COORD_AFTER");
-    return e && e[0] == 'p';
+    return !(e && (e[0] == 'm' || e[0] == 'l'));
   }();
   static const bool coord_ahead = [] {
     const char* e = std::getenv("SCONV_NET_COORD_AHEAD");
