@@ -9,6 +9,7 @@
 //   k_scatter<T>     one thread per (output row, tile): ascending-k fp32 reduction of the
 //                    row's slots (deterministic, tile invariant)
 #include <algorithm>
+#include <climits>
 #include <cstring>
 #include <numeric>
 #include <set>
@@ -586,6 +587,8 @@ void gmas_forward(Ctx& ctx, MapData& m, const WeightData& w, const sconv_exec_cf
   m.gather_tile = Tg;
   m.scatter_tile = Ts;
   const int64_t R = plan.buffer_length;
+  // slot indices (buffer rows, member deltas) are int32 on the device
+  if (R > INT32_MAX) fail(SCONV_ERR_ARG, "GMaS buffer too large: more than 2^31 - 1 padded rows");
   const size_t out_elem = dtype_size(io.out_dtype);
   if (R == 0 || m.n_in == 0) {
     if (io.res == nullptr && io.ld_out == c_out) {
