@@ -127,6 +127,62 @@ struct OutCvt<__nv_bfloat16> {
   static __device__ __forceinline__ __nv_bfloat16 from(float v) { return __float2bfloat16_rn(v); }
 };
 
+// 16-bit epilogue of one warp's 32 rows x 16 columns (lane = row): + residual, ReLU, store,
+// with every global load / store instruction covering 16 rows x 32 contiguous bytes (full
+// 32-byte sectors; the row-per-lane accesses touch each sector with 16 B twice). Lane l moves
+// the half (l & 1) of row (l >> 1) + 16h; warp shuffles carry the values between the row owner
+// and the mover. All 32 lanes must call it (rows may be invalid: never loaded or stored).
+template <class TOut>
+__device__ __forceinline__ void epilogue16_rows(TOut* out, int64_t ld_out, const TOut* res, int64_t ld_res,
+                                                int64_t row, bool valid, int col, int relu, float (&x)[16]) {
+  static_assert(sizeof(TOut) == 2, "16-bit outputs");
+  const int lane = threadIdx.x & 31, half = lane & 1;
+  long long mrow[2];
+  bool mval[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int src = (lane >> 1) + 16 * h;
+    mrow[h] = __shfl_sync(0xFFFFFFFFu, static_cast<long long>(row), src);
+    mval[h] = __shfl_sync(0xFFFFFFFFu, valid ? 1 : 0, src) != 0;
+  }
+  if (res) {
+    uint4 rv[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      rv[h] = mval[h] ? *reinterpret_cast<const uint4*>(res + mrow[h] * ld_res + col + half * 8) : make_uint4(0, 0, 0, 0);
+    const int s0 = 2 * (lane & 15), hi = lane >> 4;
+    uint32_t w[8];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t a0 = __shfl_sync(0xFFFFFFFFu, (&rv[0].x)[k], s0), a1 = __shfl_sync(0xFFFFFFFFu, (&rv[1].x)[k], s0);
+      const uint32_t b0 = __shfl_sync(0xFFFFFFFFu, (&rv[0].x)[k], s0 + 1);
+      const uint32_t b1 = __shfl_sync(0xFFFFFFFFu, (&rv[1].x)[k], s0 + 1);
+      w[k] = hi ? a1 : a0;
+      w[4 + k] = hi ? b1 : b0;
+    }
+    float r[16];
+    OutCvt<TOut>::load16(reinterpret_cast<const TOut*>(w), r);
+#pragma unroll
+    for (int e = 0; e < 16; ++e) x[e] += r[e];
+  }
+  if (relu)
+#pragma unroll
+    for (int e = 0; e < 16; ++e) x[e] = fmaxf(x[e], 0.f);
+  uint4 pk[2];
+  OutCvt<TOut>::store16(reinterpret_cast<TOut*>(pk), x);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int src = (lane >> 1) + 16 * h;
+    uint4 v;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t a = __shfl_sync(0xFFFFFFFFu, (&pk[0].x)[k], src), b = __shfl_sync(0xFFFFFFFFu, (&pk[1].x)[k], src);
+      (&v.x)[k] = half ? b : a;
+    }
+    if (mval[h]) *reinterpret_cast<uint4*>(out + mrow[h] * ld_out + col + half * 8) = v;
+  }
+}
+
 struct MaskOrder {
   int pos[32];
 };
@@ -164,6 +220,7 @@ struct FusedParams {
   int* item_counters;
   float* ws;
   int num_rb;
+  int coal_epi;  // 16-bit outputs: sector-coalesced epilogue (SCONV_FUSED_COAL=0: row per lane)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -640,6 +697,15 @@ __global__ void __launch_bounds__(kThreads, NK == 0 ? 4 : 2) k_conv_fused(const 
       for (int c0 = 0; c0 < n_tile; c0 += 16) {
         uint32_t v[16];
         tmem_ld16(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * p.block_n + c0), v);
+        if constexpr (sizeof(TOut) == 2) {
+          if (p.vec && c0 + 16 <= ncols && p.coal_epi) {  // warp-uniform: sector-coalesced path
+            float x[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) x[e] = __uint_as_float(v[e]);
+            epilogue16_rows<TOut>(out + n0, p.ld_out, res ? res + n0 : nullptr, p.ld_res, i, valid, c0, p.relu, x);
+            continue;
+          }
+        }
         if (!valid || c0 >= ncols) continue;
         float x[16];
 #pragma unroll
@@ -1015,6 +1081,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_conv_items(const __grid_constan
             tmem_ld16(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * p.block_n + c0), v);
 #pragma unroll
             for (int e = 0; e < 16; ++e) x[e] = __uint_as_float(v[e]);
+            if constexpr (sizeof(TOut) == 2) {
+              if (p.vec && c0 + 16 <= ncols && p.coal_epi) {  // warp-uniform: sector-coalesced path
+                epilogue16_rows<TOut>(out + n0, p.ld_out, res ? res + n0 : nullptr, p.ld_res, orow, valid, c0, p.relu, x);
+                continue;
+              }
+            }
           } else {
 #pragma unroll
             for (int e = 0; e < 16; ++e) x[e] = 0.f;
@@ -1401,6 +1473,7 @@ void launch_conv_items(Ctx& ctx, const FusedArgs& a, int kc, int64_t row_blocks)
               reinterpret_cast<uintptr_t>(a.out) % 16 == 0 && reinterpret_cast<uintptr_t>(a.res) % 16 == 0;
   }
   prm.bf16 = w.dtype == SCONV_BF16;
+  prm.coal_epi = coalesced_epilogue_enabled();
   prm.a_bytes = 128u * kc * 2u;
   prm.b_bytes = static_cast<uint32_t>(bn) * kc * 2u;
   prm.unit_bytes = (prm.a_bytes + prm.b_bytes + 1023u) & ~1023u;
@@ -1467,6 +1540,14 @@ void launch_conv_items(Ctx& ctx, const FusedArgs& a, int kc, int64_t row_blocks)
   }
 }
 }  // namespace
+
+bool coalesced_epilogue_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("SCONV_FUSED_COAL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 // SCONV_FUSED_ITEMS: 0 = tile-queue kernel only, 1 = work-item kernel wherever items exist,
 // unset / 2 = per conv (few-tile wide layers: work items)
@@ -1554,6 +1635,7 @@ void launch_conv_fused(Ctx& ctx, const FusedArgs& a) {
               reinterpret_cast<uintptr_t>(a.out) % 16 == 0 && reinterpret_cast<uintptr_t>(a.res) % 16 == 0;
   }
   prm.bf16 = w.dtype == SCONV_BF16;
+  prm.coal_epi = coalesced_epilogue_enabled();
   prm.a_bytes = 128u * kc * 2u;
   prm.b_bytes = static_cast<uint32_t>(bn) * kc * 2u;
   prm.unit_bytes = (prm.a_bytes + prm.b_bytes + 1023u) & ~1023u;

@@ -41,6 +41,7 @@ void build_fused_items(Ctx& ctx, MapData& m);
 // true when the fused kernel supports this layer (K3 <= 64, 16-bit operands)
 bool fused_supported(int K3, int c_in, int c_out);
 int fused_items_mode();  // SCONV_FUSED_ITEMS (conv_fused.cu)
+bool coalesced_epilogue_enabled();  // SCONV_FUSED_COAL (conv_fused.cu)
 void launch_conv_fused(Ctx& ctx, const FusedArgs& a);
 
 // f32/f16/bf16 [n][c] -> 16-bit [n][ld] (zero padded columns), dtype = operand type
