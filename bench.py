@@ -100,24 +100,33 @@ class ClockSampler:
             self.max_mhz = None
 
     def _run(self):
+        while not self.stop_ev.is_set():
+            self._sample_once()
+            self.stop_ev.wait(self.interval)
+
+    def _sample_once(self):
         nv = self.nv
         names = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40, "sw_power_cap": 0x4}
-        while not self.stop_ev.is_set():
-            try:
-                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
-                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                for k, bit in names.items():
-                    if r & bit:
-                        self.reasons.add(k)
-            except Exception:
-                pass
-            time.sleep(self.interval)
+        try:
+            self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+            r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            for k, bit in names.items():
+                if r & bit:
+                    self.reasons.add(k)
+        except Exception:
+            pass
 
     def __enter__(self):
         if self.ok:
             self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
         return self
+
+    def sample_now(self):
+        """One extra sample at a known point of the timed region (the steps are short: a 50 ms
+        interval alone may land only once inside it)."""
+        if self.ok:
+            self._sample_once()
 
     def __exit__(self, *a):
         if self.ok:
@@ -222,8 +231,10 @@ class NetWorkload:
         launch duration of the dominant kernel type)."""
         tot = self.net.algo_bytes()
         nconv = len(self.g.convs())
-        per = {k: v / nconv for k, v in tot.items() if not k.startswith("_") and k != "k_search"}
+        per = {k: v / nconv for k, v in tot.items() if not k.startswith("_") and k not in ("k_search", "k_floor_unique")}
         per["k_search"] = tot["k_search"] / max(1, tot["_k_search_launches"])  # one launch per map
+        # one cooperative launch per distinct Eq. 1 output set
+        per["k_floor_unique"] = tot["k_floor_unique"] / max(1, tot["_k_floor_unique_launches"])
         return per
 
     def map_algo_bytes(self):
@@ -470,6 +481,7 @@ def main():
             a.record(stream)
             wl.step()
             b.record(stream)
+        clk.sample_now()  # the last steps are still queued / running on the GPU
         torch.cuda.synchronize()
     launches = ctx.launch_count - launches0
     step_ms = [a.elapsed_time(b) for a, b in ev]

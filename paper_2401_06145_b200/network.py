@@ -178,11 +178,14 @@ class Network:
         the weights once (2*K3*ci*co)."""
         g = e = s = f = 0
         maps = {}  # distinct searched maps (identity 1x1 maps need no search): SURVEY §8d Map bytes
+        eq1 = {}  # distinct Eq. 1 output sets (strided convs / downsamples): floor + sort + unique
         for st in self.conv_stats():
             n, q, M, R, ci, co, kp, K3, df, res = (st[k] for k in self.STAT_KEYS)
             if K3 > 1:
                 # (+ 12|P| + 8|Q| for an Eq. 1 downsample, which creates the smaller output set)
                 maps[(n, q, M, K3)] = 8 * n + 8 * q + 8 * M + 4 * K3 + ((12 * n + 8 * q) if q < n else 0)
+            if q < n:
+                eq1[(n, q)] = 12 * n + 8 * q  # read |P| keys + indices, write |Q| keys
             if df == 1:
                 f += 2 * ci * n + 4 * K3 * q + 2 * co * q * (2 if res else 1) + 2 * K3 * ci * co
                 continue
@@ -190,7 +193,8 @@ class Network:
             e += 2 * kp * R + part_bytes * co * R + 2 * K3 * ci * co
             s += part_bytes * co * M + 4 * K3 * q + 2 * co * q * (2 if res else 1)
         return {"k_gather": g, "k_gemm_grouped": e, "k_scatter": s, "k_conv_fused": f,
-                "k_search": sum(maps.values()), "_k_search_launches": len(maps)}
+                "k_search": sum(maps.values()), "_k_search_launches": len(maps),
+                "k_floor_unique": sum(eq1.values()), "_k_floor_unique_launches": len(eq1)}
 
     def free(self):
         if self.h:
