@@ -901,6 +901,383 @@ __global__ void __launch_bounds__(32 * KZ * KZ, KZ == 3 ? 2 : 4) k_search_col(
   }
 }
 
+// Persistent, software-pipelined column search (same result as k_search_col). A CTA owns a
+// contiguous range of query chunks; each column warp walks it with a per-warp CURSOR into the
+// sorted source: the window start of chunk c + 1 is found from the start of chunk c by one
+// warp-wide probe round (32 strided loads; keys only grow along the range), so only the
+// CTA's first chunk needs the pivot search. Two window buffers per warp: while chunk c is
+// searched, chunk c + 1's window (a fixed W keys from its start, bulk copy) and chunk c + 2's
+// probe loads are in flight. A window that does not cover its chunk continues in further
+// slices (synchronously, rare). r02: k_search_col spent most of each CTA's life on the
+// dependent chain query load -> 2 pivot searches -> window copy -> search, one chunk per CTA.
+// Lane state of k_search_colp's queries for the out-of-line direct resolution below.
+template <int QPL, int KZ>
+struct ColQueries {
+  uint64_t k[QPL];
+  uint64_t d[KZ];
+  int zn[QPL];
+  int res[QPL][KZ];
+};
+
+// Resolve a lane's unresolved queries of one column directly in global memory: lower bounds by
+// interleaved binary searches over [cur, n_src) (independent loads in flight together), then
+// the short z-walk. For k_search_colp's scattered chunks only.
+template <int QPL, int KZ>
+__device__ __noinline__ ColQueries<QPL, KZ> col_resolve_direct(const uint64_t* __restrict__ src,
+                                                               const int32_t* __restrict__ src_idx, int n_src, int cur,
+                                                               ColQueries<QPL, KZ> st, bool fast, int dx, int dy,
+                                                               int scale) {
+  constexpr int zlo = (KZ % 2 == 1) ? -(KZ / 2) : 0;
+  auto ek = [&](uint64_t qk, int zi) {
+    const int tz = scale > 0 ? zi : KZ - 1 - zi;
+    uint64_t d = st.d[0];
+#pragma unroll
+    for (int z = 1; z < KZ; ++z) d = zi == z ? st.d[z] : d;
+    return fast ? qk + d : segment_key(qk, make_int3(dx, dy, (tz + zlo) * scale));
+  };
+  int blo[QPL], blen[QPL];
+  uint64_t be[QPL];
+#pragma unroll
+  for (int u = 0; u < QPL; ++u) {
+    be[u] = st.zn[u] < KZ ? ek(st.k[u], st.zn[u]) : 0;
+    blo[u] = cur;
+    blen[u] = st.zn[u] < KZ ? n_src - cur : 0;
+  }
+  // 4-ary lower bound: three independent probes per query and step (log4 dependent rounds)
+  for (bool any = true; any;) {
+    any = false;
+    uint64_t v[QPL][3];
+#pragma unroll
+    for (int u = 0; u < QPL; ++u)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const int off = static_cast<int>((static_cast<int64_t>(blen[u]) * (j + 1)) >> 2);
+        v[u][j] = blen[u] >= 4 ? __ldg(src + blo[u] + off) : 0;
+      }
+#pragma unroll
+    for (int u = 0; u < QPL; ++u) {
+      if (blen[u] <= 0) continue;
+      if (blen[u] < 4) {  // binary steps for the last few
+        const int h = blen[u] >> 1;
+        if (__ldg(src + blo[u] + h) < be[u]) {
+          blo[u] += h + 1;
+          blen[u] -= h + 1;
+        } else {
+          blen[u] = h;
+        }
+      } else {
+        // answer in [blo, blo + blen]; probes at offsets o_j = blen (j + 1) / 4
+        int lo2 = 0, hi2 = blen[u];
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          const int off = static_cast<int>((static_cast<int64_t>(blen[u]) * (j + 1)) >> 2);
+          if (v[u][j] < be[u]) lo2 = off + 1;
+        }
+#pragma unroll
+        for (int j = 2; j >= 0; --j) {
+          const int off = static_cast<int>((static_cast<int64_t>(blen[u]) * (j + 1)) >> 2);
+          if (v[u][j] >= be[u]) hi2 = off;
+        }
+        blo[u] += lo2;
+        blen[u] = hi2 - lo2;
+      }
+      any = any || blen[u] > 0;
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < QPL; ++u) {
+    if (st.zn[u] >= KZ) continue;
+    int p = blo[u];
+    const int z0 = st.zn[u];
+#pragma unroll
+    for (int zi = 0; zi < KZ; ++zi) {
+      if (zi < z0) continue;
+      const uint64_t e = ek(st.k[u], zi);
+      uint64_t v = 0;
+      while (p < n_src && (v = __ldg(src + p)) < e) ++p;
+      if (p == n_src) break;
+      if (v == e) {
+        st.res[u][zi] = src_idx ? __ldg(src_idx + p) : p;
+        ++p;
+      }
+    }
+    st.zn[u] = KZ;
+  }
+  return st;
+}
+
+template <int QPL, int KZ, int W>
+__global__ void __launch_bounds__(32 * KZ * KZ, KZ == 3 ? 2 : 4) k_search_colp(
+    const uint64_t* __restrict__ src, const int32_t* __restrict__ src_idx, int64_t n_src, int B,
+    const uint64_t* __restrict__ q, int64_t n_q, int scale, int64_t nchunk, int probe_stride,
+    int32_t* __restrict__ nbr, int32_t* __restrict__ chunk_count, unsigned long long* trace) {
+  constexpr int CQ = 32 * QPL, kWarps = KZ * KZ;
+  static_assert(W % 4 == 0, "window slices start 16-byte aligned");
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ __align__(8) uint64_t s_bar[kWarps][2];
+  const int lane = threadIdx.x & 31, col = threadIdx.x >> 5;
+  uint64_t* s_win = reinterpret_cast<uint64_t*>(smem) + int64_t{col} * 2 * W;  // [2][W]
+  int32_t* s_widx = reinterpret_cast<int32_t*>(reinterpret_cast<uint64_t*>(smem) + int64_t{kWarps} * 2 * W) +
+                    int64_t{col} * 2 * W;
+  const int64_t G = gridDim.x;
+  const int64_t cb = blockIdx.x * nchunk / G, ce = (blockIdx.x + 1) * nchunk / G;
+  if (cb >= ce) return;
+  uint64_t* bar = s_bar[col];
+  if (lane == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[0])) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[1])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  constexpr int zlo = (KZ % 2 == 1) ? -(KZ / 2) : 0;
+  const int dx = (col / KZ + zlo) * scale, dy = (col % KZ + zlo) * scale;
+  auto tz_of = [&](int zi) { return scale > 0 ? zi : KZ - 1 - zi; };
+  auto ekey = [&](uint64_t qk, int zi) { return segment_key(qk, make_int3(dx, dy, (tz_of(zi) + zlo) * scale)); };
+  // Fast segment keys: a query whose three fields are at least M = KZ |scale| inside the
+  // coordinate range gets q + delta by ONE 64-bit add (no field can carry or borrow); the
+  // saturating unpack/pack of segment_key is kept for chunks with any query near the range
+  // edge (warp-uniform choice per chunk).
+  uint64_t D[KZ];
+#pragma unroll
+  for (int zi = 0; zi < KZ; ++zi)
+    D[zi] = (static_cast<uint64_t>(static_cast<int64_t>(dx)) << 42) + (static_cast<uint64_t>(static_cast<int64_t>(dy)) << 21) +
+            static_cast<uint64_t>(static_cast<int64_t>((tz_of(zi) + zlo) * scale));
+  const uint64_t Mf = static_cast<uint64_t>(KZ) * static_cast<uint64_t>(scale < 0 ? -scale : scale);
+  constexpr uint64_t kF = (uint64_t{1} << 42) | (uint64_t{1} << 21) | 1u;
+  constexpr uint64_t kCarry = (uint64_t{1} << 63) | (uint64_t{1} << 42) | (uint64_t{1} << 21);
+  const uint64_t lowF = (Mf + 1) * kF, highF = Mf * kF;
+  auto safe_key = [&](uint64_t k) {
+    return (((k ^ lowF ^ (k - lowF)) | (k ^ highF ^ (k + highF))) & kCarry) == 0;
+  };
+  const int qb = lane * QPL;
+  const int64_t nb = (n_src + B - 1) / B;
+  auto load_keys = [&](int64_t c, uint64_t (&kk)[QPL]) {
+    const int64_t base = c * CQ + qb;
+#pragma unroll
+    for (int u = 0; u < QPL; ++u) kk[u] = base + u < n_q ? __ldg(q + base + u) : ~uint64_t{0};
+  };
+  // first position >= cur whose key is >= key, to `step` granularity (a lower bound of the
+  // exact position, never past it): 32-lane probe rounds, the stride growing 8x per round
+  auto advance = [&](int64_t cur, uint64_t key, uint64_t pv, int step) -> int64_t {
+    for (;;) {
+      const unsigned m = __ballot_sync(0xFFFFFFFFu, pv >= key);
+      if (m) return min(cur + int64_t{step} * (__ffs(m) - 1), n_src);
+      cur += int64_t{32} * step;
+      if (cur >= n_src) return n_src;
+      step *= 8;
+      const int64_t p = cur + int64_t{step} * lane + step - 1;
+      pv = p < n_src ? __ldg(src + p) : ~uint64_t{0};
+    }
+  };
+  auto probe = [&](int64_t cur) -> uint64_t {
+    const int64_t p = cur + int64_t{probe_stride} * lane + probe_stride - 1;
+    return p < n_src ? __ldg(src + p) : ~uint64_t{0};
+  };
+  uint32_t ph0 = 0, ph1 = 0;  // phase per window buffer (scalars: an indexed array would live on the stack)
+  auto issue = [&](int buf, int64_t start) -> int {
+    const int wlen = static_cast<int>(min(static_cast<int64_t>(W), n_src - start));
+    if (wlen > 0 && lane == 0) {
+      const uint32_t kb = static_cast<uint32_t>((wlen + 3) & ~3);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar[buf])),
+                   "r"(kb * 8u + (src_idx ? kb * 4u : 0u))
+                   : "memory");
+      bulk_g2s(s_win + buf * W, src + start, kb * 8u, &bar[buf]);
+      if (src_idx) bulk_g2s(s_widx + buf * W, src_idx + start, kb * 4u, &bar[buf]);
+    }
+    return wlen;
+  };
+  // query keys: chunk c's in registers (kc), chunk c + 1's loaded during chunk c (kn), and only
+  // the FIRST key of chunk c + 2 (its window start) two chunks ahead (klo)
+  uint64_t kc[QPL], kn[QPL];
+  load_keys(cb, kc);
+  uint64_t klo = cb + 1 < ce ? __ldg(q + (cb + 1) * CQ) : 0;
+  // the range's first window: pivot search (block granularity), then one round to 8 keys
+  int64_t start_c;
+  {
+    const uint64_t key_lo = ekey(__shfl_sync(0xFFFFFFFFu, kc[0], 0), 0);
+    const int64_t blo =
+        n_src == 0 ? 0 : warp_first_pivot_ge(src, n_src, B, 0, nb, key_lo, lane, ((cb * CQ * n_src) / max(n_q, int64_t{1})) / B);
+    if (blo >= nb) {
+      start_c = n_src;
+    } else {
+      const int64_t p = blo * B + 8 * lane + 7;
+      start_c = advance(blo * B, key_lo, p < n_src ? __ldg(src + p) : ~uint64_t{0}, 8);
+    }
+  }
+  int buf = 0;
+  int wlen_c = issue(buf, start_c);
+  uint64_t pv = cb + 1 < ce ? probe(start_c) : 0;
+  for (int64_t c = cb; c < ce; ++c) {
+    const bool has1 = c + 1 < ce, has2 = c + 2 < ce;
+    // (a) window of chunk c + 1 from the probe issued one iteration ago; (b) its copy; (c) the
+    // probe and query keys of chunk c + 2 -- all in flight during the search of chunk c
+    int64_t start_n = n_src;
+    int wlen_n = 0;
+    if (has1) {
+      start_n = advance(start_c, ekey(klo, 0), pv, probe_stride);
+      wlen_n = issue(buf ^ 1, start_n);
+      load_keys(c + 1, kn);
+      if (has2) {
+        pv = probe(start_n);
+        klo = __ldg(q + (c + 2) * CQ);
+      }
+    }
+    // (d) search chunk c
+    int res[QPL][KZ];
+    int zn[QPL];
+    const int64_t lo = c * CQ;
+    const int len = static_cast<int>(min(static_cast<int64_t>(CQ), n_q - lo));
+#pragma unroll
+    for (int u = 0; u < QPL; ++u) {
+      zn[u] = qb + u < len ? 0 : KZ;
+#pragma unroll
+      for (int z = 0; z < KZ; ++z) res[u][z] = -1;
+    }
+    bool ok = true;
+#pragma unroll
+    for (int u = 0; u < QPL; ++u) ok = ok && (qb + u >= len || safe_key(kc[u]));
+    const bool fast = __all_sync(0xFFFFFFFFu, ok);
+    auto ek = [&](uint64_t qk, int zi) {  // D by selects (a dynamic index would put D on the stack)
+      uint64_t d = D[0];
+#pragma unroll
+      for (int z = 1; z < KZ; ++z) d = zi == z ? D[z] : d;
+      return fast ? qk + d : ekey(qk, zi);
+    };
+    int64_t g0 = start_c;
+    int wlen = wlen_c;
+    unsigned long long t_begin = 0;
+    int nslices = 0;
+    if (trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
+    while (wlen > 0) {
+      ++nslices;
+      mbar_wait_parity(&bar[buf], buf ? ph1 : ph0);
+      if (buf) ph1 ^= 1u; else ph0 ^= 1u;
+      const uint64_t* sw = s_win + buf * W;
+      const int32_t* si = s_widx + buf * W;
+      const uint64_t last = sw[wlen - 1];
+      int pprev = 0;
+      bool more = false;
+#pragma unroll
+      for (int u = 0; u < QPL; ++u) {
+        if (zn[u] >= KZ) continue;
+        uint64_t e = ek(kc[u], zn[u]);
+        if (e > last) {
+          more = true;
+          continue;
+        }
+        int base = zn[u] == 0 ? pprev : 0;
+        if (base == 0) {  // no earlier position known: branchless lower bound over the window
+          int n = wlen;
+          while (n > 1) {
+            const int h = n >> 1;
+            base += sw[base + h - 1] < e ? h : 0;
+            n -= h;
+          }
+        } else if (sw[base] < e) {  // gallop from the lane's previous (smaller) query
+          int lo_ = base, hi_ = base + 1, step = 1;
+          while (hi_ < wlen - 1 && sw[hi_] < e) {
+            lo_ = hi_;
+            step <<= 1;
+            hi_ = min(base + step, wlen - 1);
+          }
+          int b = lo_ + 1, n = hi_ - lo_;
+          while (n > 1) {
+            const int h = n >> 1;
+            b += sw[b + h - 1] < e ? h : 0;
+            n -= h;
+          }
+          base = b;
+        }
+        if (zn[u] == 0) pprev = base;
+        int p = base;
+        const int z0 = zn[u];
+#pragma unroll
+        for (int zi = 0; zi < KZ; ++zi) {
+          if (zi < z0) continue;
+          if (zi > z0) e = ek(kc[u], zi);
+          while (p < wlen && sw[p] < e) ++p;
+          if (p == wlen) {
+            more = true;
+            break;
+          }
+          if (sw[p] == e) {
+            res[u][zi] = src_idx ? si[p] : static_cast<int32_t>(g0 + p);
+            ++p;
+          }
+          zn[u] = zi + 1;
+        }
+      }
+      __syncwarp();  // the next slice overwrites this buffer
+      if (!__any_sync(0xFFFFFFFFu, more)) break;
+      if (nslices >= 2) {
+        // Scattered chunk (its queries span many x-slices of the cloud, so a column's targets
+        // lie in many separate key ranges: up to ~20 slices at ~5 us each on the S3DIS room,
+        // the kernel's tail): resolve the rest directly in global memory (out-of-line: the rare
+        // path's registers stay out of the hot loop's allocation).
+        ColQueries<QPL, KZ> st;
+#pragma unroll
+        for (int u = 0; u < QPL; ++u) {
+          st.k[u] = kc[u];
+          st.zn[u] = zn[u];
+#pragma unroll
+          for (int z = 0; z < KZ; ++z) st.res[u][z] = res[u][z];
+        }
+#pragma unroll
+        for (int z = 0; z < KZ; ++z) st.d[z] = D[z];
+        st = col_resolve_direct<QPL, KZ>(src, src_idx, static_cast<int>(n_src), static_cast<int>(g0 + wlen), st,
+                                         fast, dx, dy, scale);
+#pragma unroll
+        for (int u = 0; u < QPL; ++u)
+#pragma unroll
+          for (int z = 0; z < KZ; ++z) res[u][z] = st.res[u][z];
+        break;
+      }
+      // rare: the window did not cover the chunk. The next slice starts at the smallest key a
+      // query still needs (found by probing forward), not right after this one: a chunk that
+      // straddles two x-slices of the cloud needs two narrow key ranges, and staging the whole
+      // range between them (up to ~10^4 keys next to a wall plane) made such chunks the
+      // kernel's tail.
+      uint64_t need = ~uint64_t{0};
+#pragma unroll
+      for (int u = 0; u < QPL; ++u)
+        if (zn[u] < KZ) need = min(need, ek(kc[u], zn[u]));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) need = min(need, __shfl_xor_sync(0xFFFFFFFFu, need, o));
+      const int64_t cur = g0 + wlen;
+      const int64_t p = cur + int64_t{64} * lane + 63;
+      g0 = advance(cur, need, p < n_src ? __ldg(src + p) : ~uint64_t{0}, 64);
+      wlen = issue(buf, g0);
+    }
+#pragma unroll
+    for (int zi = 0; zi < KZ; ++zi) {
+      const int k = col * KZ + tz_of(zi);
+      int32_t* row = nbr + int64_t{k} * n_q + lo + qb;
+      int cnt = 0;
+#pragma unroll
+      for (int u = 0; u < QPL; ++u) {
+        if (qb + u < len) row[u] = res[u][zi];
+        cnt += __popc(__ballot_sync(0xFFFFFFFFu, res[u][zi] >= 0));
+      }
+      if (lane == 0) chunk_count[int64_t{k} * nchunk + c] = cnt;
+    }
+    if (trace && lane == 0) {  // diagnostics (SCONV_SEARCH_TRACE): per (chunk, column) timing
+      unsigned long long t_end;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+      unsigned long long* tr = trace + (c * kWarps + col) * 4;
+      tr[0] = t_begin;
+      tr[1] = t_end;
+      tr[2] = static_cast<unsigned long long>(nslices) | (static_cast<unsigned long long>(blockIdx.x) << 32);
+      tr[3] = static_cast<unsigned long long>(start_c);
+    }
+    // rotate
+#pragma unroll
+    for (int u = 0; u < QPL; ++u) kc[u] = kn[u];
+    start_c = start_n;
+    wlen_c = wlen_n;
+    buf ^= 1;
+  }
+}
+
 // ---------------------------------------------------------------- derived maps (networks)
 // K = 2, stride 2s down-sampling map of a fine set P on the s-lattice onto Q = Eq. 1 of P:
 // every p has exactly one parent q = floor(p / 2s) * 2s in Q and one offset (p - q) / s in
@@ -1876,7 +2253,61 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
         return e ? std::max(4, std::atoi(e)) : 768;
       }();
       const int cap_blocks = std::max(1, cap_keys / B);
-      if (use_col) {
+      static const bool persist = [] {
+        const char* e = std::getenv("SCONV_SEARCH_PERSIST");  // A/B: 0 = one CTA per chunk (k_search_col)
+        return !(e && e[0] == '0');
+      }();
+      if (use_col && persist) {
+        const int kz = cfg.kernel_size;
+        constexpr int kW = 384;
+        const size_t smem = size_t{2} * 12 * kz * kz * kW;
+        const int scale = cfg.transposed ? -cfg.offset_scale : cfg.offset_scale;
+        // probe stride: 32 lanes cover ~4 chunk advances (a chunk of 128 queries moves the
+        // window by ~128 |P| / |Q| source keys); multiple of 4 (16-byte aligned idx slices)
+        const int64_t adv = ceil_div<int64_t>(int64_t{128} * n, std::max<int64_t>(n_out, 1));
+        const int stride = static_cast<int>(std::min<int64_t>(4 * ceil_div<int64_t>(adv, 32), 1 << 20));
+        const char* trace_path = std::getenv("SCONV_SEARCH_TRACE");
+        DevBuf trace;
+        if (trace_path) {
+          trace.alloc(size_t{32} * nchunk2 * kz * kz, st);
+          SCONV_CUDA(cudaMemsetAsync(trace.get(), 0, size_t{32} * nchunk2 * kz * kz, st));
+        }
+        auto go = [&](auto kern) {
+          set_max_smem(reinterpret_cast<const void*>(kern), smem);
+          static const int o = [&] {  // resident CTAs per SM (one init per kernel instantiation)
+            int v = 0;
+            return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kern, 32 * kz * kz, smem) == cudaSuccess && v > 0 ? v : 1;
+          }();
+          static const int cpc_env = [] {  // experiments: chunks per CTA (0: one range per resident CTA)
+            const char* e = std::getenv("SCONV_SEARCH_CPC");
+            return e ? std::atoi(e) : 0;
+          }();
+          // one chunk per CTA (the hardware scheduler balances clouds with uneven chunk costs:
+          // KITTI, S3DIS) below ~5e5 queries; above, one chunk range per resident CTA (the
+          // cursor pipeline wins on large clouds: uniform 1e6 / 1e7 1.3x / 1.4x; r02bm)
+          const bool ranges = cpc_env == 0 && n_out >= 500000;
+          const int64_t grid = ranges ? std::min<int64_t>(nchunk2, int64_t{ctx.num_sms} * o)
+                                      : ceil_div<int64_t>(nchunk2, std::max(1, cpc_env));
+          ctx.launch("k_search", [&] {
+            kern<<<static_cast<unsigned>(grid), 32 * kz * kz, smem, st>>>(src, src_idx, n, B, q, n_out, scale, nchunk2,
+                                                                           std::max(4, stride), m->nbr_in.get<int32_t>(),
+                                                                           counts.get<int32_t>(), trace.get<unsigned long long>());
+          });
+          if (trace_path) {  // diagnostics: dump {t_begin, t_end, slices | cta << 32, window start} per (chunk, column)
+            std::vector<unsigned long long> h(static_cast<size_t>(nchunk2) * kz * kz * 4);
+            SCONV_CUDA(cudaMemcpyAsync(h.data(), trace.get(), h.size() * 8, cudaMemcpyDeviceToHost, st));
+            SCONV_CUDA(cudaStreamSynchronize(st));
+            if (FILE* f = std::fopen(trace_path, "wb")) {
+              std::fwrite(h.data(), 8, h.size(), f);
+              std::fclose(f);
+            }
+          }
+        };
+        if (kz == 3)
+          go(k_search_colp<4, 3, kW>);
+        else
+          go(k_search_colp<4, 2, kW>);
+      } else if (use_col) {
         const int kz = cfg.kernel_size;
         // a 128-query chunk's column window spans ~1-2 blocks of 256: 2-block slices
         const int cap_col = std::max(1, std::min(cap_blocks, 512 / B));

@@ -110,16 +110,38 @@ def test_three_way_map_equivalence_200(ctx, oracle):
                 raise AssertionError(f"{ctx_info} backend={be}: {e}") from None
 
 
-def test_map_range_edges(ctx, oracle):
-    """Clouds touching COORD_MIN / COORD_MAX (the SPEC sentinel edge case)."""
+@pytest.mark.parametrize("K,Cq", [(5, 32), (3, 512)])
+def test_map_range_edges(ctx, oracle, K, Cq):
+    """Clouds touching COORD_MIN / COORD_MAX (the SPEC sentinel edge case). K = 3
+    with C >= 128 runs the column search: its chunks near the range edge take the saturating
+    segment keys instead of the one-add fast keys."""
     rng = np.random.default_rng(5)
     lo = random_cloud(rng, 300, 6, origin=-(2 ** 20 - 1))
     hi = random_cloud(rng, 300, 6, origin=2 ** 20 - 6)
     xyz = np.concatenate([lo, hi])
-    m = sc.KernelMap.build(ctx, xyz, False, 5, 1, 1, B=16, Cq=32)
+    m = sc.KernelMap.build(ctx, xyz, False, K, 1, 1, B=16, Cq=Cq)
     gpu = m.read()
-    ora = oracle.layer_map(xyz, False, 5, 1, 1, backend=2)
+    ora = oracle.layer_map(xyz, False, K, 1, 1, backend=2)
     assert_map_equal(gpu, ora)
+
+
+@pytest.mark.parametrize("presorted", [True, False])
+def test_map_scattered_chunks(ctx, oracle, presorted):
+    """Query chunks whose column targets lie in many separate key ranges (the S3DIS walls): a
+    slice x = 1 of 128 points at scattered y between two dense wall planes x = 0 and x = 2, so
+    the dx = -1 / +1 columns of that chunk need ~128 narrow ranges spread over a 12.8k-key wall.
+    The column search resolves such chunks by skip-ahead slices, then directly in global memory."""
+    rng = np.random.default_rng(214)
+    yy, zz = np.meshgrid(np.arange(200), np.arange(64), indexing="ij")
+    wall = lambda x: np.stack([np.full(yy.size, x), yy.ravel(), zz.ravel()], 1)  # noqa: E731
+    ys = np.sort(rng.choice(200, size=128, replace=False))
+    mid = np.stack([np.ones(128, np.int64), ys, rng.integers(0, 64, 128)], 1)
+    sparse = np.stack([np.arange(3, 700), rng.integers(0, 200, 697), rng.integers(0, 64, 697)], 1)
+    xyz = np.concatenate([wall(0), mid, wall(2), sparse]).astype(np.int32)
+    xyz = sort_rows(xyz) if presorted else xyz[rng.permutation(len(xyz))]
+    for K in (3, 2):
+        got = sc.KernelMap.build(ctx, xyz, presorted, K, 1, 1).read()
+        assert_map_equal(got, oracle.layer_map(xyz, presorted, K, 1, 1, backend=1))
 
 
 @pytest.mark.parametrize("s", [2, 4])
