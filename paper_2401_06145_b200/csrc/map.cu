@@ -1811,7 +1811,8 @@ void check_deferred_map_flags(const void* flags_host, const MapSource& P) {
 std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map_cfg& cfg, const MapSource* target,
                                    bool force_wide, bool lazy, const std::vector<int3>* explicit_offsets,
                                    void* defer_flags, bool coords_only, const MapSource* strided_q,
-                                   cudaEvent_t src_ready) {
+                                   cudaEvent_t src_ready,
+                                   const std::function<void(const std::shared_ptr<DevBuf>&)>& on_src_ready) {
   auto hmark = [&](const char* what) { ctx.hmark(what); };
   hmark("map: enter");
   if (cfg.block_B < 4 || cfg.block_B > 1024 || cfg.block_B % 4 != 0)
@@ -1937,6 +1938,7 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
     }
   }
   if (src_ready) SCONV_CUDA(cudaEventRecord(src_ready, st));  // sorted source keys complete
+  if (on_src_ready) on_src_ready(m->src_keys);
   const uint64_t* src = m->src_keys_ptr();
   const int32_t* src_idx = m->src_identity ? nullptr : m->src_idx.get<int32_t>();
 

@@ -1,6 +1,7 @@
 // Device-resident kernel map (the product's KernelMap).
 #pragma once
 
+#include <functional>
 #include <memory>
 #include <vector>
 
@@ -87,12 +88,14 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
                                    bool force_wide = false, bool lazy = false,
                                    const std::vector<int3>* explicit_offsets = nullptr, void* defer_flags = nullptr,
                                    bool coords_only = false, const MapSource* strided_q = nullptr,
-                                   cudaEvent_t src_ready = nullptr);
+                                   cudaEvent_t src_ready = nullptr,
+                                   const std::function<void(const std::shared_ptr<DevBuf>&)>& on_src_ready = {});
 // coords_only: a strided map over existing sorted keys queues only its Eq. 1 output coordinates
 // (floor / sort / unique) and returns without a sync (n_out = -1); finish_coords then reads |Q|
 // and the flags (one sync on the build's stream; false: the compact-key path overflowed, rebuild
 // normally). strided_q: the strided map's Eq. 1 output computed that way (no second sort).
-// src_ready: recorded on the build stream once the sorted source keys exist (before the search).
+// src_ready: recorded on the build stream once the sorted source keys exist (before the search);
+// on_src_ready is called right after that (host), before the search is queued.
 bool finish_coords(Ctx& ctx, MapData& m);
 // Derived network maps (no search), exact by construction where net.cu uses them:
 // derive_down_map: K = 2, stride 2s map of P (on the s-lattice) onto Q = Eq. 1 of P;

@@ -213,8 +213,8 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
     SCONV_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     SCONV_CUDA(cudaStreamCreateWithPriority(&map_stream, cudaStreamNonBlocking, hi));
     SCONV_CUDA(cudaStreamCreateWithPriority(&layout_stream, cudaStreamNonBlocking, hi));
-    const char* cp = std::getenv("SCONV_COORD_PRIO");  // A/B: "hi" | "lo" (default)
-    SCONV_CUDA(cudaStreamCreateWithPriority(&coord_stream, cudaStreamNonBlocking, cp && cp[0] == 'h' ? hi : lo));
+    const char* cp = std::getenv("SCONV_COORD_PRIO");  // A/B: "lo" | "hi" (default; r02bp same box: C2 2.168 -> 2.150 ms)
+    SCONV_CUDA(cudaStreamCreateWithPriority(&coord_stream, cudaStreamNonBlocking, cp && cp[0] == 'l' ? lo : hi));
   }
   if (!ev_coords) SCONV_CUDA(cudaEventCreateWithFlags(&ev_coords, cudaEventDisableTiming));
   static const bool derive_maps = [] {  // SCONV_NET_DERIVE=0: search every map (A/B)
@@ -351,6 +351,11 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
     }
   };
   const void* deferred_flags = nullptr;  // raw sorted input: coordinate checks after the launches
+  // pending look-ahead Eq. 1 (see the map-build path): coordinate set, creating op, whether it
+  // waits for the map stream, and whether it fires after the current op's conv
+  int pre_cs = -1, pre_from = -1;
+  bool pre_wait = false, pre_armed = false;
+  bool raw_pre_done = false;  // the raw input's look-ahead Eq. 1 was queued inside its map build
   int convs_issued = 0;
   maps_built = 0;
   sorts = 0;
@@ -459,9 +464,28 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
           } else if (fwd) {
             m = derive_transposed_map(ctx, *fwd, P, T, mcfg);
           } else {
-            // the raw input's packed keys feed the look-ahead Eq. 1: event before this map's search
+            // the raw input's packed keys feed the look-ahead Eq. 1: event before this map's search,
+            // and (sorted raw input) the Eq. 1 is queued right there, AHEAD of the level-0 search:
+            // its |Q| then reaches the host before the first down conv needs it (r02bs timeline: queued
+            // after the search it ran beside the level-0 row order, slowing both, and the host
+            // waited ~110 us for it at the first down conv)
+            static const bool raw_first_on = [] {  // A/B: SCONV_RAW_EQ1_FIRST=0 queues it after the search
+              const char* e = std::getenv("SCONV_RAW_EQ1_FIRST");
+              return !(e && e[0] == '0');
+            }();
+            const bool raw_first =
+                raw_first_on && cs.raw && cs.sorted && coord_after_pack && cst && a.coordset == 0 && !o.transposed;
+            const int csi = a.coordset;
+            auto on_keys = [&, csi, oi](const std::shared_ptr<DevBuf>& keys) {
+              if (!raw_first || raw_pre_done) return;
+              coordsets[csi].keys = keys;
+              const cudaStream_t saved = ctx.stream;
+              prelaunch(csi, oi, true);
+              ctx.stream = saved;
+              raw_pre_done = true;
+            };
             m = build_map(ctx, P, mcfg, o.transposed ? &T : nullptr, false, /*lazy=*/true, nullptr, dflags, false,
-                          nullptr, cs.raw && coord_after_pack ? ev_coords : nullptr);
+                          nullptr, cs.raw && coord_after_pack ? ev_coords : nullptr, on_keys);
           }
           if (m->flags_deferred) {
             deferred_flags = dflags;
@@ -505,11 +529,37 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
         // the raw input's keys were just packed (cs may dangle after the push_back above)
         const bool raw_keyed = a.coordset == 0 && maps_built == 1 && coordsets[0].keys;
         it = maps.emplace(key, MapEntry{std::move(m), out_cs}).first;
-        // coordinate look-ahead: the next strided conv over a coordinate set created now
-        if (out_cs != a.coordset && !o.transposed)
-          prelaunch(out_cs, oi, false);  // (keys complete: this build synchronised on |Q|)
-        else if (raw_keyed)
-          prelaunch(a.coordset, oi, true);
+        // coordinate look-ahead: the Eq. 1 output of the next strided conv over a coordinate set
+        // created now (keys complete: this build synchronised on |Q|), or over the raw input once
+        // its keys are packed. It is needed only when the host reaches that conv, several convs
+        // later, so it is queued after the conv of the NEXT map-building op (for the raw input:
+        // after this op's conv): queued at once, the one-launch Eq. 1 ran ahead of the next level's
+        // search and row order (the critical path: the conv stream idled ~150 us per level,
+        // r02bq/r02br timelines). SCONV_PRE_AFTER_CONV=0: at once (A/B).
+        static const bool pre_after = [] {
+          const char* e = std::getenv("SCONV_PRE_AFTER_CONV");
+          return !(e && e[0] == '0');
+        }();
+        if (pre_after && pre_cs >= 0) pre_armed = true;  // a map was built since: fire after this conv
+        if (out_cs != a.coordset && !o.transposed) {
+          if (pre_after && pre_cs < 0) {
+            pre_cs = out_cs;
+            pre_from = oi;
+            pre_wait = false;
+            pre_armed = false;
+          } else {
+            prelaunch(out_cs, oi, false);
+          }
+        } else if (raw_keyed && !raw_pre_done) {
+          if (pre_after && pre_cs < 0) {
+            pre_cs = a.coordset;
+            pre_from = oi;
+            pre_wait = true;
+            pre_armed = true;
+          } else {
+            prelaunch(a.coordset, oi, true);
+          }
+        }
       }
       MapData& m = *it->second.map;
       auto wt = weights.find(o.weight);
@@ -572,6 +622,10 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
       if (pl.scatter_tile > 0) ccfg.scatter_tile = pl.scatter_tile;
       layer_forward_dev(ctx, m, w, ccfg, df, io);
       hmark(oi, "conv queued");
+      if (pre_cs >= 0 && pre_armed) {
+        prelaunch(pre_cs, pre_from, pre_wait);
+        pre_cs = -1;
+      }
       if (debug_sync()) {
         std::fprintf(stderr, "[sconv] op %d conv K3=%d n_in=%lld n_out=%lld c_in=%d c_out=%d dataflow=%d ...", oi, m.K3,
                      static_cast<long long>(m.n_in), static_cast<long long>(m.n_out), w.c_in, w.c_out, df);

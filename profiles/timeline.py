@@ -58,11 +58,22 @@ with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU], acc_event
         marks.append((e0, e1))
         ctx.synchronize()
     torch.cuda.synchronize()
-ev = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
+# kernels with their host launch time: the chrome trace links each kernel to its runtime /
+# driver launch call by correlation id (same time base)
+import tempfile  # noqa: E402
+with tempfile.NamedTemporaryFile(suffix=".json") as tf:
+    prof.export_chrome_trace(tf.name)
+    trace = json.load(open(tf.name))["traceEvents"]
+api = {}
+for e in trace:
+    if e.get("cat") in ("cuda_runtime", "cuda_driver") and "correlation" in e.get("args", {}):
+        api[e["args"]["correlation"]] = e["ts"]
 kern = []
-for e in ev:
-    tr = e.time_range
-    kern.append({"name": e.name, "start": tr.start, "end": tr.end, "stream": getattr(e, "device_resource_id", 0)})
+for e in trace:
+    if e.get("cat") in ("kernel", "gpu_memcpy", "gpu_memset"):
+        c = e.get("args", {}).get("correlation")
+        kern.append({"name": e["name"], "start": e["ts"], "end": e["ts"] + e.get("dur", 0),
+                     "stream": e.get("args", {}).get("stream", e.get("tid", 0)), "launch": api.get(c)})
 kern.sort(key=lambda k: k["start"])
 # split into forwards: the first kernel of each forward is k_convert_rows or the first map kernel; use gaps > 200 us
 fw, cur = [], []
@@ -106,6 +117,7 @@ for i, f_ in enumerate(fw):
                         for g_ in sorted(gaps, reverse=True)[:12]],
            "conv_stream_kernels_us": dict(sorted(names.items(), key=lambda kv: -kv[1]))}
     rec["first_kernels"] = [{"t0": round(k["start"] - t0, 1), "t1": round(k["end"] - t0, 1), "stream": k["stream"],
+                             "launch": round(k["launch"] - t0, 1) if k.get("launch") is not None else None,
                              "name": k["name"].replace("(anonymous namespace)::", "").replace("sconvb::", "").split("(")[0][-48:]} for k in sorted(f_, key=lambda k: k["start"])[:60]]
     out.append(rec)
     print(f"forward {i}: span {rec['span_us']:.1f} us, {len(f_)} launches, conv stream busy "
@@ -117,9 +129,10 @@ if out:
     print("kernel totals of the last forward (all streams):")
     for n, v in out[-1]["all_kernels"].items():
         print(f"  {n:44s} {v['launches']:3d} {v['us']:8.1f} us")
-    print("timeline of the last forward (first 60 kernels): t0 t1 stream name")
+    print("timeline of the last forward (first 60 kernels): t0 t1 stream host-launch name")
     for k in out[-1]["first_kernels"]:
-        print(f"  {k['t0']:8.1f} {k['t1']:8.1f} {k['stream']:4d} {k['name']}")
+        la = f"{k['launch']:8.1f}" if k["launch"] is not None else "       -"
+        print(f"  {k['t0']:8.1f} {k['t1']:8.1f} {k['stream']:4d} {la} {k['name']}")
 for i, (e0, e1) in enumerate(marks):
     print(f"forward {i} event time {e0.elapsed_time(e1) * 1e3:.1f} us")
 if a.json:
