@@ -39,6 +39,15 @@ ms = sc.KernelMap.build(ctx, xyz, False, 2, 1, 2)  # strided K=2 s=2
 ms.read()
 mh = sc.KernelMap.build(ctx, xyz, False, 3, 1, 1, backend=sc.MAP_HASH)
 mh.read()
+# column search on chunks with scattered targets (skip-ahead slices + the direct global path):
+# a sparse slice between two dense wall planes (tests/test_gpu_parity.py::test_map_scattered_chunks)
+yy, zz = np.meshgrid(np.arange(200), np.arange(64), indexing="ij")
+wall = lambda x: np.stack([np.full(yy.size, x), yy.ravel(), zz.ravel()], 1)  # noqa: E731
+rg = np.random.default_rng(214)
+mid = np.stack([np.ones(128, np.int64), np.sort(rg.choice(200, 128, replace=False)), rg.integers(0, 64, 128)], 1)
+walls = np.concatenate([wall(0), mid, wall(2)]).astype(np.int32)
+walls = walls[np.lexsort((walls[:, 2], walls[:, 1], walls[:, 0]))]
+sc.KernelMap.build(ctx, walls, True, 3, 1, 1).read()
 ctx.synchronize()
 if a.net:
     coords, feats = D.kitti_scan(0, n_azimuth=120)
