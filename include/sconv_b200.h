@@ -256,6 +256,14 @@ sconv_status sconv_net_tensor_device(const sconv_net* net, int tensor, const voi
  * runs); host destination: synchronous. */
 sconv_status sconv_net_copy_tensor(sconv_ctx* ctx, const sconv_net* net, int tensor, void* dst, int dst_dtype,
                                    int dst_mem);
+/* Asynchronous host readback of a tensor's fp32 features (the serving form of
+ * sconv_net_read_tensor's feature half): the widening runs on the context stream into one of two
+ * net-owned device staging buffers, the device->host copy on the net's own copy stream, so the
+ * copy of forward i's result overlaps forward i+1's kernels. `feats` (n x channels fp32, pinned
+ * for a truly asynchronous copy) must stay untouched until sconv_net_read_wait returns. */
+sconv_status sconv_net_read_async(sconv_ctx* ctx, sconv_net* net, int tensor, float* feats);
+/* Blocks until every sconv_net_read_async of this net has landed in host memory. */
+sconv_status sconv_net_read_wait(sconv_ctx* ctx, sconv_net* net);
 sconv_status sconv_net_stats(const sconv_net* net, int* maps_built, int* convs);
 /* Coordinate-array sorts of the last forward: 1 for an unsorted input (0 when flagged sorted)
  * plus one Eq. 1 sort per distinct strided map; stride-1 layers reuse the sorted keys

@@ -811,14 +811,17 @@ sconv_status sconv_net_forward(sconv_ctx* ctx, sconv_net* net, const int32_t* xy
     P.n = n;
     P.mem = mem;
     P.sorted = in_sorted != 0;
-    // host coordinates must outlive the asynchronous forward: stage them on device
-    DevBuf staged;
+    // host inputs must outlive the asynchronous forward: staged on device by the net's input
+    // stream (double-buffered), so the copy and the map builds need not wait for the previous
+    // forward's convs on the context stream
     if (mem == SCONV_MEM_HOST && n > 0) {
-      staged.alloc(sizeof(int32_t) * 3 * n, ctx->stream);
-      SCONV_CUDA(cudaMemcpyAsync(staged.get(), xyz, sizeof(int32_t) * 3 * n, cudaMemcpyHostToDevice, ctx->stream));
-      net->input_xyz = std::move(staged);
-      P.xyz = net->input_xyz.get<int32_t>();
+      const int32_t* xd = nullptr;
+      const float* fd = nullptr;
+      net->stage_host_inputs(xyz, n, feats, f_mem, c_in, &xd, &fd);
+      P.xyz = xd;
       P.mem = SCONV_MEM_DEVICE;
+      feats = fd;
+      f_mem = SCONV_MEM_DEVICE;
     }
     net->forward(*ctx, P, feats, SCONV_F32, f_mem, c_in);
   });
@@ -886,6 +889,54 @@ sconv_status sconv_net_copy_tensor(sconv_ctx* ctx, const sconv_net* net, int ten
     convert_rows(*ctx, t.feats.get(), t.dtype, t.n, t.channels, t.ld, n->readback.get(), dst_dtype, t.channels);
     SCONV_CUDA(cudaMemcpyAsync(dst, n->readback.get(), bytes, cudaMemcpyDeviceToHost, ctx->stream));
     ctx->sync();
+  });
+}
+
+sconv_status sconv_net_read_async(sconv_ctx* ctx, sconv_net* net, int tensor, float* feats) {
+  return guarded(ctx, [&] {
+    if (!net || tensor < 0 || tensor >= static_cast<int>(net->tensors.size())) fail(SCONV_ERR_ARG, "bad tensor");
+    const NetTensor& t = net->tensors[tensor];
+    if (t.fused_away) fail(SCONV_ERR_STATE, "tensor was folded into a fused residual epilogue");
+    if (t.coordset < 0) fail(SCONV_ERR_STATE, "tensor not produced");
+    if (t.n == 0) return;
+    if (!feats) fail(SCONV_ERR_ARG, "null argument");
+    if (!net->copy_stream) {
+      SCONV_CUDA(cudaStreamCreateWithFlags(&net->copy_stream, cudaStreamNonBlocking));
+      for (int s = 0; s < 2; ++s) {
+        SCONV_CUDA(cudaEventCreateWithFlags(&net->rb_ready[s], cudaEventDisableTiming));
+        SCONV_CUDA(cudaEventCreateWithFlags(&net->rb_done[s], cudaEventDisableTiming));
+      }
+    }
+    const int s = net->rb_slot;
+    net->rb_slot ^= 1;
+    const size_t bytes = sizeof(float) * static_cast<size_t>(t.n) * t.channels;
+    // the slot's previous copy must have left the staging buffer before it is rewritten (or
+    // regrown: the old buffer's free is ordered on the context stream)
+    if (net->rb_pending[s]) SCONV_CUDA(cudaStreamWaitEvent(ctx->stream, net->rb_done[s], 0));
+    net->rb_async[s].reserve(bytes, ctx->stream);
+    convert_rows(*ctx, t.feats.get(), t.dtype, t.n, t.channels, t.ld, net->rb_async[s].get(), SCONV_F32, t.channels);
+    SCONV_CUDA(cudaEventRecord(net->rb_ready[s], ctx->stream));
+    SCONV_CUDA(cudaStreamWaitEvent(net->copy_stream, net->rb_ready[s], 0));
+    // in 2 MB chunks: the copy engine is FIFO across streams, so a whole-result copy (C2:
+    // 45.7 MB = 0.87 ms) holds back the next request's input H2D queued behind it (same box
+    // r02ch: C2 pipelined e2e 2.26 ms with 2 MB chunks vs 2.40 one copy / 8 MB; C3 1.30 vs
+    // 1.32); the small map readbacks avoid the engine altogether (map.cu d2h_small).
+    static const size_t chunk = [] {
+      const char* e = std::getenv("SCONV_RB_CHUNK_KB");
+      return static_cast<size_t>(e ? std::max(64, std::atoi(e)) : 2048) << 10;
+    }();
+    for (size_t off = 0; off < bytes; off += chunk)
+      SCONV_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(feats) + off, net->rb_async[s].get<char>() + off,
+                                 std::min(chunk, bytes - off), cudaMemcpyDeviceToHost, net->copy_stream));
+    SCONV_CUDA(cudaEventRecord(net->rb_done[s], net->copy_stream));
+    net->rb_pending[s] = true;
+  });
+}
+
+sconv_status sconv_net_read_wait(sconv_ctx* ctx, sconv_net* net) {
+  return guarded(ctx, [&] {
+    if (!net) fail(SCONV_ERR_ARG, "null argument");
+    if (net->copy_stream) SCONV_CUDA(cudaStreamSynchronize(net->copy_stream));
   });
 }
 

@@ -29,6 +29,31 @@
 namespace sconvb {
 namespace {
 
+// Small device->host readbacks (map flags, |Q|, list starts) the host syncs on: stored by a
+// one-warp kernel straight into the mapped pinned destination instead of a copy-engine memcpy,
+// so they never queue behind a large result copy on the device->host engine (a serving loop's
+// sconv_net_read_async of the previous forward: r02cc, C2 next forward's first conv +0.45 ms).
+__global__ void k_d2h_small(const unsigned* __restrict__ src, unsigned* dst, int words) {
+  for (int i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
+}
+
+void d2h_small(void* host_pinned, const void* dev, size_t bytes, cudaStream_t st) {
+  static const bool use_kernel = [] {
+    const char* e = std::getenv("SCONV_D2H_SMALL_KERNEL");
+    return !(e && e[0] == '0');
+  }();
+  void* dptr = nullptr;
+  if (use_kernel && bytes % 4 == 0 && reinterpret_cast<uintptr_t>(dev) % 4 == 0 &&
+      reinterpret_cast<uintptr_t>(host_pinned) % 4 == 0 && cudaHostGetDevicePointer(&dptr, host_pinned, 0) == cudaSuccess) {
+    k_d2h_small<<<1, 32, 0, st>>>(static_cast<const unsigned*>(dev), static_cast<unsigned*>(dptr),
+                                  static_cast<int>(bytes / 4));
+    SCONV_CUDA(cudaGetLastError());
+    return;
+  }
+  (void)cudaGetLastError();  // a non-mapped destination: plain copy
+  SCONV_CUDA(cudaMemcpyAsync(host_pinned, dev, bytes, cudaMemcpyDeviceToHost, st));
+}
+
 struct MapFlags {
   unsigned long long bad_coord;   // min over (index * 3 + axis) of out-of-range components of P
   unsigned long long bad_target;  // same for the transposed target list
@@ -1731,13 +1756,12 @@ void read_starts(Ctx& ctx, MapData& m, const void* flags, MapFlags* f) {
   if (sizeof(MapFlags) + sizeof(int32_t) * (K3 + 1) > Ctx::kPinReadbackBytes) fail(SCONV_ERR_ARG, "kernel too large");
   auto* pin2 = static_cast<unsigned char*>(ctx.pin_readback());
   if (flags) {
-    SCONV_CUDA(cudaMemcpyAsync(pin2, flags, sizeof(MapFlags), cudaMemcpyDeviceToHost, ctx.stream));
+    d2h_small(pin2, flags, sizeof(MapFlags), ctx.stream);
   } else {  // lazy map over validated keys: its flags were never initialised (nothing to check)
     std::memset(pin2, 0, sizeof(MapFlags));
     std::memset(pin2, 0xFF, 3 * sizeof(unsigned long long));
   }
-  SCONV_CUDA(cudaMemcpyAsync(pin2 + sizeof(MapFlags), m.map_start.get(), sizeof(int32_t) * (K3 + 1),
-                             cudaMemcpyDeviceToHost, ctx.stream));
+  d2h_small(pin2 + sizeof(MapFlags), m.map_start.get(), sizeof(int32_t) * (K3 + 1), ctx.stream);
   ctx.sync();
   std::memcpy(f, pin2, sizeof(MapFlags));
   m.starts.resize(K3 + 1);
@@ -1773,8 +1797,8 @@ void ensure_canonical(Ctx& ctx, MapData& m) {
 bool finish_coords(Ctx& ctx, MapData& m) {
   if (m.n_out >= 0) return true;
   auto* pin = reinterpret_cast<MapFlags*>(ctx.pin_flags());
-  SCONV_CUDA(cudaMemcpyAsync(pin, m.pending.flags.get(), sizeof(MapFlags), cudaMemcpyDeviceToHost, ctx.stream));
-  SCONV_CUDA(cudaMemcpyAsync(&pin[1], m.pend_nsel.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, ctx.stream));
+  d2h_small(pin, m.pending.flags.get(), sizeof(MapFlags), ctx.stream);
+  d2h_small(&pin[1], m.pend_nsel.get(), sizeof(int64_t), ctx.stream);
   ctx.sync();
   const MapFlags f = pin[0];
   if (f.fwide || f.wide || f.big_bucket) return false;  // the caller rebuilds with the exact path
@@ -2113,8 +2137,8 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
     if (f.target_unsorted) fail(SCONV_ERR_ARG, "query coordinates must be sorted and unique");
   };
   if (need_nout_sync) {
-    SCONV_CUDA(cudaMemcpyAsync(pin, flags, sizeof(MapFlags), cudaMemcpyDeviceToHost, st));
-    SCONV_CUDA(cudaMemcpyAsync(&pin[1], nsel.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    d2h_small(pin, flags, sizeof(MapFlags), st);
+    d2h_small(&pin[1], nsel.get(), sizeof(int64_t), st);
     static_assert(2 * sizeof(MapFlags) <= Ctx::kPinFlagsBytes, "pinned flags region");
     ctx.sync();
     // the input sort's compact key was too wide: P's keys are not valid yet, so nothing derived
@@ -2123,7 +2147,7 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
     check_flags(pin[0]);
     if (pin[0].fwide && strided_wide) {  // rare: redo the output coordinates with 64-bit keys
       strided_wide();
-      SCONV_CUDA(cudaMemcpyAsync(&pin[1], nsel.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+      d2h_small(&pin[1], nsel.get(), sizeof(int64_t), st);
       ctx.sync();
     }
     int64_t nout;
@@ -2366,7 +2390,7 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
   }
   if (defer_canonical && defer_flags && P.sorted && !P.keys && !target && !need_nout_sync) {
     // sorted raw coordinates: only range / order flags, no fallback -> checked by the caller
-    SCONV_CUDA(cudaMemcpyAsync(defer_flags, flags, sizeof(MapFlags), cudaMemcpyDeviceToHost, st));
+    d2h_small(defer_flags, flags, sizeof(MapFlags), st);
     m->flags_deferred = true;
     m->canonical = false;
     m->total = -1;
@@ -2375,7 +2399,7 @@ std::unique_ptr<MapData> build_map(Ctx& ctx, const MapSource& P, const sconv_map
     return m;
   }
   if (defer_canonical) {  // flags only (one sync), canonical lists on demand
-    SCONV_CUDA(cudaMemcpyAsync(pin, flags, sizeof(MapFlags), cudaMemcpyDeviceToHost, st));
+    d2h_small(pin, flags, sizeof(MapFlags), st);
     ctx.sync();
     const MapFlags f = pin[0];
     if (!force_wide && (f.wide || f.big_bucket)) return build_map(ctx, P, cfg, target, true, true);  // exact fallback

@@ -189,7 +189,13 @@ NetData::~NetData() {
   coordsets.clear();
   tensors.clear();
   pre_coords.clear();
-  for (cudaStream_t* sp : {&map_stream, &layout_stream, &coord_stream})
+  // input staging lives on in_stream: released (stream-ordered) before that stream is destroyed;
+  // in-flight async reads still copy out of rb_async (context stream, freed after this body)
+  for (int s = 0; s < 2; ++s) {
+    in_xyz[s].release();
+    in_feats[s].release();
+  }
+  for (cudaStream_t* sp : {&map_stream, &layout_stream, &coord_stream, &copy_stream, &in_stream})
     if (*sp) {
       cudaStreamSynchronize(*sp);
       cudaStreamDestroy(*sp);
@@ -197,6 +203,41 @@ NetData::~NetData() {
   if (ev_order) cudaEventDestroy(ev_order);
   if (ev_flags) cudaEventDestroy(ev_flags);
   if (ev_coords) cudaEventDestroy(ev_coords);
+  for (int s = 0; s < 2; ++s) {
+    if (rb_ready[s]) cudaEventDestroy(rb_ready[s]);
+    if (rb_done[s]) cudaEventDestroy(rb_done[s]);
+    if (in_ready[s]) cudaEventDestroy(in_ready[s]);
+    if (in_free[s]) cudaEventDestroy(in_free[s]);
+  }
+  if (ev_prev) cudaEventDestroy(ev_prev);
+}
+
+void NetData::stage_host_inputs(const int32_t* xyz, int64_t n, const float* feats, int f_mem, int c_in,
+                                const int32_t** xyz_dev, const float** feats_dev) {
+  if (!in_stream) {
+    SCONV_CUDA(cudaStreamCreateWithFlags(&in_stream, cudaStreamNonBlocking));
+    for (int s = 0; s < 2; ++s) {
+      SCONV_CUDA(cudaEventCreateWithFlags(&in_ready[s], cudaEventDisableTiming));
+      SCONV_CUDA(cudaEventCreateWithFlags(&in_free[s], cudaEventDisableTiming));
+    }
+  }
+  const int s = in_slot;
+  in_slot ^= 1;
+  // the forward that read this slot last must be done with it (its end on the context stream)
+  if (in_used[s]) SCONV_CUDA(cudaStreamWaitEvent(in_stream, in_free[s], 0));
+  in_xyz[s].reserve(std::max<size_t>(sizeof(int32_t) * 3 * n, 16), in_stream);
+  SCONV_CUDA(cudaMemcpyAsync(in_xyz[s].get(), xyz, sizeof(int32_t) * 3 * n, cudaMemcpyHostToDevice, in_stream));
+  *xyz_dev = in_xyz[s].get<int32_t>();
+  if (f_mem == SCONV_MEM_HOST) {
+    in_feats[s].reserve(std::max<size_t>(sizeof(float) * n * c_in, 16), in_stream);
+    SCONV_CUDA(cudaMemcpyAsync(in_feats[s].get(), feats, sizeof(float) * n * c_in, cudaMemcpyHostToDevice, in_stream));
+    *feats_dev = in_feats[s].get<float>();
+  } else {
+    *feats_dev = feats;
+  }
+  SCONV_CUDA(cudaEventRecord(in_ready[s], in_stream));
+  in_used[s] = true;
+  staged_slot = s;
 }
 
 void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f_dtype, int f_mem, int c_in) {
@@ -274,11 +315,19 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
   // the map stream starts after everything already on the context stream: the input
   // coordinates may be produced there, and the previous forward's maps (freed below, on the
   // map stream) may still be in use by its convs
+  // Host inputs staged on in_stream (sconv_net_forward): nothing on the context stream produces
+  // them, so the map streams wait only for their copy and start beside the previous forward's
+  // convs; the previous forward's maps are then released only after ev_prev (below).
+  const int in_s = staged_slot;
+  staged_slot = -1;
+  if (!ev_prev) SCONV_CUDA(cudaEventCreateWithFlags(&ev_prev, cudaEventDisableTiming));
+  SCONV_CUDA(cudaEventRecord(ev_prev, st));
+  if (in_s >= 0) SCONV_CUDA(cudaStreamWaitEvent(st, in_ready[in_s], 0));
   if (ms != st) {
-    SCONV_CUDA(cudaEventRecord(ev_order, st));
-    SCONV_CUDA(cudaStreamWaitEvent(ms, ev_order));
-    SCONV_CUDA(cudaStreamWaitEvent(ls, ev_order));
-    if (cst) SCONV_CUDA(cudaStreamWaitEvent(cst, ev_order));
+    cudaEvent_t start = in_s >= 0 ? in_ready[in_s] : ev_prev;
+    SCONV_CUDA(cudaStreamWaitEvent(ms, start));
+    SCONV_CUDA(cudaStreamWaitEvent(ls, start));
+    if (cst) SCONV_CUDA(cudaStreamWaitEvent(cst, start));
   }
   hmark(-1, "forward: streams joined");
   if (!planned) {
@@ -291,7 +340,9 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
     t.coordset = -1;
     t.fused_away = false;
   }
-  coordsets.clear();
+  // (released with the previous forward's maps at the end: its convs may still run)
+  std::vector<CoordSet> old_coordsets;
+  old_coordsets.swap(coordsets);
   // the previous forward's maps are freed at the END of this forward: ~180 stream-ordered
   // frees here would delay the first launches by ~80 us of host time (the GPU idles then)
   std::map<MapKey, MapEntry> old_maps;
@@ -711,7 +762,14 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
     SCONV_CUDA(cudaEventRecord(ev_order, ls));
     SCONV_CUDA(cudaStreamWaitEvent(st, ev_order));
   }
-  old_maps.clear();  // frees enqueued behind this forward's work on the map / layout streams
+  // frees enqueued behind this forward's work on the map / layout / coordinate streams, and
+  // behind the previous forward's convs (ev_prev: those streams may have started before them)
+  if (ms != st)
+    for (cudaStream_t s : {ms, ls, cst})
+      if (s) SCONV_CUDA(cudaStreamWaitEvent(s, ev_prev));
+  old_maps.clear();
+  old_coordsets.clear();
+  if (in_s >= 0) SCONV_CUDA(cudaEventRecord(in_free[in_s], st));
   if (deferred_flags) {  // the copy was queued right after the input's key packing: long done
     SCONV_CUDA(cudaEventSynchronize(ev_flags));
     check_deferred_map_flags(deferred_flags, raw_input);

@@ -80,6 +80,29 @@ struct NetData {
   bool planned = false;
   std::vector<std::array<double, 2>> auto_ms;  // per op: GMaS / fused ms of the tuning forward
   DevBuf readback;  // f32 staging for host reads
+  // asynchronous host reads (sconv_net_read_async): two staging buffers alternate; the D2H copy
+  // of slot s runs on copy_stream after rb_ready[s]; rb_done[s] guards the slot's next widening
+  // (and any regrowth, whose free is ordered on the context stream)
+  DevBuf rb_async[2];
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t rb_ready[2] = {nullptr, nullptr}, rb_done[2] = {nullptr, nullptr};
+  bool rb_pending[2] = {false, false};
+  int rb_slot = 0;
+  // host inputs (sconv_net_forward with host pointers) are copied on in_stream into one of two
+  // staging slots, independent of the context stream: the next request's H2D and its map builds
+  // (which wait for in_ready instead of everything on the context stream) overlap the previous
+  // forward's convs. in_free[s] (end of the forward that read slot s) guards the slot's reuse.
+  DevBuf in_xyz[2], in_feats[2];
+  cudaStream_t in_stream = nullptr;
+  cudaEvent_t in_ready[2] = {nullptr, nullptr}, in_free[2] = {nullptr, nullptr};
+  cudaEvent_t ev_prev = nullptr;  // context stream at the start of a forward (the previous one's end)
+  bool in_used[2] = {false, false};
+  int in_slot = 0;
+  int staged_slot = -1;  // slot of the inputs staged for the next forward (-1: none)
+  // copies host coordinates (n x 3) and, for f_mem == host, features (n x c_in fp32) into the
+  // next staging slot; returns their device pointers
+  void stage_host_inputs(const int32_t* xyz, int64_t n, const float* feats, int f_mem, int c_in,
+                         const int32_t** xyz_dev, const float** feats_dev);
   // per CONV op of the last forward: n_in, n_out, |M|, R_pad (0 when fused), c_in, c_out, k_pad, K3,
   // dataflow, residual folded (0/1)
   std::vector<std::array<int64_t, 10>> conv_stats;

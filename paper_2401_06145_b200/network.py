@@ -80,6 +80,19 @@ class Network:
                                                           S._ptr(f)))
         return xyz, f
 
+    def read_async(self, t, feats_out: np.ndarray):
+        """Queues the fp32 features of tensor t into feats_out (pinned for an asynchronous copy)
+        without waiting: the device->host copy runs on the net's copy stream beside the next
+        forward (sconv_net_read_async). feats_out is valid after wait_reads()."""
+        n, ch, _ = self.info(t)
+        if feats_out.shape != (n, ch) or feats_out.dtype != np.float32 or not feats_out.flags.c_contiguous:
+            raise ValueError("feats_out must be a contiguous float32 array of shape (n, channels)")
+        self.ctx.check(self.ctx.lib.sconv_net_read_async(self.ctx.h, self.h, t, S._ptr(feats_out)))
+
+    def wait_reads(self):
+        """Blocks until every read_async of this network has landed (sconv_net_read_wait)."""
+        self.ctx.check(self.ctx.lib.sconv_net_read_wait(self.ctx.h, self.h))
+
     def device_output(self):
         """(pointer, dtype, row stride) of the output tensor on device."""
         p, dt, ld = C.c_void_p(), C.c_int(), C.c_int64()

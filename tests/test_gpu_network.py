@@ -191,3 +191,30 @@ def test_batched_clouds_match_individual(ctx):
         _, fo = one.read(g.output)
         np.testing.assert_allclose(fb[a:b], fo, rtol=0, atol=1e-6 * max(np.abs(fo).max(), 1e-30))
 
+
+
+def test_read_async_pipelined(ctx):
+    """sconv_net_read_async: results of back-to-back forwards on different scans, each read back
+    while the next forward runs (two staging slots, three scans so a slot is reused), equal the
+    synchronous sconv_net_read_tensor results bit for bit; a folded tensor / bad id fail loudly."""
+    import torch
+    g = N.minkunet42()
+    w = N.init_weights(g, 1)
+    net = N.Network(ctx, g, w)
+    scans = [D.kitti_scan(s, n_azimuth=200) for s in (4, 5, 6)]
+    want = []
+    for c, f in scans:
+        net.forward(c, f)
+        want.append(net.read(g.output)[1])
+    got = []
+    for c, f in scans:
+        net.forward(c, f)
+        n, ch, _ = net.info(g.output)
+        buf = torch.empty((n, ch), dtype=torch.float32, pin_memory=True).numpy()
+        net.read_async(g.output, buf)
+        got.append(buf)
+    net.wait_reads()
+    for a, b in zip(want, got):
+        np.testing.assert_array_equal(a, b)
+    with pytest.raises(sc.InvalidArgument):
+        net.read_async(10 ** 6, got[0])
