@@ -241,6 +241,13 @@ sconv_status sconv_net_set_weights(sconv_ctx* ctx, sconv_net* net, int weight_id
  * from one sync per distinct kernel map. */
 sconv_status sconv_net_forward(sconv_ctx* ctx, sconv_net* net, const int32_t* xyz, int64_t n, int mem, int in_sorted,
                                const float* feats, int f_mem, int c_in);
+/* Queues the host->device copy of the NEXT request's host inputs (coordinates n x 3 int32, fp32
+ * features n x c_in; f_mem host or device) on the net's input stream now, so that it overlaps
+ * the current request's forward; the sconv_net_forward call with the same pointers, n, f_mem
+ * and c_in then uses the staged copy (one pending prefetch; the host buffers must not change
+ * before that forward). */
+sconv_status sconv_net_prefetch_inputs(sconv_ctx* ctx, sconv_net* net, const int32_t* xyz, int64_t n,
+                                       const float* feats, int f_mem, int c_in);
 sconv_status sconv_net_tensor_info(sconv_ctx* ctx, const sconv_net* net, int tensor, int64_t* n, int* channels,
                                    int* coordset);
 /* Host readback: coordinates (n x 3, sorted unless the tensor is the unsorted raw input) and fp32

@@ -817,13 +817,37 @@ sconv_status sconv_net_forward(sconv_ctx* ctx, sconv_net* net, const int32_t* xy
     if (mem == SCONV_MEM_HOST && n > 0) {
       const int32_t* xd = nullptr;
       const float* fd = nullptr;
-      net->stage_host_inputs(xyz, n, feats, f_mem, c_in, &xd, &fd);
+      auto& pf = net->prefetch;
+      if (pf.slot >= 0 && pf.xyz == xyz && pf.feats == feats && pf.n == n && pf.f_mem == f_mem && pf.c_in == c_in) {
+        net->staged_slot = pf.slot;  // copied by sconv_net_prefetch_inputs
+        xd = pf.xyz_dev;
+        fd = pf.feats_dev;
+      } else {
+        net->stage_host_inputs(xyz, n, feats, f_mem, c_in, &xd, &fd);
+      }
+      pf.slot = -1;
       P.xyz = xd;
       P.mem = SCONV_MEM_DEVICE;
       feats = fd;
       f_mem = SCONV_MEM_DEVICE;
     }
     net->forward(*ctx, P, feats, SCONV_F32, f_mem, c_in);
+  });
+}
+
+sconv_status sconv_net_prefetch_inputs(sconv_ctx* ctx, sconv_net* net, const int32_t* xyz, int64_t n,
+                                       const float* feats, int f_mem, int c_in) {
+  return guarded(ctx, [&] {
+    if (!net || n <= 0 || !xyz || !feats) fail(SCONV_ERR_ARG, "null argument");
+    auto& pf = net->prefetch;
+    net->stage_host_inputs(xyz, n, feats, f_mem, c_in, &pf.xyz_dev, &pf.feats_dev);
+    pf.slot = net->staged_slot;
+    net->staged_slot = -1;  // consumed by the matching sconv_net_forward only
+    pf.xyz = xyz;
+    pf.feats = feats;
+    pf.n = n;
+    pf.f_mem = f_mem;
+    pf.c_in = c_in;
   });
 }
 

@@ -223,6 +223,7 @@ void NetData::stage_host_inputs(const int32_t* xyz, int64_t n, const float* feat
   }
   const int s = in_slot;
   in_slot ^= 1;
+  if (prefetch.slot == s) prefetch.slot = -1;  // a pending prefetch in this slot is overwritten
   // the forward that read this slot last must be done with it (its end on the context stream)
   if (in_used[s]) SCONV_CUDA(cudaStreamWaitEvent(in_stream, in_free[s], 0));
   in_xyz[s].reserve(std::max<size_t>(sizeof(int32_t) * 3 * n, 16), in_stream);

@@ -99,6 +99,16 @@ struct NetData {
   bool in_used[2] = {false, false};
   int in_slot = 0;
   int staged_slot = -1;  // slot of the inputs staged for the next forward (-1: none)
+  // sconv_net_prefetch_inputs: host inputs copied ahead of their forward (one pending prefetch,
+  // matched by pointers / sizes when sconv_net_forward is called with them)
+  struct Prefetch {
+    int slot = -1;
+    const void *xyz = nullptr, *feats = nullptr;
+    int64_t n = 0;
+    int f_mem = 0, c_in = 0;
+    const int32_t* xyz_dev = nullptr;
+    const float* feats_dev = nullptr;
+  } prefetch;
   // copies host coordinates (n x 3) and, for f_mem == host, features (n x c_in fp32) into the
   // next staging slot; returns their device pointers
   void stage_host_inputs(const int32_t* xyz, int64_t n, const float* feats, int f_mem, int c_in,

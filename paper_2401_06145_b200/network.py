@@ -89,6 +89,16 @@ class Network:
             raise ValueError("feats_out must be a contiguous float32 array of shape (n, channels)")
         self.ctx.check(self.ctx.lib.sconv_net_read_async(self.ctx.h, self.h, t, S._ptr(feats_out)))
 
+    def prefetch(self, coords, feats):
+        """Queues the host->device copy of the NEXT forward's host inputs now (it overlaps the
+        current forward); forward() with the same arrays then uses the staged copy
+        (sconv_net_prefetch_inputs). The arrays must stay unchanged until that forward."""
+        if coords.dtype != np.int32 or feats.dtype != np.float32 or not coords.flags.c_contiguous \
+                or not feats.flags.c_contiguous:
+            raise ValueError("prefetch needs contiguous int32 coordinates and float32 features")
+        self.ctx.check(self.ctx.lib.sconv_net_prefetch_inputs(self.ctx.h, self.h, S._ptr(coords), len(coords),
+                                                              S._ptr(feats), S.MEM_HOST, feats.shape[1]))
+
     def wait_reads(self):
         """Blocks until every read_async of this network has landed (sconv_net_read_wait)."""
         self.ctx.check(self.ctx.lib.sconv_net_read_wait(self.ctx.h, self.h))

@@ -118,6 +118,7 @@ SIGNATURES = [
     ("sconv_net_tensor_device", _I, [_P, _I, C.POINTER(_P), C.POINTER(_I), C.POINTER(_I64)]),
     ("sconv_net_copy_tensor", _I, [_P, _P, _I, _P, _I, _I]),
     ("sconv_net_read_async", _I, [_P, _P, _I, _P]),
+    ("sconv_net_prefetch_inputs", _I, [_P, _P, _P, _I64, _P, _I, _I]),
     ("sconv_net_read_wait", _I, [_P, _P]),
     ("sconv_net_sort_count", _I, [_P, C.POINTER(_I64)]),
     ("sconv_net_conv_timings", _I, [_P, _I, C.POINTER(_D), C.POINTER(_D)]),

@@ -55,6 +55,22 @@ if a.net:
     net = N.Network(ctx, g, N.init_weights(g, 5), sc.exec_cfg(dataflow=sc.DATAFLOW_FUSED))
     net.forward(coords, feats, True)
     net.forward(coords, feats, True)
+    # serving loop: host inputs staged on the net's input stream, results read back
+    # asynchronously while the next forward runs (two staging slots each, so both are reused)
+    import torch
+    scans = [D.kitti_scan(s, n_azimuth=120) for s in (1, 2, 3)]
+    outs = []
+    for i, (c, f) in enumerate(scans + scans):
+        net.forward(c, f, True)
+        n, ch, _ = net.info(g.output)
+        outs.append(torch.empty((n, ch), dtype=torch.float32, pin_memory=True).numpy())
+        if i:
+            net.wait_reads()
+        net.read_async(g.output, outs[-1])
+    net.wait_reads()
+    for i in range(3):
+        assert np.array_equal(outs[i], outs[i + 3]), "serving loop results differ between rounds"
+    net.free()
     ctx.synchronize()
 ctx.close()
 print("sanitize run ok")

@@ -194,9 +194,10 @@ def test_batched_clouds_match_individual(ctx):
 
 
 def test_read_async_pipelined(ctx):
-    """sconv_net_read_async: results of back-to-back forwards on different scans, each read back
-    while the next forward runs (two staging slots, three scans so a slot is reused), equal the
-    synchronous sconv_net_read_tensor results bit for bit; a folded tensor / bad id fail loudly."""
+    """sconv_net_read_async + sconv_net_prefetch_inputs: back-to-back forwards on different scans,
+    each one's inputs staged while the previous forward runs and its result read back while the
+    next runs (two staging slots each, reused), equal the synchronous results bit for bit; a
+    non-matching prefetch is ignored; a bad tensor id fails loudly."""
     import torch
     g = N.minkunet42()
     w = N.init_weights(g, 1)
@@ -206,15 +207,25 @@ def test_read_async_pipelined(ctx):
     for c, f in scans:
         net.forward(c, f)
         want.append(net.read(g.output)[1])
+    pinned = [(torch.from_numpy(c).pin_memory().numpy(), torch.from_numpy(f).pin_memory().numpy()) for c, f in scans]
+    order = [0, 1, 2, 0, 2, 1]
     got = []
-    for c, f in scans:
-        net.forward(c, f)
+    for r, i in enumerate(order):
+        net.forward(*pinned[i])
+        if r + 1 < len(order):  # next request's inputs staged beside this forward
+            net.prefetch(*pinned[order[r + 1]])
         n, ch, _ = net.info(g.output)
         buf = torch.empty((n, ch), dtype=torch.float32, pin_memory=True).numpy()
         net.read_async(g.output, buf)
         got.append(buf)
     net.wait_reads()
-    for a, b in zip(want, got):
-        np.testing.assert_array_equal(a, b)
+    for i, b in zip(order, got):
+        np.testing.assert_array_equal(want[i], b)
+    # a prefetch that the next forward does not match is ignored (that forward stages its own)
+    net.prefetch(*pinned[0])
+    net.forward(*pinned[1])
+    np.testing.assert_array_equal(want[1], net.read(g.output)[1])
+    net.forward(*pinned[0])
+    np.testing.assert_array_equal(want[0], net.read(g.output)[1])
     with pytest.raises(sc.InvalidArgument):
         net.read_async(10 ** 6, got[0])
