@@ -941,14 +941,26 @@ sconv_status sconv_net_read_async(sconv_ctx* ctx, sconv_net* net, int tensor, fl
     convert_rows(*ctx, t.feats.get(), t.dtype, t.n, t.channels, t.ld, net->rb_async[s].get(), SCONV_F32, t.channels);
     SCONV_CUDA(cudaEventRecord(net->rb_ready[s], ctx->stream));
     SCONV_CUDA(cudaStreamWaitEvent(net->copy_stream, net->rb_ready[s], 0));
-    // in 2 MB chunks: the copy engine is FIFO across streams, so a whole-result copy (C2:
-    // 45.7 MB = 0.87 ms) holds back the next request's input H2D queued behind it (same box
-    // r02ch: C2 pipelined e2e 2.26 ms with 2 MB chunks vs 2.40 one copy / 8 MB; C3 1.30 vs
-    // 1.32); the small map readbacks avoid the engine altogether (map.cu d2h_small).
-    static const size_t chunk = [] {
+    // In chunks: the copy engine is FIFO across streams, so a whole-result copy (C2: 45.7 MB =
+    // 0.87 ms) holds back the next request's input H2D queued behind it (same box r02ch: C2
+    // pipelined e2e 2.26 ms with 2 MB chunks vs 2.40 one copy; r02cl / r02cm: 4 MB 2.27, 2 MB
+    // 2.26, 1 MB 2.21, 512 KB 2.17, 256 KB 2.23). Each chunk costs ~3.5 us of engine time, which
+    // only shows when the copy is the bottleneck (r02cn, C4: 25 MB per 0.19 ms forward, 0.83 ms
+    // with 2 MB chunks vs 1.00 with 512 KB): 512 KB chunks while the copy plus their overhead
+    // fits in the last forward's GPU span, else 4 MB. The small map readbacks avoid the engine
+    // altogether (map.cu d2h_small). SCONV_RB_CHUNK_KB forces a size.
+    static const long forced_kb = [] {
       const char* e = std::getenv("SCONV_RB_CHUNK_KB");
-      return static_cast<size_t>(e ? std::max(64, std::atoi(e)) : 2048) << 10;
+      return e ? std::max(64L, std::atol(e)) : 0L;
     }();
+    size_t chunk = size_t{512} << 10;
+    if (forced_kb) {
+      chunk = static_cast<size_t>(forced_kb) << 10;
+    } else if (net->last_fwd_ms >= 0.f) {
+      const double copy_ms = static_cast<double>(bytes) / 5.0e7;  // ~50 GB/s pinned D2H (r02cc)
+      const double overhead_ms = 0.0035 * static_cast<double>((bytes + chunk - 1) / chunk);
+      if (copy_ms + overhead_ms > 0.8 * net->last_fwd_ms) chunk = size_t{4} << 20;
+    }
     for (size_t off = 0; off < bytes; off += chunk)
       SCONV_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(feats) + off, net->rb_async[s].get<char>() + off,
                                  std::min(chunk, bytes - off), cudaMemcpyDeviceToHost, net->copy_stream));

@@ -210,6 +210,8 @@ NetData::~NetData() {
     if (in_free[s]) cudaEventDestroy(in_free[s]);
   }
   if (ev_prev) cudaEventDestroy(ev_prev);
+  if (fwd_t0) cudaEventDestroy(fwd_t0);
+  if (fwd_t1) cudaEventDestroy(fwd_t1);
 }
 
 void NetData::stage_host_inputs(const int32_t* xyz, int64_t n, const float* feats, int f_mem, int c_in,
@@ -323,7 +325,18 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
   staged_slot = -1;
   if (!ev_prev) SCONV_CUDA(cudaEventCreateWithFlags(&ev_prev, cudaEventDisableTiming));
   SCONV_CUDA(cudaEventRecord(ev_prev, st));
+  if (!fwd_t0) {
+    SCONV_CUDA(cudaEventCreate(&fwd_t0));
+    SCONV_CUDA(cudaEventCreate(&fwd_t1));
+  }
+  if (fwd_timed && cudaEventQuery(fwd_t1) == cudaSuccess) {  // the previous forward's span, if done
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, fwd_t0, fwd_t1) == cudaSuccess) last_fwd_ms = ms;
+  }
+  (void)cudaGetLastError();  // cudaEventQuery's cudaErrorNotReady is not an error here
+  fwd_timed = false;
   if (in_s >= 0) SCONV_CUDA(cudaStreamWaitEvent(st, in_ready[in_s], 0));
+  SCONV_CUDA(cudaEventRecord(fwd_t0, st));
   if (ms != st) {
     cudaEvent_t start = in_s >= 0 ? in_ready[in_s] : ev_prev;
     SCONV_CUDA(cudaStreamWaitEvent(ms, start));
@@ -771,6 +784,8 @@ void NetData::forward(Ctx& ctx, const MapSource& input, const void* feats, int f
   old_maps.clear();
   old_coordsets.clear();
   if (in_s >= 0) SCONV_CUDA(cudaEventRecord(in_free[in_s], st));
+  SCONV_CUDA(cudaEventRecord(fwd_t1, st));
+  fwd_timed = true;
   if (deferred_flags) {  // the copy was queued right after the input's key packing: long done
     SCONV_CUDA(cudaEventSynchronize(ev_flags));
     check_deferred_map_flags(deferred_flags, raw_input);

@@ -88,6 +88,11 @@ struct NetData {
   cudaEvent_t rb_ready[2] = {nullptr, nullptr}, rb_done[2] = {nullptr, nullptr};
   bool rb_pending[2] = {false, false};
   int rb_slot = 0;
+  // GPU span of the last completed forward on the context stream (timing events at its start /
+  // end, read once complete): sizes the async readback's chunks (sconv_net_read_async)
+  cudaEvent_t fwd_t0 = nullptr, fwd_t1 = nullptr;
+  bool fwd_timed = false;
+  float last_fwd_ms = -1.f;
   // host inputs (sconv_net_forward with host pointers) are copied on in_stream into one of two
   // staging slots, independent of the context stream: the next request's H2D and its map builds
   // (which wait for in_ready instead of everything on the context stream) overlap the previous
