@@ -223,7 +223,7 @@ class NetWorkload:
             d2h += self.out_pinned[i].nbytes
         return h2d, d2h
 
-    def e2e_run(self, k):
+    def e2e_run(self, k, fwd_ms=None):
         """k steps back to back through the public API as a serving loop runs them: every scene's
         inputs from pinned host memory (H2D inside sconv_net_forward, on the net's input stream), every scene's fp32 result
         read back with sconv_net_read_async -- its D2H copy runs on the net's copy stream beside
@@ -232,12 +232,22 @@ class NetWorkload:
         torch = self.torch
         h2d = d2h = 0
         first = True
+        # prefetch the next request's inputs when their H2D (~50 GB/s pinned) is >= 5 % of a
+        # forward (r02cq same box: C3 12 MB inputs 1.307 -> 1.290 ms, C4 27 MB 0.822 -> 0.799;
+        # r02cj: C2 3.3 MB 2.24 -> 2.54, so not there); BENCH_E2E_PREFETCH=0/1 forces it
+        env = os.environ.get("BENCH_E2E_PREFETCH")
+        in_bytes = max(c.nbytes + f.nbytes for c, f in self.pinned)
+        self.prefetch = env == "1" if env in ("0", "1") else \
+            (fwd_ms is not None and in_bytes / 5e7 >= 0.05 * fwd_ms)
         reqs = [(s, i) for s in range(k) for i in range(len(self.pinned))]
         for r, (s, i) in enumerate(reqs):
             c, f = self.pinned[i]
             self.net.forward(c, f, True)
-            # (sconv_net_prefetch_inputs here, r02cj same box: C2 2.24 -> 2.54 ms, C4 0.83 -> 0.80:
-            # the next request's map builds then start at once and slow this forward's convs)
+            # sconv_net_prefetch_inputs of the next request (BENCH_E2E_PREFETCH=1; r02cj same box:
+            # C2 2.24 -> 2.54 ms, C4 0.83 -> 0.80: the next request's map builds then start at once
+            # and slow this forward's convs)
+            if self.prefetch and r + 1 < len(reqs):
+                self.net.prefetch(*self.pinned[reqs[r + 1][1]])
             n, ch, _ = self.net.info(self.g.output)
             key = (i, s & 1)
             if self.out_pinned.get(key) is None or self.out_pinned[key].shape != (n, ch):
@@ -556,16 +566,18 @@ def main():
     e2e_t = lat_t
     if hasattr(wl, "e2e_run"):
         k_e2e = max(5, min(args.steps, 20))
-        wl.e2e_run(2)
+        fwd_ms = max_total_ms / args.steps / max(1, len(getattr(wl, "pinned", [None])))  # per request
+        wl.e2e_run(2, fwd_ms)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        h2d, d2h = wl.e2e_run(k_e2e)
+        h2d, d2h = wl.e2e_run(k_e2e, fwd_ms)
         torch.cuda.synchronize()
         e2e_t = torch.tensor([(time.perf_counter() - t0) / k_e2e], dtype=torch.float64, device="cuda")
         if dist:
             dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-        e2e_mode = ("pipelined: %d steps back to back, each step's inputs H2D from pinned memory and its fp32 result "
-                    "D2H (sconv_net_read_async, overlapping the next step's forward), host clock around all" % k_e2e)
+        e2e_mode = ("pipelined: %d steps back to back, each step's inputs H2D from pinned memory%s and its fp32 "
+                    "result D2H (sconv_net_read_async, overlapping the next step's forward), host clock around all"
+                    % (k_e2e, " (prefetched beside the previous forward)" if getattr(wl, "prefetch", False) else ""))
     e2e_pps = job_points / float(e2e_t.item())
     gc.enable()
 
